@@ -1,0 +1,148 @@
+/*
+ * dot_b200.h -- C ABI of the B200-native Dynamic PlenOctree (DOT) hot path.
+ *
+ * Drop-in boundary for the reference's operator layer `octrf._kernels`
+ * (/root/reference/pkg/src/octrf/_kernels.py), which `octrf/render.py`,
+ * `octrf/calibrate.py` and `octrf/optim.py` call with flat arrays,
+ * caller-allocated outputs and no exceptions.  Every entry point here takes
+ * plain device pointers + sizes + a cudaStream_t (as void*), returns a
+ * dot_status, never frees caller memory and never synchronises unless the
+ * comment says so.  Scratch memory is stream-ordered (cudaMallocAsync).
+ *
+ * Tree layout (canonical BFS):
+ *   node[i] >= 0 : internal node, its 8 children are node[i] .. node[i]+7
+ *                  in octant order (x -> bit 0, y -> bit 1, z -> bit 2);
+ *   node[i] <  0 : leaf, payload row = ~node[i] (the reference's pool id).
+ *   Node centres are not stored: c_child = c_parent +/- h_child in fp64,
+ *   which reproduces the reference's stored centres bit-exactly
+ *   (octree.py:228-238, 411-414).
+ *   sigma[capacity] f32, sh[capacity * sh_stride] f32 channel-major
+ *   (sh[k*B + b], octree.py:48-50), rows padded to a multiple of 4 floats.
+ */
+#ifndef DOT_B200_H
+#define DOT_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum dot_status {
+    DOT_OK = 0,
+    DOT_BAD_ARG = 1,   /* maps to octrf.errors.InputError / ConfigError     */
+    DOT_OOM = 2,       /* scratch allocation failed                          */
+    DOT_CUDA_ERR = 3,  /* launch / runtime failure, see dot_last_error()    */
+    DOT_NO_DEVICE = 4  /* no sm_100 device visible                           */
+} dot_status;
+
+typedef struct dot_tree_view {
+    const int32_t* node;      /* [n_nodes] canonical node words (device)     */
+    int64_t n_nodes;
+    const float* sigma;       /* [capacity] (device)                          */
+    const float* sh;          /* [capacity * sh_stride] (device)              */
+    int64_t capacity;
+    int32_t basis_count;      /* 1, 4, 9 or 16                               */
+    int32_t sh_stride;        /* floats per row, multiple of 4, >= 3*B       */
+    double center[3];         /* root cube centre                            */
+    double half_extent;       /* root cube half edge                         */
+    int32_t max_depth;
+    int32_t _pad;
+} dot_tree_view;
+
+/* Library identity / diagnostics. */
+int dot_abi_version(void);
+const char* dot_last_error(void);
+int dot_device_check(void);
+
+/* --- traversal (replaces count_segments_kernel / fill_segments_kernel,
+ *     _kernels.py:161-182, driven by render.segment_batch render.py:105-124) */
+int dot_trace_count(const dot_tree_view* tree, const double* origins, const double* dirs,
+                    int64_t n_rays, double t_near, double t_far, int64_t* counts,
+                    void* stream);
+int dot_trace_fill(const dot_tree_view* tree, const double* origins, const double* dirs,
+                   int64_t n_rays, double t_near, double t_far, const int64_t* offsets,
+                   int64_t* seg_leaf, double* seg_t, double* seg_delta, void* stream);
+
+/* --- fused forward: traverse + composite with early termination
+ *     (replaces segment_batch + composite_kernel, _kernels.py:185-224, as
+ *     called by render.render_rays render.py:134-152).  Any output may be
+ *     NULL.  depth = sum_i T_i Q_i (t_i + delta_i/2) (not in the reference). */
+int dot_render_fwd(const dot_tree_view* tree, const double* origins, const double* dirs,
+                   int64_t n_rays, const double* background, double early_stop_eps,
+                   double t_near, double t_far, float* rgb, float* t_final, float* wsum,
+                   float* depth, void* stream);
+
+/* --- fused forward + backward + signal (replaces segment_batch + grad_kernel
+ *     + scatter_kernel, _kernels.py:227-346, as called by
+ *     render.render_and_backprop render.py:175-225).
+ *     Accumulates (+=) into grad_sigma[capacity] f32, grad_sh[capacity*gsh_stride]
+ *     f32, signal[capacity] f64, loss_sum[1] f64 (sum over rays of the squared
+ *     error; the caller divides by n), and sets touched[capacity] u8 to 1 for
+ *     every traversed leaf (post-cut segments included, like scatter_kernel).
+ *     grad_scale is the reference's 2/n (2/n_global when rays are sharded).
+ *     rgb_out (f32 [n,3]) may be NULL.  flags: bit0 = skip post-cut touched
+ *     marking (not reference semantics). */
+int dot_render_bwd(const dot_tree_view* tree, const double* origins, const double* dirs,
+                   const double* targets, int64_t n_rays, const double* background,
+                   double early_stop_eps, double t_near, double t_far, double grad_scale,
+                   float* grad_sigma, float* grad_sh, int32_t gsh_stride, double* signal,
+                   uint8_t* touched, double* loss_sum, float* rgb_out, int32_t flags,
+                   void* stream);
+
+/* --- refine (DOT calibration, calibrate.py:202-238) ------------------------
+ * One call runs prune (one-shot or recursive) then sample on the post-prune
+ * topology and writes the refined tree directly in canonical BFS order
+ * (scene_io.py:529-541).  Inputs: the tree view (payload rows indexed by
+ * pool id = ~leaf word), pool_id[n_nodes] (pool id of every canonical node,
+ * NULL = identity), acc[capacity] f64 accumulated signals (ignored when
+ * use_sigma), parameters as CalibrationConfig (recursive: 1 = repeat the
+ * prune to a fixed point, 0 = one round, -1 = no prune at all, i.e. the
+ * reference's sample() alone; gamma = 0 and use_threshold = 0 disable the
+ * sample, i.e. prune() alone).  Because the output size is
+ * data dependent, the call is split in two:
+ *   dot_refine_plan  -> computes the selections and output sizes and stores
+ *                       them in an opaque plan (synchronises the stream once);
+ *   dot_refine_apply -> writes the new node words / payload / remap.
+ * Outputs of apply (device, caller-allocated to the sizes the plan reports):
+ *   new_node[n_new] i32, new_sigma[n_new] f32, new_sh[n_new*sh_stride] f32
+ *   (pool id == canonical id in the result; internal rows are zero),
+ *   src_index[n_new] i64: canonical old node a new node descends from
+ *     (itself for surviving nodes, the split leaf for its new children),
+ *   src_kind[n_new] u8: 0 kept, 1 merged parent (now a leaf), 2 child of a
+ *     split (payload copied), 3 split parent (now internal).
+ */
+typedef struct dot_refine_plan dot_refine_plan;
+typedef struct dot_refine_stats {
+    int64_t leaves_before, leaves_after;
+    int64_t merges_applied, splits_applied, recursion_rounds;
+    int64_t n_new_nodes;
+} dot_refine_stats;
+
+int dot_refine_plan_create(const dot_tree_view* tree, const int32_t* pool_id,
+                           const double* acc, int32_t use_sigma, double tau, double gamma,
+                           int32_t recursive, int32_t use_threshold, double threshold,
+                           dot_refine_plan** plan, dot_refine_stats* stats, void* stream);
+/* Merged-parent / split-leaf lists (canonical old indices, ascending).
+ * Pointers stay valid until dot_refine_plan_destroy. */
+int dot_refine_plan_lists(const dot_refine_plan* plan, const int64_t** merge_parents,
+                          int64_t* n_merge, const int64_t** split_leaves, int64_t* n_split,
+                          const int32_t** merge_round);
+int dot_refine_apply(const dot_refine_plan* plan, const dot_tree_view* tree,
+                     int32_t* new_node, float* new_sigma, float* new_sh,
+                     int64_t* src_index, uint8_t* src_kind, void* stream);
+void dot_refine_plan_destroy(dot_refine_plan* plan);
+
+/* --- optimizer (optim.rmsprop_step, optim.py:107-135): sparse RMSProp over
+ *     leaves with touched[pid] != 0; sigma clamped >= 0.  v_* are f64. */
+int dot_rmsprop_step(float* sigma, float* sh, int32_t sh_stride, int32_t n_sh,
+                     double* v_sigma, double* v_sh, const float* grad_sigma,
+                     const float* grad_sh, int32_t gsh_stride, const uint8_t* touched,
+                     int64_t capacity, double beta, double eps, double lr_sigma,
+                     double lr_sh, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* DOT_B200_H */

@@ -1,0 +1,120 @@
+// capi.cu -- extern "C" entry points declared in include/dot_b200.h.
+//
+// Argument validation mirrors the reference's Python-side checks
+// (render.py:38-41, 189-191; calibrate.py:36-42); kernels never raise.
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include "dot_tree.cuh"
+#include "dot_internal.h"
+
+namespace dot {
+
+static thread_local char g_err[512] = "";
+
+int set_error(int status, const char* fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+    return status;
+}
+
+int check_cuda(cudaError_t e, const char* what) {
+    if (e == cudaSuccess) return DOT_OK;
+    const int st = (e == cudaErrorMemoryAllocation) ? DOT_OOM : DOT_CUDA_ERR;
+    return set_error(st, "%s: %s", what, cudaGetErrorString(e));
+}
+
+int check_launch(const char* what) { return check_cuda(cudaGetLastError(), what); }
+
+static int validate_tree(const dot_tree_view* v) {
+    if (!v) return set_error(DOT_BAD_ARG, "tree view is NULL");
+    if (!v->node || v->n_nodes < 1) return set_error(DOT_BAD_ARG, "tree has no nodes");
+    if (!v->sigma || !v->sh) return set_error(DOT_BAD_ARG, "tree payload is NULL");
+    const int B = v->basis_count;
+    if (B != 1 && B != 4 && B != 9 && B != 16)
+        return set_error(DOT_BAD_ARG, "basis_count must be 1, 4, 9 or 16, got %d", B);
+    if (v->sh_stride != pad4(3 * B))
+        return set_error(DOT_BAD_ARG, "sh_stride must be %d for B=%d, got %d", pad4(3 * B), B,
+                         v->sh_stride);
+    if (!(v->half_extent > 0.0)) return set_error(DOT_BAD_ARG, "half_extent must be positive");
+    if ((reinterpret_cast<uintptr_t>(v->sh) & 15) != 0)
+        return set_error(DOT_BAD_ARG, "sh must be 16-byte aligned");
+    return DOT_OK;
+}
+
+}  // namespace dot
+
+using namespace dot;
+
+extern "C" {
+
+int dot_abi_version(void) { return 1; }
+
+const char* dot_last_error(void) { return g_err; }
+
+int dot_device_check(void) {
+    int dev = 0, n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0)
+        return set_error(DOT_NO_DEVICE, "no CUDA device visible");
+    cudaGetDevice(&dev);
+    cudaDeviceProp p;
+    cudaGetDeviceProperties(&p, dev);
+    if (p.major != 10) return set_error(DOT_NO_DEVICE, "device %s is sm_%d%d, need sm_100", p.name, p.major, p.minor);
+    return DOT_OK;
+}
+
+int dot_trace_count(const dot_tree_view* tree, const double* origins, const double* dirs,
+                    int64_t n_rays, double t_near, double t_far, int64_t* counts, void* stream) {
+    if (int st = validate_tree(tree)) return st;
+    if (n_rays < 0 || (n_rays && (!origins || !dirs || !counts)))
+        return set_error(DOT_BAD_ARG, "bad ray arrays");
+    return launch_trace_count(make_tree(*tree), origins, dirs, n_rays, t_near, t_far, counts,
+                              static_cast<cudaStream_t>(stream));
+}
+
+int dot_trace_fill(const dot_tree_view* tree, const double* origins, const double* dirs,
+                   int64_t n_rays, double t_near, double t_far, const int64_t* offsets,
+                   int64_t* seg_leaf, double* seg_t, double* seg_delta, void* stream) {
+    if (int st = validate_tree(tree)) return st;
+    if (n_rays < 0 || (n_rays && (!origins || !dirs || !offsets)))
+        return set_error(DOT_BAD_ARG, "bad ray arrays");
+    return launch_trace_fill(make_tree(*tree), origins, dirs, n_rays, t_near, t_far, offsets,
+                             seg_leaf, seg_t, seg_delta, static_cast<cudaStream_t>(stream));
+}
+
+int dot_render_fwd(const dot_tree_view* tree, const double* origins, const double* dirs,
+                   int64_t n_rays, const double* background, double early_stop_eps,
+                   double t_near, double t_far, float* rgb, float* t_final, float* wsum,
+                   float* depth, void* stream) {
+    if (int st = validate_tree(tree)) return st;
+    if (n_rays < 0 || (n_rays && (!origins || !dirs)) || !background)
+        return set_error(DOT_BAD_ARG, "bad ray arrays");
+    return launch_render_fwd(make_tree(*tree), origins, dirs, n_rays, background, early_stop_eps,
+                             t_near, t_far, rgb, t_final, wsum, depth,
+                             static_cast<cudaStream_t>(stream));
+}
+
+int dot_render_bwd(const dot_tree_view* tree, const double* origins, const double* dirs,
+                   const double* targets, int64_t n_rays, const double* background,
+                   double early_stop_eps, double t_near, double t_far, double grad_scale,
+                   float* grad_sigma, float* grad_sh, int32_t gsh_stride, double* signal,
+                   uint8_t* touched, double* loss_sum, float* rgb_out, int32_t flags,
+                   void* stream) {
+    if (int st = validate_tree(tree)) return st;
+    if (n_rays < 0 || (n_rays && (!origins || !dirs || !targets)) || !background)
+        return set_error(DOT_BAD_ARG, "bad ray arrays");
+    if (!grad_sigma || !grad_sh || !signal || !touched || !loss_sum)
+        return set_error(DOT_BAD_ARG, "gradient / signal outputs must not be NULL");
+    if (gsh_stride != tree->sh_stride)
+        return set_error(DOT_BAD_ARG, "gsh_stride must equal sh_stride (%d)", tree->sh_stride);
+    if ((reinterpret_cast<uintptr_t>(grad_sh) & 15) != 0)
+        return set_error(DOT_BAD_ARG, "grad_sh must be 16-byte aligned");
+    return launch_render_bwd(make_tree(*tree), origins, dirs, targets, n_rays, background,
+                             early_stop_eps, t_near, t_far, grad_scale, grad_sigma, grad_sh,
+                             signal, touched, loss_sum, rgb_out, flags,
+                             static_cast<cudaStream_t>(stream));
+}
+
+}  // extern "C"

@@ -1,0 +1,28 @@
+// dot_internal.h -- shared host-side helpers of the C ABI implementation.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+#include "../../include/dot_b200.h"
+
+namespace dot {
+
+struct TreeDev;
+
+int set_error(int status, const char* fmt, ...);
+int check_launch(const char* what);
+int check_cuda(cudaError_t e, const char* what);
+
+int launch_trace_count(const TreeDev& T, const double* o, const double* d, int64_t n,
+                       double tn, double tf, int64_t* counts, cudaStream_t s);
+int launch_trace_fill(const TreeDev& T, const double* o, const double* d, int64_t n, double tn,
+                      double tf, const int64_t* off, int64_t* leaf, double* t, double* dl,
+                      cudaStream_t s);
+int launch_render_fwd(const TreeDev& T, const double* o, const double* d, int64_t n,
+                      const double* bg, double eps, double tn, double tf, float* rgb, float* tfin,
+                      float* wsum, float* depth, cudaStream_t s);
+int launch_render_bwd(const TreeDev& T, const double* o, const double* d, const double* tgt,
+                      int64_t n, const double* bg, double eps, double tn, double tf, double gs,
+                      float* gsig, float* gsh, double* signal, uint8_t* touched, double* loss,
+                      float* rgb_out, int flags, cudaStream_t s);
+
+}  // namespace dot

@@ -1,0 +1,213 @@
+// dot_tree.cuh -- device-side tree view, exact fp64 traversal, SH shading.
+//
+// Traversal reproduces /root/reference/pkg/src/octrf/_kernels.py:56-158
+// bit-exactly: every geometry operation is an explicit round-to-nearest fp64
+// intrinsic (__dadd_rn/__dmul_rn/__ddiv_rn), so nvcc can never contract it
+// into an FMA (the Numba kernels contain none) and division is IEEE.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+#include "../../include/dot_b200.h"
+
+namespace dot {
+
+constexpr double kNudgeRel = 2e-12;  // _kernels.py:16
+
+struct TreeDev {
+    const int32_t* __restrict__ node;
+    const float* __restrict__ sigma;
+    const float* __restrict__ sh;
+    int64_t n_nodes;
+    int32_t basis_count;
+    int32_t sh_stride;
+    double cx, cy, cz, half;
+};
+
+inline TreeDev make_tree(const dot_tree_view& v) {
+    TreeDev t;
+    t.node = v.node;
+    t.sigma = v.sigma;
+    t.sh = v.sh;
+    t.n_nodes = v.n_nodes;
+    t.basis_count = v.basis_count;
+    t.sh_stride = v.sh_stride;
+    t.cx = v.center[0];
+    t.cy = v.center[1];
+    t.cz = v.center[2];
+    t.half = v.half_extent;
+    return t;
+}
+
+__device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double ddiv(double a, double b) { return __ddiv_rn(a, b); }
+
+// Located leaf: payload row, cube centre and half extent.
+struct Leaf {
+    int32_t pid;
+    double cx, cy, cz, h;
+};
+
+// _kernels.py:56-68 from the root, with child centres recomputed exactly:
+// c_child = c + (h_parent * 0.5) * sign  (octree.py:228-238).
+__device__ __forceinline__ Leaf descend(const TreeDev& T, double px, double py, double pz) {
+    double cx = T.cx, cy = T.cy, cz = T.cz, h = T.half;
+    int32_t w = __ldg(T.node);
+    while (w >= 0) {
+        const int o = (px >= cx ? 1 : 0) | (py >= cy ? 2 : 0) | (pz >= cz ? 4 : 0);
+        h = dmul(h, 0.5);
+        cx = (o & 1) ? dadd(cx, h) : dsub(cx, h);
+        cy = (o & 2) ? dadd(cy, h) : dsub(cy, h);
+        cz = (o & 4) ? dadd(cz, h) : dsub(cz, h);
+        w = __ldg(T.node + w + o);
+    }
+    Leaf L;
+    L.pid = ~w;
+    L.cx = cx;
+    L.cy = cy;
+    L.cz = cz;
+    L.h = h;
+    return L;
+}
+
+// One ray walking the tree one exact leaf segment at a time (_trace_ray).
+struct Tracer {
+    double ox, oy, oz, dx, dy, dz;
+    double t, t1, nudge0, nudge;
+
+    // Slab clip against the half-open root cube (_kernels.py:80-106).
+    __device__ __forceinline__ bool init(const TreeDev& T, double t_near, double t_far) {
+        const double rh = T.half;
+        double t0 = t_near;
+        t1 = t_far;
+        const double o3[3] = {ox, oy, oz};
+        const double d3[3] = {dx, dy, dz};
+        const double c3[3] = {T.cx, T.cy, T.cz};
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            const double lo = dsub(c3[a], rh), hi = dadd(c3[a], rh);
+            const double o = o3[a], d = d3[a];
+            if (d != 0.0) {
+                double ta = ddiv(dsub(lo, o), d), tb = ddiv(dsub(hi, o), d);
+                if (ta > tb) { const double s = ta; ta = tb; tb = s; }
+                if (ta > t0) t0 = ta;
+                if (tb < t1) t1 = tb;
+            } else if (o < lo || o >= hi) {
+                return false;
+            }
+        }
+        if (t1 <= t0) return false;
+        nudge0 = dmul(rh, kNudgeRel);
+        nudge = nudge0;
+        t = t0;
+        return true;
+    }
+
+    // _kernels.py:112-158.  Returns false when the ray has left the cube.
+    __device__ __forceinline__ bool next(const TreeDev& T, Leaf& L, double& t_entry,
+                                         double& delta) {
+        for (;;) {
+            const double probe = dadd(t, nudge);
+            if (probe >= t1) return false;
+            const double px = dadd(ox, dmul(probe, dx));
+            const double py = dadd(oy, dmul(probe, dy));
+            const double pz = dadd(oz, dmul(probe, dz));
+            L = descend(T, px, py, pz);
+            double tex = t1, cand;
+            if (dx > 0.0) { cand = ddiv(dsub(dadd(L.cx, L.h), ox), dx); if (cand < tex) tex = cand; }
+            else if (dx < 0.0) { cand = ddiv(dsub(dsub(L.cx, L.h), ox), dx); if (cand < tex) tex = cand; }
+            if (dy > 0.0) { cand = ddiv(dsub(dadd(L.cy, L.h), oy), dy); if (cand < tex) tex = cand; }
+            else if (dy < 0.0) { cand = ddiv(dsub(dsub(L.cy, L.h), oy), dy); if (cand < tex) tex = cand; }
+            if (dz > 0.0) { cand = ddiv(dsub(dadd(L.cz, L.h), oz), dz); if (cand < tex) tex = cand; }
+            else if (dz < 0.0) { cand = ddiv(dsub(dsub(L.cz, L.h), oz), dz); if (cand < tex) tex = cand; }
+            if (tex <= probe) {  // boundary roundoff stalled the walk: widen the probe
+                nudge = dmul(nudge, 4.0);
+                continue;
+            }
+            t_entry = t;
+            delta = dsub(tex, t);
+            t = tex;
+            nudge = nudge0;
+            return true;
+        }
+    }
+};
+
+// Real SH basis, svox/3DGS signs (_kernels.py:30-53), evaluated in fp64 like
+// the reference and rounded once to fp32 for the per-segment dot products.
+template <int B>
+__device__ __forceinline__ void eval_basis(double x, double y, double z, float* out) {
+    out[0] = 0.28209479177387814f;
+    if constexpr (B >= 4) {
+        const double C1 = 0.4886025119029199;
+        out[1] = float(-C1 * y);
+        out[2] = float(C1 * z);
+        out[3] = float(-C1 * x);
+    }
+    if constexpr (B >= 9) {
+        const double xx = x * x, yy = y * y, zz = z * z;
+        out[4] = float(1.0925484305920792 * x * y);
+        out[5] = float(-1.0925484305920792 * y * z);
+        out[6] = float(0.31539156525252005 * (2.0 * zz - xx - yy));
+        out[7] = float(-1.0925484305920792 * x * z);
+        out[8] = float(0.5462742152960396 * (xx - yy));
+        if constexpr (B >= 16) {
+            out[9] = float(-0.5900435899266435 * y * (3.0 * xx - yy));
+            out[10] = float(2.890611442640554 * x * y * z);
+            out[11] = float(-0.4570457994644658 * y * (4.0 * zz - xx - yy));
+            out[12] = float(0.3731763325901154 * z * (2.0 * zz - 3.0 * xx - 3.0 * yy));
+            out[13] = float(-0.4570457994644658 * x * (4.0 * zz - xx - yy));
+            out[14] = float(1.445305721320277 * z * (xx - yy));
+            out[15] = float(-0.5900435899266435 * x * (xx - 3.0 * yy));
+        }
+    }
+}
+
+__host__ __device__ constexpr int pad4(int n) { return (n + 3) & ~3; }
+
+// e_k = sum_b sh[k*B+b] * basis[b] for k = 0..2 from one 16-byte aligned row
+// (vector loads; the row is read once, never kept whole in registers).
+template <int B>
+__device__ __forceinline__ void sh_dot(const float* __restrict__ row, const float* basis,
+                                       float& e0, float& e1, float& e2) {
+    constexpr int S = pad4(3 * B);
+    const float4* r4 = reinterpret_cast<const float4*>(row);
+    float e[3] = {0.f, 0.f, 0.f};
+#pragma unroll
+    for (int j = 0; j < S / 4; ++j) {
+        const float4 v = __ldg(r4 + j);
+        const float vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int idx = 4 * j + i;
+            if (idx < 3 * B) e[idx / B] = fmaf(vv[i], basis[idx % B], e[idx / B]);
+        }
+    }
+    e0 = e[0];
+    e1 = e[1];
+    e2 = e[2];
+}
+
+// Branch-stable logistic (_kernels.py:22-27) in fp32.
+__device__ __forceinline__ float sigmoidf(float x) {
+    if (x >= 0.f) return __frcp_rn(1.f + __expf(-x));
+    const float e = __expf(x);
+    return __fdividef(e, 1.f + e);
+}
+
+// Vector reduction into global memory (REDG.E.ADD.F32x4, sm_90+).
+__device__ __forceinline__ void red_add_v4(float* addr, float a, float b, float c, float d) {
+    asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};"
+                 :: "l"(addr), "f"(a), "f"(b), "f"(c), "f"(d) : "memory");
+}
+
+__device__ __forceinline__ void red_add_f32(float* addr, float a) {
+    asm volatile("red.global.add.f32 [%0], %1;" :: "l"(addr), "f"(a) : "memory");
+}
+
+__device__ __forceinline__ void red_add_f64(double* addr, double a) {
+    asm volatile("red.global.add.f64 [%0], %1;" :: "l"(addr), "d"(a) : "memory");
+}
+
+}  // namespace dot

@@ -1,0 +1,65 @@
+// optim.cu -- sparse RMSProp leaf update (optim.py:107-135).
+//
+// Only rows with touched[pid] != 0 move; the second-moment state is fp64 like
+// the reference's RmsPropState (optim.py:70-72) and every operation is an
+// explicit round-to-nearest intrinsic so that, given the same gradients, the
+// update is bit-identical to the numpy expression
+//   v = beta*v + (1-beta)*g*g;  theta = f32(max(f64(theta) - lr*g/(sqrt(v)+eps), 0)).
+#include "dot_tree.cuh"
+#include "dot_internal.h"
+
+namespace dot {
+
+__device__ __forceinline__ float rms_update(float theta, double& v, double g, double beta,
+                                            double omb, double eps, double lr, bool clamp) {
+    v = __dadd_rn(__dmul_rn(beta, v), __dmul_rn(__dmul_rn(omb, g), g));
+    double t = __dsub_rn(double(theta), __ddiv_rn(__dmul_rn(lr, g), __dadd_rn(__dsqrt_rn(v), eps)));
+    if (clamp && !(t >= 0.0)) t = (t != t) ? t : 0.0;  // np.maximum keeps NaN
+    return float(t);
+}
+
+// One thread per (row, column); column 0 is sigma, 1..n_sh the SH coefficients.
+__global__ void rmsprop_kernel(float* __restrict__ sigma, float* __restrict__ sh, int sh_stride, int n_sh,
+                               double* __restrict__ v_sigma, double* __restrict__ v_sh,
+                               const float* __restrict__ gsig, const float* __restrict__ gsh,
+                               int gsh_stride, const uint8_t* __restrict__ touched, int64_t cap,
+                               double beta, double eps, double lr_sigma, double lr_sh) {
+    const int cols = 1 + n_sh;
+    const int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (t >= cap * cols) return;
+    const int64_t row = t / cols;
+    const int c = int(t - row * cols);
+    if (!touched[row]) return;
+    const double omb = __dsub_rn(1.0, beta);
+    if (c == 0) {
+        double v = v_sigma[row];
+        sigma[row] = rms_update(sigma[row], v, double(gsig[row]), beta, omb, eps, lr_sigma, true);
+        v_sigma[row] = v;
+    } else {
+        const int k = c - 1;
+        double v = v_sh[row * n_sh + k];
+        float* p = sh + row * sh_stride + k;
+        *p = rms_update(*p, v, double(gsh[row * gsh_stride + k]), beta, omb, eps, lr_sh, false);
+        v_sh[row * n_sh + k] = v;
+    }
+}
+
+}  // namespace dot
+
+using namespace dot;
+
+extern "C" int dot_rmsprop_step(float* sigma, float* sh, int32_t sh_stride, int32_t n_sh, double* v_sigma,
+                                double* v_sh, const float* grad_sigma, const float* grad_sh,
+                                int32_t gsh_stride, const uint8_t* touched, int64_t capacity, double beta,
+                                double eps, double lr_sigma, double lr_sh, void* stream) {
+    if (!sigma || !sh || !v_sigma || !v_sh || !grad_sigma || !grad_sh || !touched)
+        return set_error(DOT_BAD_ARG, "rmsprop: NULL argument");
+    if (!(beta > 0.0 && beta < 1.0)) return set_error(DOT_BAD_ARG, "beta must be in (0, 1), got %g", beta);
+    if (n_sh < 1 || sh_stride < n_sh || gsh_stride < n_sh) return set_error(DOT_BAD_ARG, "rmsprop: bad strides");
+    if (capacity == 0) return DOT_OK;
+    const int64_t total = capacity * (1 + n_sh);
+    rmsprop_kernel<<<unsigned((total + 255) / 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+        sigma, sh, sh_stride, n_sh, v_sigma, v_sh, grad_sigma, grad_sh, gsh_stride, touched, capacity, beta,
+        eps, lr_sigma, lr_sh);
+    return check_launch("rmsprop_kernel");
+}

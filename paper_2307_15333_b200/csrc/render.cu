@@ -1,0 +1,297 @@
+// render.cu -- traversal, fused forward and fused forward+backward kernels.
+//
+// One thread per ray.  The reference (octrf/render.py:105-225 over
+// octrf/_kernels.py:161-346) materialises every ray's segment list twice
+// (count + fill), then composites, then reduces per leaf serially.  Here the
+// traversal is streamed: a segment is consumed the moment it is produced and
+// never touches HBM; the backward recomputes the forward instead of saving
+// ~96 B of per-segment scratch, and leaf gradients / signal are reduced with
+// vector REDs (REDG.E.ADD.F32x4) straight into the per-leaf buffers.
+#include "dot_tree.cuh"
+#include "dot_internal.h"
+
+namespace dot {
+
+constexpr int kBlock = 128;
+
+__device__ __forceinline__ void load_ray(const double* __restrict__ o, const double* __restrict__ d,
+                                         int64_t r, Tracer& tr) {
+    tr.ox = __ldg(o + 3 * r + 0);
+    tr.oy = __ldg(o + 3 * r + 1);
+    tr.oz = __ldg(o + 3 * r + 2);
+    tr.dx = __ldg(d + 3 * r + 0);
+    tr.dy = __ldg(d + 3 * r + 1);
+    tr.dz = __ldg(d + 3 * r + 2);
+}
+
+// ---------------------------------------------------------------------------
+// Segment lists (parity / debug path of segment_batch).
+
+__global__ void __launch_bounds__(kBlock) trace_count_kernel(TreeDev T, const double* __restrict__ o,
+                                                             const double* __restrict__ d, int64_t n,
+                                                             double t_near, double t_far,
+                                                             int64_t* __restrict__ counts) {
+    const int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (r >= n) return;
+    Tracer tr;
+    load_ray(o, d, r, tr);
+    int64_t c = 0;
+    if (tr.init(T, t_near, t_far)) {
+        Leaf L;
+        double te, dl;
+        while (tr.next(T, L, te, dl)) ++c;
+    }
+    counts[r] = c;
+}
+
+__global__ void __launch_bounds__(kBlock) trace_fill_kernel(TreeDev T, const double* __restrict__ o,
+                                                            const double* __restrict__ d, int64_t n,
+                                                            double t_near, double t_far,
+                                                            const int64_t* __restrict__ offsets,
+                                                            int64_t* __restrict__ seg_leaf,
+                                                            double* __restrict__ seg_t,
+                                                            double* __restrict__ seg_delta) {
+    const int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (r >= n) return;
+    Tracer tr;
+    load_ray(o, d, r, tr);
+    int64_t s = offsets[r];
+    if (tr.init(T, t_near, t_far)) {
+        Leaf L;
+        double te, dl;
+        while (tr.next(T, L, te, dl)) {
+            seg_leaf[s] = L.pid;
+            seg_t[s] = te;
+            seg_delta[s] = dl;
+            ++s;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Fused forward: traverse + composite (composite_kernel, _kernels.py:185-224).
+
+template <int B>
+__global__ void __launch_bounds__(kBlock) render_fwd_kernel(
+    TreeDev T, const double* __restrict__ o, const double* __restrict__ d, int64_t n,
+    double bg0, double bg1, double bg2, double eps, double t_near, double t_far,
+    float* __restrict__ rgb, float* __restrict__ tfin_out, float* __restrict__ wsum_out,
+    float* __restrict__ depth_out) {
+    constexpr int S = pad4(3 * B);
+    const int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (r >= n) return;
+    Tracer tr;
+    load_ray(o, d, r, tr);
+    float basis[B];
+    eval_basis<B>(tr.dx, tr.dy, tr.dz, basis);
+    double trans = 1.0, c0 = 0.0, c1 = 0.0, c2 = 0.0, ws = 0.0, dep = 0.0;
+    if (tr.init(T, t_near, t_far)) {
+        Leaf L;
+        double te, dl;
+        while (tr.next(T, L, te, dl)) {
+            const double sg = double(__ldg(T.sigma + L.pid));
+            const double a = exp(-sg * dl);
+            const double q = 1.0 - a;
+            if (q > 0.0) {
+                float e0, e1, e2;
+                sh_dot<B>(T.sh + int64_t(L.pid) * S, basis, e0, e1, e2);
+                const double tq = trans * q;
+                c0 += tq * double(sigmoidf(e0));
+                c1 += tq * double(sigmoidf(e1));
+                c2 += tq * double(sigmoidf(e2));
+                ws += tq;
+                dep += tq * (te + 0.5 * dl);
+            }
+            trans *= a;
+            if (eps > 0.0 && trans < eps) break;
+        }
+    }
+    ws += trans;
+    if (rgb) {
+        rgb[3 * r + 0] = float(c0 + trans * bg0);
+        rgb[3 * r + 1] = float(c1 + trans * bg1);
+        rgb[3 * r + 2] = float(c2 + trans * bg2);
+    }
+    if (tfin_out) tfin_out[r] = float(trans);
+    if (wsum_out) wsum_out[r] = float(ws);
+    if (depth_out) depth_out[r] = float(dep);
+}
+
+// ---------------------------------------------------------------------------
+// Fused forward + backward + signal (grad_kernel + scatter_kernel,
+// _kernels.py:227-346).  Pass 1 composites to get rgb and the cut index;
+// pass 2 re-walks the ray, rebuilds T_i, Q_i, c_i, forms the suffix
+// suf_i = rgb - sum_{j<=i} T_j Q_j c_j and scatters
+//   dsigma_i = delta_i * sum_k g_k (T_i a_i c_ik - suf_ik)
+//   dsh_i[k*B+b] = g_k T_i Q_i c_ik (1 - c_ik) * basis_b
+// plus signal_i += Q_i and touched = 1 (post-cut segments: touched only).
+
+template <int B>
+__global__ void __launch_bounds__(kBlock) render_bwd_kernel(
+    TreeDev T, const double* __restrict__ o, const double* __restrict__ d,
+    const double* __restrict__ tgt, int64_t n, double bg0, double bg1, double bg2, double eps,
+    double t_near, double t_far, double grad_scale, float* __restrict__ gsig,
+    float* __restrict__ gsh, double* __restrict__ signal, uint8_t* __restrict__ touched,
+    double* __restrict__ loss_sum, float* __restrict__ rgb_out, int flags) {
+    constexpr int S = pad4(3 * B);
+    const int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    double loss = 0.0;
+    if (r < n) {
+        Tracer tr;
+        load_ray(o, d, r, tr);
+        float basis[B];
+        eval_basis<B>(tr.dx, tr.dy, tr.dz, basis);
+        const bool hit = tr.init(T, t_near, t_far);
+        const Tracer start = tr;
+        // ---- pass 1: forward to the cut
+        double trans = 1.0, c0 = 0.0, c1 = 0.0, c2 = 0.0;
+        int used = 0;
+        if (hit) {
+            Leaf L;
+            double te, dl;
+            while (tr.next(T, L, te, dl)) {
+                const double sg = double(__ldg(T.sigma + L.pid));
+                const double a = exp(-sg * dl);
+                const double q = 1.0 - a;
+                ++used;
+                if (q > 0.0) {
+                    float e0, e1, e2;
+                    sh_dot<B>(T.sh + int64_t(L.pid) * S, basis, e0, e1, e2);
+                    const double tq = trans * q;
+                    c0 += tq * double(sigmoidf(e0));
+                    c1 += tq * double(sigmoidf(e1));
+                    c2 += tq * double(sigmoidf(e2));
+                }
+                trans *= a;
+                if (eps > 0.0 && trans < eps) break;
+            }
+        }
+        const double tf = trans;
+        const double R0 = c0 + tf * bg0, R1 = c1 + tf * bg1, R2 = c2 + tf * bg2;
+        const double r0 = R0 - __ldg(tgt + 3 * r + 0);
+        const double r1 = R1 - __ldg(tgt + 3 * r + 1);
+        const double r2 = R2 - __ldg(tgt + 3 * r + 2);
+        loss = r0 * r0 + r1 * r1 + r2 * r2;
+        if (rgb_out) {
+            rgb_out[3 * r + 0] = float(R0);
+            rgb_out[3 * r + 1] = float(R1);
+            rgb_out[3 * r + 2] = float(R2);
+        }
+        const double g0 = grad_scale * r0, g1 = grad_scale * r1, g2 = grad_scale * r2;
+        // ---- pass 2: replay, reverse-mode quantities via the prefix identity
+        if (hit) {
+            tr = start;
+            Leaf L;
+            double te, dl;
+            double Ti = 1.0, p0 = 0.0, p1 = 0.0, p2 = 0.0;
+            int i = 0;
+            while (tr.next(T, L, te, dl)) {
+                const int64_t pid = L.pid;
+                if (i < used) {
+                    const double sg = double(__ldg(T.sigma + pid));
+                    const double a = exp(-sg * dl);
+                    const double q = 1.0 - a;
+                    float e0, e1, e2;
+                    sh_dot<B>(T.sh + pid * S, basis, e0, e1, e2);
+                    const float k0 = sigmoidf(e0), k1 = sigmoidf(e1), k2 = sigmoidf(e2);
+                    const double tq = Ti * q;
+                    p0 += tq * double(k0);
+                    p1 += tq * double(k1);
+                    p2 += tq * double(k2);
+                    const double tn = Ti * a;
+                    const double ds = dl * (g0 * (tn * k0 - (R0 - p0)) + g1 * (tn * k1 - (R1 - p1)) +
+                                            g2 * (tn * k2 - (R2 - p2)));
+                    red_add_f32(gsig + pid, float(ds));
+                    const float w0 = float(g0 * tq) * k0 * (1.f - k0);
+                    const float w1 = float(g1 * tq) * k1 * (1.f - k1);
+                    const float w2 = float(g2 * tq) * k2 * (1.f - k2);
+                    if (w0 != 0.f || w1 != 0.f || w2 != 0.f) {
+                        float* row = gsh + pid * S;
+#pragma unroll
+                        for (int j = 0; j < S / 4; ++j) {
+                            float v[4];
+#pragma unroll
+                            for (int u = 0; u < 4; ++u) {
+                                const int idx = 4 * j + u;
+                                const int k = idx / B;
+                                const float w = k == 0 ? w0 : (k == 1 ? w1 : w2);
+                                v[u] = idx < 3 * B ? w * basis[idx % B] : 0.f;
+                            }
+                            red_add_v4(row + 4 * j, v[0], v[1], v[2], v[3]);
+                        }
+                    }
+                    if (q != 0.0) red_add_f64(signal + pid, q);
+                    touched[pid] = 1;
+                    Ti *= a;
+                    ++i;
+                } else {
+                    if (flags & 1) break;
+                    touched[pid] = 1;
+                }
+            }
+        }
+    }
+    // ---- loss: warp reduce, one f64 RED per warp
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) loss += __shfl_down_sync(0xffffffffu, loss, off);
+    if ((threadIdx.x & 31) == 0 && loss != 0.0) red_add_f64(loss_sum, loss);
+}
+
+// ---------------------------------------------------------------------------
+
+static unsigned blocks_for(int64_t n) { return unsigned((n + kBlock - 1) / kBlock); }
+
+int launch_trace_count(const TreeDev& T, const double* o, const double* d, int64_t n,
+                       double tn, double tf, int64_t* counts, cudaStream_t s) {
+    if (n == 0) return DOT_OK;
+    trace_count_kernel<<<blocks_for(n), kBlock, 0, s>>>(T, o, d, n, tn, tf, counts);
+    return check_launch("trace_count_kernel");
+}
+
+int launch_trace_fill(const TreeDev& T, const double* o, const double* d, int64_t n, double tn,
+                      double tf, const int64_t* off, int64_t* leaf, double* t, double* dl,
+                      cudaStream_t s) {
+    if (n == 0) return DOT_OK;
+    trace_fill_kernel<<<blocks_for(n), kBlock, 0, s>>>(T, o, d, n, tn, tf, off, leaf, t, dl);
+    return check_launch("trace_fill_kernel");
+}
+
+int launch_render_fwd(const TreeDev& T, const double* o, const double* d, int64_t n,
+                      const double* bg, double eps, double tn, double tf, float* rgb, float* tfin,
+                      float* wsum, float* depth, cudaStream_t s) {
+    if (n == 0) return DOT_OK;
+#define DOT_FWD(BB)                                                                           \
+    render_fwd_kernel<BB><<<blocks_for(n), kBlock, 0, s>>>(T, o, d, n, bg[0], bg[1], bg[2], eps, \
+                                                           tn, tf, rgb, tfin, wsum, depth)
+    switch (T.basis_count) {
+        case 1: DOT_FWD(1); break;
+        case 4: DOT_FWD(4); break;
+        case 9: DOT_FWD(9); break;
+        case 16: DOT_FWD(16); break;
+        default: return set_error(DOT_BAD_ARG, "basis_count must be 1, 4, 9 or 16");
+    }
+#undef DOT_FWD
+    return check_launch("render_fwd_kernel");
+}
+
+int launch_render_bwd(const TreeDev& T, const double* o, const double* d, const double* tgt,
+                      int64_t n, const double* bg, double eps, double tn, double tf, double gs,
+                      float* gsig, float* gsh, double* signal, uint8_t* touched, double* loss,
+                      float* rgb_out, int flags, cudaStream_t s) {
+    if (n == 0) return DOT_OK;
+#define DOT_BWD(BB)                                                                          \
+    render_bwd_kernel<BB><<<blocks_for(n), kBlock, 0, s>>>(T, o, d, tgt, n, bg[0], bg[1], bg[2], \
+                                                           eps, tn, tf, gs, gsig, gsh, signal,   \
+                                                           touched, loss, rgb_out, flags)
+    switch (T.basis_count) {
+        case 1: DOT_BWD(1); break;
+        case 4: DOT_BWD(4); break;
+        case 9: DOT_BWD(9); break;
+        case 16: DOT_BWD(16); break;
+        default: return set_error(DOT_BAD_ARG, "basis_count must be 1, 4, 9 or 16");
+    }
+#undef DOT_BWD
+    return check_launch("render_bwd_kernel");
+}
+
+}  // namespace dot

@@ -1,0 +1,151 @@
+"""GPU parity of traversal, forward and backward against the reference.
+
+Two checkers: the golden fixtures (outputs of the reference itself, see
+tests/golden/make_golden.py) and the C oracle (oracle/dot_oracle.c) on
+fresh seeded inputs.  Bars (BASELINE.json north_star): leaf ids, t_entry and
+delta bit-exact; rgb / T_final / weight sum / loss / gradients / signal within
+1e-4 abs + 1e-3 rel (the CUDA path shades in fp32, accumulates in fp64).
+"""
+
+import glob
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN
+
+pytestmark = pytest.mark.gpu
+
+ATOL, RTOL = 1e-4, 1e-3
+RENDER_CASES = sorted(glob.glob(os.path.join(GOLDEN, "render_*.npz")))
+
+
+def _tree(z):
+    from paper_2307_15333_b200.octree import from_pool_arrays
+    return from_pool_arrays(z, device="cuda")
+
+
+@pytest.fixture(params=RENDER_CASES, ids=lambda p: os.path.basename(p)[7:-4])
+def case(request):
+    return np.load(request.param)
+
+
+def test_segments_bit_exact(case):
+    from paper_2307_15333_b200.render import segment_batch
+    tree = _tree(case)
+    off, leaf, t, d = segment_batch(tree, case["origins"], case["dirs"], float(case["t_near"]),
+                                    float(case["t_far"]))
+    np.testing.assert_array_equal(off, case["seg_offsets"])
+    np.testing.assert_array_equal(leaf, case["seg_leaf"])
+    np.testing.assert_array_equal(t, case["seg_t"])
+    np.testing.assert_array_equal(d, case["seg_delta"])
+
+
+@pytest.mark.parametrize("tag,eps", [("eps", 1e-4), ("noeps", 0.0)])
+def test_forward_matches_reference(case, tag, eps):
+    from paper_2307_15333_b200.render import render_rays
+    tree = _tree(case)
+    rgb, tfin, wsum = render_rays(tree, case["origins"], case["dirs"], case["bg"], eps,
+                                  float(case["t_near"]), float(case["t_far"]), return_aux=True)
+    np.testing.assert_allclose(rgb, case[f"rgb_{tag}"], atol=ATOL, rtol=RTOL)
+    np.testing.assert_allclose(tfin, case[f"tfin_{tag}"], atol=ATOL, rtol=RTOL)
+    np.testing.assert_allclose(wsum, case[f"wsum_{tag}"], atol=ATOL, rtol=RTOL)
+
+
+@pytest.mark.parametrize("tag,eps", [("eps", 1e-4), ("noeps", 0.0)])
+def test_backward_matches_reference(case, tag, eps):
+    from paper_2307_15333_b200.render import render_and_backprop
+    tree = _tree(case)
+    loss, grads, signal = render_and_backprop(tree, case["origins"], case["dirs"], case["targets"],
+                                              case["bg"], eps, float(case["t_near"]),
+                                              float(case["t_far"]))
+    assert loss == pytest.approx(float(case[f"loss_{tag}"]), rel=RTOL, abs=ATOL)
+    np.testing.assert_allclose(grads.dsigma, case[f"dsigma_{tag}"], atol=ATOL, rtol=RTOL)
+    np.testing.assert_allclose(grads.dsh, case[f"dsh_{tag}"], atol=ATOL, rtol=RTOL)
+    np.testing.assert_array_equal(grads.touched, case[f"touched_{tag}"])
+    np.testing.assert_allclose(signal, case[f"signal_{tag}"], atol=ATOL, rtol=RTOL)
+
+
+def test_config1_golden():
+    """BASELINE.json configs[0] end to end against the reference's outputs."""
+    from paper_2307_15333_b200.render import render_and_backprop, render_rays, segment_batch
+    from paper_2307_15333_b200.scene_io import load_tree_bytes
+    z = np.load(os.path.join(GOLDEN, "config1.npz"))
+    tree = load_tree_bytes(z["scene_dot1"].tobytes(), device="cuda")
+    off, leaf, t, d = segment_batch(tree, z["origins"], z["dirs"])
+    np.testing.assert_array_equal(off, z["seg_offsets"])
+    np.testing.assert_array_equal(leaf, z["seg_leaf"])
+    np.testing.assert_array_equal(t, z["seg_t"])
+    np.testing.assert_array_equal(d, z["seg_delta"])
+    rgb, tfin, wsum = render_rays(tree, z["origins"], z["dirs"], 1.0, return_aux=True)
+    np.testing.assert_allclose(rgb, z["rgb"], atol=ATOL, rtol=RTOL)
+    np.testing.assert_allclose(tfin, z["tfin"], atol=ATOL, rtol=RTOL)
+    loss, grads, signal = render_and_backprop(tree, z["origins"], z["dirs"], z["targets"], 1.0)
+    assert loss == pytest.approx(float(z["loss"]), rel=RTOL, abs=ATOL)
+    np.testing.assert_array_equal(grads.touched, z["touched"])
+    np.testing.assert_allclose(grads.dsigma[z["touched"]], z["dsigma_touched"], atol=ATOL, rtol=RTOL)
+    np.testing.assert_allclose(grads.dsh[z["touched"]], z["dsh_touched"], atol=ATOL, rtol=RTOL)
+    np.testing.assert_allclose(signal, z["signal"], atol=ATOL, rtol=RTOL)
+
+
+@pytest.mark.parametrize("B", [1, 4, 9, 16])
+def test_random_trees_vs_oracle(oracle, B):
+    """Fresh seeded irregular trees (non-canonical pools) through the C oracle."""
+    from paper_2307_15333_b200.render import render_and_backprop, render_rays, segment_batch
+    from helpers import irregular_tree, ray_batch
+    tree = irregular_tree(700 + B, B, depth=3, splits=20, merges=5, max_depth=5, device="cuda")
+    o, d = ray_batch(800 + B, 3000)
+    tg = np.random.default_rng(B).uniform(0, 1, (o.shape[0], 3))
+    ref = oracle.segment_batch(tree, o, d)
+    got = segment_batch(tree, o, d)
+    for a, b in zip(got, ref):
+        np.testing.assert_array_equal(a, b)
+    for eps in (1e-4, 0.0):
+        rgb, tf, ws = render_rays(tree, o, d, (0.1, 0.5, 0.9), eps, return_aux=True)
+        r_rgb, r_tf, r_ws = oracle.render_rays(tree, o, d, (0.1, 0.5, 0.9), eps, return_aux=True)
+        np.testing.assert_allclose(rgb, r_rgb, atol=ATOL, rtol=RTOL)
+        np.testing.assert_allclose(tf, r_tf, atol=ATOL, rtol=RTOL)
+        np.testing.assert_allclose(ws, r_ws, atol=ATOL, rtol=RTOL)
+        loss, g, sig = render_and_backprop(tree, o, d, tg, 0.3, eps)
+        r_loss, r_g, r_sig = oracle.render_and_backprop(tree, o, d, tg, 0.3, eps)
+        assert loss == pytest.approx(r_loss, rel=RTOL, abs=ATOL)
+        np.testing.assert_allclose(g.dsigma, r_g.dsigma, atol=ATOL, rtol=RTOL)
+        np.testing.assert_allclose(g.dsh, r_g.dsh, atol=ATOL, rtol=RTOL)
+        np.testing.assert_array_equal(g.touched, r_g.touched)
+        np.testing.assert_allclose(sig, r_sig, atol=ATOL, rtol=RTOL)
+
+
+def test_depth_definition(oracle):
+    from paper_2307_15333_b200.render import render_rays
+    from helpers import irregular_tree, ray_batch
+    tree = irregular_tree(901, 4, depth=2, splits=10, merges=2, max_depth=4, device="cuda")
+    o, d = ray_batch(902, 500)
+    _, depth = render_rays(tree, o, d, 1.0, return_depth=True)
+    np.testing.assert_allclose(depth, oracle.render_depth(tree, o, d), atol=ATOL, rtol=RTOL)
+
+
+def test_empty_and_miss_batches():
+    from paper_2307_15333_b200.render import render_and_backprop, render_rays
+    from helpers import irregular_tree
+    tree = irregular_tree(5, 1, depth=1, splits=0, merges=0, max_depth=3, device="cuda")
+    empty = np.zeros((0, 3))
+    assert render_rays(tree, empty, empty, 1.0).shape == (0, 3)
+    loss, g, sig = render_and_backprop(tree, empty, empty, empty, 1.0)
+    assert loss == 0.0 and g.touched.size == 0 and not sig.any()
+    o = np.array([[0.0, 0.0, 5.0], [0.0, 5.0, 0.0]])
+    d = np.array([[1.0, 0.0, 0.0], [0.0, 0.0, 1.0]])
+    tg = np.array([[1.0, 1.0, 1.0], [0.0, 0.0, 0.0]])
+    loss, g, sig = render_and_backprop(tree, o, d, tg, 1.0, early_stop_eps=0.0)
+    assert loss == pytest.approx(1.5)
+    assert g.touched.size == 0 and not g.dsigma.any() and not sig.any()
+
+
+def test_length_mismatch_raises():
+    from paper_2307_15333_b200.errors import InputError
+    from paper_2307_15333_b200.render import render_and_backprop
+    from helpers import irregular_tree, ray_batch
+    tree = irregular_tree(6, 1, depth=1, splits=0, merges=0, max_depth=3, device="cuda")
+    o, d = ray_batch(7, 4)
+    with pytest.raises(InputError):
+        render_and_backprop(tree, o, d, np.zeros((3, 3)), 0.0)
