@@ -1,0 +1,528 @@
+#!/usr/bin/env python
+"""DOT on B200 -- benchmark (one JSON line on rank 0).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Headline (BASELINE.json configs[1], NeRF-synthetic-shaped training step):
+depth-9 SH-3 scene from a 64-blob field (~2.6M leaves), rays from 100
+hemisphere cameras (800x800, r=4.03, fov 40 deg), one step = gather a
+2^20-ray batch per GPU -> fused forward+backward+signal kernel -> NCCL
+all-reduce of leaf gradients (N>1) -> sparse RMSProp -> signal accumulate.
+``value`` = rays/s over all ranks with inputs resident in HBM; ``e2e`` =
+the same step through the public API from pinned host buffers (H2D of the
+batch, D2H of the loss inside the timed region).
+
+Side measurements in the same line: ``render`` (configs[2]: 800x800 views,
+eps 1e-4), ``refine`` (configs[4]: 16M-leaf depth-10 tree, log-normal(-6,2)
+signals, tau 0.01, gamma 0.1), ``roofline`` of the dominant kernel
+(render_bwd) against the measured HBM copy bandwidth, and ``cpu_baseline``
+(the C oracle port of the reference kernels on this host's cores).
+
+``--impl reference`` times the reference's algorithm on the CPU (the C
+oracle port, all host threads) on the same workload, rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = ("rays/sec render & fwd+bwd per GPU (1/2/4/8 B200), 800x800 FPS, refine ms, "
+          "%HBM roofline")
+BATCH = 1 << 20
+N_VIEWS = 100
+W = H = 800
+RADIUS = 4.03
+EPS = 1e-4
+BG = 1.0
+# algorithmic bytes: per ray f64 origin+dir+target; per
+# composited segment sigma 4 B + SH row 12*B B read + gradient 4*(1+3B) B
+# (one RMW) + signal 8 B.
+B_SH = 16
+RAY_BYTES = 72
+SEG_BYTES = 4 + 12 * B_SH + 4 * (1 + 3 * B_SH) + 8
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            p = json.load(fh)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            threading.Thread(target=self._read, daemon=True).start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            try:
+                sm.append(float(r[1]))
+                mx = max(mx, float(r[2]))
+                for k, nm in enumerate(names):
+                    if r[5 + k].lower().startswith("active"):
+                        reasons.add(nm)
+            except Exception:
+                continue
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# workload
+
+def view_rays_torch(focal, pose, device):
+    import torch
+    xs = (torch.arange(W, dtype=torch.float64, device=device) + 0.5 - 0.5 * W) / focal
+    ys = -(torch.arange(H, dtype=torch.float64, device=device) + 0.5 - 0.5 * H) / focal
+    cam = torch.empty(H, W, 3, dtype=torch.float64, device=device)
+    cam[..., 0] = xs[None, :]
+    cam[..., 1] = ys[:, None]
+    cam[..., 2] = -1.0
+    rot = torch.as_tensor(pose[:3, :3], dtype=torch.float64, device=device)
+    world = cam.reshape(-1, 3) @ rot.T
+    world = world / torch.linalg.norm(world, dim=1, keepdim=True)
+    origins = torch.as_tensor(pose[:3, 3], dtype=torch.float64, device=device).expand_as(world).contiguous()
+    return origins, world.contiguous()
+
+
+def perturbed(tree, seed):
+    import torch
+    from paper_2307_15333_b200.octree import from_canonical_tensors
+    topo = tree.topology()
+    g = torch.Generator(device=tree.device)
+    g.manual_seed(seed)
+    sh = tree._sh_store.clone()
+    sh[:, :3 * tree.basis_count] += 0.05 * torch.randn(sh.shape[0], 3 * tree.basis_count,
+                                                       generator=g, device=tree.device)
+    return from_canonical_tensors(tree.center, tree.half_extent, tree.basis_count, tree.max_depth,
+                                  topo.node, tree._sigma, sh, topo.level_offsets)
+
+
+def build_training_pool(tree, device, n_views=N_VIEWS):
+    """All rays of the 100 training views + targets rendered from a perturbed copy."""
+    import torch
+    from paper_2307_15333_b200 import scenes
+    from paper_2307_15333_b200.render import render_rays
+    focal, poses = scenes.hemisphere_cameras(n_views, W, H, RADIUS, seed=3)
+    os_, ds_ = zip(*(view_rays_torch(focal, p, device) for p in poses))
+    origins, dirs = torch.cat(os_), torch.cat(ds_)
+    del os_, ds_
+    target_tree = perturbed(tree, 21)
+    targets = torch.empty_like(origins)
+    for lo in range(0, origins.shape[0], 1 << 22):
+        targets[lo:lo + (1 << 22)] = render_rays(target_tree, origins[lo:lo + (1 << 22)],
+                                                  dirs[lo:lo + (1 << 22)], BG).double()
+    return origins, dirs, targets
+
+
+# ---------------------------------------------------------------------------
+# our arm
+
+def run_ours(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+    from paper_2307_15333_b200 import scenes, _lib
+    from paper_2307_15333_b200.optim import RmsPropState, rmsprop_step
+    from paper_2307_15333_b200.render import BackpropWorkspace, render_and_backprop, render_rays
+    from paper_2307_15333_b200.signals import SignalBuffer
+
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    _lib.check(_lib.load().dot_device_check(), "device check")
+    t_setup = time.time()
+    tree = scenes.config2_scene(device=dev)
+    origins, dirs, targets = build_training_pool(tree, dev)
+    n_pool = origins.shape[0]
+    per_rank = BATCH
+    n_global = per_rank * world
+    gs = 2.0 / n_global
+    state = RmsPropState(tree)
+    buf = SignalBuffer(tree)
+    ws = BackpropWorkspace.for_tree(tree)
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(1234 + rank)
+    total_steps = args.warmup + args.steps
+    perm = torch.randint(0, n_pool, (total_steps + 2, per_rank), generator=gen, device=dev)
+    kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(total_steps)]
+
+    def step(k, timed_kernel=True):
+        idx = perm[k]
+        loss, grads, sig = render_and_backprop(
+            tree, origins[idx], dirs[idx], targets[idx], BG, EPS, grad_scale=gs, workspace=ws,
+            kernel_events=kev[k] if timed_kernel else None)
+        if world > 1:
+            dist.all_reduce(ws.dsigma)
+            dist.all_reduce(ws.dsh_store)
+            dist.all_reduce(ws.touched, op=dist.ReduceOp.MAX)
+        rmsprop_step(tree, grads, state)
+        buf.accumulate(sig, per_rank, validate=False)
+        return loss
+
+    for k in range(args.warmup):
+        step(k)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    setup_s = time.time() - t_setup
+    clocks = ClockSampler(local_rank).start()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    t0.record()
+    for k in range(args.warmup, total_steps):
+        step(k)
+    t1.record()
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    ms = t0.elapsed_time(t1)
+    if world > 1:
+        tt = torch.tensor([ms], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+        dist.barrier()
+    ms_step = ms / args.steps
+    value = n_global * args.steps / (ms / 1e3)
+    kern_ms = [kev[k][0].elapsed_time(kev[k][1]) for k in range(args.warmup, total_steps)]
+    kern_ms_avg = sum(kern_ms) / len(kern_ms)
+
+    # workload statistics of one batch (outside the timed region)
+    stats = torch.zeros(3, dtype=torch.int64, device=dev)
+    idx = perm[total_steps]
+    view, _ = tree.tree_view()
+    oo, dd = origins[idx].contiguous(), dirs[idx].contiguous()
+    _lib.call("dot_ray_stats", _lib.ctypes.byref(view), _lib.ptr(oo), _lib.ptr(dd), per_rank, EPS,
+              _lib.ptr(stats), _lib.stream_ptr())
+    seg, comp, qpos = [int(x) for x in stats.cpu()]
+    alg_bytes = per_rank * RAY_BYTES + comp * SEG_BYTES
+    hbm, peak_kind = peaks()
+    achieved = alg_bytes / (kern_ms_avg / 1e3) / 1e9
+
+    # e2e: public API from pinned host buffers (H2D batch + D2H loss per step)
+    host = []
+    for j in range(2):
+        idx = perm[j]
+        host.append(tuple(x[idx].cpu().pin_memory() for x in (origins, dirs, targets)))
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    for k in range(args.warmup):
+        o_h, d_h, t_h = host[k % 2]
+        loss, grads, sig = render_and_backprop(tree, o_h, d_h, t_h, BG, EPS, grad_scale=gs, workspace=ws)
+        rmsprop_step(tree, grads, state)
+        float(loss.item())
+    torch.cuda.synchronize()
+    e0.record()
+    for k in range(args.steps):
+        o_h, d_h, t_h = host[k % 2]
+        loss, grads, sig = render_and_backprop(tree, o_h, d_h, t_h, BG, EPS, grad_scale=gs, workspace=ws)
+        if world > 1:
+            dist.all_reduce(ws.dsigma)
+            dist.all_reduce(ws.dsh_store)
+            dist.all_reduce(ws.touched, op=dist.ReduceOp.MAX)
+        rmsprop_step(tree, grads, state)
+        buf.accumulate(sig, per_rank, validate=False)
+        float(loss.item())
+    e1.record()
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1)
+    if world > 1:
+        tt = torch.tensor([e2e_ms], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_ms = float(tt.item())
+    e2e_value = n_global * args.steps / (e2e_ms / 1e3)
+
+    # render (configs[2]) and refine (configs[4]) side measurements
+    render = None if args.skip_render else bench_render(tree, dev, args, world)
+    del origins, dirs, targets, perm
+    torch.cuda.empty_cache()
+    refine = None if (args.skip_refine or rank != 0) else bench_refine(dev, args)
+    cpu = None
+    if rank == 0 and not args.skip_cpu:
+        cpu = cpu_baseline(tree, args)
+
+    if rank != 0:
+        return None
+    return {
+        "metric": METRIC,
+        "value": value,
+        "unit": "rays/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms_step,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "dtype_detail": "f64 traversal/transmittance/accumulation, f32 SH shading and leaf gradients",
+        "data": "synthetic (seeded blob-field scene, random-init SH, targets from a perturbed copy)",
+        "config": {
+            "workload": "configs[1] training step: depth-9 SH-3 scene, 2^20-ray batch per GPU, "
+                        "fwd+bwd+signal, NCCL grad all-reduce (N>1), RMSProp",
+            "leaves": int(tree.leaf_count), "nodes": int(tree.topology().n_nodes),
+            "global_batch": n_global, "views": N_VIEWS, "resolution": [W, H],
+            "segments_per_ray": seg / per_rank, "composited_per_ray": comp / per_rank,
+            "l2": "inputs larger than L2 (2.6M-leaf payload 0.51 GB, 100-view ray pool 4.6 GB, "
+                  "random 2^20-ray batches)",
+            "parallelism": f"rays sharded dp{world}, tree replicated",
+        },
+        "gpu_launches": 2 * args.steps,
+        "roofline": {
+            "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+            "frac": achieved / hbm, "traffic": None, "kernel": "render_bwd_kernel<16>",
+            "kernel_ms": kern_ms_avg, "alg_bytes_per_launch": alg_bytes, "peak_kind": peak_kind,
+            "bytes_model": f"{RAY_BYTES} B/ray + {SEG_BYTES} B/composited segment",
+        },
+        "e2e": {"value": e2e_value, "unit": "rays/s", "h2d_bytes_per_step": per_rank * 72,
+                "d2h_bytes_per_step": 8, "ms_per_step": e2e_ms / args.steps},
+        "clocks": clk,
+        "render": render,
+        "refine": refine,
+        "cpu_baseline": cpu,
+        "setup_s": setup_s,
+    }
+
+
+def bench_render(tree, dev, args, world):
+    import torch
+    import torch.distributed as dist
+    from paper_2307_15333_b200 import scenes
+    from paper_2307_15333_b200.render import render_rays
+    focal, poses = scenes.hemisphere_cameras(200, W, H, RADIUS, seed=4)
+    n_views = max(4, min(2 * args.steps, 20))
+    rank = dist.get_rank() if world > 1 else 0
+    views = [view_rays_torch(focal, poses[(rank * n_views + i) % 200], dev) for i in range(n_views)]
+    for i in range(min(3, n_views)):
+        render_rays(tree, *views[i], BG, EPS)
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for o, d in views:
+        render_rays(tree, o, d, BG, EPS)
+    b.record()
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b)
+    if world > 1:
+        tt = torch.tensor([ms], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+    rays = W * H * n_views * world
+    return {"rays_per_s": rays / (ms / 1e3), "fps_800x800": n_views * world / (ms / 1e3),
+            "ms_per_view": ms / n_views, "views": n_views * world, "eps": EPS,
+            "workload": "configs[2]: 800x800 random hemisphere views, rays resident"}
+
+
+CONFIG5_SPLIT_THR = 820.0
+
+
+def config5_tree(dev):
+    from paper_2307_15333_b200 import scenes
+    field = scenes.BlobField.make(seed=5, n_blobs=64)
+    tree = scenes.adaptive_tree(field, max_depth=10, basis_count=16, split_thr=CONFIG5_SPLIT_THR,
+                                empty_thr=0.05, min_depth=4, sh_seed=50, device=dev)
+    tree.max_depth = 11  # depth-10 leaves stay eligible for sampling
+    return tree
+
+
+def bench_refine(dev, args):
+    import torch
+    from paper_2307_15333_b200.calibrate import CalibrationConfig, calibrate
+    from paper_2307_15333_b200.octree import from_canonical_tensors
+    from paper_2307_15333_b200.signals import SignalBuffer
+    base = config5_tree(dev)
+    topo = base.topology()
+    node0, sig0, sh0 = topo.node, base._sigma, base._sh_store
+    leaf = node0 < 0
+    g = torch.Generator(device=dev)
+    g.manual_seed(55)
+    acc = torch.zeros(node0.shape[0], dtype=torch.float64, device=dev)
+    acc[leaf] = torch.exp(-6.0 + 2.0 * torch.randn(int(leaf.sum()), generator=g, device=dev,
+                                                  dtype=torch.float64))
+    times, rep = [], None
+    passes = 3
+    for k in range(passes + 1):
+        tree = from_canonical_tensors(base.center, base.half_extent, 16, 11, node0.clone(),
+                                      sig0.clone(), sh0.clone(), topo.level_offsets)
+        buf = SignalBuffer(tree)
+        buf.accumulator.copy_(acc)
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        rep = calibrate(tree, buf, CalibrationConfig(tau=0.01, gamma=0.10), events=False)
+        b.record()
+        torch.cuda.synchronize()
+        if k:
+            times.append(a.elapsed_time(b))
+        n_new = tree.topology().n_nodes
+        del tree, buf
+    ms = sum(times) / len(times)
+    n_old = int(node0.shape[0])
+    row = 4 + 4 * 48
+    alg = (n_old * (4 + 8) + rep.merges_applied * 9 * row + rep.splits_applied * 9 * row
+           + n_new * (4 + row + 9))
+    return {"ms_per_pass": ms, "leaves_before": rep.leaves_before, "leaves_after": rep.leaves_after,
+            "merges": rep.merges_applied, "splits": rep.splits_applied, "nodes_before": n_old,
+            "nodes_after": int(n_new), "alg_gbs": alg / (ms / 1e3) / 1e9,
+            "workload": "configs[4]: depth-10 SH-3 tree, log-normal(-6,2) signals, tau 0.01, "
+                        "gamma 0.1, prune+sample+canonical compaction"}
+
+
+def cpu_baseline(tree, args, n_rays=1 << 16):
+    """The C oracle port of the reference kernels, all host threads, on a
+    bounded sample of the same training workload."""
+    import torch
+    from oracle import oracle as O
+    from paper_2307_15333_b200 import scenes
+    O.build()
+    focal, poses = scenes.hemisphere_cameras(N_VIEWS, W, H, RADIUS, seed=3)
+    rng = np.random.default_rng(9)
+    os_, ds_ = [], []
+    for v in rng.choice(N_VIEWS, 8, replace=False):
+        o, d = scenes.pinhole_rays(W, H, focal, poses[v])
+        pick = rng.choice(o.shape[0], n_rays // 8, replace=False)
+        os_.append(o[pick])
+        ds_.append(d[pick])
+    o, d = np.concatenate(os_), np.concatenate(ds_)
+    tg = rng.uniform(0.0, 1.0, o.shape)
+    tree._host()  # pool arrays for the oracle (outside the timing)
+    O.render_and_backprop(tree, o[:256], d[:256], tg[:256], BG, EPS)
+    t = time.perf_counter()
+    O.render_and_backprop(tree, o, d, tg, BG, EPS)
+    dt = time.perf_counter() - t
+    return {"value": o.shape[0] / dt, "unit": "rays/s", "cores": O.num_threads(), "kind": "port",
+            "sample": f"{o.shape[0]} rays (8 of the 100 training views) fwd+bwd through "
+                      "oracle/dot_oracle.c (count+fill+grad+serial scatter, OpenMP)",
+            "seconds": dt}
+
+
+# ---------------------------------------------------------------------------
+# reference arm
+
+def run_reference(args):
+    import torch
+    from oracle import oracle as O
+    from paper_2307_15333_b200 import scenes
+    O.build()
+    tree = scenes.config2_scene(device="cpu")
+    tree._host()
+    focal, poses = scenes.hemisphere_cameras(N_VIEWS, W, H, RADIUS, seed=3)
+    sample = args.ref_sample
+    rng = np.random.default_rng(11)
+    batches = []
+    for k in range(args.warmup + args.steps):
+        v = rng.integers(N_VIEWS)
+        o, d = scenes.pinhole_rays(W, H, focal, poses[v])
+        pick = rng.choice(o.shape[0], sample, replace=False)
+        batches.append((o[pick], d[pick], rng.uniform(0.0, 1.0, (sample, 3))))
+    sig = tree.sigma.numpy()
+    sh = tree.sh.numpy()
+    vs = np.zeros(tree.capacity)
+    vh = np.zeros((tree.capacity, 48))
+
+    def step(b):
+        o, d, tg = b
+        loss, g, s = O.render_and_backprop(tree, o, d, tg, BG, EPS)
+        O.rmsprop_step(sig, sh, vs, vh, g.dsigma, g.dsh, g.touched)
+        return loss
+
+    for k in range(args.warmup):
+        step(batches[k])
+    t = time.perf_counter()
+    for k in range(args.warmup, args.warmup + args.steps):
+        step(batches[k])
+    dt = time.perf_counter() - t
+    value = sample * args.steps / dt
+    return {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "rays/s", "n_gpus": 0,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": "configs[1] training step (bounded sample per step)",
+                   "leaves": int(tree.leaf_count), "sample_rays_per_step": sample},
+        "cpu_baseline": {"value": value, "unit": "rays/s", "cores": O.num_threads(), "kind": "port",
+                         "sample": f"{sample} rays per step from one random training view, "
+                                   "fwd+bwd (count+fill+grad+serial scatter) + RMSProp"},
+        "e2e": {"value": value, "unit": "rays/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--skip-render", action="store_true")
+    ap.add_argument("--skip-refine", action="store_true")
+    ap.add_argument("--skip-cpu", action="store_true")
+    ap.add_argument("--ref-sample", type=int, default=1 << 14)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        if rank == 0:
+            print(json.dumps(run_reference(args)), flush=True)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    out = run_ours(args, rank, world, local_rank)
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

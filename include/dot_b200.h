@@ -90,6 +90,12 @@ int dot_render_bwd(const dot_tree_view* tree, const double* origins, const doubl
                    uint8_t* touched, double* loss_sum, float* rgb_out, int32_t flags,
                    void* stream);
 
+/* --- workload statistics (measurement helper, no reference counterpart):
+ *     totals[0] += traversed segments, totals[1] += composited (pre-cut)
+ *     segments, totals[2] += composited segments with q > 0. */
+int dot_ray_stats(const dot_tree_view* tree, const double* origins, const double* dirs,
+                  int64_t n_rays, double early_stop_eps, uint64_t* totals, void* stream);
+
 /* --- refine (DOT calibration, calibrate.py:202-238) ------------------------
  * One call runs prune (one-shot or recursive) then sample on the post-prune
  * topology and writes the refined tree directly in canonical BFS order

@@ -51,6 +51,7 @@ _SIGNATURES = {
     "dot_render_bwd": (c_i32, [c_void_p, c_void_p, c_void_p, c_void_p, c_i64, c_void_p, c_f64, c_f64,
                                c_f64, c_f64, c_void_p, c_void_p, c_i32, c_void_p, c_void_p, c_void_p,
                                c_void_p, c_i32, c_void_p]),
+    "dot_ray_stats": (c_i32, [c_void_p, c_void_p, c_void_p, c_i64, c_f64, c_void_p, c_void_p]),
     "dot_refine_plan_create": (c_i32, [c_void_p, c_void_p, c_void_p, c_i32, c_f64, c_f64, c_i32, c_i32,
                                        c_f64, c_void_p, c_void_p, c_void_p]),
     "dot_refine_plan_lists": (c_i32, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),

@@ -156,7 +156,10 @@ def _events(plan: _Plan, remap: RefineRemap | None) -> list:
     """Reference-style event list (lazy host work; see module docstring)."""
     ev = []
     node_old = plan.topo.node.cpu().numpy().astype(np.int64)
-    for p in plan.merge_parents:
+    # the reference logs merges by (round, pool id) and splits by pool id
+    mp = plan.pool_ids(plan.merge_parents)
+    order = np.lexsort((mp, plan.merge_round))
+    for p in plan.merge_parents[order]:
         kids = node_old[p] + np.arange(8)
         ev.append(("merge", int(plan.pool_ids(np.array([p]))[0]),
                    tuple(int(k) for k in plan.pool_ids(kids))))
@@ -166,7 +169,8 @@ def _events(plan: _Plan, remap: RefineRemap | None) -> list:
         new_node = plan.tree.topology().node.cpu().numpy()
         parents = np.nonzero(kind == K_SPLITPARENT)[0]
         first = {int(src[i]): int(new_node[i]) for i in parents}
-        for leaf in plan.split_leaves:
+        sp = plan.pool_ids(plan.split_leaves)
+        for leaf in plan.split_leaves[np.argsort(sp, kind="stable")]:
             f = first[int(leaf)]
             ev.append(("split", int(plan.pool_ids(np.array([leaf]))[0]),
                        tuple(range(f, f + 8))))

@@ -25,4 +25,7 @@ int launch_render_bwd(const TreeDev& T, const double* o, const double* d, const 
                       float* gsig, float* gsh, double* signal, uint8_t* touched, double* loss,
                       float* rgb_out, int flags, cudaStream_t s);
 
+int launch_ray_stats(const TreeDev& T, const double* o, const double* d, int64_t n, double eps,
+                     unsigned long long* out, cudaStream_t s);
+
 }  // namespace dot

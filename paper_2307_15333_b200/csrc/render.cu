@@ -238,6 +238,53 @@ __global__ void __launch_bounds__(kBlock) render_bwd_kernel(
 }
 
 // ---------------------------------------------------------------------------
+// Workload statistics (measurement only): per batch totals of traversed
+// segments, composited (pre-cut) segments and composited segments with q > 0.
+
+__global__ void __launch_bounds__(kBlock) ray_stats_kernel(TreeDev T, const double* __restrict__ o,
+                                                           const double* __restrict__ d, int64_t n,
+                                                           double eps, unsigned long long* __restrict__ out) {
+    const int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    unsigned long long seg = 0, comp = 0, qpos = 0;
+    if (r < n) {
+        Tracer tr;
+        load_ray(o, d, r, tr);
+        if (tr.init(T, 0.0, __longlong_as_double(0x7ff0000000000000ll))) {
+            Leaf L;
+            double te, dl, trans = 1.0;
+            bool cut = false;
+            while (tr.next(T, L, te, dl)) {
+                ++seg;
+                if (cut) continue;
+                const double a = exp(-double(__ldg(T.sigma + L.pid)) * dl);
+                ++comp;
+                if (1.0 - a > 0.0) ++qpos;
+                trans *= a;
+                if (eps > 0.0 && trans < eps) cut = true;
+            }
+        }
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        seg += __shfl_down_sync(0xffffffffu, seg, off);
+        comp += __shfl_down_sync(0xffffffffu, comp, off);
+        qpos += __shfl_down_sync(0xffffffffu, qpos, off);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicAdd(out + 0, seg);
+        atomicAdd(out + 1, comp);
+        atomicAdd(out + 2, qpos);
+    }
+}
+
+int launch_ray_stats(const TreeDev& T, const double* o, const double* d, int64_t n, double eps,
+                     unsigned long long* out, cudaStream_t s) {
+    if (n == 0) return DOT_OK;
+    ray_stats_kernel<<<unsigned((n + kBlock - 1) / kBlock), kBlock, 0, s>>>(T, o, d, n, eps, out);
+    return check_launch("ray_stats_kernel");
+}
+
+// ---------------------------------------------------------------------------
 
 static unsigned blocks_for(int64_t n) { return unsigned((n + kBlock - 1) / kBlock); }
 

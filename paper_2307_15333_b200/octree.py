@@ -343,8 +343,8 @@ class SparseOctree:
         hp["leaf"][leaf] = 0
         hp["child"][leaf] = ids
         tid = torch.from_numpy(ids).to(self.device)
-        self._sigma[tid] = self._sigma[leaf]
-        self._sh_store[tid] = self._sh_store[leaf]
+        self._sigma[tid] = self._sigma[leaf].clone()
+        self._sh_store[tid] = self._sh_store[leaf].clone()
         self._sigma[leaf] = 0.0
         self._sh_store[leaf] = 0.0
         self.leaf_count += 7
@@ -658,6 +658,18 @@ def from_pool_arrays(arrays: dict, device=None) -> SparseOctree:
     tree._sh_store = store
     tree.leaf_count = int(((hp["alive"] == 1) & (hp["leaf"] == 1)).sum())
     tree.internal_count = int(((hp["alive"] == 1) & (hp["leaf"] == 0)).sum())
+    return tree
+
+
+def from_canonical_tensors(center, half_extent, basis_count, max_depth, node: torch.Tensor,
+                           sigma: torch.Tensor, sh_store: torch.Tensor,
+                           level_offsets: np.ndarray | None = None) -> SparseOctree:
+    """Adopt device tensors of a canonical tree (node words, sigma, padded SH store)."""
+    tree = SparseOctree(center, half_extent, basis_count, max_depth=max_depth, capacity=8,
+                        device=node.device)
+    tree._set_canonical(node, sigma, sh_store, int((node < 0).sum().item()), level_offsets)
+    tree.generation = 0
+    tree._topo.generation = 0
     return tree
 
 

@@ -131,3 +131,124 @@ def pinhole_rays(width: int, height: int, focal: float, cam_to_world: np.ndarray
     world /= np.linalg.norm(world, axis=1, keepdims=True)
     origins = np.broadcast_to(cam_to_world[:3, 3], world.shape).copy()
     return origins, world
+
+
+# ---------------------------------------------------------------------------
+# Adaptive builds for the large configurations (torch, runs on the GPU)
+
+def _field_torch(field: BlobField, pts):
+    import torch
+    mu = torch.as_tensor(field.mu, dtype=torch.float64, device=pts.device)
+    inv = torch.as_tensor(1.0 / (2.0 * field.s ** 2), dtype=torch.float64, device=pts.device)
+    p = torch.as_tensor(field.p, dtype=torch.float64, device=pts.device)
+    out = torch.zeros(pts.shape[0], dtype=torch.float64, device=pts.device)
+    for lo in range(0, mu.shape[0], 16):
+        d = pts[:, None, :] - mu[None, lo:lo + 16, :]
+        q = (d * d * inv[None, lo:lo + 16, :]).sum(-1)
+        out += (p[None, lo:lo + 16] * torch.exp(-q)).sum(-1)
+    if field.slab is not None:
+        z_top, thick, dens = field.slab
+        inside = (pts[:, 2] <= z_top) & (pts[:, 2] >= z_top - thick)
+        out = out + inside.double() * dens
+    return out
+
+
+def adaptive_tree(field: BlobField, max_depth: int, basis_count: int, split_thr: float,
+                  empty_thr: float = 0.05, min_depth: int = 3, half_extent: float = 1.0,
+                  sh_seed: int = 0, sh_std: float = 0.3, device=None, chunk: int = 1 << 21):
+    """Top-down adaptive octree over a blob field, built level by level.
+
+    A cell at depth d < max_depth splits when d < min_depth, or when the
+    density sampled at its centre and its 8 child centres spans more than
+    ``split_thr * h_child`` (a finite-difference gradient bound, so refinement
+    tracks the field's steep shells at every depth) and exceeds ``empty_thr``
+    somewhere (refinement follows the
+    field's variation, like a trained radiance field around surfaces).  Leaf
+    sigma is the density at the leaf centre (build_dense's convention,
+    octree.py:431-445); SH ~ N(0, sh_std) in canonical leaf order.  Returns a
+    canonical ``SparseOctree`` (pool id == BFS index) on ``device``.
+    """
+    import torch
+    from .octree import OCTANT_SIGNS, from_canonical_tensors
+    dev = torch.device(device) if device is not None else (
+        torch.device("cuda") if torch.cuda.is_available() else torch.device("cpu"))
+    signs = torch.as_tensor(OCTANT_SIGNS, dtype=torch.float64, device=dev)
+    centers = torch.zeros(1, 3, dtype=torch.float64, device=dev)
+    sig = _field_torch(field, centers)
+    levels = []  # (split mask, sigma) per level
+    h = half_extent
+    for d in range(max_depth + 1):
+        m = centers.shape[0]
+        if d == max_depth or m == 0:
+            levels.append((torch.zeros(m, dtype=torch.bool, device=dev), sig))
+            break
+        hc = h * 0.5
+        split = torch.empty(m, dtype=torch.bool, device=dev)
+        csig = torch.empty(m, 8, dtype=torch.float64, device=dev)
+        for lo in range(0, m, chunk):
+            c = centers[lo:lo + chunk]
+            cc = (c[:, None, :] + hc * signs[None, :, :]).reshape(-1, 3)
+            s8 = _field_torch(field, cc).reshape(-1, 8)
+            csig[lo:lo + chunk] = s8
+            allv = torch.cat([sig[lo:lo + chunk, None], s8], dim=1)
+            mx, mn = allv.max(1).values, allv.min(1).values
+            split[lo:lo + chunk] = ((mx - mn) > split_thr * hc) & (mx > empty_thr)
+        if d < min_depth:
+            split[:] = True
+        levels.append((split, sig))
+        sel = torch.nonzero(split).reshape(-1)
+        centers = (centers[sel][:, None, :] + hc * signs[None, :, :]).reshape(-1, 3)
+        sig = csig[sel].reshape(-1)
+        h = hc
+    # canonical node table
+    sizes = [lv[0].shape[0] for lv in levels]
+    starts = [0]
+    for s_ in sizes:
+        starts.append(starts[-1] + s_)
+    n = starts[-1]
+    node = torch.empty(n, dtype=torch.int32, device=dev)
+    sigma = torch.zeros(n, dtype=torch.float32, device=dev)
+    for d, (split, s_) in enumerate(levels):
+        lo, hi = starts[d], starts[d + 1]
+        rank = torch.cumsum(split.long(), 0) - split.long()
+        idx = torch.arange(lo, hi, device=dev)
+        nxt = starts[d + 1]
+        node[lo:hi] = torch.where(split, (nxt + 8 * rank).int(), (~idx).int())
+        sigma[lo:hi] = torch.where(split, torch.zeros_like(s_), s_).float()
+    leaf = node < 0
+    n_leaf = int(leaf.sum().item())
+    S = pad4_(3 * basis_count)
+    sh = torch.zeros(n, S, dtype=torch.float32, device=dev)
+    g = torch.Generator(device=dev)
+    g.manual_seed(int(sh_seed))
+    vals = torch.randn(n_leaf, 3 * basis_count, generator=g, device=dev, dtype=torch.float32) * sh_std
+    sh[torch.nonzero(leaf).reshape(-1), :3 * basis_count] = vals
+    return from_canonical_tensors((0.0, 0.0, 0.0), half_extent, basis_count, max_depth, node,
+                                  sigma, sh, level_offsets=np.asarray(starts, dtype=np.int64))
+
+
+def pad4_(n: int) -> int:
+    return (n + 3) & ~3
+
+
+def config2_scene(device=None, basis_count: int = 16):
+    """BASELINE.json configs[1]/[2]: depth-9, 64-blob field, SH-3, ~2-3M leaves."""
+    field = BlobField.make(seed=2, n_blobs=64)
+    return adaptive_tree(field, max_depth=9, basis_count=basis_count, split_thr=CONFIG2_SPLIT_THR,
+                         empty_thr=0.05, min_depth=4, sh_seed=20, device=device)
+
+
+CONFIG2_SPLIT_THR = 2.0
+
+
+def hemisphere_cameras(count: int, width: int, height: int, radius: float, seed: int,
+                       camera_angle_x: float = FOV_40):
+    """Cameras on the upper hemisphere looking at the origin (NeRF-synthetic-shaped)."""
+    rng = np.random.default_rng(seed)
+    focal = focal_from_angle(width, camera_angle_x)
+    poses = []
+    for _ in range(count):
+        az = rng.uniform(0.0, 2.0 * math.pi)
+        el = math.asin(rng.uniform(0.05, 0.95))
+        poses.append(orbit_pose(radius, az, el))
+    return focal, poses

@@ -1,0 +1,82 @@
+"""Pin the CPU oracle to the reference: every golden fixture (outputs of
+octrf itself, tests/golden/make_golden.py) must be reproduced -- bit-exactly
+for segments, rgb, gradients, signal, selections and refined pools."""
+
+import glob
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN
+
+RENDER = sorted(glob.glob(os.path.join(GOLDEN, "render_*.npz")))
+CALIB = sorted(glob.glob(os.path.join(GOLDEN, "calib_*.npz")))
+
+
+@pytest.mark.parametrize("path", RENDER, ids=lambda p: os.path.basename(p)[7:-4])
+def test_oracle_render_golden(oracle, path):
+    z = np.load(path)
+    t = oracle.PoolTree.from_arrays(z)
+    tn, tf = float(z["t_near"]), float(z["t_far"])
+    off, leaf, tt, dl = oracle.segment_batch(t, z["origins"], z["dirs"], tn, tf)
+    np.testing.assert_array_equal(off, z["seg_offsets"])
+    np.testing.assert_array_equal(leaf, z["seg_leaf"])
+    np.testing.assert_array_equal(tt, z["seg_t"])
+    np.testing.assert_array_equal(dl, z["seg_delta"])
+    for tag, eps in (("eps", 1e-4), ("noeps", 0.0)):
+        rgb, tfin, wsum = oracle.render_rays(t, z["origins"], z["dirs"], z["bg"], eps, tn, tf,
+                                             return_aux=True)
+        np.testing.assert_array_equal(rgb, z[f"rgb_{tag}"])
+        np.testing.assert_array_equal(tfin, z[f"tfin_{tag}"])
+        np.testing.assert_array_equal(wsum, z[f"wsum_{tag}"])
+        loss, g, sig = oracle.render_and_backprop(t, z["origins"], z["dirs"], z["targets"], z["bg"],
+                                                  eps, tn, tf)
+        assert loss == float(z[f"loss_{tag}"])
+        np.testing.assert_array_equal(g.dsigma, z[f"dsigma_{tag}"])
+        np.testing.assert_array_equal(g.dsh, z[f"dsh_{tag}"])
+        np.testing.assert_array_equal(g.touched, z[f"touched_{tag}"])
+        np.testing.assert_array_equal(sig, z[f"signal_{tag}"])
+
+
+@pytest.mark.parametrize("path", CALIB, ids=lambda p: os.path.basename(p)[6:-4])
+def test_oracle_calibrate_golden(oracle, path):
+    z = np.load(path)
+    t = oracle.PoolTree.from_arrays(z)
+    thr = float(z["threshold"])
+    thr = None if np.isnan(thr) else thr
+    use_sigma = str(z["target"]) == "sigma"
+    np.testing.assert_array_equal(oracle.select_prune(t, z["acc"], float(z["tau"]), use_sigma),
+                                  z["sel_prune"])
+    np.testing.assert_array_equal(
+        oracle.select_sample(t, z["acc"], float(z["gamma"]), thr, use_sigma), z["sel_sample_pre"])
+    r = oracle.calibrate(t, z["acc"], float(z["tau"]), float(z["gamma"]), bool(z["recursive"]),
+                         thr, use_sigma)
+    assert (r.merges_applied, r.splits_applied, r.recursion_rounds, r.leaves_after) == (
+        int(z["merges_applied"]), int(z["splits_applied"]), int(z["recursion_rounds"]),
+        int(z["leaves_after"]))
+    for k in ("child", "parent", "depth", "leaf", "alive", "center"):
+        np.testing.assert_array_equal(getattr(t, "_" + k), z["after_" + k])
+    np.testing.assert_array_equal(t.sigma, z["after_sigma"])
+    np.testing.assert_array_equal(t.sh, z["after_sh"])
+    np.testing.assert_array_equal(np.asarray(t._free), z["after_free"])
+    splits = [n for kind, n, _ in r.events if kind == "split"]
+    np.testing.assert_array_equal(splits, z["split_leaves"])
+
+
+def test_oracle_config1_golden(oracle):
+    from paper_2307_15333_b200.scene_io import load_tree_bytes
+    z = np.load(os.path.join(GOLDEN, "config1.npz"))
+    tree = load_tree_bytes(z["scene_dot1"].tobytes(), device="cpu")
+    off, leaf, t, d = oracle.segment_batch(tree, z["origins"], z["dirs"])
+    np.testing.assert_array_equal(off, z["seg_offsets"])
+    np.testing.assert_array_equal(leaf, z["seg_leaf"])
+    np.testing.assert_array_equal(t, z["seg_t"])
+    np.testing.assert_array_equal(d, z["seg_delta"])
+    rgb = oracle.render_rays(tree, z["origins"], z["dirs"], 1.0)
+    np.testing.assert_array_equal(rgb, z["rgb"])
+    loss, g, sig = oracle.render_and_backprop(tree, z["origins"], z["dirs"], z["targets"], 1.0)
+    assert loss == float(z["loss"])
+    np.testing.assert_array_equal(g.touched, z["touched"])
+    np.testing.assert_array_equal(g.dsigma[g.touched], z["dsigma_touched"])
+    np.testing.assert_array_equal(sig, z["signal"])
