@@ -238,7 +238,7 @@ def config2_scene(device=None, basis_count: int = 16):
                          empty_thr=0.05, min_depth=4, sh_seed=20, device=device)
 
 
-CONFIG2_SPLIT_THR = 2.0
+CONFIG2_SPLIT_THR = 800.0  # -> 2.62M leaves, 3.0M nodes (tools/tune_scenes.py)
 
 
 def hemisphere_cameras(count: int, width: int, height: int, radius: float, seed: int,
