@@ -131,6 +131,24 @@ def view_rays_torch(focal, pose, device):
     return origins, world.contiguous()
 
 
+def _spread10(v):
+    v = v & 0x3FF
+    v = (v | (v << 16)) & 0x030000FF
+    v = (v | (v << 8)) & 0x0300F00F
+    v = (v | (v << 4)) & 0x030C30C3
+    v = (v | (v << 2)) & 0x09249249
+    return v
+
+
+def morton_key(idx):
+    """(view, Morton(x, y)) key of pool indices (pool is view-major, row-major)."""
+    view = idx // (W * H)
+    pix = idx - view * (W * H)
+    y = pix // W
+    x = pix - y * W
+    return (view << 32) | (_spread10(x) << 1) | _spread10(y)
+
+
 def perturbed(tree, seed):
     import torch
     from paper_2307_15333_b200.octree import from_canonical_tensors
@@ -188,15 +206,27 @@ def run_ours(args, rank, world, local_rank):
     gen = torch.Generator(device=dev)
     gen.manual_seed(1234 + rank)
     total_steps = args.warmup + args.steps
-    perm = torch.randint(0, n_pool, (total_steps + 2, per_rank), generator=gen, device=dev)
+    # an epoch-style permutation of the 64M-ray pool, one slice per step
+    perm = torch.randperm(n_pool, generator=gen, device=dev)[:(total_steps + 2) * per_rank]
+    perm = perm.reshape(total_steps + 2, per_rank)
     kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
            for _ in range(total_steps)]
 
-    def step(k, timed_kernel=True):
+    def batch_index(k):
+        """Loader: the step's random rays, optionally reordered for coherence
+        (same ray set; loss and gradients are sums over rays)."""
         idx = perm[k]
+        if args.order == "raster":
+            idx = idx.sort().values
+        elif args.order == "morton":
+            idx = idx[torch.argsort(morton_key(idx))]
+        return idx
+
+    def step(k, timed_kernel=True):
+        idx = batch_index(k)
         loss, grads, sig = render_and_backprop(
             tree, origins[idx], dirs[idx], targets[idx], BG, EPS, grad_scale=gs, workspace=ws,
-            kernel_events=kev[k] if timed_kernel else None)
+            kernel_events=kev[k] if timed_kernel else None, kernel_flags=args.bwd_flags)
         if world > 1:
             dist.all_reduce(ws.dsigma)
             dist.all_reduce(ws.dsh_store)
@@ -310,6 +340,7 @@ def run_ours(args, rank, world, local_rank):
             "l2": "inputs larger than L2 (2.6M-leaf payload 0.51 GB, 100-view ray pool 4.6 GB, "
                   "random 2^20-ray batches)",
             "parallelism": f"rays sharded dp{world}, tree replicated",
+            "batch_order": args.order, "bwd_flags": args.bwd_flags,
         },
         "gpu_launches": 2 * args.steps,
         "roofline": {
@@ -501,6 +532,10 @@ def main():
     ap.add_argument("--skip-refine", action="store_true")
     ap.add_argument("--skip-cpu", action="store_true")
     ap.add_argument("--ref-sample", type=int, default=1 << 14)
+    ap.add_argument("--order", choices=["random", "raster", "morton"], default="random",
+                    help="batch ray order handed to the kernel (same ray set)")
+    ap.add_argument("--bwd-flags", type=int, default=0,
+                    help="dot_render_bwd flags (2 = legacy one-ray-per-thread kernel)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     world = int(os.environ.get("WORLD_SIZE", "1"))

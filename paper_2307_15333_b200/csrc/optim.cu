@@ -5,6 +5,8 @@
 // explicit round-to-nearest intrinsic so that, given the same gradients, the
 // update is bit-identical to the numpy expression
 //   v = beta*v + (1-beta)*g*g;  theta = f32(max(f64(theta) - lr*g/(sqrt(v)+eps), 0)).
+// One thread per (row, 4-column quad): float4 payload / gradient accesses and
+// 2 x double2 state accesses per thread, the touched byte read once per quad.
 #include "dot_tree.cuh"
 #include "dot_internal.h"
 
@@ -18,29 +20,44 @@ __device__ __forceinline__ float rms_update(float theta, double& v, double g, do
     return float(t);
 }
 
-// One thread per (row, column); column 0 is sigma, 1..n_sh the SH coefficients.
+template <bool VEC>
 __global__ void rmsprop_kernel(float* __restrict__ sigma, float* __restrict__ sh, int sh_stride, int n_sh,
                                double* __restrict__ v_sigma, double* __restrict__ v_sh,
                                const float* __restrict__ gsig, const float* __restrict__ gsh,
                                int gsh_stride, const uint8_t* __restrict__ touched, int64_t cap,
-                               double beta, double eps, double lr_sigma, double lr_sh) {
-    const int cols = 1 + n_sh;
+                               int quads, double beta, double eps, double lr_sigma, double lr_sh) {
     const int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (t >= cap * cols) return;
-    const int64_t row = t / cols;
-    const int c = int(t - row * cols);
+    if (t >= cap * quads) return;
+    const int64_t row = t / quads;
+    const int j = int(t - row * quads);
     if (!touched[row]) return;
     const double omb = __dsub_rn(1.0, beta);
-    if (c == 0) {
+    if (j == 0) {
         double v = v_sigma[row];
         sigma[row] = rms_update(sigma[row], v, double(gsig[row]), beta, omb, eps, lr_sigma, true);
         v_sigma[row] = v;
+    }
+    const int k0 = 4 * j;
+    float* p = sh + row * sh_stride + k0;
+    const float* g = gsh + row * gsh_stride + k0;
+    double* v = v_sh + row * n_sh + k0;
+    if (VEC) {  // n_sh % 4 == 0: all quads full and 16/32-byte aligned
+        float4 th = *reinterpret_cast<float4*>(p);
+        const float4 gg = *reinterpret_cast<const float4*>(g);
+        double2 va = reinterpret_cast<double2*>(v)[0], vb = reinterpret_cast<double2*>(v)[1];
+        th.x = rms_update(th.x, va.x, double(gg.x), beta, omb, eps, lr_sh, false);
+        th.y = rms_update(th.y, va.y, double(gg.y), beta, omb, eps, lr_sh, false);
+        th.z = rms_update(th.z, vb.x, double(gg.z), beta, omb, eps, lr_sh, false);
+        th.w = rms_update(th.w, vb.y, double(gg.w), beta, omb, eps, lr_sh, false);
+        *reinterpret_cast<float4*>(p) = th;
+        reinterpret_cast<double2*>(v)[0] = va;
+        reinterpret_cast<double2*>(v)[1] = vb;
     } else {
-        const int k = c - 1;
-        double v = v_sh[row * n_sh + k];
-        float* p = sh + row * sh_stride + k;
-        *p = rms_update(*p, v, double(gsh[row * gsh_stride + k]), beta, omb, eps, lr_sh, false);
-        v_sh[row * n_sh + k] = v;
+        for (int u = 0; u < 4 && k0 + u < n_sh; ++u) {
+            double vv = v[u];
+            p[u] = rms_update(p[u], vv, double(g[u]), beta, omb, eps, lr_sh, false);
+            v[u] = vv;
+        }
     }
 }
 
@@ -57,9 +74,18 @@ extern "C" int dot_rmsprop_step(float* sigma, float* sh, int32_t sh_stride, int3
     if (!(beta > 0.0 && beta < 1.0)) return set_error(DOT_BAD_ARG, "beta must be in (0, 1), got %g", beta);
     if (n_sh < 1 || sh_stride < n_sh || gsh_stride < n_sh) return set_error(DOT_BAD_ARG, "rmsprop: bad strides");
     if (capacity == 0) return DOT_OK;
-    const int64_t total = capacity * (1 + n_sh);
-    rmsprop_kernel<<<unsigned((total + 255) / 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
-        sigma, sh, sh_stride, n_sh, v_sigma, v_sh, grad_sigma, grad_sh, gsh_stride, touched, capacity, beta,
-        eps, lr_sigma, lr_sh);
+    const int quads = (n_sh + 3) / 4;
+    const bool vec = (n_sh % 4 == 0) && (sh_stride % 4 == 0) && (gsh_stride % 4 == 0) &&
+                     ((reinterpret_cast<uintptr_t>(sh) | reinterpret_cast<uintptr_t>(grad_sh)) & 15) == 0 &&
+                     (reinterpret_cast<uintptr_t>(v_sh) & 31) == 0;
+    const int64_t total = capacity * quads;
+    const unsigned grid = unsigned((total + 255) / 256);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (vec)
+        rmsprop_kernel<true><<<grid, 256, 0, s>>>(sigma, sh, sh_stride, n_sh, v_sigma, v_sh, grad_sigma, grad_sh,
+                                                  gsh_stride, touched, capacity, quads, beta, eps, lr_sigma, lr_sh);
+    else
+        rmsprop_kernel<false><<<grid, 256, 0, s>>>(sigma, sh, sh_stride, n_sh, v_sigma, v_sh, grad_sigma, grad_sh,
+                                                   gsh_stride, touched, capacity, quads, beta, eps, lr_sigma, lr_sh);
     return check_launch("rmsprop_kernel");
 }

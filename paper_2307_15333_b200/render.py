@@ -257,7 +257,7 @@ def render_and_backprop(tree: SparseOctree, origins, dirs, targets, background,
                         early_stop_eps: float = EPS_T, t_near: float = 0.0,
                         t_far: float = math.inf, grad_scale: float | None = None,
                         workspace: BackpropWorkspace | None = None, accumulate: bool = False,
-                        return_rgb: bool = False, kernel_events=None):
+                        return_rgb: bool = False, kernel_events=None, kernel_flags: int = 0):
     """Batch MSE loss, analytic leaf gradients and per-leaf signal (render.py:175-225).
 
     Returns (loss, GradBuffer, signal).  ``grad_scale`` defaults to the
@@ -289,7 +289,8 @@ def render_and_backprop(tree: SparseOctree, origins, dirs, targets, background,
         _lib.call("dot_render_bwd", _lib.ctypes.byref(view), _lib.ptr(o), _lib.ptr(d), _lib.ptr(t), n,
                   _bg_ptr(bg), float(early_stop_eps), float(t_near), float(t_far), gs,
                   _lib.ptr(ws.dsigma), _lib.ptr(ws.dsh_store), tree.sh_stride, _lib.ptr(ws.signal),
-                  _lib.ptr(ws.touched), _lib.ptr(ws.loss), _lib.ptr(rgb), 0, _lib.stream_ptr())
+                  _lib.ptr(ws.touched), _lib.ptr(ws.loss), _lib.ptr(rgb), int(kernel_flags),
+                  _lib.stream_ptr())
         if kernel_events is not None:
             kernel_events[1].record()
     nsh = 3 * tree.basis_count
