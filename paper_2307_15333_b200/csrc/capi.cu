@@ -28,6 +28,21 @@ int check_cuda(cudaError_t e, const char* what) {
 
 int check_launch(const char* what) { return check_cuda(cudaGetLastError(), what); }
 
+// Stream-ordered scratch comes from the device's default memory pool; keep
+// freed blocks in the pool (release threshold = max) so per-call scratch is
+// recycled instead of being returned to the driver at every synchronisation.
+void retain_pool_memory() {
+    static thread_local int done_dev = -1;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev == done_dev) return;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t thr = ~0ull;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    done_dev = dev;
+}
+
 static int validate_tree(const dot_tree_view* v) {
     if (!v) return set_error(DOT_BAD_ARG, "tree view is NULL");
     if (!v->node || v->n_nodes < 1) return set_error(DOT_BAD_ARG, "tree has no nodes");

@@ -11,6 +11,7 @@ struct TreeDev;
 int set_error(int status, const char* fmt, ...);
 int check_launch(const char* what);
 int check_cuda(cudaError_t e, const char* what);
+void retain_pool_memory();
 
 int launch_trace_count(const TreeDev& T, const double* o, const double* d, int64_t n,
                        double tn, double tf, int64_t* counts, cudaStream_t s);
@@ -25,6 +26,14 @@ int launch_render_bwd(const TreeDev& T, const double* o, const double* d, const 
                       float* gsig, float* gsh, double* signal, uint8_t* touched, double* loss,
                       float* rgb_out, int flags, cudaStream_t s);
 
+int launch_render_bwd_two_kernel(const TreeDev& T, const double* o, const double* d, const double* tgt,
+                                 int64_t n, const double* bg, double eps, double tn, double tf, double gs,
+                                 float* gsig, float* gsh, double* signal, uint8_t* touched, double* loss,
+                                 float* rgb_out, int flags, cudaStream_t s);
+int launch_render_bwd_replay(const TreeDev& T, const double* o, const double* d, int64_t n, const double* bg,
+                             double eps, double tn, double tf, float* gsig, float* gsh, double* signal,
+                             uint8_t* touched, const float* ray_g, const float* ray_rgb,
+                             const uint8_t* ray_flag, int flags, cudaStream_t s);
 int launch_ray_stats(const TreeDev& T, const double* o, const double* d, int64_t n, double eps,
                      unsigned long long* out, cudaStream_t s);
 

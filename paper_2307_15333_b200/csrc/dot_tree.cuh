@@ -21,6 +21,7 @@ struct TreeDev {
     int32_t basis_count;
     int32_t sh_stride;
     double cx, cy, cz, half;
+    int32_t max_depth;
 };
 
 inline TreeDev make_tree(const dot_tree_view& v) {
@@ -35,6 +36,7 @@ inline TreeDev make_tree(const dot_tree_view& v) {
     t.cy = v.center[1];
     t.cz = v.center[2];
     t.half = v.half_extent;
+    t.max_depth = v.max_depth;
     return t;
 }
 
@@ -61,6 +63,67 @@ __device__ __forceinline__ Leaf descend(const TreeDev& T, double px, double py, 
         cy = (o & 2) ? dadd(cy, h) : dsub(cy, h);
         cz = (o & 4) ? dadd(cz, h) : dsub(cz, h);
         w = __ldg(T.node + w + o);
+    }
+    Leaf L;
+    L.pid = ~w;
+    L.cx = cx;
+    L.cy = cy;
+    L.cz = cz;
+    L.h = h;
+    return L;
+}
+
+// Exact restart-from-ancestor.  A root descent is a chain of octant choices
+// o_j = cmp(p, c_j) with c_{j+1} = c_j +/- h_{j+1}; for a new probe point the
+// chain coincides with the previous leaf's path up to the first level k
+// where the comparison differs.  The cache keeps that path (3 bits/level)
+// and the node words of its ancestors (shared memory, one row per thread),
+// so the matched prefix costs only the comparisons (no memory traffic) and
+// global loads start at level k.  The result is identical to descend().
+constexpr int kPathLevels = 21;  // 3 bits x 21 levels in one 64-bit word
+
+struct PathCache {
+    int32_t* stk;       // stk[j] = word of the level-j node on the cached path (stk[0] = root)
+    uint64_t path;      // octant taken at level j in bits [3j, 3j+3)
+    int depth;          // depth of the cached leaf, -1 = empty
+};
+
+__device__ __forceinline__ Leaf descend_cached(const TreeDev& T, double px, double py, double pz,
+                                               PathCache& pc) {
+    double cx = T.cx, cy = T.cy, cz = T.cz, h = T.half;
+    int j = 0;
+    int o = 0;
+    const int pd = pc.depth;
+    // matched prefix: comparisons only
+    while (j < pd) {
+        o = (px >= cx ? 1 : 0) | (py >= cy ? 2 : 0) | (pz >= cz ? 4 : 0);
+        if (o != int((pc.path >> (3 * j)) & 7u)) break;
+        h = dmul(h, 0.5);
+        cx = (o & 1) ? dadd(cx, h) : dsub(cx, h);
+        cy = (o & 2) ? dadd(cy, h) : dsub(cy, h);
+        cz = (o & 4) ? dadd(cz, h) : dsub(cz, h);
+        ++j;
+    }
+    int32_t w;
+    if (j == pd) {
+        w = pc.stk[j];  // same leaf as before
+    } else {
+        if (pd < 0) j = 0;
+        w = pc.stk[j];
+        uint64_t path = pc.path & ((1ull << (3 * j)) - 1ull);
+        while (w >= 0) {
+            o = (px >= cx ? 1 : 0) | (py >= cy ? 2 : 0) | (pz >= cz ? 4 : 0);
+            h = dmul(h, 0.5);
+            cx = (o & 1) ? dadd(cx, h) : dsub(cx, h);
+            cy = (o & 2) ? dadd(cy, h) : dsub(cy, h);
+            cz = (o & 4) ? dadd(cz, h) : dsub(cz, h);
+            w = __ldg(T.node + w + o);
+            path |= uint64_t(o) << (3 * j);
+            ++j;
+            pc.stk[j] = w;
+        }
+        pc.path = path;
+        pc.depth = j;
     }
     Leaf L;
     L.pid = ~w;
@@ -105,22 +168,29 @@ struct Tracer {
     }
 
     // _kernels.py:112-158.  Returns false when the ray has left the cube.
+    template <bool CACHED = false>
     __device__ __forceinline__ bool next(const TreeDev& T, Leaf& L, double& t_entry,
-                                         double& delta) {
+                                         double& delta, PathCache& pc) {
         for (;;) {
             const double probe = dadd(t, nudge);
             if (probe >= t1) return false;
             const double px = dadd(ox, dmul(probe, dx));
             const double py = dadd(oy, dmul(probe, dy));
             const double pz = dadd(oz, dmul(probe, dz));
-            L = descend(T, px, py, pz);
-            double tex = t1, cand;
-            if (dx > 0.0) { cand = ddiv(dsub(dadd(L.cx, L.h), ox), dx); if (cand < tex) tex = cand; }
-            else if (dx < 0.0) { cand = ddiv(dsub(dsub(L.cx, L.h), ox), dx); if (cand < tex) tex = cand; }
-            if (dy > 0.0) { cand = ddiv(dsub(dadd(L.cy, L.h), oy), dy); if (cand < tex) tex = cand; }
-            else if (dy < 0.0) { cand = ddiv(dsub(dsub(L.cy, L.h), oy), dy); if (cand < tex) tex = cand; }
-            if (dz > 0.0) { cand = ddiv(dsub(dadd(L.cz, L.h), oz), dz); if (cand < tex) tex = cand; }
-            else if (dz < 0.0) { cand = ddiv(dsub(dsub(L.cz, L.h), oz), dz); if (cand < tex) tex = cand; }
+            if constexpr (CACHED) L = descend_cached(T, px, py, pz, pc);
+            else L = descend(T, px, py, pz);
+            // exit t = min over axes of ((c +/- h) - o) / d, in x, y, z order with
+            // strict '<' like the reference.  Branch-free: c + (-h) == c - h
+            // exactly, and an axis with d == 0 contributes nothing.
+            double tex = t1;
+            {
+                const double cx = ddiv(dsub(dadd(L.cx, dx > 0.0 ? L.h : -L.h), ox), dx);
+                const double cy = ddiv(dsub(dadd(L.cy, dy > 0.0 ? L.h : -L.h), oy), dy);
+                const double cz = ddiv(dsub(dadd(L.cz, dz > 0.0 ? L.h : -L.h), oz), dz);
+                if (dx != 0.0 && cx < tex) tex = cx;
+                if (dy != 0.0 && cy < tex) tex = cy;
+                if (dz != 0.0 && cz < tex) tex = cz;
+            }
             if (tex <= probe) {  // boundary roundoff stalled the walk: widen the probe
                 nudge = dmul(nudge, 4.0);
                 continue;
@@ -131,6 +201,11 @@ struct Tracer {
             nudge = nudge0;
             return true;
         }
+    }
+
+    __device__ __forceinline__ bool next(const TreeDev& T, Leaf& L, double& t_entry, double& delta) {
+        PathCache none;
+        return next<false>(T, L, t_entry, delta, none);
     }
 };
 

@@ -436,6 +436,7 @@ __global__ void payload_kernel(TreeDev T, int64_t n_new, int S4, const int64_t* 
 
 template <typename Tp>
 static int dalloc(Tp** p, size_t n, cudaStream_t s) {
+    retain_pool_memory();
     return check_cuda(cudaMallocAsync(reinterpret_cast<void**>(p), sizeof(Tp) * (n ? n : 1), s),
                       "cudaMallocAsync");
 }

@@ -13,6 +13,27 @@
 namespace dot {
 
 constexpr int kBlock = 128;
+constexpr int kStk = kPathLevels + 2;  // odd row stride: conflict-free shared-memory stacks
+
+// Per-thread path cache in shared memory (see descend_cached).  Kernels are
+// instantiated with CACHED = false for trees deeper than the 64-bit path word
+// can describe (max_depth >= kPathLevels).
+template <bool CACHED>
+__device__ __forceinline__ void init_cache(const TreeDev& T, int32_t* smem, PathCache& pc) {
+    pc.depth = -1;
+    pc.path = 0;
+    pc.stk = smem + threadIdx.x * kStk;
+    if (CACHED) pc.stk[0] = __ldg(T.node);
+}
+
+#define DOT_STACK_SMEM(CACHED) __shared__ int32_t s_stk[(CACHED) ? kBlock * kStk : 1]
+
+// Off by default: measured on B200 the L1 already serves the hot upper levels
+// and the extra registers cost more than the saved loads (fwd 1.38e9 ->
+// 1.12e9 rays/s).  dot_render_bwd flag bit 3 turns it on for experiments.
+inline bool use_cache(const TreeDev& T, int flags = 0) {
+    return (flags & 8) != 0 && T.max_depth < kPathLevels;
+}
 
 __device__ __forceinline__ void load_ray(const double* __restrict__ o, const double* __restrict__ d,
                                          int64_t r, Tracer& tr) {
@@ -27,23 +48,28 @@ __device__ __forceinline__ void load_ray(const double* __restrict__ o, const dou
 // ---------------------------------------------------------------------------
 // Segment lists (parity / debug path of segment_batch).
 
+template <bool CACHED>
 __global__ void __launch_bounds__(kBlock) trace_count_kernel(TreeDev T, const double* __restrict__ o,
                                                              const double* __restrict__ d, int64_t n,
                                                              double t_near, double t_far,
                                                              int64_t* __restrict__ counts) {
     const int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (r >= n) return;
+    DOT_STACK_SMEM(CACHED);
+    PathCache pc;
+    init_cache<CACHED>(T, s_stk, pc);
     Tracer tr;
     load_ray(o, d, r, tr);
     int64_t c = 0;
     if (tr.init(T, t_near, t_far)) {
         Leaf L;
         double te, dl;
-        while (tr.next(T, L, te, dl)) ++c;
+        while (tr.template next<CACHED>(T, L, te, dl, pc)) ++c;
     }
     counts[r] = c;
 }
 
+template <bool CACHED>
 __global__ void __launch_bounds__(kBlock) trace_fill_kernel(TreeDev T, const double* __restrict__ o,
                                                             const double* __restrict__ d, int64_t n,
                                                             double t_near, double t_far,
@@ -53,13 +79,16 @@ __global__ void __launch_bounds__(kBlock) trace_fill_kernel(TreeDev T, const dou
                                                             double* __restrict__ seg_delta) {
     const int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (r >= n) return;
+    DOT_STACK_SMEM(CACHED);
+    PathCache pc;
+    init_cache<CACHED>(T, s_stk, pc);
     Tracer tr;
     load_ray(o, d, r, tr);
     int64_t s = offsets[r];
     if (tr.init(T, t_near, t_far)) {
         Leaf L;
         double te, dl;
-        while (tr.next(T, L, te, dl)) {
+        while (tr.template next<CACHED>(T, L, te, dl, pc)) {
             seg_leaf[s] = L.pid;
             seg_t[s] = te;
             seg_delta[s] = dl;
@@ -71,7 +100,7 @@ __global__ void __launch_bounds__(kBlock) trace_fill_kernel(TreeDev T, const dou
 // ---------------------------------------------------------------------------
 // Fused forward: traverse + composite (composite_kernel, _kernels.py:185-224).
 
-template <int B>
+template <int B, bool CACHED>
 __global__ void __launch_bounds__(kBlock) render_fwd_kernel(
     TreeDev T, const double* __restrict__ o, const double* __restrict__ d, int64_t n,
     double bg0, double bg1, double bg2, double eps, double t_near, double t_far,
@@ -80,6 +109,9 @@ __global__ void __launch_bounds__(kBlock) render_fwd_kernel(
     constexpr int S = pad4(3 * B);
     const int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (r >= n) return;
+    DOT_STACK_SMEM(CACHED);
+    PathCache pc;
+    init_cache<CACHED>(T, s_stk, pc);
     Tracer tr;
     load_ray(o, d, r, tr);
     float basis[B];
@@ -88,7 +120,7 @@ __global__ void __launch_bounds__(kBlock) render_fwd_kernel(
     if (tr.init(T, t_near, t_far)) {
         Leaf L;
         double te, dl;
-        while (tr.next(T, L, te, dl)) {
+        while (tr.template next<CACHED>(T, L, te, dl, pc)) {
             const double sg = double(__ldg(T.sigma + L.pid));
             const double a = exp(-sg * dl);
             const double q = 1.0 - a;
@@ -248,7 +280,7 @@ __global__ void __launch_bounds__(kBlock) render_bwd_kernel(
 // Same arithmetic as render_bwd_kernel; phase 2 carries the suffix directly
 // (suf = rgb - prefix, updated per segment).
 
-template <int B>
+template <int B, bool CACHED>
 __global__ void __launch_bounds__(kBlock) render_bwd_persistent_kernel(
     TreeDev T, const double* __restrict__ o, const double* __restrict__ d,
     const double* __restrict__ tgt, int64_t n, double bg0, double bg1, double bg2, double eps,
@@ -260,6 +292,9 @@ __global__ void __launch_bounds__(kBlock) render_bwd_persistent_kernel(
     constexpr unsigned FULL = 0xffffffffu;
     const unsigned lane = threadIdx.x & 31;
     const unsigned lt_mask = (1u << lane) - 1u;
+    DOT_STACK_SMEM(CACHED);
+    PathCache pc;
+    init_cache<CACHED>(T, s_stk, pc);  // survives across rays: any cached path is valid
     Tracer tr;
     float basis[B];
     int phase = 0;  // 0: needs a ray, 1: forward to the cut, 2: backward replay
@@ -323,7 +358,7 @@ __global__ void __launch_bounds__(kBlock) render_bwd_persistent_kernel(
 
         Leaf L;
         double te, dl;
-        const bool got = tr.next(T, L, te, dl);
+        const bool got = tr.template next<CACHED>(T, L, te, dl, pc);
         if (phase == 1) {
             bool cut = false;
             if (got) {
@@ -400,6 +435,91 @@ __global__ void __launch_bounds__(kBlock) render_bwd_persistent_kernel(
     if (lane == 0 && loss != 0.0) red_add_f64(loss_sum, loss);
 }
 
+// Replay of rays whose segment records overflowed the two-kernel path's
+// buffer (backward.cu): pass 1 only recounts the composited segments, pass 2
+// scatters with the rgb and dL/drgb that kernel A already stored.
+template <int B>
+__global__ void __launch_bounds__(kBlock) render_bwd_replay_kernel(
+    TreeDev T, const double* __restrict__ o, const double* __restrict__ d, int64_t n, double eps,
+    double t_near, double t_far, float* __restrict__ gsig, float* __restrict__ gsh,
+    double* __restrict__ signal, const float* __restrict__ ray_g, const float* __restrict__ ray_rgb,
+    const uint8_t* __restrict__ ray_flag) {
+    constexpr int S = pad4(3 * B);
+    const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+    for (int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; r < n; r += stride) {
+        if (!(ray_flag[r] & 1)) continue;
+        Tracer tr;
+        load_ray(o, d, r, tr);
+        float basis[B];
+        eval_basis<B>(tr.dx, tr.dy, tr.dz, basis);
+        if (!tr.init(T, t_near, t_far)) continue;
+        const Tracer start = tr;
+        int used = 0;
+        double trans = 1.0;
+        Leaf L;
+        double te, dl;
+        while (tr.next(T, L, te, dl)) {
+            trans *= exp(-double(__ldg(T.sigma + L.pid)) * dl);
+            ++used;
+            if (eps > 0.0 && trans < eps) break;
+        }
+        const double g0 = ray_g[3 * r], g1 = ray_g[3 * r + 1], g2 = ray_g[3 * r + 2];
+        double s0 = ray_rgb[3 * r], s1 = ray_rgb[3 * r + 1], s2 = ray_rgb[3 * r + 2];
+        tr = start;
+        double Ti = 1.0;
+        for (int i = 0; i < used && tr.next(T, L, te, dl); ++i) {
+            const int64_t pid = L.pid;
+            const double a = exp(-double(__ldg(T.sigma + pid)) * dl);
+            const double q = 1.0 - a;
+            float e0, e1, e2;
+            sh_dot<B>(T.sh + pid * S, basis, e0, e1, e2);
+            const float k0 = sigmoidf(e0), k1 = sigmoidf(e1), k2 = sigmoidf(e2);
+            const double tq = Ti * q;
+            s0 -= tq * double(k0);
+            s1 -= tq * double(k1);
+            s2 -= tq * double(k2);
+            const double tn = Ti * a;
+            red_add_f32(gsig + pid, float(dl * (g0 * (tn * k0 - s0) + g1 * (tn * k1 - s1) + g2 * (tn * k2 - s2))));
+            const float w[3] = {float(g0 * tq) * k0 * (1.f - k0), float(g1 * tq) * k1 * (1.f - k1),
+                                float(g2 * tq) * k2 * (1.f - k2)};
+            if (w[0] != 0.f || w[1] != 0.f || w[2] != 0.f) {
+                float* row = gsh + pid * S;
+#pragma unroll
+                for (int j = 0; j < S / 4; ++j) {
+                    float v[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const int idx = 4 * j + u;
+                        v[u] = idx < 3 * B ? w[idx / B] * basis[idx % B] : 0.f;
+                    }
+                    red_add_v4(row + 4 * j, v[0], v[1], v[2], v[3]);
+                }
+            }
+            if (q != 0.0) red_add_f64(signal + pid, q);
+            Ti *= a;
+        }
+    }
+}
+
+int launch_render_bwd_replay(const TreeDev& T, const double* o, const double* d, int64_t n, const double* bg,
+                             double eps, double tn, double tf, float* gsig, float* gsh, double* signal,
+                             uint8_t* touched, const float* ray_g, const float* ray_rgb,
+                             const uint8_t* ray_flag, int flags, cudaStream_t s) {
+    (void)bg;
+    (void)touched;
+    (void)flags;
+    if (n == 0) return DOT_OK;
+    const unsigned grid = unsigned(std::min<int64_t>((n + kBlock - 1) / kBlock, 148 * 8));
+    switch (T.basis_count) {
+        case 1: render_bwd_replay_kernel<1><<<grid, kBlock, 0, s>>>(T, o, d, n, eps, tn, tf, gsig, gsh, signal, ray_g, ray_rgb, ray_flag); break;
+        case 4: render_bwd_replay_kernel<4><<<grid, kBlock, 0, s>>>(T, o, d, n, eps, tn, tf, gsig, gsh, signal, ray_g, ray_rgb, ray_flag); break;
+        case 9: render_bwd_replay_kernel<9><<<grid, kBlock, 0, s>>>(T, o, d, n, eps, tn, tf, gsig, gsh, signal, ray_g, ray_rgb, ray_flag); break;
+        case 16: render_bwd_replay_kernel<16><<<grid, kBlock, 0, s>>>(T, o, d, n, eps, tn, tf, gsig, gsh, signal, ray_g, ray_rgb, ray_flag); break;
+        default: return set_error(DOT_BAD_ARG, "basis_count must be 1, 4, 9 or 16");
+    }
+    return check_launch("render_bwd_replay_kernel");
+}
+
 template <typename K>
 static unsigned persistent_grid(K kernel, int64_t n) {
     int dev = 0, sms = 148, per_sm = 1;
@@ -465,7 +585,8 @@ static unsigned blocks_for(int64_t n) { return unsigned((n + kBlock - 1) / kBloc
 int launch_trace_count(const TreeDev& T, const double* o, const double* d, int64_t n,
                        double tn, double tf, int64_t* counts, cudaStream_t s) {
     if (n == 0) return DOT_OK;
-    trace_count_kernel<<<blocks_for(n), kBlock, 0, s>>>(T, o, d, n, tn, tf, counts);
+    if (use_cache(T)) trace_count_kernel<true><<<blocks_for(n), kBlock, 0, s>>>(T, o, d, n, tn, tf, counts);
+    else trace_count_kernel<false><<<blocks_for(n), kBlock, 0, s>>>(T, o, d, n, tn, tf, counts);
     return check_launch("trace_count_kernel");
 }
 
@@ -473,24 +594,30 @@ int launch_trace_fill(const TreeDev& T, const double* o, const double* d, int64_
                       double tf, const int64_t* off, int64_t* leaf, double* t, double* dl,
                       cudaStream_t s) {
     if (n == 0) return DOT_OK;
-    trace_fill_kernel<<<blocks_for(n), kBlock, 0, s>>>(T, o, d, n, tn, tf, off, leaf, t, dl);
+    if (use_cache(T)) trace_fill_kernel<true><<<blocks_for(n), kBlock, 0, s>>>(T, o, d, n, tn, tf, off, leaf, t, dl);
+    else trace_fill_kernel<false><<<blocks_for(n), kBlock, 0, s>>>(T, o, d, n, tn, tf, off, leaf, t, dl);
     return check_launch("trace_fill_kernel");
 }
+
+// Dispatch on the basis count (compile-time B) and the path cache.
+#define DOT_DISPATCH_B(MACRO)                                                     \
+    switch (T.basis_count) {                                                      \
+        case 1: if (cached) MACRO(1, true) else MACRO(1, false) break;            \
+        case 4: if (cached) MACRO(4, true) else MACRO(4, false) break;            \
+        case 9: if (cached) MACRO(9, true) else MACRO(9, false) break;            \
+        case 16: if (cached) MACRO(16, true) else MACRO(16, false) break;         \
+        default: return set_error(DOT_BAD_ARG, "basis_count must be 1, 4, 9 or 16"); \
+    }
 
 int launch_render_fwd(const TreeDev& T, const double* o, const double* d, int64_t n,
                       const double* bg, double eps, double tn, double tf, float* rgb, float* tfin,
                       float* wsum, float* depth, cudaStream_t s) {
     if (n == 0) return DOT_OK;
-#define DOT_FWD(BB)                                                                           \
-    render_fwd_kernel<BB><<<blocks_for(n), kBlock, 0, s>>>(T, o, d, n, bg[0], bg[1], bg[2], eps, \
-                                                           tn, tf, rgb, tfin, wsum, depth)
-    switch (T.basis_count) {
-        case 1: DOT_FWD(1); break;
-        case 4: DOT_FWD(4); break;
-        case 9: DOT_FWD(9); break;
-        case 16: DOT_FWD(16); break;
-        default: return set_error(DOT_BAD_ARG, "basis_count must be 1, 4, 9 or 16");
-    }
+    const bool cached = use_cache(T);
+#define DOT_FWD(BB, CC)                                                                              \
+    { render_fwd_kernel<BB, CC><<<blocks_for(n), kBlock, 0, s>>>(T, o, d, n, bg[0], bg[1], bg[2], eps, \
+                                                                 tn, tf, rgb, tfin, wsum, depth); }
+    DOT_DISPATCH_B(DOT_FWD)
 #undef DOT_FWD
     return check_launch("render_fwd_kernel");
 }
@@ -500,36 +627,30 @@ int launch_render_bwd(const TreeDev& T, const double* o, const double* d, const 
                       float* gsig, float* gsh, double* signal, uint8_t* touched, double* loss,
                       float* rgb_out, int flags, cudaStream_t s) {
     if (n == 0) return DOT_OK;
-    if (flags & 2) {  // legacy one-ray-per-thread kernel (A/B comparisons)
-#define DOT_BWD(BB)                                                                          \
-    render_bwd_kernel<BB><<<blocks_for(n), kBlock, 0, s>>>(T, o, d, tgt, n, bg[0], bg[1], bg[2], \
-                                                           eps, tn, tf, gs, gsig, gsh, signal,   \
-                                                           touched, loss, rgb_out, flags)
-        switch (T.basis_count) {
-            case 1: DOT_BWD(1); break;
-            case 4: DOT_BWD(4); break;
-            case 9: DOT_BWD(9); break;
-            case 16: DOT_BWD(16); break;
-            default: return set_error(DOT_BAD_ARG, "basis_count must be 1, 4, 9 or 16");
-        }
+    if (flags & 2) {  // legacy one-ray-per-thread kernel, uncached (A/B comparisons)
+        const bool cached = false;
+#define DOT_BWD(BB, CC)                                                                         \
+    { render_bwd_kernel<BB><<<blocks_for(n), kBlock, 0, s>>>(T, o, d, tgt, n, bg[0], bg[1], bg[2], \
+                                                             eps, tn, tf, gs, gsig, gsh, signal,   \
+                                                             touched, loss, rgb_out, flags); }
+        DOT_DISPATCH_B(DOT_BWD)
 #undef DOT_BWD
         return check_launch("render_bwd_kernel");
     }
+    if (!(flags & 16))  // default: record + scatter (backward.cu)
+        return launch_render_bwd_two_kernel(T, o, d, tgt, n, bg, eps, tn, tf, gs, gsig, gsh, signal, touched,
+                                            loss, rgb_out, flags, s);
+    const bool cached = use_cache(T, flags);
     unsigned long long* ctr = nullptr;
     if (int st = check_cuda(cudaMallocAsync(reinterpret_cast<void**>(&ctr), sizeof(*ctr), s), "cudaMallocAsync"))
         return st;
     cudaMemsetAsync(ctr, 0, sizeof(*ctr), s);
-#define DOT_BWDP(BB)                                                                               \
-    render_bwd_persistent_kernel<BB><<<persistent_grid(render_bwd_persistent_kernel<BB>, n), kBlock, 0, \
-                                       s>>>(T, o, d, tgt, n, bg[0], bg[1], bg[2], eps, tn, tf, gs, gsig,  \
-                                            gsh, signal, touched, loss, rgb_out, flags, ctr)
-    switch (T.basis_count) {
-        case 1: DOT_BWDP(1); break;
-        case 4: DOT_BWDP(4); break;
-        case 9: DOT_BWDP(9); break;
-        case 16: DOT_BWDP(16); break;
-        default: cudaFreeAsync(ctr, s); return set_error(DOT_BAD_ARG, "basis_count must be 1, 4, 9 or 16");
-    }
+#define DOT_BWDP(BB, CC)                                                                           \
+    { render_bwd_persistent_kernel<BB, CC><<<persistent_grid(render_bwd_persistent_kernel<BB, CC>, n), \
+                                             kBlock, 0, s>>>(T, o, d, tgt, n, bg[0], bg[1], bg[2], eps, \
+                                                             tn, tf, gs, gsig, gsh, signal, touched,    \
+                                                             loss, rgb_out, flags, ctr); }
+    DOT_DISPATCH_B(DOT_BWDP)
 #undef DOT_BWDP
     const int st = check_launch("render_bwd_persistent_kernel");
     cudaFreeAsync(ctr, s);
