@@ -90,6 +90,13 @@ int dot_render_bwd(const dot_tree_view* tree, const double* origins, const doubl
                    uint8_t* touched, double* loss_sum, float* rgb_out, int32_t flags,
                    void* stream);
 
+/* --- coherence keys (no reference counterpart): keys[i] = (origin Morton
+ *     << 32) | octahedral-direction Morton; sorting a batch by them puts rays
+ *     that walk the same cells into the same warps.  Results are sums over
+ *     rays, so the order changes only speed. */
+int dot_ray_keys(const dot_tree_view* tree, const double* origins, const double* dirs,
+                 int64_t n_rays, uint64_t* keys, void* stream);
+
 /* --- workload statistics (measurement helper, no reference counterpart):
  *     totals[0] += traversed segments, totals[1] += composited (pre-cut)
  *     segments, totals[2] += composited segments with q > 0. */

@@ -51,7 +51,8 @@ _SIGNATURES = {
     "dot_render_bwd": (c_i32, [c_void_p, c_void_p, c_void_p, c_void_p, c_i64, c_void_p, c_f64, c_f64,
                                c_f64, c_f64, c_void_p, c_void_p, c_i32, c_void_p, c_void_p, c_void_p,
                                c_void_p, c_i32, c_void_p]),
-    "dot_ray_stats": (c_i32, [c_void_p, c_void_p, c_void_p, c_i64, c_f64, c_void_p, c_void_p]),
+    "dot_ray_keys": (c_i32, [c_void_p, c_void_p, c_void_p, c_i64, c_void_p, c_void_p]),
+    "dot_ray_stats":(c_i32, [c_void_p, c_void_p, c_void_p, c_i64, c_f64, c_void_p, c_void_p]),
     "dot_refine_plan_create": (c_i32, [c_void_p, c_void_p, c_void_p, c_i32, c_f64, c_f64, c_i32, c_i32,
                                        c_f64, c_void_p, c_void_p, c_void_p]),
     "dot_refine_plan_lists": (c_i32, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),

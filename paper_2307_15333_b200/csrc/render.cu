@@ -435,6 +435,164 @@ __global__ void __launch_bounds__(kBlock) render_bwd_persistent_kernel(
     if (lane == 0 && loss != 0.0) red_add_f64(loss_sum, loss);
 }
 
+// ---------------------------------------------------------------------------
+// Buffered fused forward + backward (default).  One ray per thread; rays in
+// a batch are expected in a coherent order (the loader's Morton sort).
+// Pass 1 walks the ray ONCE: it composites up to the early-termination cut,
+// marks every traversed leaf touched (post-cut ones too, scatter_kernel
+// semantics) and buffers each composited segment (leaf, delta, alpha, colour)
+// in a per-thread local array.  Pass 2 replays the buffer in order -- no
+// second traversal, the colour of q > 0 segments is not recomputed -- and,
+// for rays with more than K composited segments, resumes the walk from the
+// tracer state saved when the buffer filled.
+
+struct BufSeg {
+    int32_t pid;
+    float delta;
+    double a;        // alpha = exp(-sigma delta) exactly as pass 1 used it
+    float k0, k1, k2;  // colour (NaN: not evaluated in pass 1, q == 0)
+    float pad;
+};
+
+template <int B, int K>
+__global__ void __launch_bounds__(kBlock) render_bwd_buffered_kernel(
+    TreeDev T, const double* __restrict__ o, const double* __restrict__ d,
+    const double* __restrict__ tgt, int64_t n, double bg0, double bg1, double bg2, double eps,
+    double t_near, double t_far, double grad_scale, float* __restrict__ gsig,
+    float* __restrict__ gsh, double* __restrict__ signal, uint8_t* __restrict__ touched,
+    double* __restrict__ loss_sum, float* __restrict__ rgb_out, int flags) {
+    constexpr int S = pad4(3 * B);
+    const int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    double loss = 0.0;
+    if (r < n) {
+        Tracer tr;
+        load_ray(o, d, r, tr);
+        float basis[B];
+        eval_basis<B>(tr.dx, tr.dy, tr.dz, basis);
+        BufSeg buf[K];
+        int used = 0;
+        double resume_t = 0.0, resume_nudge = 0.0;
+        double trans = 1.0, c0 = 0.0, c1 = 0.0, c2 = 0.0;
+        const bool hit = tr.init(T, t_near, t_far);
+        if (hit) {
+            Leaf L;
+            double te, dl;
+            bool cut = false;
+            while (tr.next(T, L, te, dl)) {
+                touched[L.pid] = 1;
+                if (cut) continue;  // post-cut: touched only
+                const double a = exp(-double(__ldg(T.sigma + L.pid)) * dl);
+                const double q = 1.0 - a;
+                float k0 = __int_as_float(0x7fc00000), k1 = k0, k2 = k0;
+                if (q > 0.0) {
+                    float e0, e1, e2;
+                    sh_dot<B>(T.sh + int64_t(L.pid) * S, basis, e0, e1, e2);
+                    k0 = sigmoidf(e0);
+                    k1 = sigmoidf(e1);
+                    k2 = sigmoidf(e2);
+                    const double tq = trans * q;
+                    c0 += tq * double(k0);
+                    c1 += tq * double(k1);
+                    c2 += tq * double(k2);
+                }
+                if (used < K) {
+                    buf[used].pid = L.pid;
+                    buf[used].delta = float(dl);
+                    buf[used].a = a;
+                    buf[used].k0 = k0;
+                    buf[used].k1 = k1;
+                    buf[used].k2 = k2;
+                } else if (used == K) {  // buffer full: remember where pass 2 resumes
+                    resume_t = te;
+                    resume_nudge = tr.nudge0;
+                }
+                ++used;
+                trans *= a;
+                if (eps > 0.0 && trans < eps) {
+                    cut = true;
+                    if (flags & 1) break;
+                }
+            }
+        }
+        const double tf = trans;
+        const double R0 = c0 + tf * bg0, R1 = c1 + tf * bg1, R2 = c2 + tf * bg2;
+        const double r0 = R0 - __ldg(tgt + 3 * r + 0);
+        const double r1 = R1 - __ldg(tgt + 3 * r + 1);
+        const double r2 = R2 - __ldg(tgt + 3 * r + 2);
+        loss = r0 * r0 + r1 * r1 + r2 * r2;
+        if (rgb_out) {
+            rgb_out[3 * r + 0] = float(R0);
+            rgb_out[3 * r + 1] = float(R1);
+            rgb_out[3 * r + 2] = float(R2);
+        }
+        const double g0 = grad_scale * r0, g1 = grad_scale * r1, g2 = grad_scale * r2;
+        // ---- pass 2: replay (suffix carried directly: suf = rgb - prefix)
+        double s0 = R0, s1 = R1, s2 = R2, Ti = 1.0;
+        if (used > K) {  // segment K onwards come from a resumed walk
+            tr.t = resume_t;
+            tr.nudge = resume_nudge;
+        }
+        Leaf L;
+        for (int i = 0; i < used; ++i) {
+            int64_t pid;
+            double a, dl;
+            float k0, k1, k2;
+            if (i < K) {
+                pid = buf[i].pid;
+                a = buf[i].a;
+                dl = buf[i].delta;
+                k0 = buf[i].k0;
+                k1 = buf[i].k1;
+                k2 = buf[i].k2;
+            } else {
+                double te;
+                tr.next(T, L, te, dl);
+                pid = L.pid;
+                a = exp(-double(__ldg(T.sigma + pid)) * dl);
+                k0 = __int_as_float(0x7fc00000);
+            }
+            if (k0 != k0) {
+                float e0, e1, e2;
+                sh_dot<B>(T.sh + pid * S, basis, e0, e1, e2);
+                k0 = sigmoidf(e0);
+                k1 = sigmoidf(e1);
+                k2 = sigmoidf(e2);
+            }
+            const double q = 1.0 - a;
+            const double tq = Ti * q;
+            s0 -= tq * double(k0);
+            s1 -= tq * double(k1);
+            s2 -= tq * double(k2);
+            const double tn = Ti * a;
+            const double ds = dl * (g0 * (tn * k0 - s0) + g1 * (tn * k1 - s1) + g2 * (tn * k2 - s2));
+            red_add_f32(gsig + pid, float(ds));
+            const float w0 = float(g0 * tq) * k0 * (1.f - k0);
+            const float w1 = float(g1 * tq) * k1 * (1.f - k1);
+            const float w2 = float(g2 * tq) * k2 * (1.f - k2);
+            if (w0 != 0.f || w1 != 0.f || w2 != 0.f) {
+                float* row = gsh + pid * S;
+#pragma unroll
+                for (int j = 0; j < S / 4; ++j) {
+                    float v[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const int idx = 4 * j + u;
+                        const int k = idx / B;
+                        const float w = k == 0 ? w0 : (k == 1 ? w1 : w2);
+                        v[u] = idx < 3 * B ? w * basis[idx % B] : 0.f;
+                    }
+                    red_add_v4(row + 4 * j, v[0], v[1], v[2], v[3]);
+                }
+            }
+            if (q != 0.0) red_add_f64(signal + pid, q);
+            Ti *= a;
+        }
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) loss += __shfl_down_sync(0xffffffffu, loss, off);
+    if ((threadIdx.x & 31) == 0 && loss != 0.0) red_add_f64(loss_sum, loss);
+}
+
 // Replay of rays whose segment records overflowed the two-kernel path's
 // buffer (backward.cu): pass 1 only recounts the composited segments, pass 2
 // scatters with the rgb and dL/drgb that kernel A already stored.
@@ -529,6 +687,65 @@ static unsigned persistent_grid(K kernel, int64_t n) {
     const int64_t full = int64_t(sms) * (per_sm > 0 ? per_sm : 1);
     const int64_t need = (n + kBlock - 1) / kBlock;
     return unsigned(need < full ? need : full);
+}
+
+// ---------------------------------------------------------------------------
+// Coherence keys: sorting a batch by (origin Morton, octahedral direction
+// Morton) puts rays that walk the same cells next to each other -- within a
+// camera the direction key is a pixel-space Z-order.  Loss, gradients and
+// signal are sums over rays, so the order changes nothing but speed.
+
+__device__ __forceinline__ unsigned long long spread_bits(unsigned long long v, int bits) {
+    unsigned long long out = 0;
+    for (int i = 0; i < bits; ++i) out |= ((v >> i) & 1ull) << (2 * i);
+    return out;
+}
+
+__device__ __forceinline__ unsigned long long spread3_10(unsigned v) {
+    unsigned long long x = v & 0x3FF;
+    x = (x | (x << 16)) & 0x030000FFull;
+    x = (x | (x << 8)) & 0x0300F00Full;
+    x = (x | (x << 4)) & 0x030C30C3ull;
+    x = (x | (x << 2)) & 0x09249249ull;
+    return x;
+}
+
+__global__ void ray_keys_kernel(TreeDev T, const double* __restrict__ o, const double* __restrict__ d,
+                                int64_t n, unsigned long long* __restrict__ keys) {
+    const int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (r >= n) return;
+    // origin: 10 bits per axis over a box 8x the root cube
+    unsigned q[3];
+    const double c3[3] = {T.cx, T.cy, T.cz};
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        double u = (o[3 * r + a] - (c3[a] - 4.0 * T.half)) / (8.0 * T.half);
+        u = fmin(fmax(u, 0.0), 0.999999);
+        q[a] = unsigned(u * 1024.0);
+    }
+    const unsigned long long om = spread3_10(q[0]) | (spread3_10(q[1]) << 1) | (spread3_10(q[2]) << 2);
+    // direction: octahedral map to [0,1)^2, 16 bits per axis
+    double x = d[3 * r], y = d[3 * r + 1], z = d[3 * r + 2];
+    const double l1 = fabs(x) + fabs(y) + fabs(z);
+    x /= l1;
+    y /= l1;
+    if (z < 0.0) {
+        const double tx = (1.0 - fabs(y)) * (x >= 0.0 ? 1.0 : -1.0);
+        const double ty = (1.0 - fabs(x)) * (y >= 0.0 ? 1.0 : -1.0);
+        x = tx;
+        y = ty;
+    }
+    const unsigned ux = unsigned(fmin(fmax(0.5 * (x + 1.0), 0.0), 0.99999) * 65536.0);
+    const unsigned uy = unsigned(fmin(fmax(0.5 * (y + 1.0), 0.0), 0.99999) * 65536.0);
+    const unsigned long long dm = spread_bits(ux, 16) | (spread_bits(uy, 16) << 1);
+    keys[r] = (om << 32) | dm;
+}
+
+int launch_ray_keys(const TreeDev& T, const double* o, const double* d, int64_t n, unsigned long long* keys,
+                    cudaStream_t s) {
+    if (n == 0) return DOT_OK;
+    ray_keys_kernel<<<unsigned((n + 255) / 256), 256, 0, s>>>(T, o, d, n, keys);
+    return check_launch("ray_keys_kernel");
 }
 
 // ---------------------------------------------------------------------------
@@ -637,9 +854,27 @@ int launch_render_bwd(const TreeDev& T, const double* o, const double* d, const 
 #undef DOT_BWD
         return check_launch("render_bwd_kernel");
     }
-    if (!(flags & 16))  // default: record + scatter (backward.cu)
+    if (flags & 64)  // record + scatter (backward.cu)
         return launch_render_bwd_two_kernel(T, o, d, tgt, n, bg, eps, tn, tf, gs, gsig, gsh, signal, touched,
                                             loss, rgb_out, flags, s);
+    if (!(flags & 16)) {  // default: buffered one-ray-per-thread
+        const bool cached = false;
+        const bool big = (flags & 128) == 0;  // K = 32 records in flight; bit 7 selects K = 16
+#define DOT_BUF(BB, CC)                                                                                     \
+    {                                                                                                       \
+        if (big)                                                                                            \
+            render_bwd_buffered_kernel<BB, 32><<<blocks_for(n), kBlock, 0, s>>>(                            \
+                T, o, d, tgt, n, bg[0], bg[1], bg[2], eps, tn, tf, gs, gsig, gsh, signal, touched, loss,    \
+                rgb_out, flags);                                                                            \
+        else                                                                                                \
+            render_bwd_buffered_kernel<BB, 16><<<blocks_for(n), kBlock, 0, s>>>(                            \
+                T, o, d, tgt, n, bg[0], bg[1], bg[2], eps, tn, tf, gs, gsig, gsh, signal, touched, loss,    \
+                rgb_out, flags);                                                                            \
+    }
+        DOT_DISPATCH_B(DOT_BUF)
+#undef DOT_BUF
+        return check_launch("render_bwd_buffered_kernel");
+    }
     const bool cached = use_cache(T, flags);
     unsigned long long* ctr = nullptr;
     if (int st = check_cuda(cudaMallocAsync(reinterpret_cast<void**>(&ctr), sizeof(*ctr), s), "cudaMallocAsync"))

@@ -30,6 +30,7 @@ from .octree import SparseOctree
 
 EPS_T = 1e-4  # early-termination transmittance threshold (render.py:23)
 UNIT_TOL = 1e-6
+COHERENT_MIN_RAYS = 1 << 14  # below this a key sort costs more than it saves
 
 
 @dataclass
@@ -257,7 +258,8 @@ def render_and_backprop(tree: SparseOctree, origins, dirs, targets, background,
                         early_stop_eps: float = EPS_T, t_near: float = 0.0,
                         t_far: float = math.inf, grad_scale: float | None = None,
                         workspace: BackpropWorkspace | None = None, accumulate: bool = False,
-                        return_rgb: bool = False, kernel_events=None, kernel_flags: int = 0):
+                        return_rgb: bool = False, kernel_events=None, kernel_flags: int = 0,
+                        coherent: bool = True):
     """Batch MSE loss, analytic leaf gradients and per-leaf signal (render.py:175-225).
 
     Returns (loss, GradBuffer, signal).  ``grad_scale`` defaults to the
@@ -280,10 +282,19 @@ def render_and_backprop(tree: SparseOctree, origins, dirs, targets, background,
     if workspace is not None and not accumulate:
         ws.zero_()
     rgb = torch.empty(n, 3, dtype=torch.float32, device=tree.device) if return_rgb else None
+    perm = None
     if n:
         gs = 2.0 / n if grad_scale is None else float(grad_scale)
         bg = _background(background)
         view, _topo = tree.tree_view()
+        if coherent and n >= COHERENT_MIN_RAYS:
+            # reorder the batch so each warp walks neighbouring cells; loss,
+            # gradients and signal are sums over rays (order-independent)
+            keys = torch.empty(n, dtype=torch.int64, device=tree.device)
+            _lib.call("dot_ray_keys", _lib.ctypes.byref(view), _lib.ptr(o), _lib.ptr(d), n,
+                      _lib.ptr(keys), _lib.stream_ptr())
+            perm = torch.argsort(keys)
+            o, d, t = o[perm], d[perm], t[perm]
         if kernel_events is not None:
             kernel_events[0].record()
         _lib.call("dot_render_bwd", _lib.ctypes.byref(view), _lib.ptr(o), _lib.ptr(d), _lib.ptr(t), n,
@@ -293,6 +304,10 @@ def render_and_backprop(tree: SparseOctree, origins, dirs, targets, background,
                   _lib.stream_ptr())
         if kernel_events is not None:
             kernel_events[1].record()
+        if perm is not None and rgb is not None:
+            unsorted = torch.empty_like(rgb)
+            unsorted[perm] = rgb
+            rgb = unsorted
     nsh = 3 * tree.basis_count
     dsh = ws.dsh_store if nsh == tree.sh_stride else ws.dsh_store[:, :nsh]
     if io.numpy:
