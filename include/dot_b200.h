@@ -114,9 +114,13 @@ int dot_ray_stats(const dot_tree_view* tree, const double* origins, const double
  * reference's sample() alone; gamma = 0 and use_threshold = 0 disable the
  * sample, i.e. prune() alone).  Because the output size is
  * data dependent, the call is split in two:
- *   dot_refine_plan  -> computes the selections and output sizes and stores
- *                       them in an opaque plan (synchronises the stream once);
- *   dot_refine_apply -> writes the new node words / payload / remap.
+ *   dot_refine_plan_create -> computes the selections and output sizes on the
+ *       device and stores them in an opaque plan (one stream synchronisation
+ *       at the end, plus one per round when recursive).  level_offsets
+ *       (host, n_level_offsets = levels + 1, BFS level boundaries) may be
+ *       NULL, in which case they are recomputed with one sync per level.
+ *   dot_refine_apply -> writes the new node words / payload / remap and the
+ *       new tree's level offsets (host array of max_levels + 1 entries).
  * Outputs of apply (device, caller-allocated to the sizes the plan reports):
  *   new_node[n_new] i32, new_sigma[n_new] f32, new_sh[n_new*sh_stride] f32
  *   (pool id == canonical id in the result; internal rows are zero),
@@ -135,15 +139,21 @@ typedef struct dot_refine_stats {
 int dot_refine_plan_create(const dot_tree_view* tree, const int32_t* pool_id,
                            const double* acc, int32_t use_sigma, double tau, double gamma,
                            int32_t recursive, int32_t use_threshold, double threshold,
+                           const int64_t* level_offsets, int32_t n_level_offsets,
                            dot_refine_plan** plan, dot_refine_stats* stats, void* stream);
-/* Merged-parent / split-leaf lists (canonical old indices, ascending).
+/* Merged-parent (by round, then canonical index) and split-leaf (ascending)
+ * lists in canonical old indices, computed on first call (synchronises).
  * Pointers stay valid until dot_refine_plan_destroy. */
-int dot_refine_plan_lists(const dot_refine_plan* plan, const int64_t** merge_parents,
+int dot_refine_plan_lists(dot_refine_plan* plan, const int64_t** merge_parents,
                           int64_t* n_merge, const int64_t** split_leaves, int64_t* n_split,
-                          const int32_t** merge_round);
+                          const int32_t** merge_round, void* stream);
 int dot_refine_apply(const dot_refine_plan* plan, const dot_tree_view* tree,
                      int32_t* new_node, float* new_sigma, float* new_sh,
-                     int64_t* src_index, uint8_t* src_kind, void* stream);
+                     int64_t* src_index, uint8_t* src_kind, int64_t* level_offsets_out,
+                     int32_t max_levels, int32_t* n_levels_out, void* stream);
+/* Per old canonical node, the prune round (1-based) that merged it, 0 = not
+ * merged: out[n_nodes] i32 device (optimizer-state remap, optim.py:89-104). */
+int dot_refine_plan_merge_rounds(const dot_refine_plan* plan, int32_t* out, void* stream);
 void dot_refine_plan_destroy(dot_refine_plan* plan);
 
 /* --- optimizer (optim.rmsprop_step, optim.py:107-135): sparse RMSProp over

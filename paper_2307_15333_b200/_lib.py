@@ -54,10 +54,12 @@ _SIGNATURES = {
     "dot_ray_keys": (c_i32, [c_void_p, c_void_p, c_void_p, c_i64, c_void_p, c_void_p]),
     "dot_ray_stats":(c_i32, [c_void_p, c_void_p, c_void_p, c_i64, c_f64, c_void_p, c_void_p]),
     "dot_refine_plan_create": (c_i32, [c_void_p, c_void_p, c_void_p, c_i32, c_f64, c_f64, c_i32, c_i32,
-                                       c_f64, c_void_p, c_void_p, c_void_p]),
-    "dot_refine_plan_lists": (c_i32, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
+                                       c_f64, c_void_p, c_i32, c_void_p, c_void_p, c_void_p]),
+    "dot_refine_plan_lists": (c_i32, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
+                                      c_void_p]),
     "dot_refine_apply": (c_i32, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
-                                 c_void_p]),
+                                 c_void_p, c_i32, c_void_p, c_void_p]),
+    "dot_refine_plan_merge_rounds": (c_i32, [c_void_p, c_void_p, c_void_p]),
     "dot_refine_plan_destroy": (None, [c_void_p]),
     "dot_rmsprop_step": (c_i32, [c_void_p, c_void_p, c_i32, c_i32, c_void_p, c_void_p, c_void_p,
                                  c_void_p, c_i32, c_void_p, c_i64, c_f64, c_f64, c_f64, c_f64,

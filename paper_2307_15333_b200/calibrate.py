@@ -59,9 +59,8 @@ class RefineRemap:
     old_pool_id: torch.Tensor | None  # int32 [n_old] pool ids (None = identity)
     src_index: torch.Tensor         # int64 [n_new]
     src_kind: torch.Tensor          # uint8 [n_new]
-    merge_parents: np.ndarray       # canonical old ids, (round, id) order
-    merge_round: np.ndarray
-    split_leaves: np.ndarray        # canonical old ids, ascending
+    merge_round: torch.Tensor       # int32 [n_old]: prune round that merged the node, 0 = none
+    rounds: int
 
 
 @dataclass
@@ -93,23 +92,40 @@ class _Plan:
         self.acc = acc
         stats = _lib.DotRefineStats()
         handle = ctypes.c_void_p()
+        off = np.ascontiguousarray(self.topo.level_offsets, dtype=np.int64)
         _lib.call("dot_refine_plan_create", ctypes.byref(self.view), _lib.ptr(self.topo.pool_id),
                   _lib.ptr(acc), int(use_sigma), float(tau), float(gamma), int(recursive),
-                  int(threshold is not None), float(threshold or 0.0), ctypes.byref(handle),
+                  int(threshold is not None), float(threshold or 0.0),
+                  off.ctypes.data_as(ctypes.c_void_p), int(off.size), ctypes.byref(handle),
                   ctypes.byref(stats), _lib.stream_ptr())
         self.handle = handle
         self.stats = stats
-        mp, nm, sl, ns, mr = (ctypes.POINTER(ctypes.c_int64)(), ctypes.c_int64(),
-                              ctypes.POINTER(ctypes.c_int64)(), ctypes.c_int64(),
-                              ctypes.POINTER(ctypes.c_int32)())
-        _lib.call("dot_refine_plan_lists", handle, ctypes.byref(mp), ctypes.byref(nm),
-                  ctypes.byref(sl), ctypes.byref(ns), ctypes.byref(mr))
-        self.merge_parents = np.ctypeslib.as_array(mp, (nm.value,)).copy() if nm.value else \
-            np.empty(0, np.int64)
-        self.merge_round = np.ctypeslib.as_array(mr, (nm.value,)).copy() if nm.value else \
-            np.empty(0, np.int32)
-        self.split_leaves = np.ctypeslib.as_array(sl, (ns.value,)).copy() if ns.value else \
-            np.empty(0, np.int64)
+        self._lists = None
+
+    def _fetch_lists(self):
+        if self._lists is None:
+            mp, nm, sl, ns, mr = (ctypes.POINTER(ctypes.c_int64)(), ctypes.c_int64(),
+                                  ctypes.POINTER(ctypes.c_int64)(), ctypes.c_int64(),
+                                  ctypes.POINTER(ctypes.c_int32)())
+            _lib.call("dot_refine_plan_lists", self.handle, ctypes.byref(mp), ctypes.byref(nm),
+                      ctypes.byref(sl), ctypes.byref(ns), ctypes.byref(mr), _lib.stream_ptr())
+            self._lists = (
+                np.ctypeslib.as_array(mp, (nm.value,)).copy() if nm.value else np.empty(0, np.int64),
+                np.ctypeslib.as_array(mr, (nm.value,)).copy() if nm.value else np.empty(0, np.int32),
+                np.ctypeslib.as_array(sl, (ns.value,)).copy() if ns.value else np.empty(0, np.int64))
+        return self._lists
+
+    @property
+    def merge_parents(self):
+        return self._fetch_lists()[0]
+
+    @property
+    def merge_round(self):
+        return self._fetch_lists()[1]
+
+    @property
+    def split_leaves(self):
+        return self._fetch_lists()[2]
 
     def pool_ids(self, canon: np.ndarray) -> np.ndarray:
         if self.topo.pool_id is None:
@@ -125,12 +141,19 @@ class _Plan:
         new_sh = torch.empty(n_new, tree.sh_stride, dtype=torch.float32, device=dev)
         src_index = torch.empty(n_new, dtype=torch.int64, device=dev)
         src_kind = torch.empty(n_new, dtype=torch.uint8, device=dev)
+        max_levels = 64
+        offs = np.zeros(max_levels + 1, dtype=np.int64)
+        nlev = ctypes.c_int32()
         _lib.call("dot_refine_apply", self.handle, ctypes.byref(self.view), _lib.ptr(new_node),
                   _lib.ptr(new_sigma), _lib.ptr(new_sh), _lib.ptr(src_index), _lib.ptr(src_kind),
+                  offs.ctypes.data_as(ctypes.c_void_p), max_levels, ctypes.byref(nlev),
                   _lib.stream_ptr())
-        remap = RefineRemap(self.topo.node, self.topo.pool_id, src_index, src_kind,
-                            self.merge_parents, self.merge_round, self.split_leaves)
-        tree._set_canonical(new_node, new_sigma, new_sh, int(self.stats.leaves_after))
+        mround = torch.empty(self.topo.n_nodes, dtype=torch.int32, device=dev)
+        _lib.call("dot_refine_plan_merge_rounds", self.handle, _lib.ptr(mround), _lib.stream_ptr())
+        remap = RefineRemap(self.topo.node, self.topo.pool_id, src_index, src_kind, mround,
+                            int(self.stats.recursion_rounds))
+        tree._set_canonical(new_node, new_sigma, new_sh, int(self.stats.leaves_after),
+                            offs[:nlev.value + 1].copy())
         return remap
 
     def close(self):
@@ -177,11 +200,14 @@ def _events(plan: _Plan, remap: RefineRemap | None) -> list:
     return ev
 
 
-def _run(tree, buffer, tau, gamma, recursive, threshold, apply=True, acc=None, events=True):
+def _run(tree, buffer, tau, gamma, recursive, threshold, apply=True, acc=None, events=True,
+         lists=False):
     a, use_sigma = _acc_for(buffer, acc)
     plan = _Plan(tree, a, use_sigma, tau, gamma, recursive, threshold)
     try:
         st = plan.stats
+        if lists or events:
+            plan._fetch_lists()  # before apply: the lists describe the old tree
         remap = plan.apply() if apply else None
         report = CalibrationReport(int(st.leaves_before), int(st.leaves_after),
                                    int(st.merges_applied), int(st.splits_applied),
@@ -198,7 +224,7 @@ def select_prune(tree, buffer: SignalBuffer, tau: float) -> np.ndarray:
     buffer.check_fresh()
     if tau < 0:
         raise ConfigError(f"tau must be >= 0, got {tau}")
-    _, plan = _run(tree, buffer, tau, 0.0, 0, None, apply=False, events=False)
+    _, plan = _run(tree, buffer, tau, 0.0, 0, None, apply=False, events=False, lists=True)
     return np.sort(plan.pool_ids(plan.merge_parents))
 
 
@@ -216,7 +242,8 @@ def select_sample(tree, buffer: SignalBuffer, gamma: float, threshold=None) -> n
     buffer.check_fresh()
     if not 0.0 <= gamma <= 1.0:
         raise ConfigError(f"gamma must be in [0, 1], got {gamma}")
-    _, plan = _run(tree, buffer, 0.0, gamma, -1, threshold, apply=False, events=False)
+    _, plan = _run(tree, buffer, 0.0, gamma, -1, threshold, apply=False, events=False,
+                   lists=True)
     return np.sort(plan.pool_ids(plan.split_leaves))
 
 

@@ -12,7 +12,8 @@
 //    signal > 0; top ceil(gamma * L) by (signal desc, pool id asc), or
 //    signal > threshold (calibrate.py:140-163).  Top-k is a radix select over
 //    the fp64 signal bits (8 x 8-bit digits) with a second radix select over
-//    pool ids for the ties at the k-th value.
+//    pool ids for the ties at the k-th value; every decision stays on the
+//    device (no host round trip between the passes).
 //  * the refined tree is emitted directly in canonical BFS order
 //    (scene_io.py:529-541), level by level: one flag scan per level decides
 //    which nodes are internal, children are either the old children (kept)
@@ -33,13 +34,19 @@ enum : uint8_t { ST_ALIVE = 1, ST_LEAF = 2, ST_MERGED = 4, ST_SPLIT = 8 };
 enum : uint8_t { K_KEPT = 0, K_MERGED = 1, K_NEWCHILD = 2, K_SPLITPARENT = 3 };
 
 constexpr int kTB = 256;
+constexpr int kMaxLevels = 64;
 
-static unsigned grid_for(int64_t n, int tb = kTB) {
-    return unsigned((n + tb - 1) / tb);
+static unsigned grid_for(int64_t n, int tb = kTB) { return unsigned((n + tb - 1) / tb); }
+
+static unsigned persistent_blocks() {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    return unsigned(sms * 8);
 }
 
 // ---------------------------------------------------------------------------
-// Small scan utility: exclusive scan of int32 values (3 phases, cub block scans).
+// Exclusive scan of int32 values (3 phases, cub block scans).
 
 constexpr int kScanItems = 4;
 constexpr int kScanTile = kTB * kScanItems;
@@ -59,7 +66,6 @@ __global__ void scan_reduce_kernel(const int32_t* __restrict__ in, int64_t n, in
 }
 
 __global__ void scan_sums_kernel(int64_t* __restrict__ sums, int64_t nb, int64_t* __restrict__ total) {
-    // single block, sequential chunks of kTB
     using BS = cub::BlockScan<int64_t, kTB>;
     __shared__ typename BS::TempStorage tmp;
     __shared__ int64_t carry;
@@ -98,10 +104,8 @@ __global__ void scan_apply_kernel(const int32_t* __restrict__ in, int64_t n,
     }
 }
 
-// Exclusive scan of in[0..n) into out; *d_total receives the sum.  Scratch
-// `sums` must hold ceil(n / kScanTile) + 1 entries.
-static int exclusive_scan(const int32_t* in, int64_t n, int64_t* out, int64_t* sums,
-                          int64_t* d_total, cudaStream_t s) {
+static int exclusive_scan(const int32_t* in, int64_t n, int64_t* out, int64_t* sums, int64_t* d_total,
+                          cudaStream_t s) {
     const int64_t nb = (n + kScanTile - 1) / kScanTile;
     if (nb == 0) return check_cuda(cudaMemsetAsync(d_total, 0, sizeof(int64_t), s), "memset");
     scan_reduce_kernel<<<unsigned(nb), kTB, 0, s>>>(in, n, sums);
@@ -111,13 +115,25 @@ static int exclusive_scan(const int32_t* in, int64_t n, int64_t* out, int64_t* s
 }
 
 // ---------------------------------------------------------------------------
-// Plan state
+// Device-side plan scalars (one struct, read back once at the end).
 
 struct RadixState {
     unsigned long long prefix;  // selected high bits so far
     unsigned long long mask;    // which bits are fixed
     long long remaining;        // how many still to take at/below the prefix
     long long eq_count;         // count of keys equal to the final prefix
+};
+
+struct PlanScalars {
+    unsigned long long n_internal;   // before prune
+    unsigned long long merges;       // all rounds
+    unsigned long long round_merges; // current round
+    unsigned long long leaves;       // post-prune leaf count
+    unsigned long long eligible;     // post-prune eligible leaves
+    long long k;                     // sample size
+    unsigned long long splits;
+    RadixState sig_rs;               // radix select over signal bits
+    RadixState tie_rs;               // radix select over (0xFFFFFFFF - pool id) among ties
 };
 
 }  // namespace dot
@@ -127,7 +143,6 @@ struct dot_refine_plan {
     int S = 0;
     int B = 0;
     bool use_sigma = false;
-    // device arrays (canonical old index space)
     uint8_t* state = nullptr;
     uint8_t* depth = nullptr;
     double* sig = nullptr;
@@ -137,9 +152,10 @@ struct dot_refine_plan {
     float* msig = nullptr;       // merged payload [M]
     float* msh = nullptr;        // merged SH [M * S]
     int64_t M = 0, K = 0;
-    int64_t* merge_list = nullptr;  // host, canonical ascending
-    int32_t* merge_round_h = nullptr;
-    int64_t* split_list = nullptr;  // host, canonical ascending
+    bool lists_ready = false;
+    std::vector<int64_t> merge_list;   // canonical, (round, index) order
+    std::vector<int32_t> merge_round_h;
+    std::vector<int64_t> split_list;   // canonical ascending
     dot_refine_stats stats{};
     int32_t max_depth = 0;
 };
@@ -150,16 +166,20 @@ __device__ __forceinline__ int32_t pid_of(const int32_t* pool_id, int64_t i) {
     return pool_id ? pool_id[i] : int32_t(i);
 }
 
-// state / depth / sig initialisation for one BFS level [s, e).
-__global__ void init_level_kernel(TreeDev T, int64_t s, int64_t e, int d, const double* __restrict__ acc,
+__constant__ int64_t c_level_off[kMaxLevels + 1];
+
+// state / depth / signal of every node; depth from the BFS level offsets.
+__global__ void init_nodes_kernel(TreeDev T, int64_t N, int n_levels, const double* __restrict__ acc,
                                   int use_sigma, uint8_t* __restrict__ state, uint8_t* __restrict__ depth,
                                   double* __restrict__ sig, int32_t* __restrict__ slot,
-                                  int32_t* __restrict__ mround, int* __restrict__ n_internal) {
-    const int64_t i = s + int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+                                  int32_t* __restrict__ mround, PlanScalars* __restrict__ ps) {
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     int internal = 0;
-    if (i < e) {
+    if (i < N) {
+        int dd = 0;
+        while (dd + 1 < n_levels && c_level_off[dd + 1] <= i) ++dd;
         const int32_t w = T.node[i];
-        depth[i] = uint8_t(d);
+        depth[i] = uint8_t(dd);
         slot[i] = -1;
         mround[i] = 0;
         if (w < 0) {
@@ -173,25 +193,39 @@ __global__ void init_level_kernel(TreeDev T, int64_t s, int64_t e, int d, const 
         }
     }
     internal = __syncthreads_count(internal);
-    if (threadIdx.x == 0 && internal) atomicAdd(n_internal, internal);
+    if (threadIdx.x == 0 && internal) atomicAdd(&ps->n_internal, (unsigned long long)internal);
+}
+
+// Warp-aggregated append of index i to list (count in *ctr).
+__device__ __forceinline__ void append(bool want, int64_t i, int64_t* list, unsigned long long* ctr) {
+    const unsigned m = __ballot_sync(0xffffffffu, want);
+    if (!m) return;
+    const unsigned lane = threadIdx.x & 31;
+    const int leader = __ffs(m) - 1;
+    unsigned long long base = 0;
+    if (int(lane) == leader) base = atomicAdd(ctr, (unsigned long long)__popc(m));
+    base = __shfl_sync(0xffffffffu, base, leader);
+    if (want) list[base + __popc(m & ((1u << lane) - 1u))] = i;
 }
 
 // Prune selection for one round: alive internal nodes whose 8 children are
-// leaves with signal <= tau.  Selected ids are appended (unordered).
+// leaves with signal <= tau.  Appended (unordered) to list.
 __global__ void prune_select_kernel(TreeDev T, int64_t N, double tau, const uint8_t* __restrict__ state,
                                     const double* __restrict__ sig, int64_t* __restrict__ list,
-                                    unsigned long long* __restrict__ count) {
+                                    PlanScalars* __restrict__ ps) {
     const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (i >= N) return;
-    const uint8_t st = state[i];
-    if ((st & ST_ALIVE) == 0 || (st & ST_LEAF)) return;
-    const int32_t c = T.node[i];
-    bool ok = true;
+    bool ok = false;
+    if (i < N) {
+        const uint8_t st = state[i];
+        if ((st & ST_ALIVE) && !(st & ST_LEAF)) {
+            const int32_t c = T.node[i];
+            ok = true;
 #pragma unroll
-    for (int o = 0; o < 8; ++o) {
-        if ((state[c + o] & ST_LEAF) == 0 || !(sig[c + o] <= tau)) ok = false;
+            for (int o = 0; o < 8; ++o)
+                if ((state[c + o] & ST_LEAF) == 0 || !(sig[c + o] <= tau)) ok = false;
+        }
     }
-    if (ok) list[atomicAdd(count, 1ull)] = i;
+    append(ok, i, list, &ps->round_merges);
 }
 
 __device__ __forceinline__ const float* leaf_row_sh(const TreeDev& T, const float* msh, const int32_t* slot,
@@ -206,73 +240,79 @@ __device__ __forceinline__ float leaf_sigma(const TreeDev& T, const float* msig,
     return T.sigma[~T.node[i]];
 }
 
-// Apply one round of merges: fp64 mean payload (sigma pairwise, SH
-// sequential), pairwise signal sum, topology flags.  One thread per parent
-// for sigma/signal/flags; SH columns handled by the column loop.
-__global__ void merge_apply_kernel(TreeDev T, const int64_t* __restrict__ list, int64_t m, int64_t slot_base,
-                                   int round, int use_sigma, uint8_t* __restrict__ state,
-                                   double* __restrict__ sig, int32_t* __restrict__ slot,
-                                   int32_t* __restrict__ mround, float* __restrict__ msig,
-                                   float* __restrict__ msh, int S, int nsh) {
-    const int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (j >= m) return;
-    const int64_t p = list[j];
-    const int32_t c = T.node[p];
-    const int64_t sl = slot_base + j;
-    double s8[8], q8[8];
+// Merged SH rows: one thread per (parent, 4-column quad); sequential fp64
+// sum over the 8 children in octant order, /8, round once.
+__global__ void merge_sh_kernel(TreeDev T, const int64_t* __restrict__ list, const PlanScalars* __restrict__ ps,
+                                int64_t slot_base, const uint8_t* __restrict__ state,
+                                const int32_t* __restrict__ slot, float* __restrict__ msh, int S, int nsh) {
+    const int64_t m = int64_t(ps->round_merges);
+    const int S4 = S / 4;
+    const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+    for (int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; t < m * S4; t += stride) {
+        const int64_t j = t / S4;
+        const int q = int(t - j * S4);
+        const int32_t c = T.node[list[j]];
+        double acc[4];
 #pragma unroll
-    for (int o = 0; o < 8; ++o) {
-        s8[o] = double(leaf_sigma(T, msig, slot, state, c + o));
-        q8[o] = sig[c + o];
-    }
-    const double ssum = ((s8[0] + s8[1]) + (s8[2] + s8[3])) + ((s8[4] + s8[5]) + (s8[6] + s8[7]));
-    const float mean_sigma = float(ssum / 8.0);
-    msig[sl] = mean_sigma;
-    const double qsum = ((q8[0] + q8[1]) + (q8[2] + q8[3])) + ((q8[4] + q8[5]) + (q8[6] + q8[7]));
-    const float* rows[8];
-#pragma unroll
-    for (int o = 0; o < 8; ++o) rows[o] = leaf_row_sh(T, msh, slot, state, c + o, S);
-    float* out = msh + sl * S;
-    for (int k = 0; k < S; ++k) {
-        if (k < nsh) {
-            double acc = double(rows[0][k]);
-#pragma unroll
-            for (int o = 1; o < 8; ++o) acc = acc + double(rows[o][k]);
-            out[k] = float(acc / 8.0);
-        } else {
-            out[k] = 0.f;
+        for (int o = 0; o < 8; ++o) {
+            const float4 v = reinterpret_cast<const float4*>(leaf_row_sh(T, msh, slot, state, c + o, S))[q];
+            if (o == 0) {
+                acc[0] = v.x; acc[1] = v.y; acc[2] = v.z; acc[3] = v.w;
+            } else {
+                acc[0] = acc[0] + double(v.x);
+                acc[1] = acc[1] + double(v.y);
+                acc[2] = acc[2] + double(v.z);
+                acc[3] = acc[3] + double(v.w);
+            }
         }
+        float4 out;
+        out.x = 4 * q + 0 < nsh ? float(acc[0] / 8.0) : 0.f;
+        out.y = 4 * q + 1 < nsh ? float(acc[1] / 8.0) : 0.f;
+        out.z = 4 * q + 2 < nsh ? float(acc[2] / 8.0) : 0.f;
+        out.w = 4 * q + 3 < nsh ? float(acc[3] / 8.0) : 0.f;
+        reinterpret_cast<float4*>(msh + (slot_base + j) * S)[q] = out;
     }
-    // children leave the topology; parent becomes a (merged) leaf
-#pragma unroll
-    for (int o = 0; o < 8; ++o) state[c + o] &= uint8_t(~ST_ALIVE);
-    sig[p] = use_sigma ? double(mean_sigma) : qsum;
-    slot[p] = int32_t(sl);
-    mround[p] = round;
-    state[p] |= ST_LEAF | ST_MERGED;
 }
 
-// Leaf / eligibility counts on the post-prune topology.
-__global__ void count_leaves_kernel(int64_t N, const uint8_t* __restrict__ state,
-                                    const uint8_t* __restrict__ depth, const double* __restrict__ sig,
-                                    int max_depth, int use_thr, double thr,
-                                    unsigned long long* __restrict__ counts) {
-    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    int leaf = 0, elig = 0;
-    if (i < N) {
-        const uint8_t st = state[i];
-        if ((st & ST_ALIVE) && (st & ST_LEAF)) {
-            leaf = 1;
-            const double s = sig[i];
-            if (depth[i] < max_depth && s > 0.0 && (!use_thr || s > thr)) elig = 1;
+// Merged sigma (pairwise) and signal (pairwise), then the topology flags.
+__global__ void merge_finish_kernel(TreeDev T, const int64_t* __restrict__ list, PlanScalars* __restrict__ ps,
+                                    int64_t slot_base, int round, int use_sigma, uint8_t* __restrict__ state,
+                                    double* __restrict__ sig, int32_t* __restrict__ slot,
+                                    int32_t* __restrict__ mround, float* __restrict__ msig) {
+    const int64_t m = int64_t(ps->round_merges);
+    const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+    for (int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; j < m; j += stride) {
+        const int64_t p = list[j];
+        const int32_t c = T.node[p];
+        double s8[8], q8[8];
+#pragma unroll
+        for (int o = 0; o < 8; ++o) {
+            s8[o] = double(leaf_sigma(T, msig, slot, state, c + o));
+            q8[o] = sig[c + o];
         }
+        const double ssum = ((s8[0] + s8[1]) + (s8[2] + s8[3])) + ((s8[4] + s8[5]) + (s8[6] + s8[7]));
+        const float mean_sigma = float(ssum / 8.0);
+        const double qsum = ((q8[0] + q8[1]) + (q8[2] + q8[3])) + ((q8[4] + q8[5]) + (q8[6] + q8[7]));
+        msig[slot_base + j] = mean_sigma;
+        sig[p] = use_sigma ? double(mean_sigma) : qsum;
+        mround[p] = round;
     }
-    leaf = __syncthreads_count(leaf);
-    elig = __syncthreads_count(elig);
-    if (threadIdx.x == 0) {
-        if (leaf) atomicAdd(counts + 0, (unsigned long long)leaf);
-        if (elig) atomicAdd(counts + 1, (unsigned long long)elig);
+}
+
+// Separate pass so no thread flips a flag another thread of the same round reads.
+__global__ void merge_flags_kernel(TreeDev T, const int64_t* __restrict__ list, PlanScalars* __restrict__ ps,
+                                   int64_t slot_base, uint8_t* __restrict__ state, int32_t* __restrict__ slot) {
+    const int64_t m = int64_t(ps->round_merges);
+    const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+    for (int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; j < m; j += stride) {
+        const int64_t p = list[j];
+        const int32_t c = T.node[p];
+#pragma unroll
+        for (int o = 0; o < 8; ++o) state[c + o] &= uint8_t(~ST_ALIVE);
+        slot[p] = int32_t(slot_base + j);
+        state[p] |= ST_LEAF | ST_MERGED;
     }
+    if (blockIdx.x == 0 && threadIdx.x == 0) ps->merges += ps->round_merges;
 }
 
 __device__ __forceinline__ unsigned long long sample_key(int64_t i, const uint8_t* state,
@@ -285,46 +325,102 @@ __device__ __forceinline__ unsigned long long sample_key(int64_t i, const uint8_
     return (unsigned long long)__double_as_longlong(s);  // positive doubles order as uint64
 }
 
-// Histogram of digit `shift` over keys matching the current prefix.
+// Leaf / eligibility counts on the post-prune topology.
+__global__ void count_leaves_kernel(int64_t N, const uint8_t* __restrict__ state,
+                                    const uint8_t* __restrict__ depth, const double* __restrict__ sig,
+                                    int max_depth, PlanScalars* __restrict__ ps) {
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    int leaf = 0, elig = 0;
+    if (i < N) {
+        const uint8_t st = state[i];
+        if ((st & ST_ALIVE) && (st & ST_LEAF)) {
+            leaf = 1;
+            elig = sample_key(i, state, depth, sig, max_depth) != 0ull;
+        }
+    }
+    leaf = __syncthreads_count(leaf);
+    elig = __syncthreads_count(elig);
+    if (threadIdx.x == 0) {
+        if (leaf) atomicAdd(&ps->leaves, (unsigned long long)leaf);
+        if (elig) atomicAdd(&ps->eligible, (unsigned long long)elig);
+    }
+}
+
+// k = min(ceil(gamma * L), #eligible) (calibrate.py:159), both radix states primed.
+__global__ void sample_k_kernel(PlanScalars* ps, double gamma) {
+    long long k = (long long)ceil(gamma * double(ps->leaves));
+    if (k > (long long)ps->eligible) k = (long long)ps->eligible;
+    ps->k = k;
+    ps->sig_rs = RadixState{0ull, 0ull, k, 0};
+    ps->tie_rs = RadixState{0ull, 0xFFFFFFFF00000000ull, 0, 0};
+}
+
+// Histogram of digit `shift` over keys matching the current prefix, with
+// warp-aggregated shared-memory increments (most keys share the high digits).
 // mode 0: signal keys; mode 1: tie keys (0xFFFFFFFF - pool id) among keys == K*.
 __global__ void radix_hist_kernel(int64_t N, int mode, const uint8_t* __restrict__ state,
                                   const uint8_t* __restrict__ depth, const double* __restrict__ sig,
                                   int max_depth, const int32_t* __restrict__ pool_id,
-                                  const RadixState* __restrict__ rs, const RadixState* __restrict__ rs0,
-                                  int shift, unsigned int* __restrict__ hist) {
+                                  const PlanScalars* __restrict__ ps, int shift, unsigned int* __restrict__ hist) {
     __shared__ unsigned int h[256];
+    const RadixState rs = mode == 0 ? ps->sig_rs : ps->tie_rs;
+    const bool skip = mode == 0 ? ps->k <= 0 : (ps->k <= 0 || ps->sig_rs.remaining == ps->sig_rs.eq_count);
+    if (skip) return;
     for (int b = threadIdx.x; b < 256; b += blockDim.x) h[b] = 0;
     __syncthreads();
-    const unsigned long long prefix = rs->prefix, mask = rs->mask;
+    const unsigned long long kstar = ps->sig_rs.prefix;
     const int64_t stride = int64_t(gridDim.x) * blockDim.x;
-    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < N; i += stride) {
-        unsigned long long key = sample_key(i, state, depth, sig, max_depth);
-        if (key == 0ull) continue;
-        if (mode == 1) {
-            if (key != rs0->prefix) continue;
-            key = 0xFFFFFFFFull - (unsigned long long)(uint32_t)pid_of(pool_id, i);
+    const int64_t n_iter = (N + stride - 1) / stride;
+    for (int64_t it = 0; it < n_iter; ++it) {
+        const int64_t i = it * stride + int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+        bool take = false;
+        unsigned bin = 0;
+        if (i < N) {
+            unsigned long long key = sample_key(i, state, depth, sig, max_depth);
+            if (key != 0ull) {
+                if (mode == 1) {
+                    if (key == kstar) {
+                        key = 0xFFFFFFFFull - (unsigned long long)(uint32_t)pid_of(pool_id, i);
+                        take = (key & rs.mask) == rs.prefix;
+                    }
+                } else {
+                    take = (key & rs.mask) == rs.prefix;
+                }
+                bin = unsigned((key >> shift) & 0xFF);
+            }
         }
-        if ((key & mask) != prefix) continue;
-        atomicAdd(&h[(key >> shift) & 0xFF], 1u);
+        const unsigned active = __ballot_sync(0xffffffffu, take);
+        if (take) {
+            const unsigned peers = __match_any_sync(active, bin);
+            if ((threadIdx.x & 31) == unsigned(__ffs(peers) - 1)) atomicAdd(&h[bin], unsigned(__popc(peers)));
+        }
     }
     __syncthreads();
     for (int b = threadIdx.x; b < 256; b += blockDim.x)
         if (h[b]) atomicAdd(hist + b, h[b]);
 }
 
-__global__ void radix_pick_kernel(RadixState* rs, unsigned int* hist, int shift) {
-    // one thread: walk digits from the top until `remaining` falls inside a bin
+__global__ void radix_pick_kernel(PlanScalars* ps, int mode, unsigned int* hist, int shift) {
     if (threadIdx.x != 0) return;
-    long long rem = rs->remaining;
-    int digit = 0;
-    for (int b = 255; b >= 0; --b) {
-        const long long c = hist[b];
-        if (rem <= c) { digit = b; rs->eq_count = c; break; }
-        rem -= c;
+    RadixState& rs = mode == 0 ? ps->sig_rs : ps->tie_rs;
+    const bool skip = mode == 0 ? ps->k <= 0 : (ps->k <= 0 || ps->sig_rs.remaining == ps->sig_rs.eq_count);
+    if (!skip) {
+        if (mode == 1 && shift == 24) rs.remaining = ps->sig_rs.remaining;
+        long long rem = rs.remaining;
+        int digit = 0;
+        for (int b = 255; b >= 0; --b) {
+            const long long c = hist[b];
+            if (rem <= c) {
+                digit = b;
+                rs.eq_count = c;
+                break;
+            }
+            rem -= c;
+        }
+        rs.remaining = rem;
+        rs.prefix |= (unsigned long long)digit << shift;
+        rs.mask |= 0xFFull << shift;
     }
-    rs->remaining = rem;
-    rs->prefix |= (unsigned long long)digit << shift;
-    rs->mask |= 0xFFull << shift;
     for (int b = 0; b < 256; ++b) hist[b] = 0;
 }
 
@@ -333,30 +429,43 @@ __global__ void radix_pick_kernel(RadixState* rs, unsigned int* hist, int shift)
 __global__ void mark_split_kernel(int64_t N, int mode, uint8_t* __restrict__ state,
                                   const uint8_t* __restrict__ depth, const double* __restrict__ sig,
                                   int max_depth, const int32_t* __restrict__ pool_id, double thr,
-                                  unsigned long long kstar, int take_all_ties,
-                                  unsigned long long tstar) {
+                                  PlanScalars* __restrict__ ps) {
     const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (i >= N) return;
-    const unsigned long long key = sample_key(i, state, depth, sig, max_depth);
-    if (key == 0ull) return;
-    bool sel;
-    if (mode == 2) {
-        sel = sig[i] > thr;
-    } else {
-        sel = key > kstar;
-        if (key == kstar) {
-            const unsigned long long tk = 0xFFFFFFFFull - (unsigned long long)(uint32_t)pid_of(pool_id, i);
-            sel = take_all_ties || tk >= tstar;
+    bool sel = false;
+    if (i < N) {
+        const unsigned long long key = sample_key(i, state, depth, sig, max_depth);
+        if (key != 0ull) {
+            if (mode == 2) {
+                sel = sig[i] > thr;
+            } else if (ps->k > 0) {
+                const unsigned long long kstar = ps->sig_rs.prefix;
+                sel = key > kstar;
+                if (key == kstar) {
+                    const bool all = ps->sig_rs.remaining == ps->sig_rs.eq_count;
+                    const unsigned long long tk =
+                        0xFFFFFFFFull - (unsigned long long)(uint32_t)pid_of(pool_id, i);
+                    sel = all || tk >= ps->tie_rs.prefix;
+                }
+            }
         }
+        if (sel) state[i] |= ST_SPLIT;
     }
-    if (sel) state[i] |= ST_SPLIT;
+    const int cnt = __syncthreads_count(sel);
+    if (threadIdx.x == 0 && cnt) atomicAdd(&ps->splits, (unsigned long long)cnt);
 }
 
-__global__ void collect_kernel(int64_t N, const uint8_t* __restrict__ state, uint8_t bit,
-                               int64_t* __restrict__ list, unsigned long long* __restrict__ count) {
+// Ordered compaction flags for the on-demand event lists.
+__global__ void flag_kernel(int64_t N, const uint8_t* __restrict__ state, const int32_t* __restrict__ mround,
+                            int which, int32_t* __restrict__ flags) {
     const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= N) return;
-    if (state[i] & bit) list[atomicAdd(count, 1ull)] = i;
+    flags[i] = which == 0 ? (mround[i] > 0) : ((state[i] & ST_SPLIT) != 0);
+}
+
+__global__ void compact_kernel(int64_t N, const int32_t* __restrict__ flags, const int64_t* __restrict__ rank,
+                               int64_t* __restrict__ out) {
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < N && flags[i]) out[rank[i]] = i;
 }
 
 // ---------------------------------------------------------------------------
@@ -408,10 +517,10 @@ __global__ void level_emit_kernel(TreeDev T, int64_t m, int64_t base, int64_t ne
 
 // Payload gather: one thread per (new node, float4 column).
 __global__ void payload_kernel(TreeDev T, int64_t n_new, int S4, const int64_t* __restrict__ src_index,
-                               const uint8_t* __restrict__ src_kind, const uint8_t* __restrict__ state,
-                               const int32_t* __restrict__ slot, const float* __restrict__ msig,
-                               const float* __restrict__ msh, const int32_t* __restrict__ new_node,
-                               float* __restrict__ new_sigma, float4* __restrict__ new_sh) {
+                               const uint8_t* __restrict__ state, const int32_t* __restrict__ slot,
+                               const float* __restrict__ msig, const float* __restrict__ msh,
+                               const int32_t* __restrict__ new_node, float* __restrict__ new_sigma,
+                               float4* __restrict__ new_sh) {
     const int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (t >= n_new * S4) return;
     const int64_t i = t / S4;
@@ -454,18 +563,41 @@ static void plan_free(dot_refine_plan* p) {
     cudaFree(p->mround);
     cudaFree(p->msig);
     cudaFree(p->msh);
-    delete[] p->merge_list;
-    delete[] p->merge_round_h;
-    delete[] p->split_list;
     delete p;
+}
+
+// Level offsets of a canonical node table (one sync per level; only used
+// when the caller does not already know them).
+static int level_offsets_of(const TreeDev& T, int64_t N, std::vector<int64_t>& off, cudaStream_t s) {
+    off.assign(1, 0);
+    int64_t lo = 0, hi = 1;
+    std::vector<int32_t> w;
+    while (lo < hi) {
+        off.push_back(hi);
+        if (int(off.size()) > kMaxLevels) return set_error(DOT_BAD_ARG, "tree deeper than %d levels", kMaxLevels);
+        w.resize(size_t(hi - lo));
+        int st = check_cuda(cudaMemcpyAsync(w.data(), T.node + lo, (hi - lo) * sizeof(int32_t),
+                                            cudaMemcpyDeviceToHost, s), "memcpy");
+        if (st == DOT_OK) st = check_cuda(cudaStreamSynchronize(s), "sync");
+        if (st) return st;
+        int64_t n_int = 0;
+        for (int32_t x : w) n_int += x >= 0;
+        lo = hi;
+        hi += 8 * n_int;
+    }
+    if (hi != N)
+        return set_error(DOT_BAD_ARG, "node table is not a canonical BFS tree (%lld reachable of %lld)",
+                         (long long)hi, (long long)N);
+    return DOT_OK;
 }
 
 extern "C" {
 
 int dot_refine_plan_create(const dot_tree_view* tree, const int32_t* pool_id, const double* acc,
                            int32_t use_sigma, double tau, double gamma, int32_t recursive,
-                           int32_t use_threshold, double threshold, dot_refine_plan** out,
-                           dot_refine_stats* stats, void* stream) {
+                           int32_t use_threshold, double threshold, const int64_t* level_offsets,
+                           int32_t n_level_offsets, dot_refine_plan** out, dot_refine_stats* stats,
+                           void* stream) {
     if (!tree || !out || !stats) return set_error(DOT_BAD_ARG, "NULL argument");
     if (!use_sigma && !acc) return set_error(DOT_BAD_ARG, "acc must not be NULL for the Q target");
     if (tau < 0.0) return set_error(DOT_BAD_ARG, "tau must be >= 0, got %g", tau);
@@ -474,6 +606,16 @@ int dot_refine_plan_create(const dot_tree_view* tree, const int32_t* pool_id, co
     const TreeDev T = make_tree(*tree);
     const int64_t N = tree->n_nodes;
     const int S = tree->sh_stride, B = tree->basis_count;
+    std::vector<int64_t> off;
+    int st = DOT_OK;
+    if (level_offsets && n_level_offsets >= 2) {
+        if (n_level_offsets - 1 > kMaxLevels) return set_error(DOT_BAD_ARG, "too many levels");
+        off.assign(level_offsets, level_offsets + n_level_offsets);
+        if (off.front() != 0 || off.back() != N) return set_error(DOT_BAD_ARG, "level offsets do not match the tree");
+    } else if ((st = level_offsets_of(T, N, off, s)) != DOT_OK) {
+        return st;
+    }
+    const int n_levels = int(off.size()) - 1;
     dot_refine_plan* p = new dot_refine_plan();
     p->N = N;
     p->S = S;
@@ -481,192 +623,95 @@ int dot_refine_plan_create(const dot_tree_view* tree, const int32_t* pool_id, co
     p->use_sigma = use_sigma != 0;
     p->pool_id = pool_id;
     p->max_depth = tree->max_depth;
-    int st = DOT_OK;
-#define TRY(x) do { if ((st = (x)) != DOT_OK) { plan_free(p); return st; } } while (0)
+    int64_t* d_list = nullptr;
+    unsigned int* d_hist = nullptr;
+    PlanScalars* d_ps = nullptr;
+    auto cleanup_tmp = [&]() {
+        cudaFreeAsync(d_list, s);
+        cudaFreeAsync(d_hist, s);
+        cudaFreeAsync(d_ps, s);
+    };
+#define TRY(x) do { if ((st = (x)) != DOT_OK) { cleanup_tmp(); plan_free(p); return st; } } while (0)
+    const int64_t mcap = N / 8 + 1;  // merges never exceed the internal-node count
     TRY(dalloc(&p->state, N, s));
     TRY(dalloc(&p->depth, N, s));
     TRY(dalloc(&p->sig, N, s));
     TRY(dalloc(&p->slot, N, s));
     TRY(dalloc(&p->mround, N, s));
-    int64_t* d_list = nullptr;
-    unsigned long long* d_cnt = nullptr;
-    int* d_int = nullptr;
-    unsigned int* d_hist = nullptr;
-    RadixState* d_rs = nullptr;
-    TRY(dalloc(&d_list, N, s));
-    TRY(dalloc(&d_cnt, 4, s));
-    TRY(dalloc(&d_int, 1, s));
+    TRY(dalloc(&p->msig, mcap, s));
+    TRY(dalloc(&p->msh, mcap * S, s));
+    TRY(dalloc(&d_list, mcap, s));
     TRY(dalloc(&d_hist, 256, s));
-    TRY(dalloc(&d_rs, 2, s));
-    auto cleanup_tmp = [&]() {
-        cudaFreeAsync(d_list, s);
-        cudaFreeAsync(d_cnt, s);
-        cudaFreeAsync(d_int, s);
-        cudaFreeAsync(d_hist, s);
-        cudaFreeAsync(d_rs, s);
-    };
-#undef TRY
-#define TRY(x) do { if ((st = (x)) != DOT_OK) { cleanup_tmp(); plan_free(p); return st; } } while (0)
+    TRY(dalloc(&d_ps, 1, s));
+    TRY(check_cuda(cudaMemsetAsync(d_ps, 0, sizeof(PlanScalars), s), "memset"));
+    TRY(check_cuda(cudaMemsetAsync(d_hist, 0, 256 * sizeof(unsigned int), s), "memset"));
+    TRY(check_cuda(cudaMemcpyToSymbolAsync(c_level_off, off.data(), off.size() * sizeof(int64_t), 0,
+                                           cudaMemcpyHostToDevice, s), "memcpy"));
+    init_nodes_kernel<<<grid_for(N), kTB, 0, s>>>(T, N, n_levels, acc, use_sigma, p->state, p->depth, p->sig,
+                                                  p->slot, p->mround, d_ps);
+    TRY(check_launch("init_nodes_kernel"));
 
-    // --- levels: depth, state, signal
-    int64_t lo = 0, hi = 1;
-    int d = 0;
-    int64_t leaves_before = 0;
-    while (lo < hi) {
-        if (d > 255) TRY(set_error(DOT_BAD_ARG, "tree deeper than 255 levels"));
-        TRY(check_cuda(cudaMemsetAsync(d_int, 0, sizeof(int), s), "memset"));
-        init_level_kernel<<<grid_for(hi - lo), kTB, 0, s>>>(T, lo, hi, d, acc, use_sigma, p->state, p->depth,
-                                                            p->sig, p->slot, p->mround, d_int);
-        TRY(check_launch("init_level_kernel"));
-        int n_int = 0;
-        TRY(check_cuda(cudaMemcpyAsync(&n_int, d_int, sizeof(int), cudaMemcpyDeviceToHost, s), "memcpy"));
-        TRY(check_cuda(cudaStreamSynchronize(s), "sync"));
-        leaves_before += (hi - lo) - n_int;
-        lo = hi;
-        hi = hi + 8 * int64_t(n_int);
-        ++d;
-    }
-    if (hi != N) TRY(set_error(DOT_BAD_ARG, "node table is not a canonical BFS tree (%lld reachable of %lld)",
-                               (long long)hi, (long long)N));
-
-    // --- prune rounds
-    std::vector<int64_t> merges;
-    std::vector<int32_t> merge_rounds;
+    // --- prune rounds (device-resident; recursion needs one read per round)
+    const unsigned pb = persistent_blocks();
     int rounds = 0;
-    // merged payload buffer grows per round
-    int64_t mcap = 0;
-    for (; recursive >= 0;) {  // recursive < 0: sample only, no prune
-        TRY(check_cuda(cudaMemsetAsync(d_cnt, 0, sizeof(unsigned long long), s), "memset"));
-        prune_select_kernel<<<grid_for(N), kTB, 0, s>>>(T, N, tau, p->state, p->sig, d_list, d_cnt);
-        TRY(check_launch("prune_select_kernel"));
+    unsigned long long merges_done = 0;
+    for (int round = 1; recursive >= 0; ++round) {  // recursive < 0: sample only
+        TRY(check_cuda(cudaMemsetAsync(&d_ps->round_merges, 0, sizeof(unsigned long long), s), "memset"));
+        prune_select_kernel<<<grid_for(N), kTB, 0, s>>>(T, N, tau, p->state, p->sig, d_list, d_ps);
+        const int64_t slot_base = int64_t(merges_done);
+        merge_sh_kernel<<<pb, kTB, 0, s>>>(T, d_list, d_ps, slot_base, p->state, p->slot, p->msh, S, 3 * B);
+        merge_finish_kernel<<<pb, kTB, 0, s>>>(T, d_list, d_ps, slot_base, round, use_sigma, p->state, p->sig,
+                                               p->slot, p->mround, p->msig);
+        merge_flags_kernel<<<pb, kTB, 0, s>>>(T, d_list, d_ps, slot_base, p->state, p->slot);
+        TRY(check_launch("prune round"));
+        if (!recursive) {  // one-shot: the count is read with the final scalars below
+            rounds = -1;
+            break;
+        }
         unsigned long long m = 0;
-        TRY(check_cuda(cudaMemcpyAsync(&m, d_cnt, sizeof(m), cudaMemcpyDeviceToHost, s), "memcpy"));
+        TRY(check_cuda(cudaMemcpyAsync(&m, &d_ps->round_merges, sizeof(m), cudaMemcpyDeviceToHost, s), "memcpy"));
         TRY(check_cuda(cudaStreamSynchronize(s), "sync"));
         if (m == 0) break;
-        const int64_t base = int64_t(merges.size());
-        if (base + int64_t(m) > mcap) {
-            const int64_t ncap = std::max<int64_t>(2 * mcap, base + int64_t(m));
-            float *ns = nullptr, *nh = nullptr;
-            TRY(dalloc(&ns, ncap, s));
-            TRY(dalloc(&nh, ncap * S, s));
-            if (base) {
-                TRY(check_cuda(cudaMemcpyAsync(ns, p->msig, base * sizeof(float), cudaMemcpyDeviceToDevice, s), "copy"));
-                TRY(check_cuda(cudaMemcpyAsync(nh, p->msh, base * S * sizeof(float), cudaMemcpyDeviceToDevice, s), "copy"));
-            }
-            if (p->msig) cudaFreeAsync(p->msig, s);
-            if (p->msh) cudaFreeAsync(p->msh, s);
-            p->msig = ns;
-            p->msh = nh;
-            mcap = ncap;
-        }
-        ++rounds;
-        merge_apply_kernel<<<grid_for(int64_t(m)), kTB, 0, s>>>(T, d_list, int64_t(m), base, rounds, use_sigma,
-                                                                 p->state, p->sig, p->slot, p->mround,
-                                                                 p->msig, p->msh, S, 3 * B);
-        TRY(check_launch("merge_apply_kernel"));
-        std::vector<int64_t> h(m);
-        TRY(check_cuda(cudaMemcpyAsync(h.data(), d_list, m * sizeof(int64_t), cudaMemcpyDeviceToHost, s), "memcpy"));
-        TRY(check_cuda(cudaStreamSynchronize(s), "sync"));
-        merges.insert(merges.end(), h.begin(), h.end());
-        merge_rounds.insert(merge_rounds.end(), m, rounds);
-        if (!recursive) break;
+        merges_done += m;
+        rounds = round;
     }
-    const int64_t M = int64_t(merges.size());
 
-    // --- sample selection
-    TRY(check_cuda(cudaMemsetAsync(d_cnt, 0, 4 * sizeof(unsigned long long), s), "memset"));
-    count_leaves_kernel<<<grid_for(N), kTB, 0, s>>>(N, p->state, p->depth, p->sig, tree->max_depth,
-                                                    use_threshold, threshold, d_cnt);
+    // --- sample selection, all decisions on the device
+    count_leaves_kernel<<<grid_for(N), kTB, 0, s>>>(N, p->state, p->depth, p->sig, tree->max_depth, d_ps);
     TRY(check_launch("count_leaves_kernel"));
-    unsigned long long cnt[2] = {0, 0};
-    TRY(check_cuda(cudaMemcpyAsync(cnt, d_cnt, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s), "memcpy"));
-    TRY(check_cuda(cudaStreamSynchronize(s), "sync"));
-    const int64_t L = int64_t(cnt[0]), n_elig = int64_t(cnt[1]);
-    int64_t k = 0;
     const bool do_sample = use_threshold || gamma > 0.0;
     if (do_sample) {
         if (use_threshold) {
-            k = n_elig;
-            if (k > 0) {
-                mark_split_kernel<<<grid_for(N), kTB, 0, s>>>(N, 2, p->state, p->depth, p->sig, tree->max_depth,
-                                                              pool_id, threshold, 0ull, 0, 0ull);
-                TRY(check_launch("mark_split_kernel"));
-            }
+            mark_split_kernel<<<grid_for(N), kTB, 0, s>>>(N, 2, p->state, p->depth, p->sig, tree->max_depth,
+                                                          pool_id, threshold, d_ps);
         } else {
-            k = std::min<int64_t>(int64_t(std::ceil(gamma * double(L))), n_elig);
-            if (k > 0) {
-                const int hist_grid = 4 * 148;
-                RadixState r0{0ull, 0ull, (long long)k, 0};
-                TRY(check_cuda(cudaMemcpyAsync(d_rs, &r0, sizeof(r0), cudaMemcpyHostToDevice, s), "memcpy"));
-                TRY(check_cuda(cudaMemsetAsync(d_hist, 0, 256 * sizeof(unsigned int), s), "memset"));
-                for (int shift = 56; shift >= 0; shift -= 8) {
-                    radix_hist_kernel<<<hist_grid, kTB, 0, s>>>(N, 0, p->state, p->depth, p->sig, tree->max_depth,
-                                                                pool_id, d_rs, d_rs, shift, d_hist);
-                    radix_pick_kernel<<<1, 32, 0, s>>>(d_rs, d_hist, shift);
-                }
-                TRY(check_launch("radix select (signal)"));
-                RadixState r1;
-                TRY(check_cuda(cudaMemcpyAsync(&r1, d_rs, sizeof(r1), cudaMemcpyDeviceToHost, s), "memcpy"));
-                TRY(check_cuda(cudaStreamSynchronize(s), "sync"));
-                const unsigned long long kstar = r1.prefix;
-                const bool all_ties = r1.remaining == r1.eq_count;
-                unsigned long long tstar = 0ull;
-                if (!all_ties) {
-                    RadixState t0{0ull, 0xFFFFFFFF00000000ull, r1.remaining, 0};
-                    TRY(check_cuda(cudaMemcpyAsync(d_rs + 1, &t0, sizeof(t0), cudaMemcpyHostToDevice, s), "memcpy"));
-                    for (int shift = 24; shift >= 0; shift -= 8) {
-                        radix_hist_kernel<<<hist_grid, kTB, 0, s>>>(N, 1, p->state, p->depth, p->sig,
-                                                                    tree->max_depth, pool_id, d_rs + 1, d_rs,
-                                                                    shift, d_hist);
-                        radix_pick_kernel<<<1, 32, 0, s>>>(d_rs + 1, d_hist, shift);
-                    }
-                    TRY(check_launch("radix select (ties)"));
-                    RadixState t1;
-                    TRY(check_cuda(cudaMemcpyAsync(&t1, d_rs + 1, sizeof(t1), cudaMemcpyDeviceToHost, s), "memcpy"));
-                    TRY(check_cuda(cudaStreamSynchronize(s), "sync"));
-                    tstar = t1.prefix;
-                }
-                mark_split_kernel<<<grid_for(N), kTB, 0, s>>>(N, 0, p->state, p->depth, p->sig, tree->max_depth,
-                                                              pool_id, 0.0, kstar, all_ties ? 1 : 0, tstar);
-                TRY(check_launch("mark_split_kernel"));
+            sample_k_kernel<<<1, 1, 0, s>>>(d_ps, gamma);
+            for (int shift = 56; shift >= 0; shift -= 8) {
+                radix_hist_kernel<<<pb, kTB, 0, s>>>(N, 0, p->state, p->depth, p->sig, tree->max_depth, pool_id,
+                                                     d_ps, shift, d_hist);
+                radix_pick_kernel<<<1, 32, 0, s>>>(d_ps, 0, d_hist, shift);
             }
+            for (int shift = 24; shift >= 0; shift -= 8) {
+                radix_hist_kernel<<<pb, kTB, 0, s>>>(N, 1, p->state, p->depth, p->sig, tree->max_depth, pool_id,
+                                                     d_ps, shift, d_hist);
+                radix_pick_kernel<<<1, 32, 0, s>>>(d_ps, 1, d_hist, shift);
+            }
+            mark_split_kernel<<<grid_for(N), kTB, 0, s>>>(N, 0, p->state, p->depth, p->sig, tree->max_depth,
+                                                          pool_id, 0.0, d_ps);
         }
+        TRY(check_launch("sample selection"));
     }
-    // collect split list (ascending canonical index)
-    int64_t K = 0;
-    std::vector<int64_t> splits;
-    if (k > 0) {
-        TRY(check_cuda(cudaMemsetAsync(d_cnt, 0, sizeof(unsigned long long), s), "memset"));
-        collect_kernel<<<grid_for(N), kTB, 0, s>>>(N, p->state, ST_SPLIT, d_list, d_cnt);
-        TRY(check_launch("collect_kernel"));
-        unsigned long long kk = 0;
-        TRY(check_cuda(cudaMemcpyAsync(&kk, d_cnt, sizeof(kk), cudaMemcpyDeviceToHost, s), "memcpy"));
-        TRY(check_cuda(cudaStreamSynchronize(s), "sync"));
-        K = int64_t(kk);
-        splits.resize(K);
-        TRY(check_cuda(cudaMemcpyAsync(splits.data(), d_list, K * sizeof(int64_t), cudaMemcpyDeviceToHost, s), "memcpy"));
-        TRY(check_cuda(cudaStreamSynchronize(s), "sync"));
-        std::sort(splits.begin(), splits.end());
-    }
+    PlanScalars ps;
+    TRY(check_cuda(cudaMemcpyAsync(&ps, d_ps, sizeof(ps), cudaMemcpyDeviceToHost, s), "memcpy"));
+    TRY(check_cuda(cudaStreamSynchronize(s), "sync"));
     cleanup_tmp();
 #undef TRY
-
-    // merge list sorted by (round, index) -- the reference's event order
-    std::vector<size_t> idx(M);
-    for (int64_t i = 0; i < M; ++i) idx[i] = size_t(i);
-    std::sort(idx.begin(), idx.end(), [&](size_t a, size_t b) {
-        return merge_rounds[a] != merge_rounds[b] ? merge_rounds[a] < merge_rounds[b] : merges[a] < merges[b];
-    });
+    const int64_t M = int64_t(ps.merges);
+    const int64_t K = int64_t(ps.splits);
+    if (rounds < 0) rounds = M > 0 ? 1 : 0;
+    const int64_t leaves_before = (N - int64_t(ps.n_internal));
     p->M = M;
     p->K = K;
-    p->merge_list = new int64_t[M ? M : 1];
-    p->merge_round_h = new int32_t[M ? M : 1];
-    for (int64_t i = 0; i < M; ++i) {
-        p->merge_list[i] = merges[idx[i]];
-        p->merge_round_h[i] = merge_rounds[idx[i]];
-    }
-    p->split_list = new int64_t[K ? K : 1];
-    for (int64_t i = 0; i < K; ++i) p->split_list[i] = splits[i];
     p->stats.leaves_before = leaves_before;
     p->stats.merges_applied = M;
     p->stats.splits_applied = K;
@@ -678,19 +723,83 @@ int dot_refine_plan_create(const dot_tree_view* tree, const int32_t* pool_id, co
     return DOT_OK;
 }
 
-int dot_refine_plan_lists(const dot_refine_plan* plan, const int64_t** merge_parents, int64_t* n_merge,
-                          const int64_t** split_leaves, int64_t* n_split, const int32_t** merge_round) {
-    if (!plan) return set_error(DOT_BAD_ARG, "NULL plan");
-    if (merge_parents) *merge_parents = plan->merge_list;
-    if (n_merge) *n_merge = plan->M;
-    if (split_leaves) *split_leaves = plan->split_list;
-    if (n_split) *n_split = plan->K;
-    if (merge_round) *merge_round = plan->merge_round_h;
+// Merged-parent and split-leaf lists, built on demand (ordered compaction on
+// the device, one download).  Merges come in the reference's event order:
+// by round, then by index.
+int dot_refine_plan_lists(dot_refine_plan* p, const int64_t** merge_parents, int64_t* n_merge,
+                          const int64_t** split_leaves, int64_t* n_split, const int32_t** merge_round,
+                          void* stream) {
+    if (!p) return set_error(DOT_BAD_ARG, "NULL plan");
+    if (!p->lists_ready) {
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        const int64_t N = p->N;
+        int32_t* flags = nullptr;
+        int64_t *rank = nullptr, *sums = nullptr, *total = nullptr, *list = nullptr;
+        int32_t* rounds = nullptr;
+        int st = DOT_OK;
+        auto cleanup = [&]() {
+            cudaFreeAsync(flags, s);
+            cudaFreeAsync(rank, s);
+            cudaFreeAsync(sums, s);
+            cudaFreeAsync(total, s);
+            cudaFreeAsync(list, s);
+        };
+#define TRY(x) do { if ((st = (x)) != DOT_OK) { cleanup(); return st; } } while (0)
+        TRY(dalloc(&flags, N, s));
+        TRY(dalloc(&rank, N, s));
+        TRY(dalloc(&sums, N / kScanTile + 2, s));
+        TRY(dalloc(&total, 1, s));
+        TRY(dalloc(&list, std::max<int64_t>(p->M, p->K) + 1, s));
+        for (int which = 0; which < 2; ++which) {
+            const int64_t cnt = which == 0 ? p->M : p->K;
+            std::vector<int64_t>& dst = which == 0 ? p->merge_list : p->split_list;
+            dst.resize(size_t(cnt));
+            if (cnt == 0) continue;
+            flag_kernel<<<grid_for(N), kTB, 0, s>>>(N, p->state, p->mround, which, flags);
+            TRY(exclusive_scan(flags, N, rank, sums, total, s));
+            compact_kernel<<<grid_for(N), kTB, 0, s>>>(N, flags, rank, list);
+            TRY(check_launch("compact_kernel"));
+            TRY(check_cuda(cudaMemcpyAsync(dst.data(), list, cnt * sizeof(int64_t), cudaMemcpyDeviceToHost, s),
+                           "memcpy"));
+        }
+        std::vector<int32_t> mr(size_t(p->M));
+        if (p->M) {
+            TRY(dalloc(&rounds, p->M, s));
+            // gather the rounds of the merged nodes
+            std::vector<int32_t> all(static_cast<size_t>(N));
+            TRY(check_cuda(cudaMemcpyAsync(all.data(), p->mround, N * sizeof(int32_t), cudaMemcpyDeviceToHost, s),
+                           "memcpy"));
+            TRY(check_cuda(cudaStreamSynchronize(s), "sync"));
+            cudaFreeAsync(rounds, s);
+            for (int64_t i = 0; i < p->M; ++i) mr[size_t(i)] = all[size_t(p->merge_list[size_t(i)])];
+            std::vector<size_t> idx(size_t(p->M));
+            for (size_t i = 0; i < idx.size(); ++i) idx[i] = i;
+            std::stable_sort(idx.begin(), idx.end(), [&](size_t a, size_t b) { return mr[a] < mr[b]; });
+            std::vector<int64_t> ml(idx.size());
+            p->merge_round_h.resize(idx.size());
+            for (size_t i = 0; i < idx.size(); ++i) {
+                ml[i] = p->merge_list[idx[i]];
+                p->merge_round_h[i] = mr[idx[i]];
+            }
+            p->merge_list.swap(ml);
+        }
+        TRY(check_cuda(cudaStreamSynchronize(s), "sync"));
+        cleanup();
+#undef TRY
+        p->lists_ready = true;
+    }
+    if (merge_parents) *merge_parents = p->merge_list.data();
+    if (n_merge) *n_merge = p->M;
+    if (split_leaves) *split_leaves = p->split_list.data();
+    if (n_split) *n_split = p->K;
+    if (merge_round) *merge_round = p->merge_round_h.data();
     return DOT_OK;
 }
 
 int dot_refine_apply(const dot_refine_plan* p, const dot_tree_view* tree, int32_t* new_node,
-                     float* new_sigma, float* new_sh, int64_t* src_index, uint8_t* src_kind, void* stream) {
+                     float* new_sigma, float* new_sh, int64_t* src_index, uint8_t* src_kind,
+                     int64_t* level_offsets_out, int32_t max_levels, int32_t* n_levels_out,
+                     void* stream) {
     if (!p || !tree) return set_error(DOT_BAD_ARG, "NULL argument");
     if (!new_node || !new_sigma || !new_sh || !src_index || !src_kind)
         return set_error(DOT_BAD_ARG, "refine outputs must not be NULL");
@@ -721,40 +830,51 @@ int dot_refine_apply(const dot_refine_plan* p, const dot_tree_view* tree, int32_
     TRY(dalloc(&rank, n_new, s));
     TRY(dalloc(&sums, n_new / kScanTile + 2, s));
     TRY(dalloc(&d_total, 1, s));
-    // level 0: the root, kept
-    const int32_t zero = 0;
-    const uint8_t kept = K_KEPT;
-    TRY(check_cuda(cudaMemcpyAsync(ent_old[0], &zero, sizeof(zero), cudaMemcpyHostToDevice, s), "memcpy"));
-    TRY(check_cuda(cudaMemcpyAsync(ent_kind[0], &kept, sizeof(kept), cudaMemcpyHostToDevice, s), "memcpy"));
+    TRY(check_cuda(cudaMemsetAsync(ent_old[0], 0, sizeof(int32_t), s), "memset"));
+    TRY(check_cuda(cudaMemsetAsync(ent_kind[0], K_KEPT, 1, s), "memset"));
     int64_t base = 0, m = 1;
-    int cur = 0;
+    int cur = 0, levels = 0;
+    std::vector<int64_t> offs(1, 0);
     while (m > 0) {
         if (base + m > n_new) TRY(set_error(DOT_CUDA_ERR, "refine apply overflow (plan/tree mismatch)"));
         level_flags_kernel<<<grid_for(m), kTB, 0, s>>>(m, ent_old[cur], ent_kind[cur], p->state, flags);
         TRY(check_launch("level_flags_kernel"));
         TRY(exclusive_scan(flags, m, rank, sums, d_total, s));
-        int64_t n_int = 0;
-        TRY(check_cuda(cudaMemcpyAsync(&n_int, d_total, sizeof(n_int), cudaMemcpyDeviceToHost, s), "memcpy"));
-        TRY(check_cuda(cudaStreamSynchronize(s), "sync"));
         const int64_t next_base = base + m;
         level_emit_kernel<<<grid_for(m), kTB, 0, s>>>(T, m, base, next_base, ent_old[cur], ent_kind[cur], flags,
                                                       rank, p->state, new_node, src_index, src_kind,
                                                       ent_old[cur ^ 1], ent_kind[cur ^ 1]);
         TRY(check_launch("level_emit_kernel"));
+        int64_t n_int = 0;
+        TRY(check_cuda(cudaMemcpyAsync(&n_int, d_total, sizeof(n_int), cudaMemcpyDeviceToHost, s), "memcpy"));
+        TRY(check_cuda(cudaStreamSynchronize(s), "sync"));
         base = next_base;
+        offs.push_back(base);
         m = 8 * n_int;
         cur ^= 1;
+        ++levels;
     }
-    if (base != n_new) TRY(set_error(DOT_CUDA_ERR, "refine apply produced %lld nodes, plan said %lld",
-                                     (long long)base, (long long)n_new));
+    if (base != n_new)
+        TRY(set_error(DOT_CUDA_ERR, "refine apply produced %lld nodes, plan said %lld", (long long)base,
+                      (long long)n_new));
     const int S4 = p->S / 4;
-    payload_kernel<<<grid_for(n_new * S4), kTB, 0, s>>>(T, n_new, S4, src_index, src_kind, p->state, p->slot,
-                                                       p->msig, p->msh, new_node, new_sigma,
+    payload_kernel<<<grid_for(n_new * S4), kTB, 0, s>>>(T, n_new, S4, src_index, p->state, p->slot, p->msig,
+                                                       p->msh, new_node, new_sigma,
                                                        reinterpret_cast<float4*>(new_sh));
     TRY(check_launch("payload_kernel"));
     cleanup();
 #undef TRY
+    if (n_levels_out) *n_levels_out = levels;
+    if (level_offsets_out)
+        for (int i = 0; i < int(offs.size()) && i < max_levels + 1; ++i) level_offsets_out[i] = offs[size_t(i)];
     return DOT_OK;
+}
+
+int dot_refine_plan_merge_rounds(const dot_refine_plan* p, int32_t* out, void* stream) {
+    if (!p || !out) return set_error(DOT_BAD_ARG, "NULL argument");
+    return check_cuda(cudaMemcpyAsync(out, p->mround, p->N * sizeof(int32_t), cudaMemcpyDeviceToDevice,
+                                      static_cast<cudaStream_t>(stream)),
+                      "memcpy");
 }
 
 void dot_refine_plan_destroy(dot_refine_plan* plan) { plan_free(plan); }
