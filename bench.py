@@ -80,7 +80,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "200"],
+                 "--format=csv,noheader,nounits", "-lms", "50"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             threading.Thread(target=self._read, daemon=True).start()
         except Exception:
@@ -345,7 +345,7 @@ def run_ours(args, rank, world, local_rank):
         "gpu_launches": 2 * args.steps,
         "roofline": {
             "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-            "frac": achieved / hbm, "traffic": None, "kernel": "render_bwd_kernel<16>",
+            "frac": achieved / hbm, "traffic": None, "kernel": "render_bwd_buffered_kernel<16,32>",
             "kernel_ms": kern_ms_avg, "alg_bytes_per_launch": alg_bytes, "peak_kind": peak_kind,
             "bytes_model": f"{RAY_BYTES} B/ray + {SEG_BYTES} B/composited segment",
         },
@@ -525,7 +525,7 @@ def run_reference(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--skip-render", action="store_true")
