@@ -171,9 +171,11 @@ struct Tracer {
     }
 
     // _kernels.py:112-158.  Returns false when the ray has left the cube.
-    template <bool CACHED = false>
+    // PREFETCH: touch the leaf's sigma and SH row (L1) right after the descent
+    // so those gathers overlap the exit-face divisions below.
+    template <bool CACHED = false, bool PREFETCH = false>
     __device__ __forceinline__ bool next(const TreeDev& T, Leaf& L, double& t_entry,
-                                         double& delta, PathCache& pc) {
+                                         double& delta, PathCache& pc, bool want_payload = true) {
         for (;;) {
             const double probe = dadd(t, nudge);
             if (probe >= t1) return false;
@@ -182,6 +184,12 @@ struct Tracer {
             const double pz = dadd(oz, dmul(probe, dz));
             if constexpr (CACHED) L = descend_cached(T, px, py, pz, pc);
             else L = descend(T, px, py, pz);
+            if (PREFETCH && want_payload) {
+                const char* row = reinterpret_cast<const char*>(T.sh + int64_t(L.pid) * T.sh_stride);
+                asm volatile("prefetch.global.L1 [%0];" :: "l"(T.sigma + L.pid));
+                asm volatile("prefetch.global.L1 [%0];" :: "l"(row));
+                if (T.sh_stride > 32) asm volatile("prefetch.global.L1 [%0];" :: "l"(row + 128));
+            }
             // exit t = min over axes of ((c +/- h) - o) / d, in x, y, z order with
             // strict '<' like the reference.  Branch-free: c + (-h) == c - h
             // exactly, and an axis with d == 0 contributes nothing.
@@ -208,7 +216,13 @@ struct Tracer {
 
     __device__ __forceinline__ bool next(const TreeDev& T, Leaf& L, double& t_entry, double& delta) {
         PathCache none;
-        return next<false>(T, L, t_entry, delta, none);
+        return next<false, false>(T, L, t_entry, delta, none);
+    }
+
+    __device__ __forceinline__ bool next_prefetch(const TreeDev& T, Leaf& L, double& t_entry,
+                                                  double& delta, bool want_payload = true) {
+        PathCache none;
+        return next<false, true>(T, L, t_entry, delta, none, want_payload);
     }
 };
 

@@ -16,6 +16,9 @@ constexpr int kBlock = 128;
 #ifndef DOT_FWD_MINB
 #define DOT_FWD_MINB 8  // forward: 64 registers -> 8 blocks (32 warps) per SM
 #endif
+#ifndef DOT_FWD_PREFETCH
+#define DOT_FWD_PREFETCH true
+#endif
 constexpr int kStk = kPathLevels + 2;  // odd row stride: conflict-free shared-memory stacks
 
 // Per-thread path cache in shared memory (see descend_cached).  Kernels are
@@ -123,7 +126,7 @@ __global__ void __launch_bounds__(kBlock, DOT_FWD_MINB) render_fwd_kernel(
     if (tr.init(T, t_near, t_far)) {
         Leaf L;
         double te, dl;
-        while (tr.template next<CACHED>(T, L, te, dl, pc)) {
+        while (tr.template next<CACHED, DOT_FWD_PREFETCH>(T, L, te, dl, pc)) {
             const double sg = double(__ldg(T.sigma + L.pid));
             const double a = exp(-sg * dl);
             const double q = 1.0 - a;
@@ -457,13 +460,47 @@ struct BufSeg {
     float pad;
 };
 
-template <int B, int K, int MINB = 1>
+// Segment buffer: per-thread local array (GBUF = false) or an explicit global
+// SoA scratch (entry i of ray r at gbuf[i * n + r], coalesced across a warp)
+// accessed with streaming (.cs) hints so it does not evict the node table
+// and payload rows from L1.
+template <bool GBUF, int K>
+struct SegBuffer {
+    BufSeg local[GBUF ? 1 : K];
+    BufSeg* g;
+    int64_t stride;
+    __device__ __forceinline__ void put(int i, const BufSeg& e) {
+        if constexpr (GBUF) {
+            const float4* s = reinterpret_cast<const float4*>(&e);
+            float4* p = reinterpret_cast<float4*>(g + int64_t(i) * stride);
+            __stcs(p, s[0]);
+            __stcs(p + 1, s[1]);
+        } else {
+            local[i] = e;
+        }
+    }
+    __device__ __forceinline__ BufSeg get(int i) const {
+        if constexpr (GBUF) {
+            BufSeg e;
+            const float4* p = reinterpret_cast<const float4*>(g + int64_t(i) * stride);
+            float4* s = reinterpret_cast<float4*>(&e);
+            s[0] = __ldcs(p);
+            s[1] = __ldcs(p + 1);
+            return e;
+        } else {
+            return local[i];
+        }
+    }
+};
+
+template <int B, int K, int MINB = 1, bool GBUF = false>
 __global__ void __launch_bounds__(kBlock, MINB) render_bwd_buffered_kernel(
     TreeDev T, const double* __restrict__ o, const double* __restrict__ d,
     const double* __restrict__ tgt, int64_t n, double bg0, double bg1, double bg2, double eps,
     double t_near, double t_far, double grad_scale, float* __restrict__ gsig,
     float* __restrict__ gsh, double* __restrict__ signal, uint8_t* __restrict__ touched,
-    double* __restrict__ loss_sum, float* __restrict__ rgb_out, int flags) {
+    double* __restrict__ loss_sum, float* __restrict__ rgb_out, int flags,
+    BufSeg* __restrict__ gbuf) {
     constexpr int S = pad4(3 * B);
     double loss = 0.0;
     // one ray per thread, blocks scheduled dynamically by the hardware (a
@@ -475,7 +512,9 @@ __global__ void __launch_bounds__(kBlock, MINB) render_bwd_buffered_kernel(
         load_ray(o, d, r, tr);
         float basis[B];
         eval_basis<B>(tr.dx, tr.dy, tr.dz, basis);
-        BufSeg buf[K];
+        SegBuffer<GBUF, K> buf;
+        buf.g = gbuf + r;
+        buf.stride = n;
         int used = 0;
         double resume_t = 0.0, resume_nudge = 0.0;
         double trans = 1.0, c0 = 0.0, c1 = 0.0, c2 = 0.0;
@@ -484,7 +523,7 @@ __global__ void __launch_bounds__(kBlock, MINB) render_bwd_buffered_kernel(
             Leaf L;
             double te, dl;
             bool cut = false;
-            while (tr.next(T, L, te, dl)) {
+            while (tr.next_prefetch(T, L, te, dl, !cut)) {
                 touched[L.pid] = 1;
                 if (cut) continue;  // post-cut: touched only
                 const double a = exp(-double(__ldg(T.sigma + L.pid)) * dl);
@@ -502,12 +541,15 @@ __global__ void __launch_bounds__(kBlock, MINB) render_bwd_buffered_kernel(
                     c2 += tq * double(k2);
                 }
                 if (used < K) {
-                    buf[used].pid = L.pid;
-                    buf[used].delta = float(dl);
-                    buf[used].a = a;
-                    buf[used].k0 = k0;
-                    buf[used].k1 = k1;
-                    buf[used].k2 = k2;
+                    BufSeg e;
+                    e.pid = L.pid;
+                    e.delta = float(dl);
+                    e.a = a;
+                    e.k0 = k0;
+                    e.k1 = k1;
+                    e.k2 = k2;
+                    e.pad = 0.f;
+                    buf.put(used, e);
                 } else if (used == K) {  // buffer full: remember where pass 2 resumes
                     resume_t = te;
                     resume_nudge = tr.nudge0;
@@ -544,12 +586,13 @@ __global__ void __launch_bounds__(kBlock, MINB) render_bwd_buffered_kernel(
             double a, dl;
             float k0, k1, k2;
             if (i < K) {
-                pid = buf[i].pid;
-                a = buf[i].a;
-                dl = buf[i].delta;
-                k0 = buf[i].k0;
-                k1 = buf[i].k1;
-                k2 = buf[i].k2;
+                const BufSeg e = buf.get(i);
+                pid = e.pid;
+                a = e.a;
+                dl = e.delta;
+                k0 = e.k0;
+                k1 = e.k1;
+                k2 = e.k2;
             } else {
                 double te;
                 tr.next(T, L, te, dl);
@@ -879,20 +922,34 @@ int launch_render_bwd(const TreeDev& T, const double* o, const double* d, const 
     if (!(flags & 16)) {  // default: buffered one-ray-per-thread
         const bool cached = false;
         const bool big = (flags & 128) == 0;  // K = 32 records in flight; bit 7 selects K = 16
-#define DOT_BUF_LAUNCH(BB, KK, MB)                                                                  \
-    render_bwd_buffered_kernel<BB, KK, MB><<<blocks_for(n), kBlock, 0, s>>>(                        \
+        BufSeg* gbuf = nullptr;
+        const bool use_gbuf = (flags & 4096) != 0;
+        if (use_gbuf) {
+            retain_pool_memory();
+            if (int st = check_cuda(cudaMallocAsync(reinterpret_cast<void**>(&gbuf),
+                                                    size_t(n) * (big ? 32 : 16) * sizeof(BufSeg), s),
+                                    "cudaMallocAsync"))
+                return st;
+        }
+#define DOT_BUF_LAUNCH(BB, KK, MB, GB)                                                              \
+    render_bwd_buffered_kernel<BB, KK, MB, GB><<<blocks_for(n), kBlock, 0, s>>>(                    \
         T, o, d, tgt, n, bg[0], bg[1], bg[2], eps, tn, tf, gs, gsig, gsh, signal, touched, loss,    \
-        rgb_out, flags)
+        rgb_out, flags, gbuf)
 #define DOT_BUF(BB, CC)                                                                           \
     {                                                                                             \
-        if (!big) DOT_BUF_LAUNCH(BB, 16, 8);                                                      \
-        else if (flags & 1024) DOT_BUF_LAUNCH(BB, 32, 10);  /* occupancy experiments */           \
-        else if (flags & 2048) DOT_BUF_LAUNCH(BB, 32, 12);                                        \
-        else DOT_BUF_LAUNCH(BB, 32, 8);  /* 64 regs: measured best (3.0 vs 3.4 ms at 116 regs) */ \
+        if (use_gbuf) {                                                                           \
+            if (big) DOT_BUF_LAUNCH(BB, 32, 8, true);                                             \
+            else DOT_BUF_LAUNCH(BB, 16, 8, true);                                                 \
+        } else if (!big) DOT_BUF_LAUNCH(BB, 16, 8, false);                                        \
+        else if (flags & 1024) DOT_BUF_LAUNCH(BB, 32, 10, false); /* occupancy experiments */     \
+        else if (flags & 2048) DOT_BUF_LAUNCH(BB, 32, 12, false);                                 \
+        else DOT_BUF_LAUNCH(BB, 32, 8, false); /* 64 regs: measured best (3.0 vs 3.4 ms at 116) */ \
     }
         DOT_DISPATCH_B(DOT_BUF)
 #undef DOT_BUF
-        return check_launch("render_bwd_buffered_kernel");
+        const int st = check_launch("render_bwd_buffered_kernel");
+        if (gbuf) cudaFreeAsync(gbuf, s);
+        return st;
     }
     const bool cached = use_cache(T, flags);
     unsigned long long* ctr = nullptr;

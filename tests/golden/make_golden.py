@@ -283,7 +283,67 @@ def main():
     acc = np.zeros(t.capacity); acc[lv] = rng.uniform(0.0, 1.0, lv.size) * 10.0 ** rng.integers(-8, 0, lv.size)
     calib_case("merge_order", t, acc, 0.05, 0.05, True)
 
+    remap_case()
+    train_case()
     config1()
+
+
+def remap_case():
+    """RmsPropState.remap across a recursive calibrate (optim.py:89-104)."""
+    from octrf.optim import RmsPropState
+    from octrf.scene_io import _level_order
+    rng = np.random.default_rng(500)
+    t = irregular_tree(501, depth=3, basis_count=4, splits=8, merges=2, resplits=2, max_depth=5)
+    out = dict(pool_arrays(t))
+    lv = t.leaf_ids()
+    acc = np.zeros(t.capacity)
+    acc[lv] = np.where(rng.uniform(size=lv.size) < 0.985, 0.0, rng.uniform(0.0, 5.0, lv.size))
+    state = RmsPropState(t)
+    state.v_sigma[:] = rng.uniform(0.0, 1e-3, t.capacity)
+    state.v_sh[:] = rng.uniform(0.0, 1e-3, state.v_sh.shape)
+    out.update(acc=acc, v_sigma=state.v_sigma.copy(), v_sh=state.v_sh.copy())
+    buf = SignalBuffer(t)
+    buf.accumulator[:] = acc
+    report = calibrate(t, buf, CalibrationConfig(tau=0.0, gamma=0.1, recursive=True))
+    state.remap(report)
+    order, _ = _level_order(t)
+    is_leaf = t._leaf[order] == 1
+    out.update(tau=np.float64(0.0), gamma=np.float64(0.1),
+               rounds=np.int64(report.recursion_rounds), merges=np.int64(report.merges_applied),
+               splits=np.int64(report.splits_applied),
+               canon_is_leaf=is_leaf, canon_v_sigma=state.v_sigma[order],
+               canon_v_sh=state.v_sh[order])
+    np.savez_compressed(os.path.join(HERE, "optim_remap.npz"), **out)
+    print("remap", report.to_json())
+
+
+class _Bundle:
+    def __init__(self, origins, dirs, targets):
+        self.origins, self.dirs, self.targets, self.heldout = origins, dirs, targets, []
+
+
+def train_case():
+    """A short train() run (optim.py:169-195): loss per epoch and leaf counts."""
+    from octrf.optim import TrainConfig, train
+    from octrf.sh import sh_from_rgb
+    sh_in = sh_from_rgb(np.array([0.8, 0.3, 0.2]), 1)
+
+    def ball(c):
+        inside = np.linalg.norm(c, axis=1) <= 0.55
+        return np.where(inside, 8.0, 0.0), np.where(inside[:, None], sh_in, 0.0)
+
+    truth = build_dense(3, (0.0, 0.0, 0.0), 1.0, 1, ball, max_depth=5)
+    o, d = ray_set(601, 2000, specials=False, miss_fraction=0.05)
+    targets = render_rays(truth, o, d, 1.0, early_stop_eps=0.0)
+    trainee = build_dense(2, (0.0, 0.0, 0.0), 1.0, 1, LeafPayload(0.3, [0.0, 0.0, 0.0]), max_depth=5)
+    cfg = TrainConfig(epochs=6, interval=2, tau=0.5, gamma=0.1, batch_size=500, seed=3)
+    _, hist = train(trainee, _Bundle(o, d, targets), cfg)
+    out = dict(origins=o, dirs=d, targets=targets,
+               loss=np.array([h["loss"] for h in hist]),
+               leaf_count=np.array([h["leaf_count"] for h in hist]),
+               final_dot1=np.frombuffer(dot1_bytes(trainee), dtype=np.uint8))
+    np.savez_compressed(os.path.join(HERE, "train_small.npz"), **out)
+    print("train", [round(h["loss"], 6) for h in hist], [h["leaf_count"] for h in hist])
 
 
 if __name__ == "__main__":

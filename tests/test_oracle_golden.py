@@ -80,3 +80,17 @@ def test_oracle_config1_golden(oracle):
     np.testing.assert_array_equal(g.touched, z["touched"])
     np.testing.assert_array_equal(g.dsigma[g.touched], z["dsigma_touched"])
     np.testing.assert_array_equal(sig, z["signal"])
+
+
+def test_oracle_remap_golden(oracle):
+    """RmsPropState.remap restatement vs the reference across 3 prune rounds."""
+    z = np.load(os.path.join(GOLDEN, "optim_remap.npz"))
+    t = oracle.PoolTree.from_arrays(z)
+    r = oracle.calibrate(t, z["acc"], float(z["tau"]), float(z["gamma"]), True)
+    assert r.recursion_rounds == int(z["rounds"])
+    vs, vh = oracle.rmsprop_remap(z["v_sigma"].copy(), z["v_sh"].copy(), r.events, t.capacity)
+    c = t.canonical()
+    leaf = z["canon_is_leaf"]
+    np.testing.assert_array_equal(c["is_leaf"] == 1, leaf)
+    np.testing.assert_array_equal(vs[c["order"]][leaf], z["canon_v_sigma"][leaf])
+    np.testing.assert_array_equal(vh[c["order"]][leaf], z["canon_v_sh"][leaf])
