@@ -96,6 +96,9 @@ int dot_render_bwd(const dot_tree_view* tree, const double* origins, const doubl
  *     rays, so the order changes only speed. */
 int dot_ray_keys(const dot_tree_view* tree, const double* origins, const double* dirs,
                  int64_t n_rays, uint64_t* keys, void* stream);
+/* 31-bit keys (origin 4 bits/axis, direction 10x9 bits): half the sort passes. */
+int dot_ray_keys32(const dot_tree_view* tree, const double* origins, const double* dirs,
+                   int64_t n_rays, int32_t* keys, void* stream);
 
 /* --- workload statistics (measurement helper, no reference counterpart):
  *     totals[0] += traversed segments, totals[1] += composited (pre-cut)

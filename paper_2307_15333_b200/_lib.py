@@ -52,6 +52,7 @@ _SIGNATURES = {
                                c_f64, c_f64, c_void_p, c_void_p, c_i32, c_void_p, c_void_p, c_void_p,
                                c_void_p, c_i32, c_void_p]),
     "dot_ray_keys": (c_i32, [c_void_p, c_void_p, c_void_p, c_i64, c_void_p, c_void_p]),
+    "dot_ray_keys32": (c_i32, [c_void_p, c_void_p, c_void_p, c_i64, c_void_p, c_void_p]),
     "dot_ray_stats":(c_i32, [c_void_p, c_void_p, c_void_p, c_i64, c_f64, c_void_p, c_void_p]),
     "dot_refine_plan_create": (c_i32, [c_void_p, c_void_p, c_void_p, c_i32, c_f64, c_f64, c_i32, c_i32,
                                        c_f64, c_void_p, c_i32, c_void_p, c_void_p, c_void_p]),

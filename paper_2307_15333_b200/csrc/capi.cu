@@ -140,6 +140,13 @@ int dot_ray_keys(const dot_tree_view* tree, const double* origins, const double*
                            static_cast<cudaStream_t>(stream));
 }
 
+int dot_ray_keys32(const dot_tree_view* tree, const double* origins, const double* dirs, int64_t n_rays,
+                   int32_t* keys, void* stream) {
+    if (int st = validate_tree(tree)) return st;
+    if (n_rays < 0 || (n_rays && (!origins || !dirs || !keys))) return set_error(DOT_BAD_ARG, "bad arrays");
+    return launch_ray_keys32(make_tree(*tree), origins, dirs, n_rays, keys, static_cast<cudaStream_t>(stream));
+}
+
 int dot_ray_stats(const dot_tree_view* tree, const double* origins, const double* dirs, int64_t n_rays,
                   double early_stop_eps, uint64_t* totals, void* stream) {
     if (int st = validate_tree(tree)) return st;

@@ -36,6 +36,8 @@ int launch_render_bwd_replay(const TreeDev& T, const double* o, const double* d,
                              const uint8_t* ray_flag, int flags, cudaStream_t s);
 int launch_ray_keys(const TreeDev& T, const double* o, const double* d, int64_t n, unsigned long long* keys,
                     cudaStream_t s);
+int launch_ray_keys32(const TreeDev& T, const double* o, const double* d, int64_t n, int32_t* keys,
+                      cudaStream_t s);
 int launch_ray_stats(const TreeDev& T, const double* o, const double* d, int64_t n, double eps,
                      unsigned long long* out, cudaStream_t s);
 

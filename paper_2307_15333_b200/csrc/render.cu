@@ -759,6 +759,44 @@ __device__ __forceinline__ unsigned long long spread3_10(unsigned v) {
     return x;
 }
 
+// 31-bit variant (int32 keys sort in half the radix passes): origin 4 bits per
+// axis (12 bits), direction 10 x 9 bits (19 bits).
+__global__ void ray_keys32_kernel(TreeDev T, const double* __restrict__ o, const double* __restrict__ d,
+                                  int64_t n, int32_t* __restrict__ keys) {
+    const int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (r >= n) return;
+    unsigned q[3];
+    const double c3[3] = {T.cx, T.cy, T.cz};
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        double u = (o[3 * r + a] - (c3[a] - 4.0 * T.half)) / (8.0 * T.half);
+        u = fmin(fmax(u, 0.0), 0.999999);
+        q[a] = unsigned(u * 16.0);
+    }
+    const unsigned om = unsigned(spread3_10(q[0]) | (spread3_10(q[1]) << 1) | (spread3_10(q[2]) << 2));
+    double x = d[3 * r], y = d[3 * r + 1], z = d[3 * r + 2];
+    const double l1 = fabs(x) + fabs(y) + fabs(z);
+    x /= l1;
+    y /= l1;
+    if (z < 0.0) {
+        const double tx = (1.0 - fabs(y)) * (x >= 0.0 ? 1.0 : -1.0);
+        const double ty = (1.0 - fabs(x)) * (y >= 0.0 ? 1.0 : -1.0);
+        x = tx;
+        y = ty;
+    }
+    const unsigned ux = unsigned(fmin(fmax(0.5 * (x + 1.0), 0.0), 0.99999) * 1024.0);
+    const unsigned uy = unsigned(fmin(fmax(0.5 * (y + 1.0), 0.0), 0.99999) * 512.0);
+    const unsigned dm = unsigned(spread_bits(ux, 10) | (spread_bits(uy, 9) << 1));
+    keys[r] = int32_t((om << 19) | dm);
+}
+
+int launch_ray_keys32(const TreeDev& T, const double* o, const double* d, int64_t n, int32_t* keys,
+                      cudaStream_t s) {
+    if (n == 0) return DOT_OK;
+    ray_keys32_kernel<<<unsigned((n + 255) / 256), 256, 0, s>>>(T, o, d, n, keys);
+    return check_launch("ray_keys32_kernel");
+}
+
 __global__ void ray_keys_kernel(TreeDev T, const double* __restrict__ o, const double* __restrict__ d,
                                 int64_t n, unsigned long long* __restrict__ keys) {
     const int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;

@@ -19,6 +19,7 @@ and gradients, float64 signal); host torch tensors are copied with
 from __future__ import annotations
 
 import math
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -31,6 +32,7 @@ from .octree import SparseOctree
 EPS_T = 1e-4  # early-termination transmittance threshold (render.py:23)
 UNIT_TOL = 1e-6
 COHERENT_MIN_RAYS = 1 << 14  # below this a key sort costs more than it saves
+COHERENT_KEY_BITS = int(os.environ.get("DOT_COHERENT_KEY_BITS", "32"))
 
 
 @dataclass
@@ -290,9 +292,14 @@ def render_and_backprop(tree: SparseOctree, origins, dirs, targets, background,
         if coherent and n >= COHERENT_MIN_RAYS:
             # reorder the batch so each warp walks neighbouring cells; loss,
             # gradients and signal are sums over rays (order-independent)
-            keys = torch.empty(n, dtype=torch.int64, device=tree.device)
-            _lib.call("dot_ray_keys", _lib.ctypes.byref(view), _lib.ptr(o), _lib.ptr(d), n,
-                      _lib.ptr(keys), _lib.stream_ptr())
+            if COHERENT_KEY_BITS == 32:  # 31-bit keys: half the radix-sort passes
+                keys = torch.empty(n, dtype=torch.int32, device=tree.device)
+                _lib.call("dot_ray_keys32", _lib.ctypes.byref(view), _lib.ptr(o), _lib.ptr(d), n,
+                          _lib.ptr(keys), _lib.stream_ptr())
+            else:
+                keys = torch.empty(n, dtype=torch.int64, device=tree.device)
+                _lib.call("dot_ray_keys", _lib.ctypes.byref(view), _lib.ptr(o), _lib.ptr(d), n,
+                          _lib.ptr(keys), _lib.stream_ptr())
             perm = torch.argsort(keys)
             o, d, t = o[perm], d[perm], t[perm]
         if kernel_events is not None:
