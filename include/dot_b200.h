@@ -73,6 +73,16 @@ int dot_render_fwd(const dot_tree_view* tree, const double* origins, const doubl
                    double t_near, double t_far, float* rgb, float* t_final, float* wsum,
                    float* depth, void* stream);
 
+/* --- camera rendering with in-kernel rays (render.render_image,
+ *     render.py:228-241, over scene_io.Camera.rays, scene_io.py:77-91):
+ *     cam_to_world is the host 4x4 row-major matrix (f64, read at launch),
+ *     rgb is f32 [height*width*3] row-major; t_final / depth may be NULL.
+ *     Each warp renders an 8x4 pixel tile. */
+int dot_render_camera(const dot_tree_view* tree, const double* cam_to_world, double focal,
+                      int32_t width, int32_t height, const double* background,
+                      double early_stop_eps, float* rgb, float* t_final, float* depth,
+                      void* stream);
+
 /* --- fused forward + backward + signal (replaces segment_batch + grad_kernel
  *     + scatter_kernel, _kernels.py:227-346, as called by
  *     render.render_and_backprop render.py:175-225).

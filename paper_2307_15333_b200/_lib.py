@@ -48,7 +48,9 @@ _SIGNATURES = {
                                c_void_p, c_void_p, c_void_p]),
     "dot_render_fwd": (c_i32, [c_void_p, c_void_p, c_void_p, c_i64, c_void_p, c_f64, c_f64, c_f64,
                                c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
-    "dot_render_bwd": (c_i32, [c_void_p, c_void_p, c_void_p, c_void_p, c_i64, c_void_p, c_f64, c_f64,
+    "dot_render_camera": (c_i32, [c_void_p, c_void_p, c_f64, c_i32, c_i32, c_void_p, c_f64, c_void_p,
+                                  c_void_p, c_void_p, c_void_p]),
+    "dot_render_bwd":(c_i32, [c_void_p, c_void_p, c_void_p, c_void_p, c_i64, c_void_p, c_f64, c_f64,
                                c_f64, c_f64, c_void_p, c_void_p, c_i32, c_void_p, c_void_p, c_void_p,
                                c_void_p, c_i32, c_void_p]),
     "dot_ray_keys": (c_i32, [c_void_p, c_void_p, c_void_p, c_i64, c_void_p, c_void_p]),

@@ -147,6 +147,16 @@ int dot_ray_keys32(const dot_tree_view* tree, const double* origins, const doubl
     return launch_ray_keys32(make_tree(*tree), origins, dirs, n_rays, keys, static_cast<cudaStream_t>(stream));
 }
 
+int dot_render_camera(const dot_tree_view* tree, const double* cam_to_world, double focal, int32_t width,
+                      int32_t height, const double* background, double early_stop_eps, float* rgb,
+                      float* t_final, float* depth, void* stream) {
+    if (int st = validate_tree(tree)) return st;
+    if (!cam_to_world || !background || !rgb || width < 0 || height < 0 || !(focal > 0.0))
+        return set_error(DOT_BAD_ARG, "bad camera arguments");
+    return launch_render_camera(make_tree(*tree), cam_to_world, focal, width, height, background, early_stop_eps,
+                                rgb, t_final, depth, static_cast<cudaStream_t>(stream));
+}
+
 int dot_ray_stats(const dot_tree_view* tree, const double* origins, const double* dirs, int64_t n_rays,
                   double early_stop_eps, uint64_t* totals, void* stream) {
     if (int st = validate_tree(tree)) return st;

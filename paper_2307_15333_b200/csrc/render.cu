@@ -739,6 +739,99 @@ static unsigned persistent_grid(K kernel, int64_t n) {
 }
 
 // ---------------------------------------------------------------------------
+// Camera rendering with in-kernel ray generation (scene_io.py:77-91 pixel
+// convention: direction (x+0.5-W/2)/f, -(y+0.5-H/2)/f, -1 rotated by the
+// camera's 3x3 and normalised; origin = camera position).  Each warp covers
+// an 8x4 pixel tile so its rays walk neighbouring cells; no ray arrays are
+// read.  (The direction is computed in fp64 with its own operation order, so
+// it may differ from numpy's BLAS product in the last ulp.)
+
+struct CameraDev {
+    double r[9];  // row-major cam_to_world rotation
+    double t[3];
+    double focal;
+    int32_t width, height;
+};
+
+template <int B>
+__global__ void __launch_bounds__(kBlock, DOT_FWD_MINB) render_camera_kernel(
+    TreeDev T, CameraDev cam, double bg0, double bg1, double bg2, double eps, float* __restrict__ rgb,
+    float* __restrict__ tfin_out, float* __restrict__ depth_out) {
+    constexpr int S = pad4(3 * B);
+    // block = 4 warps = 16x8 pixels; warp w covers an 8x4 tile
+    const int tiles_x = (cam.width + 15) / 16;
+    const int bx = blockIdx.x % tiles_x, by = blockIdx.x / tiles_x;
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int x = bx * 16 + (w & 1) * 8 + (lane & 7);
+    const int y = by * 8 + (w >> 1) * 4 + (lane >> 3);
+    if (x >= cam.width || y >= cam.height) return;
+    const double xs = (double(x) + 0.5 - 0.5 * cam.width) / cam.focal;
+    const double ys = -(double(y) + 0.5 - 0.5 * cam.height) / cam.focal;
+    double dx = cam.r[0] * xs + cam.r[1] * ys - cam.r[2];
+    double dy = cam.r[3] * xs + cam.r[4] * ys - cam.r[5];
+    double dz = cam.r[6] * xs + cam.r[7] * ys - cam.r[8];
+    const double nrm = sqrt(dx * dx + dy * dy + dz * dz);
+    Tracer tr;
+    tr.ox = cam.t[0];
+    tr.oy = cam.t[1];
+    tr.oz = cam.t[2];
+    tr.dx = dx / nrm;
+    tr.dy = dy / nrm;
+    tr.dz = dz / nrm;
+    float basis[B];
+    eval_basis<B>(tr.dx, tr.dy, tr.dz, basis);
+    double trans = 1.0, c0 = 0.0, c1 = 0.0, c2 = 0.0, dep = 0.0;
+    if (tr.init(T, 0.0, __longlong_as_double(0x7ff0000000000000ll))) {
+        Leaf L;
+        double te, dl;
+        PathCache pc;
+        while (tr.template next<false, DOT_FWD_PREFETCH>(T, L, te, dl, pc)) {
+            const double a = exp(-double(__ldg(T.sigma + L.pid)) * dl);
+            const double q = 1.0 - a;
+            if (q > 0.0) {
+                float e0, e1, e2;
+                sh_dot<B>(T.sh + int64_t(L.pid) * S, basis, e0, e1, e2);
+                const double tq = trans * q;
+                c0 += tq * double(sigmoidf(e0));
+                c1 += tq * double(sigmoidf(e1));
+                c2 += tq * double(sigmoidf(e2));
+                dep += tq * (te + 0.5 * dl);
+            }
+            trans *= a;
+            if (eps > 0.0 && trans < eps) break;
+        }
+    }
+    const int64_t p = int64_t(y) * cam.width + x;
+    rgb[3 * p + 0] = float(c0 + trans * bg0);
+    rgb[3 * p + 1] = float(c1 + trans * bg1);
+    rgb[3 * p + 2] = float(c2 + trans * bg2);
+    if (tfin_out) tfin_out[p] = float(trans);
+    if (depth_out) depth_out[p] = float(dep);
+}
+
+int launch_render_camera(const TreeDev& T, const double* cam_to_world, double focal, int width, int height,
+                         const double* bg, double eps, float* rgb, float* tfin, float* depth, cudaStream_t s) {
+    if (width <= 0 || height <= 0) return DOT_OK;
+    CameraDev cam;
+    for (int i = 0; i < 3; ++i) {
+        for (int j = 0; j < 3; ++j) cam.r[3 * i + j] = cam_to_world[4 * i + j];
+        cam.t[i] = cam_to_world[4 * i + 3];
+    }
+    cam.focal = focal;
+    cam.width = width;
+    cam.height = height;
+    const unsigned blocks = unsigned(((width + 15) / 16) * ((height + 7) / 8));
+    switch (T.basis_count) {
+        case 1: render_camera_kernel<1><<<blocks, kBlock, 0, s>>>(T, cam, bg[0], bg[1], bg[2], eps, rgb, tfin, depth); break;
+        case 4: render_camera_kernel<4><<<blocks, kBlock, 0, s>>>(T, cam, bg[0], bg[1], bg[2], eps, rgb, tfin, depth); break;
+        case 9: render_camera_kernel<9><<<blocks, kBlock, 0, s>>>(T, cam, bg[0], bg[1], bg[2], eps, rgb, tfin, depth); break;
+        case 16: render_camera_kernel<16><<<blocks, kBlock, 0, s>>>(T, cam, bg[0], bg[1], bg[2], eps, rgb, tfin, depth); break;
+        default: return set_error(DOT_BAD_ARG, "basis_count must be 1, 4, 9 or 16");
+    }
+    return check_launch("render_camera_kernel");
+}
+
+// ---------------------------------------------------------------------------
 // Coherence keys: sorting a batch by (origin Morton, octahedral direction
 // Morton) puts rays that walk the same cells next to each other -- within a
 // camera the direction key is a pixel-space Z-order.  Loss, gradients and

@@ -334,10 +334,37 @@ def render_and_backprop(tree: SparseOctree, origins, dirs, targets, background,
     return out
 
 
+def render_view(tree: SparseOctree, camera, background, early_stop_eps: float = EPS_T,
+                return_aux: bool = False):
+    """Render a pinhole ``Camera`` with in-kernel ray generation (8x4-pixel
+    warp tiles, no ray arrays); returns a device tensor [H, W, 3] (f32), plus
+    (T_final, depth) [H, W] with return_aux."""
+    dev = tree.device
+    H, W = int(camera.height), int(camera.width)
+    rgb = torch.empty(H, W, 3, dtype=torch.float32, device=dev)
+    tfin = torch.empty(H, W, dtype=torch.float32, device=dev) if return_aux else None
+    depth = torch.empty(H, W, dtype=torch.float32, device=dev) if return_aux else None
+    m = np.ascontiguousarray(camera.cam_to_world, dtype=np.float64).reshape(4, 4)
+    bg = _background(background)
+    view, _topo = tree.tree_view()
+    _lib.call("dot_render_camera", _lib.ctypes.byref(view), m.ctypes.data_as(_lib.c_void_p),
+              float(camera.focal), W, H, _bg_ptr(bg), float(early_stop_eps), _lib.ptr(rgb),
+              _lib.ptr(tfin), _lib.ptr(depth), _lib.stream_ptr())
+    return (rgb, tfin, depth) if return_aux else rgb
+
+
 def render_image(tree: SparseOctree, camera, background, worker_count: int | None = None,
-                 early_stop_eps: float = EPS_T, chunk: int = 65536) -> np.ndarray:
-    """H x W x 3 image (render.py:228-241).  ``worker_count`` and ``chunk``
-    are accepted for API compatibility; results never depend on them."""
+                 early_stop_eps: float = EPS_T, chunk: int = 65536,
+                 exact_rays: bool = False) -> np.ndarray:
+    """H x W x 3 float64 image (render.py:228-241).
+
+    Pinhole cameras (``cam_to_world``/``focal``) are rendered with in-kernel
+    rays (``render_view``); ``exact_rays=True`` -- or any other camera
+    object with ``rays()`` -- renders ``camera.rays()`` instead, i.e. the very
+    same f64 rays as the reference.  ``worker_count`` and ``chunk`` are
+    accepted for API compatibility; results never depend on them."""
+    if not exact_rays and all(hasattr(camera, a) for a in ("cam_to_world", "focal")):
+        return render_view(tree, camera, background, early_stop_eps).double().cpu().numpy()
     origins, dirs = camera.rays()
     rgb = render_rays(tree, origins, dirs, background, early_stop_eps)
     return np.asarray(rgb).reshape(camera.height, camera.width, 3)

@@ -141,6 +141,30 @@ def test_empty_and_miss_batches():
     assert g.touched.size == 0 and not g.dsigma.any() and not sig.any()
 
 
+@pytest.mark.parametrize("size", [(64, 64), (37, 23)])
+def test_camera_render_in_kernel_rays(oracle, size):
+    """render_image with in-kernel camera rays (8x4 warp tiles, odd image sizes)
+    vs the reference path on camera.rays() through the oracle."""
+    from paper_2307_15333_b200 import scenes
+    from paper_2307_15333_b200.render import render_image, render_view
+    from paper_2307_15333_b200.scene_io import Camera, load_tree_bytes
+    z = np.load(os.path.join(GOLDEN, "config1.npz"))
+    tree = load_tree_bytes(z["scene_dot1"].tobytes(), device="cuda")
+    W, H = size
+    cam = Camera(W, H, scenes.focal_from_angle(W, scenes.FOV_40),
+                 scenes.orbit_pose(**scenes.CONFIG1_POSE))
+    img = render_image(tree, cam, 1.0)
+    o, d = cam.rays()
+    want = oracle.render_rays(tree, o, d, 1.0).reshape(H, W, 3)
+    np.testing.assert_allclose(img, want, atol=ATOL, rtol=RTOL)
+    exact = render_image(tree, cam, 1.0, exact_rays=True)
+    np.testing.assert_allclose(exact, want, atol=ATOL, rtol=RTOL)
+    rgb, tfin, depth = render_view(tree, cam, 1.0, return_aux=True)
+    assert rgb.shape == (H, W, 3) and tfin.shape == (H, W)
+    np.testing.assert_allclose(depth.cpu().numpy().reshape(-1), oracle.render_depth(tree, o, d),
+                               atol=ATOL, rtol=RTOL)
+
+
 def test_length_mismatch_raises():
     from paper_2307_15333_b200.errors import InputError
     from paper_2307_15333_b200.render import render_and_backprop
