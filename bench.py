@@ -222,16 +222,21 @@ def run_ours(args, rank, world, local_rank):
             idx = idx[torch.argsort(morton_key(idx))]
         return idx
 
+    from paper_2307_15333_b200.parallel import allreduce_grads_overlapped
+
+    def exchange_and_update(grads):
+        """NCCL all-reduce of the leaf gradients in row chunks, each chunk's
+        RMSProp update issued as soon as its reduction lands (N = 1: one update)."""
+        allreduce_grads_overlapped(ws.dsigma, ws.dsh_store, ws.touched,
+                                   lambda lo, hi: rmsprop_step(tree, grads, state, rows=(lo, hi)),
+                                   chunks=args.ar_chunks)
+
     def step(k, timed_kernel=True):
         idx = batch_index(k)
         loss, grads, sig = render_and_backprop(
             tree, origins[idx], dirs[idx], targets[idx], BG, EPS, grad_scale=gs, workspace=ws,
             kernel_events=kev[k] if timed_kernel else None, kernel_flags=args.bwd_flags)
-        if world > 1:
-            dist.all_reduce(ws.dsigma)
-            dist.all_reduce(ws.dsh_store)
-            dist.all_reduce(ws.touched, op=dist.ReduceOp.MAX)
-        rmsprop_step(tree, grads, state)
+        exchange_and_update(grads)
         buf.accumulate(sig, per_rank, validate=False)
         return loss
 
@@ -283,18 +288,14 @@ def run_ours(args, rank, world, local_rank):
     for k in range(args.warmup):
         o_h, d_h, t_h = host[k % 2]
         loss, grads, sig = render_and_backprop(tree, o_h, d_h, t_h, BG, EPS, grad_scale=gs, workspace=ws)
-        rmsprop_step(tree, grads, state)
+        exchange_and_update(grads)
         float(loss.item())
     torch.cuda.synchronize()
     e0.record()
     for k in range(args.steps):
         o_h, d_h, t_h = host[k % 2]
         loss, grads, sig = render_and_backprop(tree, o_h, d_h, t_h, BG, EPS, grad_scale=gs, workspace=ws)
-        if world > 1:
-            dist.all_reduce(ws.dsigma)
-            dist.all_reduce(ws.dsh_store)
-            dist.all_reduce(ws.touched, op=dist.ReduceOp.MAX)
-        rmsprop_step(tree, grads, state)
+        exchange_and_update(grads)
         buf.accumulate(sig, per_rank, validate=False)
         float(loss.item())
     e1.record()
@@ -553,6 +554,8 @@ def main():
     ap.add_argument("--ref-sample", type=int, default=1 << 14)
     ap.add_argument("--order", choices=["random", "raster", "morton"], default="random",
                     help="batch ray order handed to the kernel (same ray set)")
+    ap.add_argument("--ar-chunks", type=int, default=4,
+                    help="row chunks of the overlapped gradient all-reduce (N > 1)")
     ap.add_argument("--bwd-flags", type=int, default=0,
                     help="dot_render_bwd flags (2 = legacy one-ray-per-thread kernel)")
     args = ap.parse_args()

@@ -44,6 +44,43 @@ def allreduce_grads(dsigma: torch.Tensor, dsh: torch.Tensor, touched: torch.Tens
         dist.all_reduce(loss_sum, group=group)
 
 
+def chunk_bounds(n_rows: int, chunks: int) -> list[tuple[int, int]]:
+    """Row ranges of a chunked gradient exchange (aligned to 64 rows)."""
+    cuts = sorted({min(n_rows, ((n_rows * k) // chunks + 63) // 64 * 64) for k in range(chunks + 1)})
+    cuts[0], cuts[-1] = 0, n_rows
+    return [(a, b) for a, b in zip(cuts, cuts[1:]) if b > a]
+
+
+def allreduce_grads_overlapped(dsigma: torch.Tensor, dsh: torch.Tensor, touched: torch.Tensor,
+                               on_chunk, loss_sum: torch.Tensor | None = None, chunks: int = 4,
+                               group=None) -> None:
+    """All-reduce the per-leaf gradients in row chunks (async) and call
+    ``on_chunk(lo, hi)`` -- the optimizer update of rows [lo, hi) -- as soon
+    as each chunk's reduction has landed, so the collective of chunk k+1
+    overlaps the update of chunk k.  Equivalent to allreduce_grads followed
+    by one update over all rows."""
+    n = dsigma.shape[0]
+    if not dist.is_initialized() or dist.get_world_size(group) == 1:
+        on_chunk(0, n)
+        return
+    parts = chunk_bounds(n, chunks)
+    pending = []
+    for lo, hi in parts:
+        pending.append((
+            dist.all_reduce(dsigma[lo:hi], group=group, async_op=True),
+            dist.all_reduce(dsh[lo:hi], group=group, async_op=True),
+            dist.all_reduce(touched[lo:hi], op=dist.ReduceOp.MAX, group=group, async_op=True)))
+    if loss_sum is not None:
+        pending.append((dist.all_reduce(loss_sum, group=group, async_op=True),))
+    for (lo, hi), handles in zip(parts, pending):
+        for h in handles:
+            h.wait()
+        on_chunk(lo, hi)
+    for h in pending[len(parts):]:
+        for hh in h:
+            hh.wait()
+
+
 def allreduce_signal(accumulator: torch.Tensor, group=None) -> None:
     """Sum per-rank signal accumulators before a refine."""
     if dist.is_initialized() and dist.get_world_size(group) > 1:

@@ -164,6 +164,31 @@ def test_refine_render_neutral_split():
     tree.validate()
 
 
+def test_rmsprop_row_chunks_equal_full_update():
+    """rows=(lo, hi) updates (used to overlap the gradient all-reduce) compose
+    to exactly the full update."""
+    from paper_2307_15333_b200.optim import RmsPropState, rmsprop_step
+    from paper_2307_15333_b200.parallel import chunk_bounds
+    from paper_2307_15333_b200.render import render_and_backprop
+    from helpers import irregular_tree, ray_batch
+    o, d = ray_batch(12, 4000)
+    tg = np.random.default_rng(13).uniform(0, 1, (4000, 3))
+    trees = [irregular_tree(11, 16, depth=3, splits=20, max_depth=5, device="cuda") for _ in range(2)]
+    _, g, _ = render_and_backprop(trees[0], o, d, tg, 1.0)  # one gradient for both updates
+    g.generation = trees[1].generation
+    outs = []
+    for j, tree in enumerate(trees):
+        st = RmsPropState(tree)
+        if j == 0:
+            rmsprop_step(tree, g, st)
+        else:
+            for lo, hi in chunk_bounds(tree.capacity, 5):
+                rmsprop_step(tree, g, st, rows=(lo, hi))
+        outs.append((tree.sigma.cpu(), tree.sh.cpu(), st.v_sigma.cpu(), st.v_sh.cpu()))
+    for a, b in zip(*outs):
+        assert torch.equal(a, b)
+
+
 def test_rmsprop_bit_exact_vs_oracle(oracle):
     from paper_2307_15333_b200.optim import RmsPropState, rmsprop_step
     from paper_2307_15333_b200.render import GradBuffer
