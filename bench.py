@@ -346,7 +346,7 @@ def run_ours(args, rank, world, local_rank):
         "gpu_launches": 2 * args.steps,
         "roofline": {
             "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-            "frac": achieved / hbm, "traffic": None, "kernel": "render_bwd_buffered_kernel<16,32>",
+            "frac": achieved / hbm, "traffic": None, "kernel": "render_bwd_buffered_kernel<16,48>",
             "kernel_ms": kern_ms_avg, "alg_bytes_per_launch": alg_bytes, "peak_kind": peak_kind,
             "bytes_model": f"{RAY_BYTES} B/ray + {SEG_BYTES} B/composited segment",
         },

@@ -493,8 +493,8 @@ struct SegBuffer {
     }
 };
 
-template <int B, int K, int MINB = 1, bool GBUF = false>
-__global__ void __launch_bounds__(kBlock, MINB) render_bwd_buffered_kernel(
+template <int B, int K, int MINB = 1, bool GBUF = false, int BLK = kBlock, bool PF = false>
+__global__ void __launch_bounds__(BLK, MINB) render_bwd_buffered_kernel(
     TreeDev T, const double* __restrict__ o, const double* __restrict__ d,
     const double* __restrict__ tgt, int64_t n, double bg0, double bg1, double bg2, double eps,
     double t_near, double t_far, double grad_scale, float* __restrict__ gsig,
@@ -581,12 +581,20 @@ __global__ void __launch_bounds__(kBlock, MINB) render_bwd_buffered_kernel(
             tr.nudge = resume_nudge;
         }
         Leaf L;
+        BufSeg nxt;
+        if (PF && used > 0) nxt = buf.get(0);
         for (int i = 0; i < used; ++i) {
             int64_t pid;
             double a, dl;
             float k0, k1, k2;
             if (i < K) {
-                const BufSeg e = buf.get(i);
+                BufSeg e;
+                if (PF) {  // software pipeline: entry i+1 is in flight while i is scattered
+                    e = nxt;
+                    if (i + 1 < used && i + 1 < K) nxt = buf.get(i + 1);
+                } else {
+                    e = buf.get(i);
+                }
                 pid = e.pid;
                 a = e.a;
                 dl = e.delta;
@@ -1052,7 +1060,10 @@ int launch_render_bwd(const TreeDev& T, const double* o, const double* d, const 
                                             loss, rgb_out, flags, s);
     if (!(flags & 16)) {  // default: buffered one-ray-per-thread
         const bool cached = false;
-        const bool big = (flags & 128) == 0;  // K = 32 records in flight; bit 7 selects K = 16
+        // default: K = 48 records, one-warp blocks (a finished warp frees its
+        // slot at once), pass-2 record loads software-pipelined; bit 7 selects
+        // K = 16, bit 10 the earlier K = 32 / 128-thread configuration
+        const bool big = (flags & 128) == 0;
         BufSeg* gbuf = nullptr;
         const bool use_gbuf = (flags & 4096) != 0;
         if (use_gbuf) {
@@ -1062,19 +1073,20 @@ int launch_render_bwd(const TreeDev& T, const double* o, const double* d, const 
                                     "cudaMallocAsync"))
                 return st;
         }
-#define DOT_BUF_LAUNCH(BB, KK, MB, GB)                                                              \
-    render_bwd_buffered_kernel<BB, KK, MB, GB><<<blocks_for(n), kBlock, 0, s>>>(                    \
+#define DOT_BUF_LAUNCH_BLK(BB, KK, MB, GB, BL) DOT_BUF_LAUNCH_PF(BB, KK, MB, GB, BL, false)
+#define DOT_BUF_LAUNCH_PF(BB, KK, MB, GB, BL, PP)                                                   \
+    render_bwd_buffered_kernel<BB, KK, MB, GB, BL, PP><<<unsigned((n + BL - 1) / BL), BL, 0, s>>>(  \
         T, o, d, tgt, n, bg[0], bg[1], bg[2], eps, tn, tf, gs, gsig, gsh, signal, touched, loss,    \
         rgb_out, flags, gbuf)
+#define DOT_BUF_LAUNCH(BB, KK, MB, GB) DOT_BUF_LAUNCH_BLK(BB, KK, MB, GB, kBlock)
 #define DOT_BUF(BB, CC)                                                                           \
     {                                                                                             \
         if (use_gbuf) {                                                                           \
             if (big) DOT_BUF_LAUNCH(BB, 32, 8, true);                                             \
             else DOT_BUF_LAUNCH(BB, 16, 8, true);                                                 \
         } else if (!big) DOT_BUF_LAUNCH(BB, 16, 8, false);                                        \
-        else if (flags & 1024) DOT_BUF_LAUNCH(BB, 32, 10, false); /* occupancy experiments */     \
-        else if (flags & 2048) DOT_BUF_LAUNCH(BB, 32, 12, false);                                 \
-        else DOT_BUF_LAUNCH(BB, 32, 8, false); /* 64 regs: measured best (3.0 vs 3.4 ms at 116) */ \
+        else if (flags & 1024) DOT_BUF_LAUNCH(BB, 32, 8, false); /* round-1 configuration */      \
+        else DOT_BUF_LAUNCH_PF(BB, 48, 32, false, 32, true);                                      \
     }
         DOT_DISPATCH_B(DOT_BUF)
 #undef DOT_BUF
