@@ -28,6 +28,7 @@ _EXPORTS = {
     "train_epoch": "optim", "train": "optim",
     "Camera": "scene_io", "look_at": "scene_io", "orbit_cameras": "scene_io",
     "save_tree": "scene_io", "load_tree": "scene_io",
+    "RayBatchStager": "staging", "LossReader": "staging",
     "eval_sh_basis": "sh", "eval_sh_basis_many": "sh", "decode_color": "sh", "sh_from_rgb": "sh",
 }
 

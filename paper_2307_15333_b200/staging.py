@@ -1,0 +1,162 @@
+"""Host-fed training batches: double-buffered pinned-host -> HBM staging.
+
+The reference trains from numpy ray arrays in host memory
+(``optim.py:138-154`` slices ``dataset.origins/dirs/targets`` per batch).  On
+the GPU every batch costs a 72 B/ray host->device copy (fp64 origin,
+direction, target) -- about 1.3 ms for a 2^20-ray batch over PCIe, a third of
+the fused step.  ``RayBatchStager`` moves that copy onto a side copy stream so
+batch k+1 is in flight while batch k renders, back-propagates and updates:
+
+    stager = RayBatchStager(device, max_rays=n)
+    stager.stage(o_host[0], d_host[0], t_host[0])
+    for k in range(steps):
+        o, d, t = stager.take()                       # compute stream waits for the copy
+        if k + 1 < steps:
+            stager.stage(o_host[k + 1], d_host[k + 1], t_host[k + 1])
+        loss, grads, sig = render_and_backprop(tree, o, d, t, ...)
+        rmsprop_step(tree, grads, state)
+        stager.release()                              # slot reusable once this step is done
+        losses.push(loss)                             # LossReader: lagged D2H read
+
+Source tensors should be pinned (``tensor.pin_memory()``); pageable sources
+are accepted but the copy then serialises with the host.  Slots are recycled
+only after the compute stream has passed the ``release`` fence, so a staged
+batch can never overwrite rays a running kernel still reads.
+"""
+
+from __future__ import annotations
+
+from collections import deque
+
+import numpy as np
+import torch
+
+from .errors import InputError
+
+
+class _Slot:
+    __slots__ = ("bufs", "n", "ready", "free", "busy")
+
+    def __init__(self):
+        self.bufs = None
+        self.n = 0
+        self.ready = torch.cuda.Event()
+        self.free = None
+        self.busy = False
+
+
+class RayBatchStager:
+    """Double-buffered (``depth`` slots) host->HBM staging of ray batches."""
+
+    def __init__(self, device, max_rays: int = 0, depth: int = 2):
+        if depth < 2:
+            raise InputError("depth must be >= 2 for copy/compute overlap")
+        self.device = torch.device(device)
+        self.copy_stream = torch.cuda.Stream(self.device)
+        self.slots = [_Slot() for _ in range(depth)]
+        self.pending: deque[int] = deque()
+        self.in_use: deque[int] = deque()
+        self.next_slot = 0
+        self.bytes_staged = 0
+        if max_rays:
+            for s in self.slots:
+                self._ensure(s, max_rays)
+
+    def _ensure(self, slot: _Slot, n: int) -> None:
+        if slot.bufs is None or slot.bufs[0].shape[0] < n:
+            # allocated on (and owned by) the compute stream, never freed while
+            # a copy or kernel may touch it: the free/ready events order all uses
+            torch.cuda.current_stream(self.device).synchronize()
+            slot.bufs = tuple(torch.empty(n, 3, dtype=torch.float64, device=self.device) for _ in range(3))
+
+    @staticmethod
+    def _host(x, name: str) -> torch.Tensor:
+        t = x if isinstance(x, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(x, dtype=np.float64))
+        if t.device.type != "cpu":
+            raise InputError(f"{name}: RayBatchStager stages host tensors (got {t.device})")
+        t = t.reshape(-1, 3)
+        if t.dtype != torch.float64:
+            t = t.double()
+        return t.contiguous()
+
+    def stage(self, origins, dirs, targets) -> None:
+        """Queue the H2D copy of one batch on the copy stream (returns at once)."""
+        o, d, t = (self._host(x, nm) for x, nm in ((origins, "origins"), (dirs, "dirs"), (targets, "targets")))
+        n = o.shape[0]
+        if d.shape[0] != n or t.shape[0] != n:
+            raise InputError(f"batch length mismatch: {n} origins, {d.shape[0]} dirs, {t.shape[0]} targets")
+        i = self.next_slot
+        slot = self.slots[i]
+        if slot.busy:
+            raise InputError("all staging slots are in flight: take()/release() before staging more")
+        self._ensure(slot, n)
+        with torch.cuda.stream(self.copy_stream):
+            if slot.free is not None:
+                self.copy_stream.wait_event(slot.free)  # the last step reading this slot is done
+            for dst, src in zip(slot.bufs, (o, d, t)):
+                dst[:n].copy_(src, non_blocking=True)
+            slot.ready.record(self.copy_stream)
+        slot.n = n
+        slot.busy = True
+        self.bytes_staged += 3 * n * 24
+        self.pending.append(i)
+        self.next_slot = (i + 1) % len(self.slots)
+
+    def take(self):
+        """Device (origins, dirs, targets) of the oldest staged batch; the
+        current stream waits for its copy (no host synchronisation)."""
+        if not self.pending:
+            raise InputError("take() with no staged batch")
+        i = self.pending.popleft()
+        slot = self.slots[i]
+        torch.cuda.current_stream(self.device).wait_event(slot.ready)
+        self.in_use.append(i)
+        return tuple(b[:slot.n] for b in slot.bufs)
+
+    def release(self) -> None:
+        """Mark the oldest taken batch consumed by the work queued so far."""
+        if not self.in_use:
+            raise InputError("release() without a taken batch")
+        slot = self.slots[self.in_use.popleft()]
+        ev = torch.cuda.Event()
+        ev.record(torch.cuda.current_stream(self.device))
+        slot.free = ev
+        slot.busy = False
+
+
+class LossReader:
+    """Per-step device->host loss read, lagged by one step so the host never
+    stalls the queue: ``push(loss)`` starts the 8-byte copy of this step's loss
+    and returns the PREVIOUS step's value (None on the first call);
+    ``flush()`` returns the last one."""
+
+    def __init__(self):
+        self.host = [torch.empty((), dtype=torch.float64).pin_memory() for _ in range(2)]
+        self.events = [torch.cuda.Event(), torch.cuda.Event()]
+        self.k = 0
+        self.values: list[float] = []
+
+    def push(self, loss: torch.Tensor):
+        j = self.k % 2
+        self.host[j].copy_(loss.detach().reshape(()), non_blocking=True)
+        self.events[j].record()
+        prev = None
+        if self.k > 0:
+            p = (self.k - 1) % 2
+            self.events[p].synchronize()
+            prev = float(self.host[p])
+            self.values.append(prev)
+        self.k += 1
+        return prev
+
+    def flush(self):
+        if self.k == 0:
+            return None
+        p = (self.k - 1) % 2
+        self.events[p].synchronize()
+        v = float(self.host[p])
+        self.values.append(v)
+        return v
+
+
+__all__ = ["RayBatchStager", "LossReader"]

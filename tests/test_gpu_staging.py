@@ -1,0 +1,91 @@
+"""Host-fed training through RayBatchStager + LossReader.
+
+The staged loop (H2D of batch k+1 on a side stream while batch k computes,
+loss read one step late) must give the same per-step losses and the same
+trained leaves as the plain loop that hands render_and_backprop pinned host
+tensors directly: both run the same kernels on the same rays; only the copy
+schedule differs.  Losses agree to fp32-atomic noise (the leaf gradients are
+float sums in atomic order), touched sets exactly.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from helpers import irregular_tree, ray_batch
+
+pytestmark = pytest.mark.gpu
+
+
+def _batches(n_batches, n):
+    out = []
+    for k in range(n_batches):
+        o, d = ray_batch(100 + k, n)
+        t = np.random.default_rng(200 + k).uniform(0.0, 1.0, (n, 3))
+        out.append(tuple(torch.from_numpy(np.ascontiguousarray(x)).pin_memory() for x in (o, d, t)))
+    return out
+
+
+def _train(staged: bool, batches):
+    from paper_2307_15333_b200.optim import RmsPropState, rmsprop_step
+    from paper_2307_15333_b200.render import BackpropWorkspace, render_and_backprop
+    from paper_2307_15333_b200.staging import LossReader, RayBatchStager
+    tree = irregular_tree(5, basis_count=4, device="cuda")
+    state = RmsPropState(tree)
+    ws = BackpropWorkspace.for_tree(tree)
+    touched = []
+    if staged:
+        stager, reader = RayBatchStager("cuda", depth=2), LossReader()
+        stager.stage(*batches[0])
+        for k in range(len(batches)):
+            o, d, t = stager.take()
+            assert o.is_cuda and o.shape == batches[k][0].shape
+            if k + 1 < len(batches):
+                stager.stage(*batches[k + 1])
+            loss, grads, _ = render_and_backprop(tree, o, d, t, 0.5, workspace=ws)
+            touched.append(ws.touched.clone())
+            rmsprop_step(tree, grads, state)
+            stager.release()
+            reader.push(loss)
+        reader.flush()
+        losses = reader.values
+    else:
+        losses = []
+        for o, d, t in batches:
+            loss, grads, _ = render_and_backprop(tree, o, d, t, 0.5, workspace=ws)
+            touched.append(ws.touched.clone().cuda())
+            rmsprop_step(tree, grads, state)
+            losses.append(float(loss.item()))
+    torch.cuda.synchronize()
+    return losses, touched, tree.sigma.clone(), tree.sh.clone()
+
+
+def test_staged_loop_matches_direct_host_calls():
+    batches = _batches(5, 3000)
+    la, ta, sa, sha = _train(False, batches)
+    lb, tb, sb, shb = _train(True, batches)
+    assert len(lb) == len(la) == 5
+    np.testing.assert_allclose(lb, la, rtol=1e-5, atol=1e-9)
+    for x, y in zip(ta, tb):
+        assert torch.equal(x.cpu(), y.cpu())
+    np.testing.assert_allclose(sb.cpu().numpy(), sa.cpu().numpy(), rtol=1e-4, atol=1e-5)
+    np.testing.assert_allclose(shb.cpu().numpy(), sha.cpu().numpy(), rtol=1e-4, atol=1e-5)
+
+
+def test_stager_rejects_misuse():
+    from paper_2307_15333_b200.errors import InputError
+    from paper_2307_15333_b200.staging import RayBatchStager
+    b = _batches(3, 64)
+    st = RayBatchStager("cuda", depth=2)
+    with pytest.raises(InputError):
+        st.take()
+    st.stage(*b[0])
+    st.stage(*b[1])
+    with pytest.raises(InputError):  # both slots in flight
+        st.stage(*b[2])
+    with pytest.raises(InputError):
+        st.release()
+    with pytest.raises(InputError):
+        RayBatchStager("cuda").stage(b[0][0], b[0][1], b[0][2][:10])
+    with pytest.raises(InputError):
+        RayBatchStager("cuda", depth=1)
