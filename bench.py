@@ -116,7 +116,7 @@ class ClockSampler:
 # ---------------------------------------------------------------------------
 # workload
 
-def view_rays_torch(focal, pose, device):
+def view_rays_torch(focal, pose, device, W=W, H=H):
     import torch
     xs = (torch.arange(W, dtype=torch.float64, device=device) + 0.5 - 0.5 * W) / focal
     ys = -(torch.arange(H, dtype=torch.float64, device=device) + 0.5 - 0.5 * H) / focal
@@ -140,7 +140,7 @@ def _spread10(v):
     return v
 
 
-def morton_key(idx):
+def morton_key(idx, W=W, H=H):
     """(view, Morton(x, y)) key of pool indices (pool is view-major, row-major)."""
     view = idx // (W * H)
     pix = idx - view * (W * H)
@@ -162,13 +162,46 @@ def perturbed(tree, seed):
                                   topo.node, tree._sigma, sh, topo.level_offsets)
 
 
-def build_training_pool(tree, device, n_views=N_VIEWS):
-    """All rays of the 100 training views + targets rendered from a perturbed copy."""
-    import torch
+class Workload:
+    """A training-step workload: scene, camera rig, pool views, batch per rank."""
+
+    def __init__(self, key, scene, cameras, w, h, views, batch, scaling, desc, l2):
+        self.key, self.scene, self.cameras = key, scene, cameras
+        self.W, self.H, self.views, self.batch = w, h, views, batch
+        self.scaling, self.desc, self.l2 = scaling, desc, l2
+
+
+def workloads():
     from paper_2307_15333_b200 import scenes
+    return {
+        "c2": Workload(
+            "c2", lambda dev: scenes.config2_scene(device=dev),
+            lambda: scenes.hemisphere_cameras(N_VIEWS, W, H, RADIUS, seed=3), W, H, N_VIEWS,
+            lambda world: BATCH, "weak",
+            "configs[1] training step: depth-9 SH-3 scene, 2^20-ray batch per GPU, "
+            "fwd+bwd+signal, NCCL grad all-reduce (N>1), RMSProp",
+            "inputs larger than L2 (2.6M-leaf payload 0.51 GB, 100-view ray pool 4.6 GB, "
+            "random 2^20-ray batches)"),
+        "c4": Workload(
+            "c4", lambda dev: scenes.config4_scene(device=dev),
+            lambda: scenes.ring_cameras(32, 1920, 1080, 3.0, seed=6), 1920, 1080, 32,
+            lambda world: (1 << 21) // world, "strong",
+            "configs[3] training step: depth-10 SH-3 scene over the 2x bbox (256 anisotropic "
+            "blobs + ground slab), 1920x1080 ring cameras, 2^21-ray global batch sharded over "
+            "the GPUs, fwd+bwd+signal, NCCL grad all-reduce (N>1), RMSProp",
+            "inputs larger than L2 (8.5M-leaf payload 1.9 GB, 32-view ray pool 4.8 GB, "
+            "random 2^21-ray global batches)"),
+    }
+
+
+def build_training_pool(tree, device, wl=None):
+    """All rays of the workload's training views + targets rendered from a perturbed copy."""
+    import torch
     from paper_2307_15333_b200.render import render_rays
-    focal, poses = scenes.hemisphere_cameras(n_views, W, H, RADIUS, seed=3)
-    os_, ds_ = zip(*(view_rays_torch(focal, p, device) for p in poses))
+    if wl is None:
+        wl = workloads()["c2"]
+    focal, poses = wl.cameras()
+    os_, ds_ = zip(*(view_rays_torch(focal, p, device, wl.W, wl.H) for p in poses))
     origins, dirs = torch.cat(os_), torch.cat(ds_)
     del os_, ds_
     target_tree = perturbed(tree, 21)
@@ -194,10 +227,11 @@ def run_ours(args, rank, world, local_rank):
     torch.cuda.set_device(dev)
     _lib.check(_lib.load().dot_device_check(), "device check")
     t_setup = time.time()
-    tree = scenes.config2_scene(device=dev)
-    origins, dirs, targets = build_training_pool(tree, dev)
+    wl = workloads()[args.workload]
+    tree = wl.scene(dev)
+    origins, dirs, targets = build_training_pool(tree, dev, wl)
     n_pool = origins.shape[0]
-    per_rank = BATCH
+    per_rank = wl.batch(world)
     n_global = per_rank * world
     gs = 2.0 / n_global
     state = RmsPropState(tree)
@@ -219,7 +253,7 @@ def run_ours(args, rank, world, local_rank):
         if args.order == "raster":
             idx = idx.sort().values
         elif args.order == "morton":
-            idx = idx[torch.argsort(morton_key(idx))]
+            idx = idx[torch.argsort(morton_key(idx, wl.W, wl.H))]
         return idx
 
     from paper_2307_15333_b200.parallel import allreduce_grads_overlapped, chunk_bounds
@@ -335,12 +369,13 @@ def run_ours(args, rank, world, local_rank):
     e2e_value = n_global * args.steps / (e2e_ms / 1e3)
 
     # render (configs[2]) and refine (configs[4]) side measurements
-    render = None if args.skip_render else bench_render(tree, dev, args, world)
+    side = wl.key == "c2"  # render/refine/CPU legs belong to the default (configs[1]) line
+    render = None if (args.skip_render or not side) else bench_render(tree, dev, args, world)
     del origins, dirs, targets, perm
     torch.cuda.empty_cache()
-    refine = None if (args.skip_refine or rank != 0) else bench_refine(dev, args)
+    refine = None if (args.skip_refine or rank != 0 or not side) else bench_refine(dev, args)
     cpu = None
-    if rank == 0 and not args.skip_cpu:
+    if rank == 0 and not args.skip_cpu and side:
         cpu = cpu_baseline(tree, args)
 
     if rank != 0:
@@ -354,19 +389,17 @@ def run_ours(args, rank, world, local_rank):
         "warmup": args.warmup,
         "ms_per_step": ms_step,
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": wl.scaling,
         "vs_baseline": None,
         "dtype": "f64",
         "dtype_detail": "f64 traversal/transmittance/accumulation, f32 SH shading and leaf gradients",
         "data": "synthetic (seeded blob-field scene, random-init SH, targets from a perturbed copy)",
         "config": {
-            "workload": "configs[1] training step: depth-9 SH-3 scene, 2^20-ray batch per GPU, "
-                        "fwd+bwd+signal, NCCL grad all-reduce (N>1), RMSProp",
+            "workload": wl.desc,
             "leaves": int(tree.leaf_count), "nodes": int(tree.topology().n_nodes),
-            "global_batch": n_global, "views": N_VIEWS, "resolution": [W, H],
+            "global_batch": n_global, "views": wl.views, "resolution": [wl.W, wl.H],
             "segments_per_ray": seg / per_rank, "composited_per_ray": comp / per_rank,
-            "l2": "inputs larger than L2 (2.6M-leaf payload 0.51 GB, 100-view ray pool 4.6 GB, "
-                  "random 2^20-ray batches)",
+            "l2": wl.l2,
             "parallelism": f"rays sharded dp{world}, tree replicated",
             "batch_order": args.order, "bwd_flags": args.bwd_flags,
         },
@@ -584,6 +617,8 @@ def main():
     ap.add_argument("--skip-refine", action="store_true")
     ap.add_argument("--skip-cpu", action="store_true")
     ap.add_argument("--ref-sample", type=int, default=1 << 14)
+    ap.add_argument("--workload", choices=["c2", "c4"], default="c2",
+                    help="c2 = configs[1] (the headline line), c4 = configs[3] (8.5M leaves, 1080p)")
     ap.add_argument("--order", choices=["random", "raster", "morton"], default="random",
                     help="batch ray order handed to the kernel (same ray set)")
     ap.add_argument("--ar-chunks", type=int, default=4,

@@ -241,6 +241,36 @@ def config2_scene(device=None, basis_count: int = 16):
 CONFIG2_SPLIT_THR = 800.0  # -> 2.62M leaves, 3.0M nodes (tools/tune_scenes.py)
 
 
+def config4_field() -> BlobField:
+    """BASELINE.json configs[3]: 256 anisotropic blobs over the 2x bbox plus a
+    dense ground slab whose underside is the bbox floor (so only its top face
+    is a density discontinuity)."""
+    return BlobField.make(seed=4, n_blobs=256, anisotropic=True, scale=2.0, slab=(-1.5, 0.5, 30.0))
+
+
+def config4_scene(device=None, basis_count: int = 16, split_thr: float | None = None):
+    """BASELINE.json configs[3] (Tanks&Temples-shaped): depth 10 over [-2, 2]^3, SH-3, ~8M leaves."""
+    return adaptive_tree(config4_field(), max_depth=10, basis_count=basis_count,
+                         split_thr=CONFIG4_SPLIT_THR if split_thr is None else split_thr,
+                         empty_thr=0.05, min_depth=4, half_extent=2.0, sh_seed=40, device=device)
+
+
+CONFIG4_SPLIT_THR = 1000.0  # -> 8.52M leaves, 9.74M nodes (tools/tune_c4.py; 2000 stops at depth 4)
+
+
+def ring_cameras(count: int, width: int, height: int, radius: float, seed: int,
+                 elevation_jitter_deg: float = 15.0, camera_angle_x: float = FOV_40):
+    """Cameras on a ring around the origin at +/- jittered elevation (configs[3])."""
+    rng = np.random.default_rng(seed)
+    focal = focal_from_angle(width, camera_angle_x)
+    poses = []
+    for i in range(count):
+        az = 2.0 * math.pi * i / count
+        el = math.radians(rng.uniform(-elevation_jitter_deg, elevation_jitter_deg))
+        poses.append(orbit_pose(radius, az, el))
+    return focal, poses
+
+
 def hemisphere_cameras(count: int, width: int, height: int, radius: float, seed: int,
                        camera_angle_x: float = FOV_40):
     """Cameras on the upper hemisphere looking at the origin (NeRF-synthetic-shaped)."""

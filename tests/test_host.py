@@ -184,6 +184,27 @@ def test_adaptive_scene_small_cpu():
     assert tree.topology().pool_id is None
 
 
+def test_config4_rig_and_field():
+    """configs[3] stand-ins: ring cameras at r = 3 with |elevation| <= 15 deg
+    looking at the origin; slab underside on the 2x bbox floor."""
+    import math
+    from paper_2307_15333_b200 import scenes
+    focal, poses = scenes.ring_cameras(32, 1920, 1080, 3.0, seed=6)
+    assert focal == pytest.approx(0.5 * 1920 / math.tan(0.5 * scenes.FOV_40))
+    for p in poses:
+        eye = p[:3, 3]
+        assert np.linalg.norm(eye) == pytest.approx(3.0)
+        assert abs(math.degrees(math.asin(eye[2] / 3.0))) <= 15.0 + 1e-9
+        np.testing.assert_allclose(-p[:3, 2], -eye / 3.0, atol=1e-12)  # camera looks along -z
+    f = scenes.config4_field()
+    z_top, thick, dens = f.slab
+    assert z_top - thick == pytest.approx(-2.0) and dens > 0
+    assert f.mu.shape == (256, 3) and np.abs(f.mu).max() <= 1.2
+    tree = scenes.adaptive_tree(f, max_depth=5, basis_count=1, split_thr=1000.0, min_depth=2,
+                                half_extent=2.0, device="cpu")
+    tree.validate()
+
+
 def test_sh_basis_matches_kernel_constants():
     from paper_2307_15333_b200.sh import eval_sh_basis
     b = eval_sh_basis(3, np.array([0.0, 0.0, 1.0]))
