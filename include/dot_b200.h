@@ -47,13 +47,28 @@ typedef struct dot_tree_view {
     double center[3];         /* root cube centre                            */
     double half_extent;       /* root cube half edge                         */
     int32_t max_depth;
-    int32_t _pad;
+    int32_t locate_level;     /* L of the locate table, 0 = none             */
+    const int32_t* locate;    /* [8^L] from dot_locate_build, or NULL        */
 } dot_tree_view;
 
 /* Library identity / diagnostics. */
 int dot_abi_version(void);
 const char* dot_last_error(void);
 int dot_device_check(void);
+
+/* --- locate table (no reference counterpart; accelerates _descend,
+ *     _kernels.py:56-68): for a dyadic root (half_extent a power of two,
+ *     centre a multiple of half * 2^-20, max_depth <= 21, capacity < 2^26)
+ *     table[x + (y << L) + (z << 2L)] (8^L int32, device) receives the node
+ *     word at depth L on the path to grid cell (x, y, z), or
+ *     INT32_MIN | depth << 26 | pool_id for a leaf shallower than L.  The
+ *     traversal kernels then replace the first L dependent node loads of
+ *     every root descent by one table load (exact: same leaf as the fp64
+ *     descent).  Set view.locate / view.locate_level to use it; a view whose
+ *     root is not dyadic ignores it.  Returns DOT_BAD_ARG for non-dyadic
+ *     roots or L outside 1..9. */
+int dot_locate_supported(const dot_tree_view* tree);
+int dot_locate_build(const dot_tree_view* tree, int32_t level, int32_t* table, void* stream);
 
 /* --- traversal (replaces count_segments_kernel / fill_segments_kernel,
  *     _kernels.py:161-182, driven by render.segment_batch render.py:105-124) */

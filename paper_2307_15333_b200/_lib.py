@@ -16,6 +16,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libdot_b200.so")
 
 DOT_OK, DOT_BAD_ARG, DOT_OOM, DOT_CUDA_ERR, DOT_NO_DEVICE = range(5)
+ABI_VERSION = 2
 
 c_void_p = ctypes.c_void_p
 c_i64 = ctypes.c_int64
@@ -27,7 +28,8 @@ class DotTreeView(ctypes.Structure):
     _fields_ = [
         ("node", c_void_p), ("n_nodes", c_i64), ("sigma", c_void_p), ("sh", c_void_p),
         ("capacity", c_i64), ("basis_count", c_i32), ("sh_stride", c_i32),
-        ("center", c_f64 * 3), ("half_extent", c_f64), ("max_depth", c_i32), ("_pad", c_i32),
+        ("center", c_f64 * 3), ("half_extent", c_f64), ("max_depth", c_i32),
+        ("locate_level", c_i32), ("locate", c_void_p),
     ]
 
 
@@ -43,6 +45,8 @@ _SIGNATURES = {
     "dot_abi_version": (c_i32, []),
     "dot_last_error": (ctypes.c_char_p, []),
     "dot_device_check": (c_i32, []),
+    "dot_locate_supported": (c_i32, [c_void_p]),
+    "dot_locate_build": (c_i32, [c_void_p, c_i32, c_void_p, c_void_p]),
     "dot_trace_count": (c_i32, [c_void_p, c_void_p, c_void_p, c_i64, c_f64, c_f64, c_void_p, c_void_p]),
     "dot_trace_fill": (c_i32, [c_void_p, c_void_p, c_void_p, c_i64, c_f64, c_f64, c_void_p, c_void_p,
                                c_void_p, c_void_p, c_void_p]),
@@ -92,6 +96,9 @@ def load(path: str = LIB_PATH):
             fn = getattr(lib, name)
             fn.restype = res
             fn.argtypes = args
+        if lib.dot_abi_version() != ABI_VERSION:
+            raise ExtensionError(f"{path} has ABI {lib.dot_abi_version()}, expected {ABI_VERSION}; "
+                                 "rebuild it with `python -m paper_2307_15333_b200.build`")
         _lib = lib
         return lib
 

@@ -65,7 +65,7 @@ using namespace dot;
 
 extern "C" {
 
-int dot_abi_version(void) { return 1; }
+int dot_abi_version(void) { return 2; }
 
 const char* dot_last_error(void) { return g_err; }
 
@@ -78,6 +78,22 @@ int dot_device_check(void) {
     cudaGetDeviceProperties(&p, dev);
     if (p.major != 10) return set_error(DOT_NO_DEVICE, "device %s is sm_%d%d, need sm_100", p.name, p.major, p.minor);
     return DOT_OK;
+}
+
+int dot_locate_supported(const dot_tree_view* tree) {
+    if (validate_tree(tree)) return 0;
+    return locate_dyadic(*tree) ? 1 : 0;
+}
+
+int dot_locate_build(const dot_tree_view* tree, int32_t level, int32_t* table, void* stream) {
+    if (int st = validate_tree(tree)) return st;
+    if (!locate_dyadic(*tree))
+        return set_error(DOT_BAD_ARG, "locate table needs a dyadic root (half_extent a power of two, "
+                                      "centre a multiple of half * 2^-20, max_depth <= 21, capacity < 2^26)");
+    if (level < 1 || level > 9 || false)
+        return set_error(DOT_BAD_ARG, "locate level must be in 1..9, got %d", level);
+    if (!table) return set_error(DOT_BAD_ARG, "locate table is NULL");
+    return launch_locate_build(make_tree(*tree), level, table, static_cast<cudaStream_t>(stream));
 }
 
 int dot_trace_count(const dot_tree_view* tree, const double* origins, const double* dirs,

@@ -40,6 +40,7 @@ int launch_ray_keys32(const TreeDev& T, const double* o, const double* d, int64_
                       cudaStream_t s);
 int launch_render_camera(const TreeDev& T, const double* cam_to_world, double focal, int width, int height,
                          const double* bg, double eps, float* rgb, float* tfin, float* depth, cudaStream_t s);
+int launch_locate_build(const TreeDev& T, int level, int32_t* table, cudaStream_t s);
 int launch_ray_stats(const TreeDev& T, const double* o, const double* d, int64_t n, double eps,
                      unsigned long long* out, cudaStream_t s);
 

@@ -5,6 +5,8 @@
 // intrinsic (__dadd_rn/__dmul_rn/__ddiv_rn), so nvcc can never contract it
 // into an FMA (the Numba kernels contain none) and division is IEEE.
 #pragma once
+#include <climits>
+#include <cmath>
 #include <cstdint>
 #include <cuda_runtime.h>
 #include "../../include/dot_b200.h"
@@ -22,7 +24,33 @@ struct TreeDev {
     int32_t sh_stride;
     double cx, cy, cz, half;
     int32_t max_depth;
+    // Locate table (dyadic trees only, see descend_grid): node word at depth
+    // loc_level for every cell of the 2^L x 2^L x 2^L grid; NULL = disabled.
+    const int32_t* __restrict__ loc;
+    int32_t loc_level;
+    double loc_scale;          // 2^(kLocBits-1) / half  (a power of two)
+    double loc_lo[3];          // (center - half) * loc_scale (integers)
 };
+
+constexpr int kLocBits = 21;                 // cell coordinates at depth 21
+constexpr int32_t kLocLeafFlag = INT32_MIN;  // table entry: leaf shallower than L
+constexpr int kLocPidBits = 26;              // entry = flag | depth << 26 | pid
+
+// True when every node centre down to depth kLocBits is an exact multiple of
+// half * 2^-kLocBits, so the fp64 comparisons of the descent can be restated
+// exactly in integer cell coordinates (descend_grid).
+inline bool locate_dyadic(const dot_tree_view& v) {
+    int e = 0;
+    if (!(v.half_extent > 0.0) || std::frexp(v.half_extent, &e) != 0.5) return false;
+    if (v.max_depth > kLocBits || v.max_depth < 0) return false;
+    if (v.capacity >= (int64_t(1) << kLocPidBits)) return false;
+    const double s = std::ldexp(1.0, kLocBits - 1) / v.half_extent;
+    for (int a = 0; a < 3; ++a) {
+        const double cs = v.center[a] * s;  // exact (power-of-two scale)
+        if (!(std::fabs(cs) < 1125899906842624.0) || std::floor(cs) != cs) return false;
+    }
+    return true;
+}
 // (Staging the upper levels in shared memory was measured and rejected: the
 // hot top levels already hit L1, and the per-level shared/global select
 // slowed the forward by 9 %.)
@@ -40,6 +68,16 @@ inline TreeDev make_tree(const dot_tree_view& v) {
     t.cz = v.center[2];
     t.half = v.half_extent;
     t.max_depth = v.max_depth;
+    t.loc = nullptr;
+    t.loc_level = 0;
+    t.loc_scale = 0.0;
+    t.loc_lo[0] = t.loc_lo[1] = t.loc_lo[2] = 0.0;
+    if (v.locate && v.locate_level > 0 && v.locate_level <= 9 && locate_dyadic(v)) {
+        t.loc = v.locate;
+        t.loc_level = v.locate_level;
+        t.loc_scale = std::ldexp(1.0, kLocBits - 1) / v.half_extent;
+        for (int a = 0; a < 3; ++a) t.loc_lo[a] = (v.center[a] - v.half_extent) * t.loc_scale;
+    }
     return t;
 }
 
@@ -56,7 +94,10 @@ struct Leaf {
 
 // _kernels.py:56-68 from the root, with child centres recomputed exactly:
 // c_child = c + (h_parent * 0.5) * sign  (octree.py:228-238).
+__device__ __forceinline__ Leaf descend_grid(const TreeDev& T, double px, double py, double pz);
+
 __device__ __forceinline__ Leaf descend(const TreeDev& T, double px, double py, double pz) {
+    if (T.loc) return descend_grid(T, px, py, pz);
     double cx = T.cx, cy = T.cy, cz = T.cz, h = T.half;
     int32_t w = __ldg(T.node);
     while (w >= 0) {
@@ -73,6 +114,55 @@ __device__ __forceinline__ Leaf descend(const TreeDev& T, double px, double py, 
     L.cy = cy;
     L.cz = cz;
     L.h = h;
+    return L;
+}
+
+// Exact integer restatement of descend() for dyadic trees (locate_dyadic).
+// With s = 2^20 / h (a power of two) every centre c_j at depth j < 21 has
+// c_j * s integer, and scaling by s is exact, so
+//     p >= c_j  <=>  floor(p * s) >= c_j * s  <=>  bit (20 - j) of
+//     ix = floor(p * s) - (c_root - h) * s  is set
+// (given the higher bits select the same cell).  Points that round outside
+// the root cube clamp to 0 / 2^21 - 1, i.e. "all comparisons false / true";
+// NaN clamps to 0 (every comparison false), exactly like the fp64 chain.
+// The first loc_level levels are one load from the locate table; the leaf
+// centre c = lo + (2 i_d + 1) h_d is the same exact value the fp64
+// recurrence c + (h * 0.5) * sign produces (both are exactly representable).
+__device__ __forceinline__ double pow2i(int e) {  // 2^e, |e| < 1000
+    return __longlong_as_double(int64_t(1023 + e) << 52);
+}
+
+__device__ __forceinline__ Leaf descend_grid(const TreeDev& T, double px, double py, double pz) {
+    const double s = T.loc_scale, top = double((1 << kLocBits) - 1);
+    const double fx = fmin(fmax(dsub(floor(dmul(px, s)), T.loc_lo[0]), 0.0), top);
+    const double fy = fmin(fmax(dsub(floor(dmul(py, s)), T.loc_lo[1]), 0.0), top);
+    const double fz = fmin(fmax(dsub(floor(dmul(pz, s)), T.loc_lo[2]), 0.0), top);
+    const int ix = __double2int_rz(fx), iy = __double2int_rz(fy), iz = __double2int_rz(fz);
+    const int Lv = T.loc_level, k = kLocBits - Lv;
+    const int32_t e = __ldg(T.loc + ((ix >> k) | ((iy >> k) << Lv) | ((iz >> k) << (2 * Lv))));
+    int dep, pid;
+    if (e >= 0) {
+        int32_t w = e;
+        dep = Lv;
+        do {
+            const int b = kLocBits - 1 - dep;
+            const int o = ((ix >> b) & 1) | (((iy >> b) & 1) << 1) | (((iz >> b) & 1) << 2);
+            w = __ldg(T.node + w + o);
+            ++dep;
+        } while (w >= 0);
+        pid = ~w;
+    } else {
+        dep = (e >> kLocPidBits) & 31;
+        pid = e & ((1 << kLocPidBits) - 1);
+    }
+    const double hd = dmul(T.half, pow2i(-dep));
+    const int sh = kLocBits - dep;
+    Leaf L;
+    L.pid = pid;
+    L.h = hd;
+    L.cx = dadd(dsub(T.cx, T.half), dmul(double(2 * (ix >> sh) + 1), hd));
+    L.cy = dadd(dsub(T.cy, T.half), dmul(double(2 * (iy >> sh) + 1), hd));
+    L.cz = dadd(dsub(T.cz, T.half), dmul(double(2 * (iz >> sh) + 1), hd));
     return L;
 }
 

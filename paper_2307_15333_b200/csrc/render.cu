@@ -576,6 +576,7 @@ __global__ void __launch_bounds__(BLK, MINB) render_bwd_buffered_kernel(
         const double g0 = grad_scale * r0, g1 = grad_scale * r1, g2 = grad_scale * r2;
         // ---- pass 2: replay (suffix carried directly: suf = rgb - prefix)
         double s0 = R0, s1 = R1, s2 = R2, Ti = 1.0;
+        if (flags & 8192) used = 0;  // diagnostic: pass 1 only
         if (used > K) {  // segment K onwards come from a resumed walk
             tr.t = resume_t;
             tr.nudge = resume_nudge;
@@ -622,10 +623,15 @@ __global__ void __launch_bounds__(BLK, MINB) render_bwd_buffered_kernel(
             s2 -= tq * double(k2);
             const double tn = Ti * a;
             const double ds = dl * (g0 * (tn * k0 - s0) + g1 * (tn * k1 - s1) + g2 * (tn * k2 - s2));
-            red_add_f32(gsig + pid, float(ds));
             const float w0 = float(g0 * tq) * k0 * (1.f - k0);
             const float w1 = float(g1 * tq) * k1 * (1.f - k1);
             const float w2 = float(g2 * tq) * k2 * (1.f - k2);
+            if (flags & 16384) {  // diagnostic: no reductions
+                if (ds == 12345.0 && w0 == 1.f) red_add_f32(gsig + pid, w1 + w2);
+                Ti *= a;
+                continue;
+            }
+            red_add_f32(gsig + pid, float(ds));
             if (w0 != 0.f || w1 != 0.f || w2 != 0.f) {
                 float* row = gsh + pid * S;
 #pragma unroll
@@ -986,6 +992,31 @@ int launch_ray_stats(const TreeDev& T, const double* o, const double* d, int64_t
 // ---------------------------------------------------------------------------
 
 static unsigned blocks_for(int64_t n) { return unsigned((n + kBlock - 1) / kBlock); }
+
+// Locate table: one thread per depth-L cell walks the node table from the
+// root with the cell's octant bits (integer only) and stores the node word at
+// depth L, or the leaf it stops at (flag | depth << 26 | pool id).
+__global__ void locate_build_kernel(TreeDev T, int level, int32_t* __restrict__ table) {
+    const int64_t cells = int64_t(1) << (3 * level);
+    const int64_t c = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (c >= cells) return;
+    const int mask = (1 << level) - 1;
+    const int x = int(c) & mask, y = int(c >> level) & mask, z = int(c >> (2 * level)) & mask;
+    int32_t w = T.node[0];
+    int dep = 0;
+    while (w >= 0 && dep < level) {
+        const int b = level - 1 - dep;
+        w = T.node[w + (((x >> b) & 1) | (((y >> b) & 1) << 1) | (((z >> b) & 1) << 2))];
+        ++dep;
+    }
+    table[c] = w >= 0 ? w : (kLocLeafFlag | (dep << kLocPidBits) | ~w);
+}
+
+int launch_locate_build(const TreeDev& T, int level, int32_t* table, cudaStream_t s) {
+    const int64_t cells = int64_t(1) << (3 * level);
+    locate_build_kernel<<<blocks_for(cells), kBlock, 0, s>>>(T, level, table);
+    return check_launch("locate_build_kernel");
+}
 
 // Grid for grid-stride kernels: every SM filled to its occupancy limit.
 template <typename K>

@@ -23,7 +23,9 @@ pool; the host arrays are materialised only if a host API asks for them.
 
 from __future__ import annotations
 
+import ctypes
 import math
+import os
 from dataclasses import dataclass, field
 from typing import Callable, Sequence, Union
 
@@ -84,10 +86,17 @@ class DeviceTopology:
     node: torch.Tensor                 # int32 [n_nodes], device
     pool_id: torch.Tensor | None       # int32 [n_nodes] pool id per canonical node, None = identity
     level_offsets: np.ndarray          # int64 [levels + 1], BFS level boundaries
+    locate: torch.Tensor | None = None  # int32 [8^L] locate table (dot_locate_build)
+    locate_level: int = -1             # -1 = not built yet, 0 = not used
 
     @property
     def n_nodes(self) -> int:
         return int(self.node.shape[0])
+
+
+def locate_level_default() -> int:
+    """Level of the traversal locate table (env DOT_LOCATE_LEVEL, 0 = off)."""
+    return int(os.environ.get("DOT_LOCATE_LEVEL", "7"))
 
 
 class SparseOctree:
@@ -240,7 +249,29 @@ class SparseOctree:
             v.center[k] = float(self.center[k])
         v.half_extent = self.half_extent
         v.max_depth = self.max_depth
+        v.locate_level = 0
+        v.locate = None
+        self._attach_locate(v, topo)
         return v, topo
+
+    def _attach_locate(self, v, topo: DeviceTopology) -> None:
+        """Locate table of this generation (built once, lazily): replaces the
+        first L node loads of every traversal descent by one table load; used
+        only for dyadic roots, where it is exact (dot_b200.h)."""
+        from . import _lib
+        if topo.locate_level < 0:
+            topo.locate_level = 0
+            want = locate_level_default()
+            deepest = len(topo.level_offsets) - 2
+            lib = _lib.load()
+            if want > 0 and 0 < deepest <= 21 and lib.dot_locate_supported(ctypes.byref(v)):
+                lv = min(want, deepest)
+                table = torch.empty(1 << (3 * lv), dtype=torch.int32, device=self.device)
+                _lib.call("dot_locate_build", ctypes.byref(v), lv, _lib.ptr(table), _lib.stream_ptr())
+                topo.locate, topo.locate_level = table, lv
+        if topo.locate_level > 0 and _lib.load().dot_locate_supported(ctypes.byref(v)):
+            v.locate_level = topo.locate_level
+            v.locate = topo.locate.data_ptr()
 
     # ------------------------------------------------------------------
     # Queries (octree.py:115-181)

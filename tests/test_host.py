@@ -29,7 +29,7 @@ def test_library_exports_every_header_symbol():
     for s in syms:
         assert hasattr(lib, s), s
     assert set(syms) == set(_lib.symbols())
-    assert lib.dot_abi_version() == 1
+    assert lib.dot_abi_version() == _lib.ABI_VERSION == 2
 
 
 def test_library_is_sm100a():
@@ -210,3 +210,37 @@ def test_sh_basis_matches_kernel_constants():
     b = eval_sh_basis(3, np.array([0.0, 0.0, 1.0]))
     assert b[0] == pytest.approx(0.28209479177387814)
     assert b[2] == pytest.approx(0.4886025119029199)
+
+
+def test_locate_dyadic_predicate():
+    """dot_locate_supported is host-only (no GPU needed): the locate table is
+    used exactly when the integer restatement of the descent is exact."""
+    import ctypes
+    from paper_2307_15333_b200 import _lib
+    lib = _lib.load()
+    dummy = (ctypes.c_int32 * 4)()
+    sh = (ctypes.c_float * 16)()
+
+    def view(center, half, max_depth=9, capacity=1000):
+        v = _lib.DotTreeView()
+        v.node = ctypes.addressof(dummy)
+        v.n_nodes = 1
+        v.sigma = ctypes.addressof(sh)
+        v.sh = (ctypes.addressof(sh) + 15) // 16 * 16
+        v.capacity = capacity
+        v.basis_count = 1
+        v.sh_stride = 4
+        for k in range(3):
+            v.center[k] = center[k]
+        v.half_extent = half
+        v.max_depth = max_depth
+        return lib.dot_locate_supported(ctypes.byref(v))
+
+    assert view((0, 0, 0), 1.0) == 1
+    assert view((0.5, -0.25, 2.0), 0.5) == 1
+    assert view((2.0 ** -20, 0, 0), 1.0) == 1
+    assert view((2.0 ** -21, 0, 0), 1.0) == 0
+    assert view((0.1, 0, 0), 1.0) == 0
+    assert view((0, 0, 0), 0.75) == 0
+    assert view((0, 0, 0), 1.0, max_depth=22) == 0
+    assert view((0, 0, 0), 1.0, capacity=1 << 26) == 0
