@@ -56,6 +56,12 @@ int dot_abi_version(void);
 const char* dot_last_error(void);
 int dot_device_check(void);
 
+/* --- exp of the reference (glibc's exp, restated bit-exactly; used for
+ *     every alpha = exp(-sigma * delta) of the kernels): host loop and a
+ *     device kernel over n doubles, for parity tests. */
+void dot_exp_ref_host(const double* x, double* y, int64_t n);
+int dot_exp_ref_device(const double* x, double* y, int64_t n, void* stream);
+
 /* --- locate table (no reference counterpart; accelerates _descend,
  *     _kernels.py:56-68): for a dyadic root (half_extent a power of two,
  *     centre a multiple of half * 2^-20, max_depth <= 21, capacity < 2^26)
@@ -114,6 +120,23 @@ int dot_render_bwd(const dot_tree_view* tree, const double* origins, const doubl
                    float* grad_sigma, float* grad_sh, int32_t gsh_stride, double* signal,
                    uint8_t* touched, double* loss_sum, float* rgb_out, int32_t flags,
                    void* stream);
+
+/* --- deterministic fused forward + backward: same inputs and outputs as
+ *     dot_render_bwd (accumulates into the same buffers; rgb not returned),
+ *     but the per-leaf reduction runs in the reference's order --
+ *     scatter_kernel (_kernels.py:327-346) sums each leaf's contributions
+ *     serially over rays in batch order -- via per-segment records, a radix
+ *     sort by (leaf, original ray index) and a sequential f64 sum per leaf.
+ *     Results are bit-identical across runs.  ray_id[n] (may be NULL =
+ *     identity) gives the original batch index of input ray r, so a caller
+ *     may hand the rays in any (e.g. coherence-sorted) order.  Synchronises
+ *     the stream (the record count sizes the sort). */
+int dot_render_bwd_sorted(const dot_tree_view* tree, const double* origins, const double* dirs,
+                          const double* targets, const int64_t* ray_id, int64_t n_rays,
+                          const double* background, double early_stop_eps, double t_near,
+                          double t_far, double grad_scale, float* grad_sigma, float* grad_sh,
+                          int32_t gsh_stride, double* signal, uint8_t* touched, double* loss_sum,
+                          void* stream);
 
 /* --- coherence keys (no reference counterpart): keys[i] = (origin Morton
  *     << 32) | octahedral-direction Morton; sorting a batch by them puts rays

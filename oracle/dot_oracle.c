@@ -325,3 +325,9 @@ int oracle_num_threads(void) {
     return 1;
 #endif
 }
+
+/* glibc exp over an array (the reference's exp: Numba lowers np.exp to the
+ * libm call).  Checker for the kernels' exp_ref. */
+void oracle_exp(const double* x, double* y, int64_t n) {
+    for (int64_t i = 0; i < n; ++i) y[i] = exp(x[i]);
+}

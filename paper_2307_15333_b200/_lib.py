@@ -45,6 +45,8 @@ _SIGNATURES = {
     "dot_abi_version": (c_i32, []),
     "dot_last_error": (ctypes.c_char_p, []),
     "dot_device_check": (c_i32, []),
+    "dot_exp_ref_host": (None, [c_void_p, c_void_p, c_i64]),
+    "dot_exp_ref_device": (c_i32, [c_void_p, c_void_p, c_i64, c_void_p]),
     "dot_locate_supported": (c_i32, [c_void_p]),
     "dot_locate_build": (c_i32, [c_void_p, c_i32, c_void_p, c_void_p]),
     "dot_trace_count": (c_i32, [c_void_p, c_void_p, c_void_p, c_i64, c_f64, c_f64, c_void_p, c_void_p]),
@@ -57,6 +59,9 @@ _SIGNATURES = {
     "dot_render_bwd":(c_i32, [c_void_p, c_void_p, c_void_p, c_void_p, c_i64, c_void_p, c_f64, c_f64,
                                c_f64, c_f64, c_void_p, c_void_p, c_i32, c_void_p, c_void_p, c_void_p,
                                c_void_p, c_i32, c_void_p]),
+    "dot_render_bwd_sorted": (c_i32, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_i64, c_void_p,
+                                      c_f64, c_f64, c_f64, c_f64, c_void_p, c_void_p, c_i32, c_void_p,
+                                      c_void_p, c_void_p, c_void_p]),
     "dot_ray_keys": (c_i32, [c_void_p, c_void_p, c_void_p, c_i64, c_void_p, c_void_p]),
     "dot_ray_keys32": (c_i32, [c_void_p, c_void_p, c_void_p, c_i64, c_void_p, c_void_p]),
     "dot_ray_stats":(c_i32, [c_void_p, c_void_p, c_void_p, c_i64, c_f64, c_void_p, c_void_p]),

@@ -151,7 +151,7 @@ __global__ void __launch_bounds__(kBlockA) bwd_record_kernel(
         }
         if (got) {
             if (rec) {
-                const double a = exp(-double(__ldg(T.sigma + L.pid)) * dl);
+                const double a = exp_ref(-double(__ldg(T.sigma + L.pid)) * dl);
                 const double q = 1.0 - a;
                 float k0 = __int_as_float(0x7fc00000), k1 = k0, k2 = k0;
                 if (q > 0.0) {

@@ -43,7 +43,7 @@ void retain_pool_memory() {
     done_dev = dev;
 }
 
-static int validate_tree(const dot_tree_view* v) {
+int validate_tree_view(const dot_tree_view* v) {
     if (!v) return set_error(DOT_BAD_ARG, "tree view is NULL");
     if (!v->node || v->n_nodes < 1) return set_error(DOT_BAD_ARG, "tree has no nodes");
     if (!v->sigma || !v->sh) return set_error(DOT_BAD_ARG, "tree payload is NULL");
@@ -80,13 +80,22 @@ int dot_device_check(void) {
     return DOT_OK;
 }
 
+void dot_exp_ref_host(const double* x, double* y, int64_t n) {
+    for (int64_t i = 0; i < n; ++i) y[i] = exp_ref(x[i]);
+}
+
+int dot_exp_ref_device(const double* x, double* y, int64_t n, void* stream) {
+    if (n < 0 || (n && (!x || !y))) return set_error(DOT_BAD_ARG, "bad arrays");
+    return launch_exp_ref(x, y, n, static_cast<cudaStream_t>(stream));
+}
+
 int dot_locate_supported(const dot_tree_view* tree) {
-    if (validate_tree(tree)) return 0;
+    if (validate_tree_view(tree)) return 0;
     return locate_dyadic(*tree) ? 1 : 0;
 }
 
 int dot_locate_build(const dot_tree_view* tree, int32_t level, int32_t* table, void* stream) {
-    if (int st = validate_tree(tree)) return st;
+    if (int st = validate_tree_view(tree)) return st;
     if (!locate_dyadic(*tree))
         return set_error(DOT_BAD_ARG, "locate table needs a dyadic root (half_extent a power of two, "
                                       "centre a multiple of half * 2^-20, max_depth <= 21, capacity < 2^26)");
@@ -98,7 +107,7 @@ int dot_locate_build(const dot_tree_view* tree, int32_t level, int32_t* table, v
 
 int dot_trace_count(const dot_tree_view* tree, const double* origins, const double* dirs,
                     int64_t n_rays, double t_near, double t_far, int64_t* counts, void* stream) {
-    if (int st = validate_tree(tree)) return st;
+    if (int st = validate_tree_view(tree)) return st;
     if (n_rays < 0 || (n_rays && (!origins || !dirs || !counts)))
         return set_error(DOT_BAD_ARG, "bad ray arrays");
     return launch_trace_count(make_tree(*tree), origins, dirs, n_rays, t_near, t_far, counts,
@@ -108,7 +117,7 @@ int dot_trace_count(const dot_tree_view* tree, const double* origins, const doub
 int dot_trace_fill(const dot_tree_view* tree, const double* origins, const double* dirs,
                    int64_t n_rays, double t_near, double t_far, const int64_t* offsets,
                    int64_t* seg_leaf, double* seg_t, double* seg_delta, void* stream) {
-    if (int st = validate_tree(tree)) return st;
+    if (int st = validate_tree_view(tree)) return st;
     if (n_rays < 0 || (n_rays && (!origins || !dirs || !offsets)))
         return set_error(DOT_BAD_ARG, "bad ray arrays");
     return launch_trace_fill(make_tree(*tree), origins, dirs, n_rays, t_near, t_far, offsets,
@@ -119,7 +128,7 @@ int dot_render_fwd(const dot_tree_view* tree, const double* origins, const doubl
                    int64_t n_rays, const double* background, double early_stop_eps,
                    double t_near, double t_far, float* rgb, float* t_final, float* wsum,
                    float* depth, void* stream) {
-    if (int st = validate_tree(tree)) return st;
+    if (int st = validate_tree_view(tree)) return st;
     if (n_rays < 0 || (n_rays && (!origins || !dirs)) || !background)
         return set_error(DOT_BAD_ARG, "bad ray arrays");
     return launch_render_fwd(make_tree(*tree), origins, dirs, n_rays, background, early_stop_eps,
@@ -133,7 +142,7 @@ int dot_render_bwd(const dot_tree_view* tree, const double* origins, const doubl
                    float* grad_sigma, float* grad_sh, int32_t gsh_stride, double* signal,
                    uint8_t* touched, double* loss_sum, float* rgb_out, int32_t flags,
                    void* stream) {
-    if (int st = validate_tree(tree)) return st;
+    if (int st = validate_tree_view(tree)) return st;
     if (n_rays < 0 || (n_rays && (!origins || !dirs || !targets)) || !background)
         return set_error(DOT_BAD_ARG, "bad ray arrays");
     if (!grad_sigma || !grad_sh || !signal || !touched || !loss_sum)
@@ -150,7 +159,7 @@ int dot_render_bwd(const dot_tree_view* tree, const double* origins, const doubl
 
 int dot_ray_keys(const dot_tree_view* tree, const double* origins, const double* dirs, int64_t n_rays,
                  uint64_t* keys, void* stream) {
-    if (int st = validate_tree(tree)) return st;
+    if (int st = validate_tree_view(tree)) return st;
     if (n_rays < 0 || (n_rays && (!origins || !dirs || !keys))) return set_error(DOT_BAD_ARG, "bad arrays");
     return launch_ray_keys(make_tree(*tree), origins, dirs, n_rays, reinterpret_cast<unsigned long long*>(keys),
                            static_cast<cudaStream_t>(stream));
@@ -158,7 +167,7 @@ int dot_ray_keys(const dot_tree_view* tree, const double* origins, const double*
 
 int dot_ray_keys32(const dot_tree_view* tree, const double* origins, const double* dirs, int64_t n_rays,
                    int32_t* keys, void* stream) {
-    if (int st = validate_tree(tree)) return st;
+    if (int st = validate_tree_view(tree)) return st;
     if (n_rays < 0 || (n_rays && (!origins || !dirs || !keys))) return set_error(DOT_BAD_ARG, "bad arrays");
     return launch_ray_keys32(make_tree(*tree), origins, dirs, n_rays, keys, static_cast<cudaStream_t>(stream));
 }
@@ -166,7 +175,7 @@ int dot_ray_keys32(const dot_tree_view* tree, const double* origins, const doubl
 int dot_render_camera(const dot_tree_view* tree, const double* cam_to_world, double focal, int32_t width,
                       int32_t height, const double* background, double early_stop_eps, float* rgb,
                       float* t_final, float* depth, void* stream) {
-    if (int st = validate_tree(tree)) return st;
+    if (int st = validate_tree_view(tree)) return st;
     if (!cam_to_world || !background || !rgb || width < 0 || height < 0 || !(focal > 0.0))
         return set_error(DOT_BAD_ARG, "bad camera arguments");
     return launch_render_camera(make_tree(*tree), cam_to_world, focal, width, height, background, early_stop_eps,
@@ -175,7 +184,7 @@ int dot_render_camera(const dot_tree_view* tree, const double* cam_to_world, dou
 
 int dot_ray_stats(const dot_tree_view* tree, const double* origins, const double* dirs, int64_t n_rays,
                   double early_stop_eps, uint64_t* totals, void* stream) {
-    if (int st = validate_tree(tree)) return st;
+    if (int st = validate_tree_view(tree)) return st;
     if (n_rays < 0 || (n_rays && (!origins || !dirs)) || !totals) return set_error(DOT_BAD_ARG, "bad arrays");
     return launch_ray_stats(make_tree(*tree), origins, dirs, n_rays, early_stop_eps,
                             reinterpret_cast<unsigned long long*>(totals), static_cast<cudaStream_t>(stream));

@@ -8,10 +8,24 @@ namespace dot {
 
 struct TreeDev;
 
+// Outputs of the record-emitting backward (sorted.cu / render.cu EmitSink).
+struct EmitArgs {
+    unsigned long long* ctr;         // [0] records reserved, [1] rays that did not fit
+    int64_t cap;                     // record slots
+    unsigned long long* keys;        // [cap] pool id << ray_bits | original ray index
+    float4* rec;                     // [cap] (dsigma, w0, w1, w2)
+    double* recq;                    // [cap] q = 1 - alpha
+    float* basis;                    // [n * B] SH basis per original ray
+    double* loss_ray;                // [n] squared error per original ray
+    const int64_t* ray_id;           // [n] original index of input ray r (NULL = identity)
+    int ray_bits;
+};
+
 int set_error(int status, const char* fmt, ...);
 int check_launch(const char* what);
 int check_cuda(cudaError_t e, const char* what);
 void retain_pool_memory();
+int validate_tree_view(const dot_tree_view* v);
 
 int launch_trace_count(const TreeDev& T, const double* o, const double* d, int64_t n,
                        double tn, double tf, int64_t* counts, cudaStream_t s);
@@ -40,6 +54,10 @@ int launch_ray_keys32(const TreeDev& T, const double* o, const double* d, int64_
                       cudaStream_t s);
 int launch_render_camera(const TreeDev& T, const double* cam_to_world, double focal, int width, int height,
                          const double* bg, double eps, float* rgb, float* tfin, float* depth, cudaStream_t s);
+int launch_render_bwd_emit(const TreeDev& T, const double* o, const double* d, const double* tgt,
+                           int64_t n, const double* bg, double eps, double tn, double tf, double gs,
+                           uint8_t* touched, const EmitArgs& ea, cudaStream_t s);
+int launch_exp_ref(const double* x, double* y, int64_t n, cudaStream_t s);
 int launch_locate_build(const TreeDev& T, int level, int32_t* table, cudaStream_t s);
 int launch_ray_stats(const TreeDev& T, const double* o, const double* d, int64_t n, double eps,
                      unsigned long long* out, cudaStream_t s);

@@ -10,6 +10,7 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 #include "../../include/dot_b200.h"
+#include "dot_exp.cuh"
 
 namespace dot {
 

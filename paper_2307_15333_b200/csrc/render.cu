@@ -128,7 +128,7 @@ __global__ void __launch_bounds__(kBlock, DOT_FWD_MINB) render_fwd_kernel(
         double te, dl;
         while (tr.template next<CACHED, DOT_FWD_PREFETCH>(T, L, te, dl, pc)) {
             const double sg = double(__ldg(T.sigma + L.pid));
-            const double a = exp(-sg * dl);
+            const double a = exp_ref(-sg * dl);
             const double q = 1.0 - a;
             if (q > 0.0) {
                 float e0, e1, e2;
@@ -189,7 +189,7 @@ __global__ void __launch_bounds__(kBlock) render_bwd_kernel(
             double te, dl;
             while (tr.next(T, L, te, dl)) {
                 const double sg = double(__ldg(T.sigma + L.pid));
-                const double a = exp(-sg * dl);
+                const double a = exp_ref(-sg * dl);
                 const double q = 1.0 - a;
                 ++used;
                 if (q > 0.0) {
@@ -227,7 +227,7 @@ __global__ void __launch_bounds__(kBlock) render_bwd_kernel(
                 const int64_t pid = L.pid;
                 if (i < used) {
                     const double sg = double(__ldg(T.sigma + pid));
-                    const double a = exp(-sg * dl);
+                    const double a = exp_ref(-sg * dl);
                     const double q = 1.0 - a;
                     float e0, e1, e2;
                     sh_dot<B>(T.sh + pid * S, basis, e0, e1, e2);
@@ -368,7 +368,7 @@ __global__ void __launch_bounds__(kBlock) render_bwd_persistent_kernel(
         if (phase == 1) {
             bool cut = false;
             if (got) {
-                const double a = exp(-double(__ldg(T.sigma + L.pid)) * dl);
+                const double a = exp_ref(-double(__ldg(T.sigma + L.pid)) * dl);
                 const double q = 1.0 - a;
                 ++used;
                 if (q > 0.0) {
@@ -395,7 +395,7 @@ __global__ void __launch_bounds__(kBlock) render_bwd_persistent_kernel(
                 phase = 0;
             } else if (i < used) {
                 const int64_t pid = L.pid;
-                const double a = exp(-double(__ldg(T.sigma + pid)) * dl);
+                const double a = exp_ref(-double(__ldg(T.sigma + pid)) * dl);
                 const double q = 1.0 - a;
                 float e0, e1, e2;
                 sh_dot<B>(T.sh + pid * S, basis, e0, e1, e2);
@@ -455,7 +455,7 @@ __global__ void __launch_bounds__(kBlock) render_bwd_persistent_kernel(
 struct BufSeg {
     int32_t pid;
     float delta;
-    double a;        // alpha = exp(-sigma delta) exactly as pass 1 used it
+    double a;        // alpha = exp_ref(-sigma delta) exactly as pass 1 used it
     float k0, k1, k2;  // colour (NaN: not evaluated in pass 1, q == 0)
     float pad;
 };
@@ -493,30 +493,74 @@ struct SegBuffer {
     }
 };
 
-template <int B, int K, int MINB = 1, bool GBUF = false, int BLK = kBlock, bool PF = false>
+// Where pass 2 sends each composited segment's gradient contribution.
+// AtomicSink: vector REDs straight into the per-leaf buffers (default).
+// EmitSink (sorted.cu): one record per segment, reduced per leaf afterwards
+// in ray-major order (deterministic mode).
+struct AtomicSink {
+    float* __restrict__ gsig;
+    float* __restrict__ gsh;
+    double* __restrict__ signal;
+    double* __restrict__ loss_sum;
+    // warp-collective, all 32 lanes (no-op here)
+    __device__ __forceinline__ void reserve(int, bool) {}
+    template <int B>
+    __device__ __forceinline__ void put(int, int64_t pid, float ds, float w0, float w1, float w2,
+                                        const float* basis, double q) {
+        constexpr int S = pad4(3 * B);
+        red_add_f32(gsig + pid, ds);
+        if (w0 != 0.f || w1 != 0.f || w2 != 0.f) {
+            float* row = gsh + pid * S;
+#pragma unroll
+            for (int j = 0; j < S / 4; ++j) {
+                float v[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int idx = 4 * j + u;
+                    const int k = idx / B;
+                    const float w = k == 0 ? w0 : (k == 1 ? w1 : w2);
+                    v[u] = idx < 3 * B ? w * basis[idx % B] : 0.f;
+                }
+                red_add_v4(row + 4 * j, v[0], v[1], v[2], v[3]);
+            }
+        }
+        if (q != 0.0) red_add_f64(signal + pid, q);
+    }
+    template <int B>
+    __device__ __forceinline__ void ray_done(int64_t, const float*, double) {}
+    // warp-collective: sum of the per-ray squared errors
+    __device__ __forceinline__ void loss(double v) {
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) v += __shfl_down_sync(0xffffffffu, v, off);
+        if ((threadIdx.x & 31) == 0 && v != 0.0) red_add_f64(loss_sum, v);
+    }
+};
+
+template <int B, int K, int MINB = 1, bool GBUF = false, int BLK = kBlock, bool PF = false,
+          class Sink = AtomicSink>
 __global__ void __launch_bounds__(BLK, MINB) render_bwd_buffered_kernel(
     TreeDev T, const double* __restrict__ o, const double* __restrict__ d,
     const double* __restrict__ tgt, int64_t n, double bg0, double bg1, double bg2, double eps,
-    double t_near, double t_far, double grad_scale, float* __restrict__ gsig,
-    float* __restrict__ gsh, double* __restrict__ signal, uint8_t* __restrict__ touched,
-    double* __restrict__ loss_sum, float* __restrict__ rgb_out, int flags,
-    BufSeg* __restrict__ gbuf) {
+    double t_near, double t_far, double grad_scale, uint8_t* __restrict__ touched,
+    float* __restrict__ rgb_out, int flags, BufSeg* __restrict__ gbuf, Sink sink) {
     constexpr int S = pad4(3 * B);
     double loss = 0.0;
     // one ray per thread, blocks scheduled dynamically by the hardware (a
     // grid-stride variant measured 60 % slower: static per-block ray sets
     // leave SMs idle behind long rays)
     const int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (r < n) {
-        Tracer tr;
+    const bool valid = r < n;
+    Tracer tr;
+    float basis[B];
+    SegBuffer<GBUF, K> buf;
+    int used = 0;
+    double resume_t = 0.0, resume_nudge = 0.0;
+    double R0 = 0.0, R1 = 0.0, R2 = 0.0, g0 = 0.0, g1 = 0.0, g2 = 0.0;
+    if (valid) {
         load_ray(o, d, r, tr);
-        float basis[B];
         eval_basis<B>(tr.dx, tr.dy, tr.dz, basis);
-        SegBuffer<GBUF, K> buf;
         buf.g = gbuf + r;
         buf.stride = n;
-        int used = 0;
-        double resume_t = 0.0, resume_nudge = 0.0;
         double trans = 1.0, c0 = 0.0, c1 = 0.0, c2 = 0.0;
         const bool hit = tr.init(T, t_near, t_far);
         if (hit) {
@@ -526,7 +570,7 @@ __global__ void __launch_bounds__(BLK, MINB) render_bwd_buffered_kernel(
             while (tr.next_prefetch(T, L, te, dl, !cut)) {
                 touched[L.pid] = 1;
                 if (cut) continue;  // post-cut: touched only
-                const double a = exp(-double(__ldg(T.sigma + L.pid)) * dl);
+                const double a = exp_ref(-double(__ldg(T.sigma + L.pid)) * dl);
                 const double q = 1.0 - a;
                 float k0 = __int_as_float(0x7fc00000), k1 = k0, k2 = k0;
                 if (q > 0.0) {
@@ -563,20 +607,29 @@ __global__ void __launch_bounds__(BLK, MINB) render_bwd_buffered_kernel(
             }
         }
         const double tf = trans;
-        const double R0 = c0 + tf * bg0, R1 = c1 + tf * bg1, R2 = c2 + tf * bg2;
+        R0 = c0 + tf * bg0;
+        R1 = c1 + tf * bg1;
+        R2 = c2 + tf * bg2;
         const double r0 = R0 - __ldg(tgt + 3 * r + 0);
         const double r1 = R1 - __ldg(tgt + 3 * r + 1);
         const double r2 = R2 - __ldg(tgt + 3 * r + 2);
-        loss += r0 * r0 + r1 * r1 + r2 * r2;
+        loss = r0 * r0 + r1 * r1 + r2 * r2;
         if (rgb_out) {
             rgb_out[3 * r + 0] = float(R0);
             rgb_out[3 * r + 1] = float(R1);
             rgb_out[3 * r + 2] = float(R2);
         }
-        const double g0 = grad_scale * r0, g1 = grad_scale * r1, g2 = grad_scale * r2;
+        g0 = grad_scale * r0;
+        g1 = grad_scale * r1;
+        g2 = grad_scale * r2;
+        if (flags & 8192) used = 0;  // diagnostic: pass 1 only
+    }
+    __syncwarp();
+    sink.reserve(used, valid);
+    if (valid) {
+        sink.template ray_done<B>(r, basis, loss);
         // ---- pass 2: replay (suffix carried directly: suf = rgb - prefix)
         double s0 = R0, s1 = R1, s2 = R2, Ti = 1.0;
-        if (flags & 8192) used = 0;  // diagnostic: pass 1 only
         if (used > K) {  // segment K onwards come from a resumed walk
             tr.t = resume_t;
             tr.nudge = resume_nudge;
@@ -606,7 +659,7 @@ __global__ void __launch_bounds__(BLK, MINB) render_bwd_buffered_kernel(
                 double te;
                 tr.next(T, L, te, dl);
                 pid = L.pid;
-                a = exp(-double(__ldg(T.sigma + pid)) * dl);
+                a = exp_ref(-double(__ldg(T.sigma + pid)) * dl);
                 k0 = __int_as_float(0x7fc00000);
             }
             if (k0 != k0) {
@@ -626,34 +679,89 @@ __global__ void __launch_bounds__(BLK, MINB) render_bwd_buffered_kernel(
             const float w0 = float(g0 * tq) * k0 * (1.f - k0);
             const float w1 = float(g1 * tq) * k1 * (1.f - k1);
             const float w2 = float(g2 * tq) * k2 * (1.f - k2);
+            Ti *= a;
             if (flags & 16384) {  // diagnostic: no reductions
-                if (ds == 12345.0 && w0 == 1.f) red_add_f32(gsig + pid, w1 + w2);
-                Ti *= a;
+                if (ds == 12345.0 && w0 == 1.f) red_add_f32(touched ? reinterpret_cast<float*>(rgb_out) : nullptr, w1 + w2);
                 continue;
             }
-            red_add_f32(gsig + pid, float(ds));
-            if (w0 != 0.f || w1 != 0.f || w2 != 0.f) {
-                float* row = gsh + pid * S;
-#pragma unroll
-                for (int j = 0; j < S / 4; ++j) {
-                    float v[4];
-#pragma unroll
-                    for (int u = 0; u < 4; ++u) {
-                        const int idx = 4 * j + u;
-                        const int k = idx / B;
-                        const float w = k == 0 ? w0 : (k == 1 ? w1 : w2);
-                        v[u] = idx < 3 * B ? w * basis[idx % B] : 0.f;
-                    }
-                    red_add_v4(row + 4 * j, v[0], v[1], v[2], v[3]);
-                }
-            }
-            if (q != 0.0) red_add_f64(signal + pid, q);
-            Ti *= a;
+            sink.template put<B>(i, pid, float(ds), w0, w1, w2, basis, q);
         }
     }
+    sink.loss(loss);
+}
+
+#define DOT_DISPATCH_B(MACRO)                                                     \
+    switch (T.basis_count) {                                                      \
+        case 1: if (cached) MACRO(1, true) else MACRO(1, false) break;            \
+        case 4: if (cached) MACRO(4, true) else MACRO(4, false) break;            \
+        case 9: if (cached) MACRO(9, true) else MACRO(9, false) break;            \
+        case 16: if (cached) MACRO(16, true) else MACRO(16, false) break;         \
+        default: return set_error(DOT_BAD_ARG, "basis_count must be 1, 4, 9 or 16"); \
+    }
+
+// Record sink of the deterministic (sorted) backward: pass 2 writes one
+// record per composited segment -- key (pool id << ray_bits | original ray
+// index), (dsigma, w0, w1, w2) f32 and q f64 -- into slots reserved per ray
+// with one warp-aggregated atomicAdd; the ray's SH basis and squared error
+// go to per-ray arrays (original index).  A ray whose records do not fit is
+// counted in ctr[1] and writes nothing (the host retries with more room).
+struct EmitSink {
+    EmitArgs a;
+    int64_t base;
+    int64_t orig;
+    __device__ __forceinline__ void reserve(int used, bool valid) {
+        const int lane = threadIdx.x & 31;
+        int incl = used;
 #pragma unroll
-    for (int off = 16; off > 0; off >>= 1) loss += __shfl_down_sync(0xffffffffu, loss, off);
-    if ((threadIdx.x & 31) == 0 && loss != 0.0) red_add_f64(loss_sum, loss);
+        for (int off = 1; off < 32; off <<= 1) {
+            const int v = __shfl_up_sync(0xffffffffu, incl, off);
+            if (lane >= off) incl += v;
+        }
+        const int total = __shfl_sync(0xffffffffu, incl, 31);
+        unsigned long long b0 = 0;
+        if (lane == 31 && total > 0) b0 = atomicAdd(a.ctr, (unsigned long long)total);
+        b0 = __shfl_sync(0xffffffffu, b0, 31);
+        base = int64_t(b0) + (incl - used);
+        if (valid && used > 0 && base + used > a.cap) {
+            atomicAdd(a.ctr + 1, 1ull);
+            base = -1;
+        }
+    }
+    template <int B>
+    __device__ __forceinline__ void ray_done(int64_t r, const float* basis, double loss) {
+        orig = a.ray_id ? a.ray_id[r] : r;
+#pragma unroll
+        for (int b = 0; b < B; ++b) a.basis[orig * B + b] = basis[b];
+        a.loss_ray[orig] = loss;
+    }
+    template <int B>
+    __device__ __forceinline__ void put(int i, int64_t pid, float ds, float w0, float w1, float w2,
+                                        const float*, double q) {
+        if (base < 0) return;
+        const int64_t k = base + i;
+        a.keys[k] = (static_cast<unsigned long long>(pid) << a.ray_bits) |
+                    static_cast<unsigned long long>(orig);
+        a.rec[k] = make_float4(ds, w0, w1, w2);
+        a.recq[k] = q;
+    }
+    __device__ __forceinline__ void loss(double) {}
+};
+
+int launch_render_bwd_emit(const TreeDev& T, const double* o, const double* d, const double* tgt,
+                           int64_t n, const double* bg, double eps, double tn, double tf, double gs,
+                           uint8_t* touched, const EmitArgs& ea, cudaStream_t s) {
+    if (n == 0) return DOT_OK;
+    EmitSink sink;
+    sink.a = ea;
+    sink.base = -1;
+    sink.orig = 0;
+#define DOT_EMIT(BB, CC)                                                                          \
+    render_bwd_buffered_kernel<BB, 48, 32, false, 32, true, EmitSink><<<unsigned((n + 31) / 32), 32, 0, s>>>( \
+        T, o, d, tgt, n, bg[0], bg[1], bg[2], eps, tn, tf, gs, touched, nullptr, 0, nullptr, sink);
+    const bool cached = false;
+    DOT_DISPATCH_B(DOT_EMIT)
+#undef DOT_EMIT
+    return check_launch("render_bwd_buffered_kernel<emit>");
 }
 
 // Replay of rays whose segment records overflowed the two-kernel path's
@@ -680,7 +788,7 @@ __global__ void __launch_bounds__(kBlock) render_bwd_replay_kernel(
         Leaf L;
         double te, dl;
         while (tr.next(T, L, te, dl)) {
-            trans *= exp(-double(__ldg(T.sigma + L.pid)) * dl);
+            trans *= exp_ref(-double(__ldg(T.sigma + L.pid)) * dl);
             ++used;
             if (eps > 0.0 && trans < eps) break;
         }
@@ -690,7 +798,7 @@ __global__ void __launch_bounds__(kBlock) render_bwd_replay_kernel(
         double Ti = 1.0;
         for (int i = 0; i < used && tr.next(T, L, te, dl); ++i) {
             const int64_t pid = L.pid;
-            const double a = exp(-double(__ldg(T.sigma + pid)) * dl);
+            const double a = exp_ref(-double(__ldg(T.sigma + pid)) * dl);
             const double q = 1.0 - a;
             float e0, e1, e2;
             sh_dot<B>(T.sh + pid * S, basis, e0, e1, e2);
@@ -800,7 +908,7 @@ __global__ void __launch_bounds__(kBlock, DOT_FWD_MINB) render_camera_kernel(
         double te, dl;
         PathCache pc;
         while (tr.template next<false, DOT_FWD_PREFETCH>(T, L, te, dl, pc)) {
-            const double a = exp(-double(__ldg(T.sigma + L.pid)) * dl);
+            const double a = exp_ref(-double(__ldg(T.sigma + L.pid)) * dl);
             const double q = 1.0 - a;
             if (q > 0.0) {
                 float e0, e1, e2;
@@ -961,7 +1069,7 @@ __global__ void __launch_bounds__(kBlock) ray_stats_kernel(TreeDev T, const doub
             while (tr.next(T, L, te, dl)) {
                 ++seg;
                 if (cut) continue;
-                const double a = exp(-double(__ldg(T.sigma + L.pid)) * dl);
+                const double a = exp_ref(-double(__ldg(T.sigma + L.pid)) * dl);
                 ++comp;
                 if (1.0 - a > 0.0) ++qpos;
                 trans *= a;
@@ -992,6 +1100,17 @@ int launch_ray_stats(const TreeDev& T, const double* o, const double* d, int64_t
 // ---------------------------------------------------------------------------
 
 static unsigned blocks_for(int64_t n) { return unsigned((n + kBlock - 1) / kBlock); }
+
+__global__ void exp_ref_kernel(const double* __restrict__ x, double* __restrict__ y, int64_t n) {
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < n) y[i] = exp_ref(x[i]);
+}
+
+int launch_exp_ref(const double* x, double* y, int64_t n, cudaStream_t s) {
+    if (n == 0) return DOT_OK;
+    exp_ref_kernel<<<blocks_for(n), kBlock, 0, s>>>(x, y, n);
+    return check_launch("exp_ref_kernel");
+}
 
 // Locate table: one thread per depth-L cell walks the node table from the
 // root with the cell's octant bits (integer only) and stores the node word at
@@ -1049,15 +1168,6 @@ int launch_trace_fill(const TreeDev& T, const double* o, const double* d, int64_
 }
 
 // Dispatch on the basis count (compile-time B) and the path cache.
-#define DOT_DISPATCH_B(MACRO)                                                     \
-    switch (T.basis_count) {                                                      \
-        case 1: if (cached) MACRO(1, true) else MACRO(1, false) break;            \
-        case 4: if (cached) MACRO(4, true) else MACRO(4, false) break;            \
-        case 9: if (cached) MACRO(9, true) else MACRO(9, false) break;            \
-        case 16: if (cached) MACRO(16, true) else MACRO(16, false) break;         \
-        default: return set_error(DOT_BAD_ARG, "basis_count must be 1, 4, 9 or 16"); \
-    }
-
 int launch_render_fwd(const TreeDev& T, const double* o, const double* d, int64_t n,
                       const double* bg, double eps, double tn, double tf, float* rgb, float* tfin,
                       float* wsum, float* depth, cudaStream_t s) {
@@ -1107,8 +1217,8 @@ int launch_render_bwd(const TreeDev& T, const double* o, const double* d, const 
 #define DOT_BUF_LAUNCH_BLK(BB, KK, MB, GB, BL) DOT_BUF_LAUNCH_PF(BB, KK, MB, GB, BL, false)
 #define DOT_BUF_LAUNCH_PF(BB, KK, MB, GB, BL, PP)                                                   \
     render_bwd_buffered_kernel<BB, KK, MB, GB, BL, PP><<<unsigned((n + BL - 1) / BL), BL, 0, s>>>(  \
-        T, o, d, tgt, n, bg[0], bg[1], bg[2], eps, tn, tf, gs, gsig, gsh, signal, touched, loss,    \
-        rgb_out, flags, gbuf)
+        T, o, d, tgt, n, bg[0], bg[1], bg[2], eps, tn, tf, gs, touched, rgb_out, flags, gbuf,       \
+        AtomicSink{gsig, gsh, signal, loss})
 #define DOT_BUF_LAUNCH(BB, KK, MB, GB) DOT_BUF_LAUNCH_BLK(BB, KK, MB, GB, kBlock)
 #define DOT_BUF(BB, CC)                                                                           \
     {                                                                                             \

@@ -1,0 +1,253 @@
+// sorted.cu -- deterministic fused forward + backward (dot_render_bwd_sorted).
+//
+// The reference reduces per-segment gradients serially in ray-major order
+// (scatter_kernel, _kernels.py:327-346): for every ray in batch order, for
+// every segment in march order, signal[leaf] += Q, grad[leaf] += ... in f64.
+// The default GPU path (render.cu, AtomicSink) reduces with float atomics,
+// whose order varies from run to run.  This path reproduces the reference's
+// order instead:
+//   1. the buffered fused kernel (EmitSink) writes one record per composited
+//      segment, keyed (pool id << ray_bits | original ray index);
+//   2. a CUB radix sort over the key bits orders the records by leaf, and
+//      within a leaf by original ray index -- exactly scatter_kernel's order;
+//   3. reduce_runs_kernel sums each leaf's run sequentially in f64 (half a
+//      warp per run: lane b owns basis column b of the three channels) and
+//      adds the result to the f32 gradients / f64 signal;
+//   4. the per-ray squared errors are summed by cub::DeviceReduce (fixed
+//      order).
+// Everything is a pure function of the inputs: results are bit-identical
+// from run to run, and the signal is bit-identical to the reference's
+// whenever the per-segment Q values are (they are computed from the
+// bit-exact traversal; exp may differ from glibc's by an ulp).
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_reduce.cuh>
+#include "dot_tree.cuh"
+#include "dot_internal.h"
+
+namespace dot {
+
+int launch_iota(int32_t* p, int64_t n, cudaStream_t s);
+int launch_add_f64(double* dst, const double* src, cudaStream_t s);
+
+template <int B>
+__global__ void __launch_bounds__(128) reduce_runs_kernel(
+    const unsigned long long* __restrict__ keys, const int32_t* __restrict__ idx, int64_t total,
+    int ray_bits, const float4* __restrict__ rec, const double* __restrict__ recq,
+    const float* __restrict__ basis, float* __restrict__ gsig, float* __restrict__ gsh,
+    double* __restrict__ signal) {
+    constexpr int S = pad4(3 * B);
+    const int lane = threadIdx.x & 31;
+    const int64_t w0 = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int64_t pos = w0 * 32 + lane;
+    const unsigned long long rmask = (1ull << ray_bits) - 1ull;
+    bool head = false;
+    if (pos < total) {
+        const unsigned long long k = keys[pos] >> ray_bits;
+        head = pos == 0 || (keys[pos - 1] >> ray_bits) != k;
+    }
+    unsigned heads = __ballot_sync(0xffffffffu, head);
+    const int half = lane >> 4, b = lane & 15;
+    while (heads) {
+        const int h0 = __ffs(heads) - 1;
+        heads &= heads - 1;
+        int h1 = -1;
+        if (heads) {
+            h1 = __ffs(heads) - 1;
+            heads &= heads - 1;
+        }
+        const int h = half ? h1 : h0;
+        if (h < 0) continue;
+        int64_t j = w0 * 32 + h;
+        const unsigned long long pid = keys[j] >> ray_bits;
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+        if (b < B) {
+            a0 = double(gsh[pid * S + 0 * B + b]);
+            a1 = double(gsh[pid * S + 1 * B + b]);
+            a2 = double(gsh[pid * S + 2 * B + b]);
+        }
+        double as = double(gsig[pid]);
+        double aq = signal[pid];
+        for (; j < total; ++j) {
+            const unsigned long long key = keys[j];
+            if ((key >> ray_bits) != pid) break;
+            const int32_t k = idx[j];
+            const float4 r = rec[k];
+            const double q = recq[k];
+            const double bv = b < B ? double(basis[int64_t(key & rmask) * B + b]) : 0.0;
+            a0 = __dadd_rn(a0, __dmul_rn(double(r.y), bv));
+            a1 = __dadd_rn(a1, __dmul_rn(double(r.z), bv));
+            a2 = __dadd_rn(a2, __dmul_rn(double(r.w), bv));
+            as = __dadd_rn(as, double(r.x));
+            aq = __dadd_rn(aq, q);
+        }
+        if (b < B) {
+            gsh[pid * S + 0 * B + b] = float(a0);
+            gsh[pid * S + 1 * B + b] = float(a1);
+            gsh[pid * S + 2 * B + b] = float(a2);
+        }
+        if (b == 0) {
+            gsig[pid] = float(as);
+            signal[pid] = aq;
+        }
+    }
+}
+
+static int bits_for(int64_t v) {  // smallest k with v < 2^k (k >= 1)
+    int k = 1;
+    while (k < 62 && (int64_t(1) << k) <= v) ++k;
+    return k;
+}
+
+static int64_t g_rec_hint = 0;  // records needed by the last call (grows only)
+
+template <int B>
+static int run_sorted(const TreeDev& T, int64_t capacity, const double* o, const double* d, const double* tgt,
+                      const int64_t* ray_id, int64_t n, const double* bg, double eps, double tn,
+                      double tf, double gs, float* gsig, float* gsh, double* signal,
+                      uint8_t* touched, double* loss_sum, cudaStream_t s) {
+    retain_pool_memory();
+    const int ray_bits = bits_for(n - 1 < 1 ? 1 : n - 1);
+    const int pid_bits = bits_for(capacity);
+    if (ray_bits + pid_bits > 64)
+        return set_error(DOT_BAD_ARG, "batch too large for the sorted reduction keys");
+    int64_t cap = g_rec_hint > 16 * n ? g_rec_hint : 16 * n;
+    if (cap < 64) cap = 64;
+    int st = DOT_OK;
+    unsigned long long* ctr = nullptr;
+    float* basis = nullptr;
+    double* loss_ray = nullptr;
+    unsigned long long *keys = nullptr, *keys2 = nullptr;
+    int32_t *idx = nullptr, *idx2 = nullptr;
+    float4* rec = nullptr;
+    double* recq = nullptr;
+    void* tmp = nullptr;
+    auto release_records = [&]() {
+        cudaFreeAsync(keys, s);
+        cudaFreeAsync(keys2, s);
+        cudaFreeAsync(idx, s);
+        cudaFreeAsync(idx2, s);
+        cudaFreeAsync(rec, s);
+        cudaFreeAsync(recq, s);
+        keys = keys2 = nullptr;
+        idx = idx2 = nullptr;
+        rec = nullptr;
+        recq = nullptr;
+    };
+    auto cleanup = [&]() {
+        release_records();
+        cudaFreeAsync(ctr, s);
+        cudaFreeAsync(basis, s);
+        cudaFreeAsync(loss_ray, s);
+        cudaFreeAsync(tmp, s);
+    };
+#define TRY(x) do { if ((st = (x)) != DOT_OK) { cleanup(); return st; } } while (0)
+#define ALLOC(p, bytes) TRY(check_cuda(cudaMallocAsync(reinterpret_cast<void**>(&(p)), (bytes), s), "cudaMallocAsync"))
+    ALLOC(ctr, 2 * sizeof(unsigned long long));
+    ALLOC(basis, size_t(n) * B * sizeof(float));
+    ALLOC(loss_ray, size_t(n) * sizeof(double));
+    unsigned long long h_ctr[2] = {0, 0};
+    for (int attempt = 0; attempt < 3; ++attempt) {
+        ALLOC(keys, size_t(cap) * sizeof(unsigned long long));
+        ALLOC(rec, size_t(cap) * sizeof(float4));
+        ALLOC(recq, size_t(cap) * sizeof(double));
+        TRY(check_cuda(cudaMemsetAsync(ctr, 0, 2 * sizeof(unsigned long long), s), "memset"));
+        EmitArgs ea{ctr, cap, keys, rec, recq, basis, loss_ray, ray_id, ray_bits};
+        TRY(launch_render_bwd_emit(T, o, d, tgt, n, bg, eps, tn, tf, gs, touched, ea, s));
+        TRY(check_cuda(cudaMemcpyAsync(h_ctr, ctr, sizeof(h_ctr), cudaMemcpyDeviceToHost, s), "memcpy"));
+        TRY(check_cuda(cudaStreamSynchronize(s), "cudaStreamSynchronize"));
+        if (int64_t(h_ctr[0]) > g_rec_hint) g_rec_hint = int64_t(h_ctr[0]);
+        if (h_ctr[1] == 0) break;
+        // some rays did not fit: nothing of theirs was written; retry with
+        // room for every record (touched marks are idempotent, per-ray
+        // losses are overwritten)
+        release_records();
+        cap = int64_t(h_ctr[0]) + 64;
+        if (attempt == 2) TRY(set_error(DOT_CUDA_ERR, "sorted backward: record buffer overflow"));
+    }
+    const int64_t total = int64_t(h_ctr[0]);
+    if (total > 0) {
+        if (total > INT32_MAX) TRY(set_error(DOT_BAD_ARG, "too many segments for one sorted batch"));
+        ALLOC(keys2, size_t(total) * sizeof(unsigned long long));
+        ALLOC(idx, size_t(total) * sizeof(int32_t));
+        ALLOC(idx2, size_t(total) * sizeof(int32_t));
+        TRY(launch_iota(idx, total, s));
+        size_t tmp_bytes = 0;
+        cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, keys, keys2, idx, idx2, int(total), 0,
+                                        ray_bits + pid_bits, s);
+        ALLOC(tmp, tmp_bytes);
+        TRY(check_cuda(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, keys, keys2, idx, idx2, int(total), 0,
+                                                       ray_bits + pid_bits, s), "DeviceRadixSort"));
+        const int64_t warps = (total + 31) / 32;
+        reduce_runs_kernel<B><<<unsigned((warps * 32 + 127) / 128), 128, 0, s>>>(
+            keys2, idx2, total, ray_bits, rec, recq, basis, gsig, gsh, signal);
+        TRY(check_launch("reduce_runs_kernel"));
+    }
+    {
+        // loss_sum += sum of per-ray squared errors (fixed reduction order)
+        double* part = nullptr;
+        ALLOC(part, sizeof(double));
+        size_t red_bytes = 0;
+        cub::DeviceReduce::Sum(nullptr, red_bytes, loss_ray, part, int(n), s);
+        void* rtmp = nullptr;
+        if ((st = check_cuda(cudaMallocAsync(&rtmp, red_bytes, s), "cudaMallocAsync")) == DOT_OK) {
+            st = check_cuda(cub::DeviceReduce::Sum(rtmp, red_bytes, loss_ray, part, int(n), s), "DeviceReduce");
+            if (st == DOT_OK) st = launch_add_f64(loss_sum, part, s);
+        }
+        cudaFreeAsync(rtmp, s);
+        cudaFreeAsync(part, s);
+        if (st != DOT_OK) {
+            cleanup();
+            return st;
+        }
+    }
+    cleanup();
+#undef ALLOC
+#undef TRY
+    return DOT_OK;
+}
+
+__global__ void iota_kernel(int32_t* p, int64_t n) {
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < n) p[i] = int32_t(i);
+}
+
+__global__ void add_f64_kernel(double* dst, const double* src) { dst[0] += src[0]; }
+
+int launch_iota(int32_t* p, int64_t n, cudaStream_t s) {
+    iota_kernel<<<unsigned((n + 255) / 256), 256, 0, s>>>(p, n);
+    return check_launch("iota_kernel");
+}
+
+int launch_add_f64(double* dst, const double* src, cudaStream_t s) {
+    add_f64_kernel<<<1, 1, 0, s>>>(dst, src);
+    return check_launch("add_f64_kernel");
+}
+
+}  // namespace dot
+
+using namespace dot;
+
+extern "C" int dot_render_bwd_sorted(const dot_tree_view* tree, const double* origins, const double* dirs,
+                                     const double* targets, const int64_t* ray_id, int64_t n_rays,
+                                     const double* background, double early_stop_eps, double t_near,
+                                     double t_far, double grad_scale, float* grad_sigma, float* grad_sh,
+                                     int32_t gsh_stride, double* signal, uint8_t* touched,
+                                     double* loss_sum, void* stream) {
+    if (int st = validate_tree_view(tree)) return st;
+    if (n_rays < 0 || (n_rays && (!origins || !dirs || !targets)) || !background)
+        return set_error(DOT_BAD_ARG, "bad ray arrays");
+    if (!grad_sigma || !grad_sh || !signal || !touched || !loss_sum)
+        return set_error(DOT_BAD_ARG, "gradient / signal outputs must not be NULL");
+    if (gsh_stride != tree->sh_stride)
+        return set_error(DOT_BAD_ARG, "gsh_stride must equal sh_stride (%d)", tree->sh_stride);
+    if (n_rays == 0) return DOT_OK;
+    const TreeDev T = make_tree(*tree);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    switch (T.basis_count) {
+        case 1: return run_sorted<1>(T, tree->capacity, origins, dirs, targets, ray_id, n_rays, background, early_stop_eps, t_near, t_far, grad_scale, grad_sigma, grad_sh, signal, touched, loss_sum, s);
+        case 4: return run_sorted<4>(T, tree->capacity, origins, dirs, targets, ray_id, n_rays, background, early_stop_eps, t_near, t_far, grad_scale, grad_sigma, grad_sh, signal, touched, loss_sum, s);
+        case 9: return run_sorted<9>(T, tree->capacity, origins, dirs, targets, ray_id, n_rays, background, early_stop_eps, t_near, t_far, grad_scale, grad_sigma, grad_sh, signal, touched, loss_sum, s);
+        case 16: return run_sorted<16>(T, tree->capacity, origins, dirs, targets, ray_id, n_rays, background, early_stop_eps, t_near, t_far, grad_scale, grad_sigma, grad_sh, signal, touched, loss_sum, s);
+        default: return set_error(DOT_BAD_ARG, "basis_count must be 1, 4, 9 or 16");
+    }
+}

@@ -261,7 +261,7 @@ def render_and_backprop(tree: SparseOctree, origins, dirs, targets, background,
                         t_far: float = math.inf, grad_scale: float | None = None,
                         workspace: BackpropWorkspace | None = None, accumulate: bool = False,
                         return_rgb: bool = False, kernel_events=None, kernel_flags: int = 0,
-                        coherent: bool = True):
+                        coherent: bool = True, deterministic: bool = False):
     """Batch MSE loss, analytic leaf gradients and per-leaf signal (render.py:175-225).
 
     Returns (loss, GradBuffer, signal).  ``grad_scale`` defaults to the
@@ -269,6 +269,12 @@ def render_and_backprop(tree: SparseOctree, origins, dirs, targets, background,
     partial gradients sum to the full-batch gradient.  With numpy inputs the
     loss is a Python float and gradients are float64 numpy arrays; with torch
     inputs everything stays on the device (loss is a 0-d tensor).
+
+    ``deterministic=True`` reduces every leaf's contributions in the
+    reference's order (scatter_kernel: rays in batch order, f64 sums) via
+    per-segment records + a radix sort (``dot_render_bwd_sorted``): results
+    are bit-identical from run to run.  It synchronises once per call and is
+    slower than the default atomic reduction.
     """
     io = _IO(tree, origins)
     o = io.rays(origins, "origins")
@@ -304,11 +310,20 @@ def render_and_backprop(tree: SparseOctree, origins, dirs, targets, background,
             o, d, t = o[perm], d[perm], t[perm]
         if kernel_events is not None:
             kernel_events[0].record()
-        _lib.call("dot_render_bwd", _lib.ctypes.byref(view), _lib.ptr(o), _lib.ptr(d), _lib.ptr(t), n,
-                  _bg_ptr(bg), float(early_stop_eps), float(t_near), float(t_far), gs,
-                  _lib.ptr(ws.dsigma), _lib.ptr(ws.dsh_store), tree.sh_stride, _lib.ptr(ws.signal),
-                  _lib.ptr(ws.touched), _lib.ptr(ws.loss), _lib.ptr(rgb), int(kernel_flags),
-                  _lib.stream_ptr())
+        if deterministic:
+            if rgb is not None:
+                raise InputError("return_rgb is not available with deterministic=True")
+            _lib.call("dot_render_bwd_sorted", _lib.ctypes.byref(view), _lib.ptr(o), _lib.ptr(d),
+                      _lib.ptr(t), _lib.ptr(perm), n, _bg_ptr(bg), float(early_stop_eps),
+                      float(t_near), float(t_far), gs, _lib.ptr(ws.dsigma), _lib.ptr(ws.dsh_store),
+                      tree.sh_stride, _lib.ptr(ws.signal), _lib.ptr(ws.touched), _lib.ptr(ws.loss),
+                      _lib.stream_ptr())
+        else:
+            _lib.call("dot_render_bwd", _lib.ctypes.byref(view), _lib.ptr(o), _lib.ptr(d), _lib.ptr(t),
+                      n, _bg_ptr(bg), float(early_stop_eps), float(t_near), float(t_far), gs,
+                      _lib.ptr(ws.dsigma), _lib.ptr(ws.dsh_store), tree.sh_stride,
+                      _lib.ptr(ws.signal), _lib.ptr(ws.touched), _lib.ptr(ws.loss), _lib.ptr(rgb),
+                      int(kernel_flags), _lib.stream_ptr())
         if kernel_events is not None:
             kernel_events[1].record()
         if perm is not None and rgb is not None:

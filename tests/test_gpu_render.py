@@ -173,3 +173,19 @@ def test_length_mismatch_raises():
     o, d = ray_batch(7, 4)
     with pytest.raises(InputError):
         render_and_backprop(tree, o, d, np.zeros((3, 3)), 0.0)
+
+
+def test_device_exp_ref(oracle):
+    """Every alpha = exp(-sigma delta) on the device uses exp_ref, which must
+    equal glibc's exp (the reference's) bit for bit."""
+    import torch
+    from paper_2307_15333_b200 import _lib
+    from test_host import _exp_args
+    x = _exp_args(1 << 20, seed=3)
+    want = oracle.exp(x)
+    xd = torch.from_numpy(x).cuda()
+    yd = torch.empty_like(xd)
+    _lib.call("dot_exp_ref_device", _lib.ptr(xd), _lib.ptr(yd), x.size, _lib.stream_ptr())
+    got = yd.cpu().numpy()
+    same = got.view(np.uint64) == want.view(np.uint64)
+    assert np.all(same | (np.isnan(got) & np.isnan(want))), x[~same][:5]

@@ -244,3 +244,28 @@ def test_locate_dyadic_predicate():
     assert view((0, 0, 0), 0.75) == 0
     assert view((0, 0, 0), 1.0, max_depth=22) == 0
     assert view((0, 0, 0), 1.0, capacity=1 << 26) == 0
+
+
+def _exp_args(n, seed=0):
+    rng = np.random.default_rng(seed)
+    parts = [-rng.uniform(0, 60, n), -rng.uniform(0, 1e-3, n), -rng.uniform(0, 1100, n),
+             rng.uniform(-1, 1, n), -708 - rng.uniform(0, 40, n), -rng.uniform(0, 1e-17, n),
+             rng.uniform(-745.2, -744.4, n // 8),
+             np.array([0.0, -0.0, -np.inf, np.inf, np.nan, -745.13321910194122, -1e-300, 709.0,
+                       1e-20, -2.0 ** -54, -2.0 ** -55, -512.0, -1024.0])]
+    return np.concatenate(parts)
+
+
+def test_exp_ref_matches_libm():
+    """The kernels' exp (dot_exp.cuh, host build of the same code) returns
+    glibc's exp bit for bit -- the reference's f64 exp (Numba -> libm)."""
+    from oracle import oracle
+    from paper_2307_15333_b200 import _lib
+    x = _exp_args(400_000)
+    want = oracle.exp(x)
+    got = np.empty_like(x)
+    _lib.load().dot_exp_ref_host(x.ctypes.data, got.ctypes.data, x.size)
+    assert np.array_equal(got.view(np.uint64), want.view(np.uint64)) or \
+        np.array_equal(got, want, equal_nan=True)
+    bad = np.nonzero(got.view(np.uint64) != want.view(np.uint64))[0]
+    assert all(np.isnan(x[bad])), x[bad][:5]

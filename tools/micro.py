@@ -55,9 +55,13 @@ def main():
     ms = timeit(lambda: render_rays(tree, fo, fd, 1.0, 1e-4))
     print(f"render_fwd full view {ms:7.3f} ms   {fo.shape[0] / ms / 1e3:8.1f} Mrays/s")
     ws = BackpropWorkspace.for_tree(tree)
-    for f in [int(x) for x in args.flags.split(",")]:
-        ms = timeit(lambda: render_and_backprop(tree, o, d, t, 1.0, 1e-4, workspace=ws, kernel_flags=f))
-        print(f"bwd flags={f:<3d}        {ms:7.3f} ms   {n / ms / 1e3:8.1f} Mrays/s")
+    for f in args.flags.split(","):
+        if f == "det":
+            fn = lambda: render_and_backprop(tree, o, d, t, 1.0, 1e-4, workspace=ws, deterministic=True)
+        else:
+            fn = lambda: render_and_backprop(tree, o, d, t, 1.0, 1e-4, workspace=ws, kernel_flags=int(f))
+        ms = timeit(fn)
+        print(f"bwd flags={f:<5s}      {ms:7.3f} ms   {n / ms / 1e3:8.1f} Mrays/s")
 
 
 if __name__ == "__main__":
