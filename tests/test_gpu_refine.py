@@ -215,3 +215,23 @@ def test_rmsprop_bit_exact_vs_oracle(oracle):
     np.testing.assert_array_equal(tree.sh.cpu().numpy(), sh0)
     np.testing.assert_array_equal(st.v_sigma.cpu().numpy(), vs)
     np.testing.assert_array_equal(st.v_sh.cpu().numpy(), vh)
+
+
+def test_config1_end_to_end_deterministic_refine_bytes_identical():
+    """Our deterministic backward's signal (bit-identical to the reference's)
+    drives our refine: the refined tree is byte-identical to the reference's
+    calibrate output on the same scene and rays (configs[0] end to end)."""
+    from paper_2307_15333_b200.calibrate import CalibrationConfig, calibrate
+    from paper_2307_15333_b200.render import render_and_backprop
+    from paper_2307_15333_b200.scene_io import load_tree_bytes, tree_bytes
+    from paper_2307_15333_b200.signals import SignalBuffer
+    z = np.load(os.path.join(GOLDEN, "config1.npz"))
+    tree = load_tree_bytes(z["scene_dot1"].tobytes(), device="cuda")
+    _, _, sig = render_and_backprop(tree, z["origins"], z["dirs"], z["targets"], 1.0,
+                                    deterministic=True)
+    buf = SignalBuffer(tree)
+    buf.accumulate(sig, z["origins"].shape[0])
+    rep = calibrate(tree, buf, CalibrationConfig(tau=0.01, gamma=0.05))
+    assert rep.merges_applied == int(z["calib_merges"])
+    assert rep.splits_applied == int(z["calib_splits"])
+    assert hashlib.sha256(tree_bytes(tree)).hexdigest() == str(z["calib_sha256"])
