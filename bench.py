@@ -55,6 +55,17 @@ RAY_BYTES = 72
 SEG_BYTES = 4 + 12 * B_SH + 4 * (1 + 3 * B_SH) + 8
 
 
+def measured_traffic(kernel):
+    """DRAM bytes per launch of `kernel` from the committed ncu --set full
+    capture (tools/summarise_profiles.py -> profiles/traffic.json)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
+            t = json.load(fh)[kernel]
+        return float(t["dram_bytes_per_launch"]), t["capture"]
+    except Exception:
+        return None, None
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
@@ -283,11 +294,17 @@ def run_ours(args, rank, world, local_rank):
     clocks = ClockSampler(local_rank).start()
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
+    # ncu --profile-from-start off captures exactly the timed steps
+    profile_range = bool(os.environ.get("DOT_PROFILE_RANGE"))
+    if profile_range:
+        torch.cuda.profiler.start()
     t0.record()
     for k in range(args.warmup, total_steps):
         step(k)
     t1.record()
     torch.cuda.synchronize()
+    if profile_range:
+        torch.cuda.profiler.stop()
     clk = clocks.stop()
     ms = t0.elapsed_time(t1)
     if world > 1:
@@ -311,6 +328,10 @@ def run_ours(args, rank, world, local_rank):
     alg_bytes = per_rank * RAY_BYTES + comp * SEG_BYTES
     hbm, peak_kind = peaks()
     achieved = alg_bytes / (kern_ms_avg / 1e3) / 1e9
+    traffic, traffic_src = measured_traffic("render_bwd_buffered")
+    # REDs per launch: dsigma for every composited segment, 12 x F32x4 SH rows
+    # and one f64 signal add for every segment with q > 0
+    reds = comp + 13 * qpos
 
     # e2e: public API from pinned host buffers (H2D batch + D2H loss per step).
     # Headline: RayBatchStager overlaps step k+1's H2D copy (side copy stream)
@@ -408,9 +429,11 @@ def run_ours(args, rank, world, local_rank):
         "gpu_launches": (2 + (1 if world == 1 else len(chunk_bounds(tree.capacity, args.ar_chunks)))) * args.steps,
         "roofline": {
             "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-            "frac": achieved / hbm, "traffic": None, "kernel": "render_bwd_buffered_kernel<16,48>",
+            "frac": achieved / hbm, "traffic": traffic, "traffic_source": traffic_src,
+            "kernel": "render_bwd_buffered_kernel<16,48>",
             "kernel_ms": kern_ms_avg, "alg_bytes_per_launch": alg_bytes, "peak_kind": peak_kind,
             "bytes_model": f"{RAY_BYTES} B/ray + {SEG_BYTES} B/composited segment",
+            "atomics_per_launch": reds, "atomics_per_s": reds / (kern_ms_avg / 1e3),
         },
         "e2e": {"value": e2e_value, "unit": "rays/s", "h2d_bytes_per_step": per_rank * 72,
                 "d2h_bytes_per_step": 8, "ms_per_step": e2e_ms / args.steps,
@@ -466,7 +489,26 @@ def bench_render(tree, dev, args, world):
         tt = torch.tensor([ms_cam], device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms_cam = float(tt.item())
+    # roofline of render_camera_kernel: per view 12 B/pixel rgb out (rays are
+    # generated in-kernel: 0 B in) + per composited segment sigma 4 B + the
+    # 192 B SH row when q > 0; counts from dot_ray_stats
+    from paper_2307_15333_b200 import _lib
+    stats = torch.zeros(3, dtype=torch.int64, device=dev)
+    tv, _ = tree.tree_view()
+    for o, d in views:
+        _lib.call("dot_ray_stats", _lib.ctypes.byref(tv), _lib.ptr(o), _lib.ptr(d), o.shape[0], EPS,
+                  _lib.ptr(stats), _lib.stream_ptr())
+    seg, comp, qpos = [int(x) for x in stats.cpu()]
+    alg = W * H * n_views * 12 + comp * 4 + qpos * 12 * B_SH
+    hbm, peak_kind = peaks()
+    achieved = alg / n_views / (ms_cam / n_views / 1e3) / 1e9
     return {"rays_per_s": rays / (ms_cam / 1e3), "fps_800x800": n_views * world / (ms_cam / 1e3),
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                         "frac": achieved / hbm, "peak_kind": peak_kind,
+                         "kernel": "render_camera_kernel<16>", "alg_bytes_per_view": alg / n_views,
+                         "bytes_model": "12 B/pixel + 4 B/composited segment + 192 B/segment with q>0",
+                         "composited_per_ray": comp / (W * H * n_views),
+                         "segments_per_ray": seg / (W * H * n_views)},
             "ms_per_view": ms_cam / n_views, "views": n_views * world, "eps": EPS,
             "workload": "configs[2]: 800x800 random hemisphere views, render_view (in-kernel rays)",
             "rays_resident": {"rays_per_s": rays / (ms / 1e3), "ms_per_view": ms / n_views,
