@@ -278,9 +278,11 @@ def run_ours(args, rank, world, local_rank):
 
     def step(k, timed_kernel=True):
         idx = batch_index(k)
+        # the batch is read in place from the resident pool (ray_index): no gather
         loss, grads, sig = render_and_backprop(
-            tree, origins[idx], dirs[idx], targets[idx], BG, EPS, grad_scale=gs, workspace=ws,
-            kernel_events=kev[k] if timed_kernel else None, kernel_flags=args.bwd_flags)
+            tree, origins, dirs, targets, BG, EPS, grad_scale=gs, workspace=ws,
+            kernel_events=kev[k] if timed_kernel else None, kernel_flags=args.bwd_flags,
+            ray_index=idx)
         exchange_and_update(grads)
         buf.accumulate(sig, per_rank, validate=False)
         return loss

@@ -112,10 +112,17 @@ int dot_render_camera(const dot_tree_view* tree, const double* cam_to_world, dou
  *     error; the caller divides by n), and sets touched[capacity] u8 to 1 for
  *     every traversed leaf (post-cut segments included, like scatter_kernel).
  *     grad_scale is the reference's 2/n (2/n_global when rays are sharded).
- *     rgb_out (f32 [n,3]) may be NULL.  flags: bit0 = skip post-cut touched
- *     marking (not reference semantics). */
+ *     ray_index (may be NULL = 0..n-1) names the n rays to process: ray r of
+ *     the batch is origins/dirs/targets[ray_index[r]], read in place (a
+ *     caller passes a coherence-sorted order, or a batch drawn from a larger
+ *     resident ray pool, without gathering); rgb_out (f32, indexed like the
+ *     arrays) may be NULL.  flags: bit 0 = skip post-cut touched marking
+ *     (not reference semantics); bit 15 = per-lane REDs instead of the
+ *     warp-cooperative SH-row scatter; bits 13 / 14 = timing diagnostics
+ *     (pass 1 only / no reductions: results are incomplete). */
 int dot_render_bwd(const dot_tree_view* tree, const double* origins, const double* dirs,
-                   const double* targets, int64_t n_rays, const double* background,
+                   const double* targets, const int64_t* ray_index, int64_t n_rays,
+                   const double* background,
                    double early_stop_eps, double t_near, double t_far, double grad_scale,
                    float* grad_sigma, float* grad_sh, int32_t gsh_stride, double* signal,
                    uint8_t* touched, double* loss_sum, float* rgb_out, int32_t flags,
@@ -127,12 +134,13 @@ int dot_render_bwd(const dot_tree_view* tree, const double* origins, const doubl
  *     scatter_kernel (_kernels.py:327-346) sums each leaf's contributions
  *     serially over rays in batch order -- via per-segment records, a radix
  *     sort by (leaf, original ray index) and a sequential f64 sum per leaf.
- *     Results are bit-identical across runs.  ray_id[n] (may be NULL =
- *     identity) gives the original batch index of input ray r, so a caller
- *     may hand the rays in any (e.g. coherence-sorted) order.  Synchronises
- *     the stream (the record count sizes the sort). */
+ *     Results are bit-identical across runs.  ray_index (may be NULL) must
+ *     be a permutation of 0..n-1: rays are read at ray_index[r] and the
+ *     reduction order is the order of the caller's arrays, so the batch may
+ *     be processed in any (e.g. coherence-sorted) order.  Synchronises the
+ *     stream (the record count sizes the sort). */
 int dot_render_bwd_sorted(const dot_tree_view* tree, const double* origins, const double* dirs,
-                          const double* targets, const int64_t* ray_id, int64_t n_rays,
+                          const double* targets, const int64_t* ray_index, int64_t n_rays,
                           const double* background, double early_stop_eps, double t_near,
                           double t_far, double grad_scale, float* grad_sigma, float* grad_sh,
                           int32_t gsh_stride, double* signal, uint8_t* touched, double* loss_sum,
@@ -144,9 +152,10 @@ int dot_render_bwd_sorted(const dot_tree_view* tree, const double* origins, cons
  *     rays, so the order changes only speed. */
 int dot_ray_keys(const dot_tree_view* tree, const double* origins, const double* dirs,
                  int64_t n_rays, uint64_t* keys, void* stream);
-/* 31-bit keys (origin 4 bits/axis, direction 10x9 bits): half the sort passes. */
+/* 31-bit keys (origin 4 bits/axis, direction 10x9 bits): half the sort
+ * passes.  ray_index (may be NULL) as in dot_render_bwd. */
 int dot_ray_keys32(const dot_tree_view* tree, const double* origins, const double* dirs,
-                   int64_t n_rays, int32_t* keys, void* stream);
+                   const int64_t* ray_index, int64_t n_rays, int32_t* keys, void* stream);
 
 /* --- workload statistics (measurement helper, no reference counterpart):
  *     totals[0] += traversed segments, totals[1] += composited (pre-cut)

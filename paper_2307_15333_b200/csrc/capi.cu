@@ -65,7 +65,7 @@ using namespace dot;
 
 extern "C" {
 
-int dot_abi_version(void) { return 2; }
+int dot_abi_version(void) { return 3; }
 
 const char* dot_last_error(void) { return g_err; }
 
@@ -137,7 +137,8 @@ int dot_render_fwd(const dot_tree_view* tree, const double* origins, const doubl
 }
 
 int dot_render_bwd(const dot_tree_view* tree, const double* origins, const double* dirs,
-                   const double* targets, int64_t n_rays, const double* background,
+                   const double* targets, const int64_t* ray_index, int64_t n_rays,
+                   const double* background,
                    double early_stop_eps, double t_near, double t_far, double grad_scale,
                    float* grad_sigma, float* grad_sh, int32_t gsh_stride, double* signal,
                    uint8_t* touched, double* loss_sum, float* rgb_out, int32_t flags,
@@ -151,7 +152,7 @@ int dot_render_bwd(const dot_tree_view* tree, const double* origins, const doubl
         return set_error(DOT_BAD_ARG, "gsh_stride must equal sh_stride (%d)", tree->sh_stride);
     if ((reinterpret_cast<uintptr_t>(grad_sh) & 15) != 0)
         return set_error(DOT_BAD_ARG, "grad_sh must be 16-byte aligned");
-    return launch_render_bwd(make_tree(*tree), origins, dirs, targets, n_rays, background,
+    return launch_render_bwd(make_tree(*tree), origins, dirs, targets, ray_index, n_rays, background,
                              early_stop_eps, t_near, t_far, grad_scale, grad_sigma, grad_sh,
                              signal, touched, loss_sum, rgb_out, flags,
                              static_cast<cudaStream_t>(stream));
@@ -165,11 +166,12 @@ int dot_ray_keys(const dot_tree_view* tree, const double* origins, const double*
                            static_cast<cudaStream_t>(stream));
 }
 
-int dot_ray_keys32(const dot_tree_view* tree, const double* origins, const double* dirs, int64_t n_rays,
-                   int32_t* keys, void* stream) {
+int dot_ray_keys32(const dot_tree_view* tree, const double* origins, const double* dirs,
+                   const int64_t* ray_index, int64_t n_rays, int32_t* keys, void* stream) {
     if (int st = validate_tree_view(tree)) return st;
     if (n_rays < 0 || (n_rays && (!origins || !dirs || !keys))) return set_error(DOT_BAD_ARG, "bad arrays");
-    return launch_ray_keys32(make_tree(*tree), origins, dirs, n_rays, keys, static_cast<cudaStream_t>(stream));
+    return launch_ray_keys32(make_tree(*tree), origins, dirs, ray_index, n_rays, keys,
+                             static_cast<cudaStream_t>(stream));
 }
 
 int dot_render_camera(const dot_tree_view* tree, const double* cam_to_world, double focal, int32_t width,

@@ -17,7 +17,6 @@ struct EmitArgs {
     double* recq;                    // [cap] q = 1 - alpha
     float* basis;                    // [n * B] SH basis per original ray
     double* loss_ray;                // [n] squared error per original ray
-    const int64_t* ray_id;           // [n] original index of input ray r (NULL = identity)
     int ray_bits;
 };
 
@@ -36,27 +35,18 @@ int launch_render_fwd(const TreeDev& T, const double* o, const double* d, int64_
                       const double* bg, double eps, double tn, double tf, float* rgb, float* tfin,
                       float* wsum, float* depth, cudaStream_t s);
 int launch_render_bwd(const TreeDev& T, const double* o, const double* d, const double* tgt,
-                      int64_t n, const double* bg, double eps, double tn, double tf, double gs,
-                      float* gsig, float* gsh, double* signal, uint8_t* touched, double* loss,
-                      float* rgb_out, int flags, cudaStream_t s);
-
-int launch_render_bwd_two_kernel(const TreeDev& T, const double* o, const double* d, const double* tgt,
-                                 int64_t n, const double* bg, double eps, double tn, double tf, double gs,
-                                 float* gsig, float* gsh, double* signal, uint8_t* touched, double* loss,
-                                 float* rgb_out, int flags, cudaStream_t s);
-int launch_render_bwd_replay(const TreeDev& T, const double* o, const double* d, int64_t n, const double* bg,
-                             double eps, double tn, double tf, float* gsig, float* gsh, double* signal,
-                             uint8_t* touched, const float* ray_g, const float* ray_rgb,
-                             const uint8_t* ray_flag, int flags, cudaStream_t s);
+                      const int64_t* ray_idx, int64_t n, const double* bg, double eps, double tn,
+                      double tf, double gs, float* gsig, float* gsh, double* signal,
+                      uint8_t* touched, double* loss, float* rgb_out, int flags, cudaStream_t s);
 int launch_ray_keys(const TreeDev& T, const double* o, const double* d, int64_t n, unsigned long long* keys,
                     cudaStream_t s);
-int launch_ray_keys32(const TreeDev& T, const double* o, const double* d, int64_t n, int32_t* keys,
-                      cudaStream_t s);
+int launch_ray_keys32(const TreeDev& T, const double* o, const double* d, const int64_t* ray_idx,
+                      int64_t n, int32_t* keys, cudaStream_t s);
 int launch_render_camera(const TreeDev& T, const double* cam_to_world, double focal, int width, int height,
                          const double* bg, double eps, float* rgb, float* tfin, float* depth, cudaStream_t s);
 int launch_render_bwd_emit(const TreeDev& T, const double* o, const double* d, const double* tgt,
-                           int64_t n, const double* bg, double eps, double tn, double tf, double gs,
-                           uint8_t* touched, const EmitArgs& ea, cudaStream_t s);
+                           const int64_t* ray_idx, int64_t n, const double* bg, double eps, double tn,
+                           double tf, double gs, uint8_t* touched, const EmitArgs& ea, cudaStream_t s);
 int launch_exp_ref(const double* x, double* y, int64_t n, cudaStream_t s);
 int launch_locate_build(const TreeDev& T, int level, int32_t* table, cudaStream_t s);
 int launch_ray_stats(const TreeDev& T, const double* o, const double* d, int64_t n, double eps,

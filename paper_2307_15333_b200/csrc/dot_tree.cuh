@@ -167,67 +167,6 @@ __device__ __forceinline__ Leaf descend_grid(const TreeDev& T, double px, double
     return L;
 }
 
-// Exact restart-from-ancestor.  A root descent is a chain of octant choices
-// o_j = cmp(p, c_j) with c_{j+1} = c_j +/- h_{j+1}; for a new probe point the
-// chain coincides with the previous leaf's path up to the first level k
-// where the comparison differs.  The cache keeps that path (3 bits/level)
-// and the node words of its ancestors (shared memory, one row per thread),
-// so the matched prefix costs only the comparisons (no memory traffic) and
-// global loads start at level k.  The result is identical to descend().
-constexpr int kPathLevels = 21;  // 3 bits x 21 levels in one 64-bit word
-
-struct PathCache {
-    int32_t* stk;       // stk[j] = word of the level-j node on the cached path (stk[0] = root)
-    uint64_t path;      // octant taken at level j in bits [3j, 3j+3)
-    int depth;          // depth of the cached leaf, -1 = empty
-};
-
-__device__ __forceinline__ Leaf descend_cached(const TreeDev& T, double px, double py, double pz,
-                                               PathCache& pc) {
-    double cx = T.cx, cy = T.cy, cz = T.cz, h = T.half;
-    int j = 0;
-    int o = 0;
-    const int pd = pc.depth;
-    // matched prefix: comparisons only
-    while (j < pd) {
-        o = (px >= cx ? 1 : 0) | (py >= cy ? 2 : 0) | (pz >= cz ? 4 : 0);
-        if (o != int((pc.path >> (3 * j)) & 7u)) break;
-        h = dmul(h, 0.5);
-        cx = (o & 1) ? dadd(cx, h) : dsub(cx, h);
-        cy = (o & 2) ? dadd(cy, h) : dsub(cy, h);
-        cz = (o & 4) ? dadd(cz, h) : dsub(cz, h);
-        ++j;
-    }
-    int32_t w;
-    if (j == pd) {
-        w = pc.stk[j];  // same leaf as before
-    } else {
-        if (pd < 0) j = 0;
-        w = pc.stk[j];
-        uint64_t path = pc.path & ((1ull << (3 * j)) - 1ull);
-        while (w >= 0) {
-            o = (px >= cx ? 1 : 0) | (py >= cy ? 2 : 0) | (pz >= cz ? 4 : 0);
-            h = dmul(h, 0.5);
-            cx = (o & 1) ? dadd(cx, h) : dsub(cx, h);
-            cy = (o & 2) ? dadd(cy, h) : dsub(cy, h);
-            cz = (o & 4) ? dadd(cz, h) : dsub(cz, h);
-            w = __ldg(T.node + w + o);
-            path |= uint64_t(o) << (3 * j);
-            ++j;
-            pc.stk[j] = w;
-        }
-        pc.path = path;
-        pc.depth = j;
-    }
-    Leaf L;
-    L.pid = ~w;
-    L.cx = cx;
-    L.cy = cy;
-    L.cz = cz;
-    L.h = h;
-    return L;
-}
-
 // One ray walking the tree one exact leaf segment at a time (_trace_ray).
 struct Tracer {
     double ox, oy, oz, dx, dy, dz;
@@ -264,17 +203,16 @@ struct Tracer {
     // _kernels.py:112-158.  Returns false when the ray has left the cube.
     // PREFETCH: touch the leaf's sigma and SH row (L1) right after the descent
     // so those gathers overlap the exit-face divisions below.
-    template <bool CACHED = false, bool PREFETCH = false>
-    __device__ __forceinline__ bool next(const TreeDev& T, Leaf& L, double& t_entry,
-                                         double& delta, PathCache& pc, bool want_payload = true) {
+    template <bool PREFETCH>
+    __device__ __forceinline__ bool step(const TreeDev& T, Leaf& L, double& t_entry, double& delta,
+                                         bool want_payload) {
         for (;;) {
             const double probe = dadd(t, nudge);
             if (probe >= t1) return false;
             const double px = dadd(ox, dmul(probe, dx));
             const double py = dadd(oy, dmul(probe, dy));
             const double pz = dadd(oz, dmul(probe, dz));
-            if constexpr (CACHED) L = descend_cached(T, px, py, pz, pc);
-            else L = descend(T, px, py, pz);
+            L = descend(T, px, py, pz);
             if (PREFETCH && want_payload) {
                 const char* row = reinterpret_cast<const char*>(T.sh + int64_t(L.pid) * T.sh_stride);
                 asm volatile("prefetch.global.L1 [%0];" :: "l"(T.sigma + L.pid));
@@ -306,14 +244,12 @@ struct Tracer {
     }
 
     __device__ __forceinline__ bool next(const TreeDev& T, Leaf& L, double& t_entry, double& delta) {
-        PathCache none;
-        return next<false, false>(T, L, t_entry, delta, none);
+        return step<false>(T, L, t_entry, delta, false);
     }
 
     __device__ __forceinline__ bool next_prefetch(const TreeDev& T, Leaf& L, double& t_entry,
                                                   double& delta, bool want_payload = true) {
-        PathCache none;
-        return next<false, true>(T, L, t_entry, delta, none, want_payload);
+        return step<true>(T, L, t_entry, delta, want_payload);
     }
 };
 

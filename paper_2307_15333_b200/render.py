@@ -19,7 +19,6 @@ and gradients, float64 signal); host torch tensors are copied with
 from __future__ import annotations
 
 import math
-import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -32,7 +31,6 @@ from .octree import SparseOctree
 EPS_T = 1e-4  # early-termination transmittance threshold (render.py:23)
 UNIT_TOL = 1e-6
 COHERENT_MIN_RAYS = 1 << 14  # below this a key sort costs more than it saves
-COHERENT_KEY_BITS = int(os.environ.get("DOT_COHERENT_KEY_BITS", "32"))
 
 
 @dataclass
@@ -261,7 +259,7 @@ def render_and_backprop(tree: SparseOctree, origins, dirs, targets, background,
                         t_far: float = math.inf, grad_scale: float | None = None,
                         workspace: BackpropWorkspace | None = None, accumulate: bool = False,
                         return_rgb: bool = False, kernel_events=None, kernel_flags: int = 0,
-                        coherent: bool = True, deterministic: bool = False):
+                        coherent: bool = True, deterministic: bool = False, ray_index=None):
     """Batch MSE loss, analytic leaf gradients and per-leaf signal (render.py:175-225).
 
     Returns (loss, GradBuffer, signal).  ``grad_scale`` defaults to the
@@ -270,18 +268,33 @@ def render_and_backprop(tree: SparseOctree, origins, dirs, targets, background,
     loss is a Python float and gradients are float64 numpy arrays; with torch
     inputs everything stays on the device (loss is a 0-d tensor).
 
+    ``ray_index`` (device int64 tensor, optional; not in the reference) makes
+    the batch ``origins[ray_index]`` etc. -- e.g. a random slice of a
+    resident ray pool -- read in place by the kernel instead of gathered.
+    ``coherent`` reorders the batch internally (origin / direction Morton
+    keys) so each warp walks neighbouring cells; results are sums over rays.
+
     ``deterministic=True`` reduces every leaf's contributions in the
     reference's order (scatter_kernel: rays in batch order, f64 sums) via
     per-segment records + a radix sort (``dot_render_bwd_sorted``): results
-    are bit-identical from run to run.  It synchronises once per call and is
-    slower than the default atomic reduction.
+    are bit-identical from run to run and the signal equals the reference's
+    bit for bit.  It synchronises once per call and is slower than the
+    default (warp-cooperative atomic) reduction.
     """
     io = _IO(tree, origins)
     o = io.rays(origins, "origins")
     d = io.rays(dirs, "dirs")
     t = io.rays(targets, "targets")
-    n = o.shape[0]
-    if t.shape[0] != n or d.shape[0] != n:
+    if ray_index is not None:
+        idx = torch.as_tensor(ray_index, device=tree.device).reshape(-1).to(torch.int64)
+        if o.shape[0] != d.shape[0] or o.shape[0] != t.shape[0]:
+            raise InputError("origins, dirs and targets must have the same length")
+        if deterministic:  # the reference order is the batch order: materialise it
+            o, d, t, idx = o[idx], d[idx], t[idx], None
+    else:
+        idx = None
+    n = int(idx.shape[0]) if idx is not None else o.shape[0]
+    if idx is None and (t.shape[0] != n or d.shape[0] != n):
         raise InputError(f"batch length mismatch: {n} origins, {d.shape[0]} dirs, "
                          f"{t.shape[0]} targets")
     ws = workspace if workspace is not None else BackpropWorkspace.for_tree(tree)
@@ -289,47 +302,39 @@ def render_and_backprop(tree: SparseOctree, origins, dirs, targets, background,
         raise InputError("workspace capacity does not match the tree")
     if workspace is not None and not accumulate:
         ws.zero_()
+    if return_rgb and idx is not None:
+        raise InputError("return_rgb is not available with ray_index")
     rgb = torch.empty(n, 3, dtype=torch.float32, device=tree.device) if return_rgb else None
-    perm = None
     if n:
         gs = 2.0 / n if grad_scale is None else float(grad_scale)
         bg = _background(background)
         view, _topo = tree.tree_view()
         if coherent and n >= COHERENT_MIN_RAYS:
-            # reorder the batch so each warp walks neighbouring cells; loss,
-            # gradients and signal are sums over rays (order-independent)
-            if COHERENT_KEY_BITS == 32:  # 31-bit keys: half the radix-sort passes
-                keys = torch.empty(n, dtype=torch.int32, device=tree.device)
-                _lib.call("dot_ray_keys32", _lib.ctypes.byref(view), _lib.ptr(o), _lib.ptr(d), n,
-                          _lib.ptr(keys), _lib.stream_ptr())
-            else:
-                keys = torch.empty(n, dtype=torch.int64, device=tree.device)
-                _lib.call("dot_ray_keys", _lib.ctypes.byref(view), _lib.ptr(o), _lib.ptr(d), n,
-                          _lib.ptr(keys), _lib.stream_ptr())
+            # visit the batch in coherence order: sort 31-bit (origin, direction)
+            # Morton keys and hand the kernel the permuted index (no gathers)
+            keys = torch.empty(n, dtype=torch.int32, device=tree.device)
+            _lib.call("dot_ray_keys32", _lib.ctypes.byref(view), _lib.ptr(o), _lib.ptr(d),
+                      _lib.ptr(idx), n, _lib.ptr(keys), _lib.stream_ptr())
             perm = torch.argsort(keys)
-            o, d, t = o[perm], d[perm], t[perm]
+            idx = perm if idx is None else idx[perm]
         if kernel_events is not None:
             kernel_events[0].record()
         if deterministic:
             if rgb is not None:
                 raise InputError("return_rgb is not available with deterministic=True")
             _lib.call("dot_render_bwd_sorted", _lib.ctypes.byref(view), _lib.ptr(o), _lib.ptr(d),
-                      _lib.ptr(t), _lib.ptr(perm), n, _bg_ptr(bg), float(early_stop_eps),
+                      _lib.ptr(t), _lib.ptr(idx), n, _bg_ptr(bg), float(early_stop_eps),
                       float(t_near), float(t_far), gs, _lib.ptr(ws.dsigma), _lib.ptr(ws.dsh_store),
                       tree.sh_stride, _lib.ptr(ws.signal), _lib.ptr(ws.touched), _lib.ptr(ws.loss),
                       _lib.stream_ptr())
         else:
             _lib.call("dot_render_bwd", _lib.ctypes.byref(view), _lib.ptr(o), _lib.ptr(d), _lib.ptr(t),
-                      n, _bg_ptr(bg), float(early_stop_eps), float(t_near), float(t_far), gs,
-                      _lib.ptr(ws.dsigma), _lib.ptr(ws.dsh_store), tree.sh_stride,
-                      _lib.ptr(ws.signal), _lib.ptr(ws.touched), _lib.ptr(ws.loss), _lib.ptr(rgb),
-                      int(kernel_flags), _lib.stream_ptr())
+                      _lib.ptr(idx), n, _bg_ptr(bg), float(early_stop_eps), float(t_near),
+                      float(t_far), gs, _lib.ptr(ws.dsigma), _lib.ptr(ws.dsh_store),
+                      tree.sh_stride, _lib.ptr(ws.signal), _lib.ptr(ws.touched),
+                      _lib.ptr(ws.loss), _lib.ptr(rgb), int(kernel_flags), _lib.stream_ptr())
         if kernel_events is not None:
             kernel_events[1].record()
-        if perm is not None and rgb is not None:
-            unsorted = torch.empty_like(rgb)
-            unsorted[perm] = rgb
-            rgb = unsorted
     nsh = 3 * tree.basis_count
     dsh = ws.dsh_store if nsh == tree.sh_stride else ws.dsh_store[:, :nsh]
     if io.numpy:

@@ -2,8 +2,8 @@
 
     python tools/micro.py [--batch 20] [--order morton]
 Prints ms per call for render_fwd on the training batch and for the backward
-variants (flags: 0 record+scatter, 1 skip post-cut touched, 16 persistent
-single kernel, 2 legacy one-ray-per-thread)."""
+(dot_render_bwd flags: 0 default warp-cooperative scatter, 32768 per-lane
+REDs, 8192 / 16384 timing diagnostics; "det" = deterministic sorted path)."""
 import argparse
 import os
 import sys
@@ -33,7 +33,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--batch", type=int, default=20)
     ap.add_argument("--order", default="morton")
-    ap.add_argument("--flags", default="0,1,16,2")
+    ap.add_argument("--flags", default="0,32768,det")
     args = ap.parse_args()
     dev = torch.device("cuda")
     tree = scenes.config2_scene(device=dev)
