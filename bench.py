@@ -230,8 +230,7 @@ def run_ours(args, rank, world, local_rank):
     import torch
     import torch.distributed as dist
     from paper_2307_15333_b200 import scenes, _lib
-    from paper_2307_15333_b200.optim import RmsPropState, rmsprop_step
-    from paper_2307_15333_b200.render import BackpropWorkspace, render_and_backprop, render_rays
+    from paper_2307_15333_b200.optim import RmsPropState
     from paper_2307_15333_b200.signals import SignalBuffer
 
     dev = torch.device("cuda", local_rank)
@@ -247,7 +246,6 @@ def run_ours(args, rank, world, local_rank):
     gs = 2.0 / n_global
     state = RmsPropState(tree)
     buf = SignalBuffer(tree)
-    ws = BackpropWorkspace.for_tree(tree)
     gen = torch.Generator(device=dev)
     gen.manual_seed(1234 + rank)
     total_steps = args.warmup + args.steps
@@ -267,25 +265,24 @@ def run_ours(args, rank, world, local_rank):
             idx = idx[torch.argsort(morton_key(idx, wl.W, wl.H))]
         return idx
 
+    from paper_2307_15333_b200.optim import StepWorkspace, train_step
     from paper_2307_15333_b200.parallel import allreduce_grads_overlapped, chunk_bounds
+    sws = StepWorkspace(tree, buf)
+    ws = sws.ws
 
-    def exchange_and_update(grads):
+    def exchange(update):
         """NCCL all-reduce of the leaf gradients in row chunks, each chunk's
         RMSProp update issued as soon as its reduction lands (N = 1: one update)."""
-        allreduce_grads_overlapped(ws.dsigma, ws.dsh_store, ws.touched,
-                                   lambda lo, hi: rmsprop_step(tree, grads, state, rows=(lo, hi)),
+        allreduce_grads_overlapped(ws.dsigma, ws.dsh_store, ws.touched, update,
                                    chunks=args.ar_chunks)
 
     def step(k, timed_kernel=True):
-        idx = batch_index(k)
         # the batch is read in place from the resident pool (ray_index): no gather
-        loss, grads, sig = render_and_backprop(
-            tree, origins, dirs, targets, BG, EPS, grad_scale=gs, workspace=ws,
-            kernel_events=kev[k] if timed_kernel else None, kernel_flags=args.bwd_flags,
-            ray_index=idx)
-        exchange_and_update(grads)
-        buf.accumulate(sig, per_rank, validate=False)
-        return loss
+        return train_step(tree, origins, dirs, targets, state, buf, sws, BG, EPS,
+                          ray_index=batch_index(k), grad_scale=gs,
+                          exchange=exchange if world > 1 else None,
+                          kernel_events=kev[k] if timed_kernel else None,
+                          kernel_flags=args.bwd_flags)
 
     for k in range(args.warmup):
         step(k)
@@ -347,12 +344,13 @@ def run_ours(args, rank, world, local_rank):
         host.append(tuple(x[idx].cpu().pin_memory() for x in (origins, dirs, targets)))
     torch.cuda.synchronize()
 
+    ex = exchange if world > 1 else None
+
     def serial_loop(steps):
         for k in range(steps):
             o_h, d_h, t_h = host[k % 2]
-            loss, grads, sig = render_and_backprop(tree, o_h, d_h, t_h, BG, EPS, grad_scale=gs, workspace=ws)
-            exchange_and_update(grads)
-            buf.accumulate(sig, per_rank, validate=False)
+            loss = train_step(tree, o_h, d_h, t_h, state, buf, sws, BG, EPS, grad_scale=gs,
+                              exchange=ex)
             float(loss.item())
 
     stager = RayBatchStager(dev, max_rays=per_rank)
@@ -364,9 +362,8 @@ def run_ours(args, rank, world, local_rank):
             o_d, d_d, t_d = stager.take()
             if k + 1 < steps:
                 stager.stage(*host[(k + 1) % 2])
-            loss, grads, sig = render_and_backprop(tree, o_d, d_d, t_d, BG, EPS, grad_scale=gs, workspace=ws)
-            exchange_and_update(grads)
-            buf.accumulate(sig, per_rank, validate=False)
+            loss = train_step(tree, o_d, d_d, t_d, state, buf, sws, BG, EPS, grad_scale=gs,
+                              exchange=ex)
             stager.release()
             reader.push(loss)
         reader.flush()
@@ -439,8 +436,8 @@ def run_ours(args, rank, world, local_rank):
         },
         "e2e": {"value": e2e_value, "unit": "rays/s", "h2d_bytes_per_step": per_rank * 72,
                 "d2h_bytes_per_step": 8, "ms_per_step": e2e_ms / args.steps,
-                "api": "RayBatchStager (H2D of step k+1 overlaps step k) + render_and_backprop + "
-                       "rmsprop_step + LossReader (loss read one step late)",
+                "api": "RayBatchStager (H2D of step k+1 overlaps step k) + optim.train_step "
+                       "(render_and_backprop + rmsprop_step) + LossReader (loss read one step late)",
                 "serial_ms_per_step": e2e_serial_ms / args.steps},
         "clocks": clk,
         "render": render,

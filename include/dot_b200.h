@@ -217,12 +217,15 @@ int dot_refine_plan_merge_rounds(const dot_refine_plan* plan, int32_t* out, void
 void dot_refine_plan_destroy(dot_refine_plan* plan);
 
 /* --- optimizer (optim.rmsprop_step, optim.py:107-135): sparse RMSProp over
- *     leaves with touched[pid] != 0; sigma clamped >= 0.  v_* are f64. */
+ *     leaves with touched[pid] != 0; sigma clamped >= 0.  v_* are f64.
+ *     flags bit 0 ("consume"): zero each updated row's gradients after use,
+ *     so the next batch can accumulate into the same buffers without a
+ *     memset (rows that were not touched hold zero gradients already). */
 int dot_rmsprop_step(float* sigma, float* sh, int32_t sh_stride, int32_t n_sh,
-                     double* v_sigma, double* v_sh, const float* grad_sigma,
-                     const float* grad_sh, int32_t gsh_stride, const uint8_t* touched,
+                     double* v_sigma, double* v_sh, float* grad_sigma,
+                     float* grad_sh, int32_t gsh_stride, const uint8_t* touched,
                      int64_t capacity, double beta, double eps, double lr_sigma,
-                     double lr_sh, void* stream);
+                     double lr_sh, int32_t flags, void* stream);
 
 #ifdef __cplusplus
 }

@@ -65,7 +65,7 @@ using namespace dot;
 
 extern "C" {
 
-int dot_abi_version(void) { return 3; }
+int dot_abi_version(void) { return 4; }
 
 const char* dot_last_error(void) { return g_err; }
 

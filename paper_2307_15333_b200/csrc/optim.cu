@@ -15,6 +15,14 @@ namespace dot {
 __device__ __forceinline__ float rms_update(float theta, double& v, double g, double beta,
                                             double omb, double eps, double lr, bool clamp) {
     v = __dadd_rn(__dmul_rn(beta, v), __dmul_rn(__dmul_rn(omb, g), g));
+    // g == 0 (e.g. leaves touched only past the early-termination cut): the
+    // step lr*g / (sqrt(v) + eps) is exactly +-0 for any finite v, so theta
+    // is unchanged -- skip the IEEE sqrt and division (bit-identical result)
+    if (g == 0.0 && v <= 1.7976931348623157e308) {
+        double t = double(theta);
+        if (clamp && !(t >= 0.0)) t = (t != t) ? t : 0.0;
+        return float(t);
+    }
     double t = __dsub_rn(double(theta), __ddiv_rn(__dmul_rn(lr, g), __dadd_rn(__dsqrt_rn(v), eps)));
     if (clamp && !(t >= 0.0)) t = (t != t) ? t : 0.0;  // np.maximum keeps NaN
     return float(t);
@@ -23,9 +31,10 @@ __device__ __forceinline__ float rms_update(float theta, double& v, double g, do
 template <bool VEC, int MINB = 1>
 __global__ void __launch_bounds__(256, MINB) rmsprop_kernel(float* __restrict__ sigma, float* __restrict__ sh, int sh_stride, int n_sh,
                                double* __restrict__ v_sigma, double* __restrict__ v_sh,
-                               const float* __restrict__ gsig, const float* __restrict__ gsh,
+                               float* __restrict__ gsig, float* __restrict__ gsh,
                                int gsh_stride, const uint8_t* __restrict__ touched, int64_t cap,
-                               int quads, double beta, double eps, double lr_sigma, double lr_sh) {
+                               int quads, double beta, double eps, double lr_sigma, double lr_sh,
+                               bool consume) {
     const int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (t >= cap * quads) return;
     const int64_t row = t / quads;
@@ -36,10 +45,11 @@ __global__ void __launch_bounds__(256, MINB) rmsprop_kernel(float* __restrict__ 
         double v = v_sigma[row];
         sigma[row] = rms_update(sigma[row], v, double(gsig[row]), beta, omb, eps, lr_sigma, true);
         v_sigma[row] = v;
+        if (consume) gsig[row] = 0.f;
     }
     const int k0 = 4 * j;
     float* p = sh + row * sh_stride + k0;
-    const float* g = gsh + row * gsh_stride + k0;
+    float* g = gsh + row * gsh_stride + k0;
     double* v = v_sh + row * n_sh + k0;
     if (VEC) {  // n_sh % 4 == 0: all quads full and 16/32-byte aligned
         float4 th = *reinterpret_cast<float4*>(p);
@@ -52,11 +62,13 @@ __global__ void __launch_bounds__(256, MINB) rmsprop_kernel(float* __restrict__ 
         *reinterpret_cast<float4*>(p) = th;
         reinterpret_cast<double2*>(v)[0] = va;
         reinterpret_cast<double2*>(v)[1] = vb;
+        if (consume) *reinterpret_cast<float4*>(g) = make_float4(0.f, 0.f, 0.f, 0.f);
     } else {
         for (int u = 0; u < 4 && k0 + u < n_sh; ++u) {
             double vv = v[u];
             p[u] = rms_update(p[u], vv, double(g[u]), beta, omb, eps, lr_sh, false);
             v[u] = vv;
+            if (consume) g[u] = 0.f;
         }
     }
 }
@@ -66,9 +78,9 @@ __global__ void __launch_bounds__(256, MINB) rmsprop_kernel(float* __restrict__ 
 using namespace dot;
 
 extern "C" int dot_rmsprop_step(float* sigma, float* sh, int32_t sh_stride, int32_t n_sh, double* v_sigma,
-                                double* v_sh, const float* grad_sigma, const float* grad_sh,
+                                double* v_sh, float* grad_sigma, float* grad_sh,
                                 int32_t gsh_stride, const uint8_t* touched, int64_t capacity, double beta,
-                                double eps, double lr_sigma, double lr_sh, void* stream) {
+                                double eps, double lr_sigma, double lr_sh, int32_t flags, void* stream) {
     if (!sigma || !sh || !v_sigma || !v_sh || !grad_sigma || !grad_sh || !touched)
         return set_error(DOT_BAD_ARG, "rmsprop: NULL argument");
     if (!(beta > 0.0 && beta < 1.0)) return set_error(DOT_BAD_ARG, "beta must be in (0, 1), got %g", beta);
@@ -85,9 +97,11 @@ extern "C" int dot_rmsprop_step(float* sigma, float* sh, int32_t sh_stride, int3
     // unconstrained 48-register build, 8 blocks (32 regs) spills and loses.
     if (vec)
         rmsprop_kernel<true, 6><<<grid, 256, 0, s>>>(sigma, sh, sh_stride, n_sh, v_sigma, v_sh, grad_sigma, grad_sh,
-                                                     gsh_stride, touched, capacity, quads, beta, eps, lr_sigma, lr_sh);
+                                                     gsh_stride, touched, capacity, quads, beta, eps, lr_sigma, lr_sh,
+                                                     (flags & 1) != 0);
     else
         rmsprop_kernel<false><<<grid, 256, 0, s>>>(sigma, sh, sh_stride, n_sh, v_sigma, v_sh, grad_sigma, grad_sh,
-                                                   gsh_stride, touched, capacity, quads, beta, eps, lr_sigma, lr_sh);
+                                                   gsh_stride, touched, capacity, quads, beta, eps, lr_sigma, lr_sh,
+                                                   (flags & 1) != 0);
     return check_launch("rmsprop_kernel");
 }
