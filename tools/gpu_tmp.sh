@@ -1,4 +1,3 @@
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests -m gpu -q -x > gpurun_out/pytest_all.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_all.log
-timeout 600 python bench.py --skip-cpu --skip-render --skip-refine > gpurun_out/bench.json 2> gpurun_out/bench.err
-DOT_PROFILE_RANGE=1 timeout 300 ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv python bench.py --steps 3 --warmup 3 --skip-cpu --skip-render --skip-refine > gpurun_out/ncu_list.log 2>&1
+for wo in 0 1; do echo "WO=$wo"; DOT_WARP_ORDER=$wo timeout 300 python tools/micro.py --order random --flags 0,0 --batch 20; done > gpurun_out/micro_wo.log 2>&1
+DOT_WARP_ORDER=1 timeout 300 python -m pytest tests/test_gpu_render.py -q -x >> gpurun_out/micro_wo.log 2>&1
