@@ -549,10 +549,15 @@ def bench_refine(dev, args):
         buf.accumulator.copy_(acc)
         torch.cuda.synchronize()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        prof = k == passes and bool(os.environ.get("DOT_PROFILE_REFINE"))
+        if prof:
+            torch.cuda.profiler.start()
         a.record()
         rep = calibrate(tree, buf, CalibrationConfig(tau=0.01, gamma=0.10), events=False)
         b.record()
         torch.cuda.synchronize()
+        if prof:
+            torch.cuda.profiler.stop()
         if k:
             times.append(a.elapsed_time(b))
         n_new = tree.topology().n_nodes

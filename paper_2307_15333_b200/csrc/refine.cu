@@ -515,32 +515,56 @@ __global__ void level_emit_kernel(TreeDev T, int64_t m, int64_t base, int64_t ne
     }
 }
 
-// Payload gather: one thread per (new node, float4 column).
-__global__ void payload_kernel(TreeDev T, int64_t n_new, int S4, const int64_t* __restrict__ src_index,
-                               const uint8_t* __restrict__ state, const int32_t* __restrict__ slot,
-                               const float* __restrict__ msig, const float* __restrict__ msh,
-                               const int32_t* __restrict__ new_node, float* __restrict__ new_sigma,
-                               float4* __restrict__ new_sh) {
-    const int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (t >= n_new * S4) return;
-    const int64_t i = t / S4;
-    const int j = int(t - i * S4);
-    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+// Payload gather, warp-cooperative: a warp owns 32 consecutive new nodes;
+// lane l resolves node l's source row (merged parent -> merge buffer, other
+// leaves -> old payload row, internal -> zeros) once, then the warp streams
+// the 32 rows in 16-byte chunks with consecutive lanes on consecutive
+// chunks -- stores fully coalesced (new rows are contiguous), loads
+// coalesced wherever consecutive new leaves come from consecutive old rows
+// (the common case: BFS order is preserved between kept siblings).  All of a
+// lane's chunk loads are issued before its stores.
+template <int S4>
+__global__ void __launch_bounds__(256) payload_kernel(
+    TreeDev T, int64_t n_new, const int64_t* __restrict__ src_index,
+    const uint8_t* __restrict__ state, const int32_t* __restrict__ slot,
+    const float* __restrict__ msig, const float* __restrict__ msh,
+    const int32_t* __restrict__ new_node, float* __restrict__ new_sigma, float4* __restrict__ new_sh) {
+    const int lane = threadIdx.x & 31;
+    const int64_t base = ((int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5) * 32;
+    if (base >= n_new) return;
+    const int64_t i = base + lane;
+    const float4* src = nullptr;  // row of node i (NULL: zeros)
     float sg = 0.f;
-    if (new_node[i] < 0) {  // leaf in the new tree
+    if (i < n_new && new_node[i] < 0) {
         const int64_t o = src_index[i];
         if (state[o] & ST_MERGED) {
             const int32_t sl = slot[o];
-            v = reinterpret_cast<const float4*>(msh)[int64_t(sl) * S4 + j];
+            src = reinterpret_cast<const float4*>(msh) + int64_t(sl) * S4;
             sg = msig[sl];
         } else {
             const int32_t pid = ~T.node[o];
-            v = __ldg(reinterpret_cast<const float4*>(T.sh) + int64_t(pid) * S4 + j);
+            src = reinterpret_cast<const float4*>(T.sh) + int64_t(pid) * S4;
             sg = __ldg(T.sigma + pid);
         }
     }
-    new_sh[t] = v;
-    if (j == 0) new_sigma[i] = sg;
+    if (i < n_new) new_sigma[i] = sg;
+    const int rows = int(n_new - base < 32 ? n_new - base : 32);
+    const int chunks = rows * S4;
+    float4 v[S4];
+#pragma unroll
+    for (int k = 0; k < S4; ++k) {
+        const int c = k * 32 + lane;
+        const int r = c / S4;
+        const float4* p = reinterpret_cast<const float4*>(
+            __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(src), r & 31));
+        v[k] = (c < chunks && p) ? __ldg(p + (c - r * S4)) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    float4* dst = new_sh + base * S4;
+#pragma unroll
+    for (int k = 0; k < S4; ++k) {
+        const int c = k * 32 + lane;
+        if (c < chunks) dst[c] = v[k];
+    }
 }
 
 template <typename Tp>
@@ -857,11 +881,22 @@ int dot_refine_apply(const dot_refine_plan* p, const dot_tree_view* tree, int32_
     if (base != n_new)
         TRY(set_error(DOT_CUDA_ERR, "refine apply produced %lld nodes, plan said %lld", (long long)base,
                       (long long)n_new));
-    const int S4 = p->S / 4;
-    payload_kernel<<<grid_for(n_new * S4), kTB, 0, s>>>(T, n_new, S4, src_index, p->state, p->slot, p->msig,
-                                                       p->msh, new_node, new_sigma,
-                                                       reinterpret_cast<float4*>(new_sh));
-    TRY(check_launch("payload_kernel"));
+    {
+        const unsigned grid = grid_for(((n_new + 31) / 32) * 32);
+        float4* nsh = reinterpret_cast<float4*>(new_sh);
+#define DOT_PAYLOAD(S4V)                                                                              \
+        payload_kernel<S4V><<<grid, kTB, 0, s>>>(T, n_new, src_index, p->state, p->slot, p->msig, p->msh, \
+                                                 new_node, new_sigma, nsh)
+        switch (p->S / 4) {
+            case 1: DOT_PAYLOAD(1); break;
+            case 3: DOT_PAYLOAD(3); break;
+            case 7: DOT_PAYLOAD(7); break;
+            case 12: DOT_PAYLOAD(12); break;
+            default: TRY(set_error(DOT_BAD_ARG, "unsupported SH row width %d", p->S));
+        }
+#undef DOT_PAYLOAD
+        TRY(check_launch("payload_kernel"));
+    }
     cleanup();
 #undef TRY
     if (n_levels_out) *n_levels_out = levels;
