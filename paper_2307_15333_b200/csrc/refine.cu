@@ -134,6 +134,7 @@ struct PlanScalars {
     unsigned long long splits;
     RadixState sig_rs;               // radix select over signal bits
     RadixState tie_rs;               // radix select over (0xFFFFFFFF - pool id) among ties
+    unsigned long long n_cand;       // candidates compacted after the first passes
 };
 
 }  // namespace dot
@@ -358,10 +359,16 @@ __global__ void sample_k_kernel(PlanScalars* ps, double gamma) {
 // Histogram of digit `shift` over keys matching the current prefix, with
 // warp-aggregated shared-memory increments (most keys share the high digits).
 // mode 0: signal keys; mode 1: tie keys (0xFFFFFFFF - pool id) among keys == K*.
+// One radix pass of the top-k select.  The first passes scan every node;
+// after them radix_compact_kernel keeps only the keys still matching the
+// selected prefix (a ~1/16-binade slice), and the remaining passes run over
+// that candidate list (ckey / cidx, count in ps->n_cand).
 __global__ void radix_hist_kernel(int64_t N, int mode, const uint8_t* __restrict__ state,
                                   const uint8_t* __restrict__ depth, const double* __restrict__ sig,
                                   int max_depth, const int32_t* __restrict__ pool_id,
-                                  const PlanScalars* __restrict__ ps, int shift, unsigned int* __restrict__ hist) {
+                                  const PlanScalars* __restrict__ ps, int shift, unsigned int* __restrict__ hist,
+                                  const unsigned long long* __restrict__ ckey = nullptr,
+                                  const int32_t* __restrict__ cidx = nullptr) {
     __shared__ unsigned int h[256];
     const RadixState rs = mode == 0 ? ps->sig_rs : ps->tie_rs;
     const bool skip = mode == 0 ? ps->k <= 0 : (ps->k <= 0 || ps->sig_rs.remaining == ps->sig_rs.eq_count);
@@ -369,14 +376,16 @@ __global__ void radix_hist_kernel(int64_t N, int mode, const uint8_t* __restrict
     for (int b = threadIdx.x; b < 256; b += blockDim.x) h[b] = 0;
     __syncthreads();
     const unsigned long long kstar = ps->sig_rs.prefix;
+    const int64_t M = ckey ? int64_t(ps->n_cand) : N;
     const int64_t stride = int64_t(gridDim.x) * blockDim.x;
-    const int64_t n_iter = (N + stride - 1) / stride;
+    const int64_t n_iter = (M + stride - 1) / stride;
     for (int64_t it = 0; it < n_iter; ++it) {
-        const int64_t i = it * stride + int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+        const int64_t j = it * stride + int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
         bool take = false;
         unsigned bin = 0;
-        if (i < N) {
-            unsigned long long key = sample_key(i, state, depth, sig, max_depth);
+        if (j < M) {
+            const int64_t i = ckey ? int64_t(cidx[j]) : j;
+            unsigned long long key = ckey ? ckey[j] : sample_key(i, state, depth, sig, max_depth);
             if (key != 0ull) {
                 if (mode == 1) {
                     if (key == kstar) {
@@ -398,6 +407,31 @@ __global__ void radix_hist_kernel(int64_t N, int mode, const uint8_t* __restrict
     __syncthreads();
     for (int b = threadIdx.x; b < 256; b += blockDim.x)
         if (h[b]) atomicAdd(hist + b, h[b]);
+}
+
+__global__ void radix_compact_kernel(int64_t N, const uint8_t* __restrict__ state,
+                                     const uint8_t* __restrict__ depth, const double* __restrict__ sig,
+                                     int max_depth, PlanScalars* __restrict__ ps,
+                                     unsigned long long* __restrict__ ckey, int32_t* __restrict__ cidx) {
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    const RadixState rs = ps->sig_rs;
+    bool take = false;
+    unsigned long long key = 0;
+    if (i < N && ps->k > 0) {
+        key = sample_key(i, state, depth, sig, max_depth);
+        take = key != 0ull && (key & rs.mask) == rs.prefix;
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, take);
+    if (!m) return;
+    const int lane = threadIdx.x & 31;
+    unsigned long long base = 0;
+    if (lane == __ffs(m) - 1) base = atomicAdd(&ps->n_cand, (unsigned long long)__popc(m));
+    base = __shfl_sync(0xffffffffu, base, __ffs(m) - 1);
+    if (take) {
+        const unsigned long long at = base + __popc(m & ((1u << lane) - 1u));
+        ckey[at] = key;
+        cidx[at] = int32_t(i);
+    }
 }
 
 __global__ void radix_pick_kernel(PlanScalars* ps, int mode, unsigned int* hist, int shift) {
@@ -650,7 +684,11 @@ int dot_refine_plan_create(const dot_tree_view* tree, const int32_t* pool_id, co
     int64_t* d_list = nullptr;
     unsigned int* d_hist = nullptr;
     PlanScalars* d_ps = nullptr;
+    unsigned long long* d_ckey = nullptr;
+    int32_t* d_cidx = nullptr;
     auto cleanup_tmp = [&]() {
+        cudaFreeAsync(d_ckey, s);
+        cudaFreeAsync(d_cidx, s);
         cudaFreeAsync(d_list, s);
         cudaFreeAsync(d_hist, s);
         cudaFreeAsync(d_ps, s);
@@ -710,14 +748,21 @@ int dot_refine_plan_create(const dot_tree_view* tree, const int32_t* pool_id, co
                                                           pool_id, threshold, d_ps);
         } else {
             sample_k_kernel<<<1, 1, 0, s>>>(d_ps, gamma);
+            TRY(dalloc(&d_ckey, N, s));
+            TRY(dalloc(&d_cidx, N, s));
             for (int shift = 56; shift >= 0; shift -= 8) {
+                const bool cand = shift < 48;  // after two full passes: candidates only
+                if (shift == 40)
+                    radix_compact_kernel<<<grid_for(N), kTB, 0, s>>>(N, p->state, p->depth, p->sig,
+                                                                     tree->max_depth, d_ps, d_ckey, d_cidx);
                 radix_hist_kernel<<<pb, kTB, 0, s>>>(N, 0, p->state, p->depth, p->sig, tree->max_depth, pool_id,
-                                                     d_ps, shift, d_hist);
+                                                     d_ps, shift, d_hist, cand ? d_ckey : nullptr,
+                                                     cand ? d_cidx : nullptr);
                 radix_pick_kernel<<<1, 32, 0, s>>>(d_ps, 0, d_hist, shift);
             }
-            for (int shift = 24; shift >= 0; shift -= 8) {
+            for (int shift = 24; shift >= 0; shift -= 8) {  // ties: all keys equal the k-th, all candidates
                 radix_hist_kernel<<<pb, kTB, 0, s>>>(N, 1, p->state, p->depth, p->sig, tree->max_depth, pool_id,
-                                                     d_ps, shift, d_hist);
+                                                     d_ps, shift, d_hist, d_ckey, d_cidx);
                 radix_pick_kernel<<<1, 32, 0, s>>>(d_ps, 1, d_hist, shift);
             }
             mark_split_kernel<<<grid_for(N), kTB, 0, s>>>(N, 0, p->state, p->depth, p->sig, tree->max_depth,
