@@ -159,6 +159,7 @@ struct dot_refine_plan {
     std::vector<int64_t> split_list;   // canonical ascending
     dot_refine_stats stats{};
     int32_t max_depth = 0;
+    std::vector<int64_t> level_off;    // old canonical BFS level boundaries
 };
 
 namespace dot {
@@ -549,6 +550,86 @@ __global__ void level_emit_kernel(TreeDev T, int64_t m, int64_t base, int64_t ne
     }
 }
 
+// ---------------------------------------------------------------------------
+// Canonical rebuild in one scan.  The new tree's BFS order keeps the relative
+// order of surviving nodes inside a level, so with
+//   f(i) = 1 if old node i is internal after the refine (alive internal and
+//          not merged, or a leaf selected for splitting), and
+//   R(i) = exclusive prefix sum of f over the old BFS order,
+// the children block of an internal-after node i at level L starts at
+//   new_base[L+1] + 8 (R(i) - R(off[L])),
+// every surviving non-root node sits at its parent's block + octant, and a
+// split leaf's 8 new children fill its block (scene_io.py:529-541 order).
+
+__global__ void rebuild_flags_kernel(TreeDev T, int64_t N, const uint8_t* __restrict__ state,
+                                     int32_t* __restrict__ flags, int32_t* __restrict__ parent) {
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= N) return;
+    const uint8_t st = state[i];
+    const bool alive = (st & ST_ALIVE) != 0;
+    flags[i] = alive && (!(st & ST_LEAF) || (st & ST_SPLIT)) ? 1 : 0;
+    if (alive && !(st & ST_LEAF)) {
+        const int32_t c = T.node[i];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) parent[c + k] = int32_t(i);
+    }
+}
+
+// new_base[L] (new level offsets) and rb[L] = R(off[L]), one thread.
+__global__ void rebuild_levels_kernel(int n_levels, const int64_t* __restrict__ rank,
+                                      const int64_t* __restrict__ total, int64_t* __restrict__ new_base,
+                                      int64_t* __restrict__ rb) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    int64_t base = 0, count = 1;
+    for (int L = 0; L < n_levels; ++L) {
+        const int64_t r0 = rank[c_level_off[L]];
+        const int64_t r1 = (L + 1 < n_levels) ? rank[c_level_off[L + 1]] : *total;
+        rb[L] = r0;
+        new_base[L] = base;
+        base += count;
+        count = 8 * (r1 - r0);  // nodes of new level L + 1
+    }
+    new_base[n_levels] = base;  // the split children of the deepest level
+    new_base[n_levels + 1] = base + count;
+}
+
+__global__ void rebuild_emit_kernel(TreeDev T, int64_t N, const uint8_t* __restrict__ state,
+                                    const uint8_t* __restrict__ depth, const int32_t* __restrict__ flags,
+                                    const int32_t* __restrict__ parent, const int64_t* __restrict__ rank,
+                                    const int64_t* __restrict__ new_base, const int64_t* __restrict__ rb,
+                                    int32_t* __restrict__ new_node, int64_t* __restrict__ src_index,
+                                    uint8_t* __restrict__ src_kind) {
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= N) return;
+    const uint8_t st = state[i];
+    if (!(st & ST_ALIVE)) return;
+    const int L = depth[i];
+    int64_t g = 0;
+    if (i > 0) {
+        const int32_t P = parent[i];
+        g = new_base[L] + 8 * (rank[P] - rb[L - 1]) + (i - T.node[P]);
+    }
+    src_index[g] = i;
+    if (flags[i]) {
+        const int64_t cb = new_base[L + 1] + 8 * (rank[i] - rb[L]);
+        new_node[g] = int32_t(cb);
+        if (st & ST_LEAF) {  // split: 8 new leaves copying this (original or merged) leaf
+            src_kind[g] = K_SPLITPARENT;
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                new_node[cb + k] = ~int32_t(cb + k);
+                src_index[cb + k] = i;
+                src_kind[cb + k] = K_NEWCHILD;
+            }
+        } else {
+            src_kind[g] = K_KEPT;
+        }
+    } else {
+        new_node[g] = ~int32_t(g);
+        src_kind[g] = (st & ST_MERGED) ? K_MERGED : K_KEPT;
+    }
+}
+
 // Payload gather, warp-cooperative: a warp owns 32 consecutive new nodes;
 // lane l resolves node l's source row (merged parent -> merge buffer, other
 // leaves -> old payload row, internal -> zeros) once, then the warp streams
@@ -675,6 +756,7 @@ int dot_refine_plan_create(const dot_tree_view* tree, const int32_t* pool_id, co
     }
     const int n_levels = int(off.size()) - 1;
     dot_refine_plan* p = new dot_refine_plan();
+    p->level_off = off;
     p->N = N;
     p->S = S;
     p->B = B;
@@ -877,55 +959,41 @@ int dot_refine_apply(const dot_refine_plan* p, const dot_tree_view* tree, int32_
     const TreeDev T = make_tree(*tree);
     const int64_t n_new = p->stats.n_new_nodes;
     int st = DOT_OK;
-    int32_t *ent_old[2] = {nullptr, nullptr}, *flags = nullptr;
-    uint8_t* ent_kind[2] = {nullptr, nullptr};
-    int64_t *rank = nullptr, *sums = nullptr, *d_total = nullptr;
+    const int64_t N = p->N;
+    const int n_levels = int(p->level_off.size()) - 1;
+    if (n_levels + 2 > kMaxLevels) return set_error(DOT_BAD_ARG, "tree too deep");
+    int32_t *flags = nullptr, *parent = nullptr;
+    int64_t *rank = nullptr, *sums = nullptr, *d_total = nullptr, *d_base = nullptr, *d_rb = nullptr;
     auto cleanup = [&]() {
-        for (int b = 0; b < 2; ++b) {
-            cudaFreeAsync(ent_old[b], s);
-            cudaFreeAsync(ent_kind[b], s);
-        }
         cudaFreeAsync(flags, s);
+        cudaFreeAsync(parent, s);
         cudaFreeAsync(rank, s);
         cudaFreeAsync(sums, s);
         cudaFreeAsync(d_total, s);
+        cudaFreeAsync(d_base, s);
+        cudaFreeAsync(d_rb, s);
     };
 #define TRY(x) do { if ((st = (x)) != DOT_OK) { cleanup(); return st; } } while (0)
-    for (int b = 0; b < 2; ++b) {
-        TRY(dalloc(&ent_old[b], n_new, s));
-        TRY(dalloc(&ent_kind[b], n_new, s));
-    }
-    TRY(dalloc(&flags, n_new, s));
-    TRY(dalloc(&rank, n_new, s));
-    TRY(dalloc(&sums, n_new / kScanTile + 2, s));
+    TRY(dalloc(&flags, N, s));
+    TRY(dalloc(&parent, N, s));
+    TRY(dalloc(&rank, N, s));
+    TRY(dalloc(&sums, N / kScanTile + 2, s));
     TRY(dalloc(&d_total, 1, s));
-    TRY(check_cuda(cudaMemsetAsync(ent_old[0], 0, sizeof(int32_t), s), "memset"));
-    TRY(check_cuda(cudaMemsetAsync(ent_kind[0], K_KEPT, 1, s), "memset"));
-    int64_t base = 0, m = 1;
-    int cur = 0, levels = 0;
-    std::vector<int64_t> offs(1, 0);
-    while (m > 0) {
-        if (base + m > n_new) TRY(set_error(DOT_CUDA_ERR, "refine apply overflow (plan/tree mismatch)"));
-        level_flags_kernel<<<grid_for(m), kTB, 0, s>>>(m, ent_old[cur], ent_kind[cur], p->state, flags);
-        TRY(check_launch("level_flags_kernel"));
-        TRY(exclusive_scan(flags, m, rank, sums, d_total, s));
-        const int64_t next_base = base + m;
-        level_emit_kernel<<<grid_for(m), kTB, 0, s>>>(T, m, base, next_base, ent_old[cur], ent_kind[cur], flags,
-                                                      rank, p->state, new_node, src_index, src_kind,
-                                                      ent_old[cur ^ 1], ent_kind[cur ^ 1]);
-        TRY(check_launch("level_emit_kernel"));
-        int64_t n_int = 0;
-        TRY(check_cuda(cudaMemcpyAsync(&n_int, d_total, sizeof(n_int), cudaMemcpyDeviceToHost, s), "memcpy"));
-        TRY(check_cuda(cudaStreamSynchronize(s), "sync"));
-        base = next_base;
-        offs.push_back(base);
-        m = 8 * n_int;
-        cur ^= 1;
-        ++levels;
-    }
-    if (base != n_new)
-        TRY(set_error(DOT_CUDA_ERR, "refine apply produced %lld nodes, plan said %lld", (long long)base,
-                      (long long)n_new));
+    TRY(dalloc(&d_base, kMaxLevels + 2, s));
+    TRY(dalloc(&d_rb, kMaxLevels + 2, s));
+    TRY(check_cuda(cudaMemcpyToSymbolAsync(c_level_off, p->level_off.data(),
+                                           p->level_off.size() * sizeof(int64_t), 0,
+                                           cudaMemcpyHostToDevice, s), "memcpy"));
+    rebuild_flags_kernel<<<grid_for(N), kTB, 0, s>>>(T, N, p->state, flags, parent);
+    TRY(check_launch("rebuild_flags_kernel"));
+    TRY(exclusive_scan(flags, N, rank, sums, d_total, s));
+    rebuild_levels_kernel<<<1, 1, 0, s>>>(n_levels, rank, d_total, d_base, d_rb);
+    rebuild_emit_kernel<<<grid_for(N), kTB, 0, s>>>(T, N, p->state, p->depth, flags, parent, rank, d_base,
+                                                    d_rb, new_node, src_index, src_kind);
+    TRY(check_launch("rebuild_emit_kernel"));
+    std::vector<int64_t> nb(size_t(n_levels) + 2);
+    TRY(check_cuda(cudaMemcpyAsync(nb.data(), d_base, nb.size() * sizeof(int64_t), cudaMemcpyDeviceToHost, s),
+                   "memcpy"));
     {
         const unsigned grid = grid_for(((n_new + 31) / 32) * 32);
         float4* nsh = reinterpret_cast<float4*>(new_sh);
@@ -942,8 +1010,19 @@ int dot_refine_apply(const dot_refine_plan* p, const dot_tree_view* tree, int32_
 #undef DOT_PAYLOAD
         TRY(check_launch("payload_kernel"));
     }
+    TRY(check_cuda(cudaStreamSynchronize(s), "sync"));
     cleanup();
 #undef TRY
+    // new level offsets: nb[0..n_levels+1]; the last level may be empty
+    std::vector<int64_t> offs;
+    for (int L = 0; L <= n_levels + 1; ++L) {
+        if (L > 0 && nb[size_t(L)] == nb[size_t(L) - 1]) break;
+        offs.push_back(nb[size_t(L)]);
+    }
+    const int levels = int(offs.size()) - 1;
+    if (offs.back() != n_new)
+        return set_error(DOT_CUDA_ERR, "refine apply produced %lld nodes, plan said %lld",
+                         (long long)offs.back(), (long long)n_new);
     if (n_levels_out) *n_levels_out = levels;
     if (level_offsets_out)
         for (int i = 0; i < int(offs.size()) && i < max_levels + 1; ++i) level_offsets_out[i] = offs[size_t(i)];
