@@ -65,3 +65,54 @@ def test_short_training_run_matches_reference():
                                   ref.topology().node.cpu().numpy())
     np.testing.assert_allclose(trainee.sigma.cpu().numpy(), ref.sigma.cpu().numpy(),
                                atol=1e-3, rtol=1e-3)
+
+
+def _batch_setup(seed=11, B=16, n=1 << 15):
+    from helpers import irregular_tree, ray_batch
+    tree = irregular_tree(seed, B, depth=3, splits=80, merges=6, resplits=20, max_depth=6, device="cuda")
+    o, d = ray_batch(seed + 1, 3 * n)
+    t = np.random.default_rng(seed + 2).uniform(0, 1, (o.shape[0], 3))
+    o, d, t = (torch.from_numpy(x).cuda() for x in (o, d, t))
+    idx = torch.randperm(o.shape[0], generator=torch.Generator().manual_seed(seed))[:n].cuda()
+    return tree, o, d, t, idx
+
+
+def test_train_step_equals_unfused_step():
+    """optim.train_step (in-place batch, signal into the accumulator,
+    gradients consumed by the optimizer) == render_and_backprop on the
+    gathered batch + rmsprop_step + SignalBuffer.accumulate."""
+    from paper_2307_15333_b200.octree import from_canonical_tensors
+    from paper_2307_15333_b200.optim import RmsPropState, StepWorkspace, rmsprop_step, train_step
+    from paper_2307_15333_b200.render import BackpropWorkspace, render_and_backprop
+    from paper_2307_15333_b200.signals import SignalBuffer
+    tree, o, d, t, idx = _batch_setup()
+    topo = tree.topology()
+
+    def clone():
+        return from_canonical_tensors(tree.center, tree.half_extent, tree.basis_count, tree.max_depth,
+                                      topo.node.clone(), tree._sigma.clone(), tree._sh_store.clone(),
+                                      topo.level_offsets) if topo.pool_id is None else None
+
+    if topo.pool_id is not None:  # make the tree canonical first
+        from paper_2307_15333_b200.scene_io import load_tree_bytes, tree_bytes
+        tree = load_tree_bytes(tree_bytes(tree), device="cuda")
+        topo = tree.topology()
+    a, b = clone(), clone()
+    sa, sb = RmsPropState(a), RmsPropState(b)
+    ba, bb = SignalBuffer(a), SignalBuffer(b)
+    ws = BackpropWorkspace.for_tree(a)
+    sws = StepWorkspace(b, bb)
+    for k in range(2):
+        sl = idx[k * 8192:(k + 1) * 8192]
+        loss_a, g, sig = render_and_backprop(a, o[sl], d[sl], t[sl], 0.5, workspace=ws)
+        rmsprop_step(a, g, sa)
+        ba.accumulate(sig, sl.numel())
+        loss_b = train_step(b, o, d, t, sb, bb, sws, 0.5, ray_index=sl)
+        assert float(loss_b) == pytest.approx(float(loss_a), rel=1e-9)
+    torch.testing.assert_close(b.sigma, a.sigma, atol=1e-5, rtol=1e-4)
+    torch.testing.assert_close(b.sh, a.sh, atol=1e-5, rtol=1e-4)
+    torch.testing.assert_close(sb.v_sh, sa.v_sh, atol=1e-9, rtol=1e-3)
+    # step 2 runs on payloads that already differ by fp32-atomic noise
+    torch.testing.assert_close(bb.accumulator, ba.accumulator, atol=1e-9, rtol=1e-4)
+    assert bb.epoch_rays == ba.epoch_rays
+    assert not bool(sws.ws.dsigma.any()) and not bool(sws.ws.dsh_store.any())

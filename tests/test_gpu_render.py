@@ -189,3 +189,31 @@ def test_device_exp_ref(oracle):
     got = yd.cpu().numpy()
     same = got.view(np.uint64) == want.view(np.uint64)
     assert np.all(same | (np.isnan(got) & np.isnan(want))), x[~same][:5]
+
+
+def test_ray_index_reads_in_place():
+    """render_and_backprop(ray_index=...) == the same call on the gathered
+    batch (atomic path within fp32-atomic noise; deterministic path bit for
+    bit, including the reduction order)."""
+    import torch
+    from helpers import irregular_tree, ray_batch
+    from paper_2307_15333_b200.render import render_and_backprop
+    tree = irregular_tree(21, 9, depth=3, splits=60, max_depth=6, device="cuda")
+    o, d = ray_batch(22, 60000)
+    t = np.random.default_rng(23).uniform(0, 1, (o.shape[0], 3))
+    o, d, t = (torch.from_numpy(x).cuda() for x in (o, d, t))
+    idx = torch.randperm(o.shape[0], generator=torch.Generator().manual_seed(1))[:40000].cuda()
+    l1, g1, s1 = render_and_backprop(tree, o[idx], d[idx], t[idx], 0.2)
+    g1 = (g1.dsigma.clone(), g1.dsh.clone(), g1.touched_mask.clone())
+    s1 = s1.clone()
+    l2, g2, s2 = render_and_backprop(tree, o, d, t, 0.2, ray_index=idx)
+    assert float(l2) == pytest.approx(float(l1), rel=1e-9)
+    torch.testing.assert_close(g2.dsigma, g1[0], atol=1e-6, rtol=1e-4)
+    torch.testing.assert_close(g2.dsh, g1[1], atol=1e-6, rtol=1e-4)
+    assert torch.equal(g2.touched_mask, g1[2])
+    torch.testing.assert_close(s2, s1, atol=1e-12, rtol=1e-12)
+    _, h1, r1 = render_and_backprop(tree, o[idx], d[idx], t[idx], 0.2, deterministic=True)
+    h1 = (h1.dsigma.clone(), h1.dsh.clone())
+    r1 = r1.clone()
+    _, h2, r2 = render_and_backprop(tree, o, d, t, 0.2, ray_index=idx, deterministic=True)
+    assert torch.equal(h2.dsigma, h1[0]) and torch.equal(h2.dsh, h1[1]) and torch.equal(r2, r1)
