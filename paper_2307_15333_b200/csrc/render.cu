@@ -16,7 +16,7 @@ namespace dot {
 
 constexpr int kBlock = 128;
 constexpr int kFwdMinBlocks = 8;   // forward: 64 registers -> 8 blocks (32 warps) per SM
-constexpr int kBwdRecords = 48;    // composited segments buffered per ray (pass 1 -> pass 2)
+constexpr int kBwdRecords = 128;   // composited segments buffered per ray (pass 1 -> pass 2); longer rays resume the walk
 
 static unsigned blocks_for(int64_t n) { return unsigned((n + kBlock - 1) / kBlock); }
 

@@ -217,3 +217,32 @@ def test_ray_index_reads_in_place():
     r1 = r1.clone()
     _, h2, r2 = render_and_backprop(tree, o, d, t, 0.2, ray_index=idx, deterministic=True)
     assert torch.equal(h2.dsigma, h1[0]) and torch.equal(h2.dsh, h1[1]) and torch.equal(r2, r1)
+
+
+def test_long_rays_resume_past_the_record_buffer(oracle):
+    """Rays with more composited segments than the backward's per-ray record
+    buffer (128) resume their walk in pass 2: a dense depth-6 tree, eps = 0
+    and low density make diagonal rays composite ~190 segments."""
+    from paper_2307_15333_b200.octree import build_dense
+    from paper_2307_15333_b200.render import render_and_backprop
+    rng = np.random.default_rng(5)
+
+    def init(c):
+        return rng.uniform(0.0, 0.3, len(c)), rng.normal(0.0, 0.5, (len(c), 3))
+
+    tree = build_dense(6, (0.0, 0.0, 0.0), 1.0, 1, init, max_depth=6, device="cuda")
+    n = 600
+    o = np.tile([-1.5, -1.4, -1.3], (n, 1)) + rng.uniform(-0.2, 0.2, (n, 3))
+    d = np.ones((n, 3)) + rng.uniform(-0.05, 0.05, (n, 3))
+    d /= np.linalg.norm(d, axis=1, keepdims=True)
+    tg = rng.uniform(0, 1, (n, 3))
+    r_off, _, _, _ = oracle.segment_batch(tree, o, d)
+    assert np.diff(r_off).max() > 160
+    for det in (False, True):
+        loss, g, sig = render_and_backprop(tree, o, d, tg, 0.5, 0.0, deterministic=det)
+        r_loss, r_g, r_sig = oracle.render_and_backprop(tree, o, d, tg, 0.5, 0.0)
+        assert loss == pytest.approx(r_loss, rel=RTOL, abs=ATOL)
+        np.testing.assert_allclose(g.dsigma, r_g.dsigma, atol=ATOL, rtol=RTOL)
+        np.testing.assert_allclose(g.dsh, r_g.dsh, atol=ATOL, rtol=RTOL)
+        np.testing.assert_array_equal(g.touched, r_g.touched)
+        np.testing.assert_allclose(sig, r_sig, atol=ATOL, rtol=RTOL)
