@@ -88,7 +88,7 @@ class _Plan:
 
     def __init__(self, tree, acc, use_sigma, tau, gamma, recursive, threshold):
         self.tree = tree
-        self.view, self.topo = tree.tree_view()
+        self.view, self.topo = tree.tree_view(locate=False)
         self.acc = acc
         stats = _lib.DotRefineStats()
         handle = ctypes.c_void_p()

@@ -96,7 +96,7 @@ class DeviceTopology:
 
 def locate_level_default() -> int:
     """Level of the traversal locate table (env DOT_LOCATE_LEVEL, 0 = off)."""
-    return int(os.environ.get("DOT_LOCATE_LEVEL", "7"))
+    return int(os.environ.get("DOT_LOCATE_LEVEL", "8"))
 
 
 class SparseOctree:
@@ -230,8 +230,9 @@ class SparseOctree:
         self._hp = None
         self._free = []
 
-    def tree_view(self):
-        """C-ABI ``dot_tree_view`` of the current generation (+ keepalive)."""
+    def tree_view(self, locate: bool = True):
+        """C-ABI ``dot_tree_view`` of the current generation (+ keepalive).
+        ``locate=False`` (refine) skips building the traversal locate table."""
         from ._lib import DotTreeView
         if self.device.type != "cuda":
             raise ConfigError("the tree payload is not on a CUDA device; the B200 kernels "
@@ -251,7 +252,8 @@ class SparseOctree:
         v.max_depth = self.max_depth
         v.locate_level = 0
         v.locate = None
-        self._attach_locate(v, topo)
+        if locate:
+            self._attach_locate(v, topo)
         return v, topo
 
     def _attach_locate(self, v, topo: DeviceTopology) -> None:

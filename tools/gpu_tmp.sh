@@ -1,3 +1,2 @@
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests -m gpu -q -x > gpurun_out/pytest_all.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_all.log
-timeout 300 python tools/micro.py --order random --flags 0,0 > gpurun_out/micro.log 2>&1
+for L in 7 8 7 8; do echo "L=$L"; DOT_LOCATE_LEVEL=$L timeout 600 python bench.py --skip-cpu --skip-refine --steps 20 | python -c "import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print(d['value'], d['roofline']['kernel_ms'], d['render']['rays_per_s'])"; done > gpurun_out/bench_L.log 2>&1
