@@ -164,6 +164,23 @@ struct dot_refine_plan {
 
 namespace dot {
 
+// Block-wide sum of a per-thread count, one atomicAdd per block (the N-wide
+// kernels run grid-stride on persistent_blocks(): ~1k atomics per counter
+// instead of one per 256-thread block).
+__device__ __forceinline__ void block_add(unsigned long long* dst, unsigned v) {
+    __shared__ unsigned part[32];
+    v = __reduce_add_sync(0xffffffffu, v);
+    const int w = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) part[w] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long t = 0;
+        for (int k = 0; k < nw; ++k) t += part[k];
+        if (t) atomicAdd(dst, t);
+    }
+}
+
 __device__ __forceinline__ int32_t pid_of(const int32_t* pool_id, int64_t i) {
     return pool_id ? pool_id[i] : int32_t(i);
 }
@@ -171,13 +188,14 @@ __device__ __forceinline__ int32_t pid_of(const int32_t* pool_id, int64_t i) {
 __constant__ int64_t c_level_off[kMaxLevels + 1];
 
 // state / depth / signal of every node; depth from the BFS level offsets.
-__global__ void init_nodes_kernel(TreeDev T, int64_t N, int n_levels, const double* __restrict__ acc,
-                                  int use_sigma, uint8_t* __restrict__ state, uint8_t* __restrict__ depth,
-                                  double* __restrict__ sig, int32_t* __restrict__ slot,
-                                  int32_t* __restrict__ mround, PlanScalars* __restrict__ ps) {
-    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    int internal = 0;
-    if (i < N) {
+__global__ void __launch_bounds__(256) init_nodes_kernel(
+    TreeDev T, int64_t N, int n_levels, const double* __restrict__ acc, int use_sigma,
+    uint8_t* __restrict__ state, uint8_t* __restrict__ depth, double* __restrict__ sig,
+    int32_t* __restrict__ slot, int32_t* __restrict__ mround, PlanScalars* __restrict__ ps) {
+    unsigned internal = 0;
+    const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+#pragma unroll 4
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < N; i += stride) {
         int dd = 0;
         while (dd + 1 < n_levels && c_level_off[dd + 1] <= i) ++dd;
         const int32_t w = T.node[i];
@@ -191,11 +209,10 @@ __global__ void init_nodes_kernel(TreeDev T, int64_t N, int n_levels, const doub
         } else {
             state[i] = ST_ALIVE;
             sig[i] = 0.0;
-            internal = 1;
+            ++internal;
         }
     }
-    internal = __syncthreads_count(internal);
-    if (threadIdx.x == 0 && internal) atomicAdd(&ps->n_internal, (unsigned long long)internal);
+    block_add(&ps->n_internal, internal);
 }
 
 // Warp-aggregated append of index i to list (count in *ctr).
@@ -328,24 +345,102 @@ __device__ __forceinline__ unsigned long long sample_key(int64_t i, const uint8_
 }
 
 // Leaf / eligibility counts on the post-prune topology.
-__global__ void count_leaves_kernel(int64_t N, const uint8_t* __restrict__ state,
-                                    const uint8_t* __restrict__ depth, const double* __restrict__ sig,
-                                    int max_depth, PlanScalars* __restrict__ ps) {
-    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    int leaf = 0, elig = 0;
-    if (i < N) {
+// 16 consecutive 64-bit keys / state bytes per thread with 16-byte vector
+// loads (the N-wide passes below are bandwidth passes: one key or byte per
+// thread left them at ~1.2 TB/s).
+__device__ __forceinline__ void load16_keys(const unsigned long long* __restrict__ a, int64_t i0, int64_t N,
+                                            unsigned long long* v) {
+    if (i0 + 16 <= N) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const ulonglong2 x = reinterpret_cast<const ulonglong2*>(a + i0)[k];
+            v[2 * k] = x.x;
+            v[2 * k + 1] = x.y;
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < 16; ++k) v[k] = i0 + k < N ? a[i0 + k] : 0ull;
+    }
+}
+
+// Post-prune sample keys of every node in one coalesced pass (16 nodes per
+// thread, 16-byte vector loads): keys[i] = sample_key(i) (0 = not eligible),
+// the live-leaf and eligible counts, and the histogram of the keys' top byte
+// (the first radix pass of the top-k select, which does not depend on k).
+__global__ void __launch_bounds__(256) sample_keys_kernel(
+    int64_t N, const uint8_t* __restrict__ state, const uint8_t* __restrict__ depth,
+    const double* __restrict__ sig, int max_depth, unsigned long long* __restrict__ keys,
+    unsigned int* __restrict__ hist, PlanScalars* __restrict__ ps) {
+    __shared__ unsigned int h[256];
+    for (int b = threadIdx.x; b < 256; b += blockDim.x) h[b] = 0;
+    __syncthreads();
+    unsigned leaf = 0, elig = 0;
+    const int64_t chunks = (N + 15) / 16;
+    const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+    for (int64_t c = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; c < chunks; c += stride) {
+        const int64_t i0 = 16 * c;
+        uint8_t st[16], dp[16];
+        double sg[16];
+        if (i0 + 16 <= N) {
+            *reinterpret_cast<uint4*>(st) = *reinterpret_cast<const uint4*>(state + i0);
+            *reinterpret_cast<uint4*>(dp) = *reinterpret_cast<const uint4*>(depth + i0);
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const double2 v = reinterpret_cast<const double2*>(sig + i0)[k];
+                sg[2 * k] = v.x;
+                sg[2 * k + 1] = v.y;
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < 16; ++k) {
+                const bool in = i0 + k < N;
+                st[k] = in ? state[i0 + k] : 0;
+                dp[k] = in ? depth[i0 + k] : 0;
+                sg[k] = in ? sig[i0 + k] : 0.0;
+            }
+        }
+        unsigned long long kv[16];
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+            const bool lf = (st[k] & ST_ALIVE) && (st[k] & ST_LEAF);
+            const bool el = lf && dp[k] < max_depth && sg[k] > 0.0;
+            leaf += lf;
+            elig += el;
+            kv[k] = el ? (unsigned long long)__double_as_longlong(sg[k]) : 0ull;
+        }
+        if (i0 + 16 <= N) {
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+                reinterpret_cast<ulonglong2*>(keys + i0)[k] = make_ulonglong2(kv[2 * k], kv[2 * k + 1]);
+        } else {
+            for (int k = 0; k < 16 && i0 + k < N; ++k) keys[i0 + k] = kv[k];
+        }
+#pragma unroll
+        for (int k = 0; k < 16; ++k)
+            if (kv[k]) atomicAdd(&h[unsigned(kv[k] >> 56)], 1u);
+    }
+    block_add(&ps->leaves, leaf);
+    block_add(&ps->eligible, elig);
+    __syncthreads();
+    for (int b = threadIdx.x; b < 256; b += blockDim.x)
+        if (h[b]) atomicAdd(hist + b, h[b]);
+}
+
+__global__ void __launch_bounds__(256) count_leaves_kernel(
+    int64_t N, const uint8_t* __restrict__ state, const uint8_t* __restrict__ depth,
+    const double* __restrict__ sig, int max_depth, PlanScalars* __restrict__ ps) {
+    unsigned leaf = 0, elig = 0;
+    const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+#pragma unroll 4
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < N; i += stride) {
         const uint8_t st = state[i];
         if ((st & ST_ALIVE) && (st & ST_LEAF)) {
-            leaf = 1;
-            elig = sample_key(i, state, depth, sig, max_depth) != 0ull;
+            ++leaf;
+            elig += depth[i] < max_depth && sig[i] > 0.0;  // sample_key != 0
         }
     }
-    leaf = __syncthreads_count(leaf);
-    elig = __syncthreads_count(elig);
-    if (threadIdx.x == 0) {
-        if (leaf) atomicAdd(&ps->leaves, (unsigned long long)leaf);
-        if (elig) atomicAdd(&ps->eligible, (unsigned long long)elig);
-    }
+    block_add(&ps->leaves, leaf);
+    block_add(&ps->eligible, elig);
 }
 
 // k = min(ceil(gamma * L), #eligible) (calibrate.py:159), both radix states primed.
@@ -368,8 +463,8 @@ __global__ void radix_hist_kernel(int64_t N, int mode, const uint8_t* __restrict
                                   const uint8_t* __restrict__ depth, const double* __restrict__ sig,
                                   int max_depth, const int32_t* __restrict__ pool_id,
                                   const PlanScalars* __restrict__ ps, int shift, unsigned int* __restrict__ hist,
-                                  const unsigned long long* __restrict__ ckey = nullptr,
-                                  const int32_t* __restrict__ cidx = nullptr) {
+                                  const unsigned long long* __restrict__ ckey,
+                                  const int32_t* __restrict__ cidx, const unsigned long long* __restrict__ nkey) {
     __shared__ unsigned int h[256];
     const RadixState rs = mode == 0 ? ps->sig_rs : ps->tie_rs;
     const bool skip = mode == 0 ? ps->k <= 0 : (ps->k <= 0 || ps->sig_rs.remaining == ps->sig_rs.eq_count);
@@ -377,6 +472,21 @@ __global__ void radix_hist_kernel(int64_t N, int mode, const uint8_t* __restrict
     for (int b = threadIdx.x; b < 256; b += blockDim.x) h[b] = 0;
     __syncthreads();
     const unsigned long long kstar = ps->sig_rs.prefix;
+    if (!ckey && mode == 0) {  // full pass over the key array, 16 keys per thread
+        const int64_t chunks = (N + 15) / 16;
+        const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+        for (int64_t c = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; c < chunks; c += stride) {
+            unsigned long long v[16];
+            load16_keys(nkey, 16 * c, N, v);
+#pragma unroll
+            for (int k = 0; k < 16; ++k)
+                if (v[k] != 0ull && (v[k] & rs.mask) == rs.prefix) atomicAdd(&h[unsigned((v[k] >> shift) & 0xFF)], 1u);
+        }
+        __syncthreads();
+        for (int b = threadIdx.x; b < 256; b += blockDim.x)
+            if (h[b]) atomicAdd(hist + b, h[b]);
+        return;
+    }
     const int64_t M = ckey ? int64_t(ps->n_cand) : N;
     const int64_t stride = int64_t(gridDim.x) * blockDim.x;
     const int64_t n_iter = (M + stride - 1) / stride;
@@ -386,7 +496,7 @@ __global__ void radix_hist_kernel(int64_t N, int mode, const uint8_t* __restrict
         unsigned bin = 0;
         if (j < M) {
             const int64_t i = ckey ? int64_t(cidx[j]) : j;
-            unsigned long long key = ckey ? ckey[j] : sample_key(i, state, depth, sig, max_depth);
+            unsigned long long key = ckey ? ckey[j] : nkey[j];
             if (key != 0ull) {
                 if (mode == 1) {
                     if (key == kstar) {
@@ -410,65 +520,151 @@ __global__ void radix_hist_kernel(int64_t N, int mode, const uint8_t* __restrict
         if (h[b]) atomicAdd(hist + b, h[b]);
 }
 
-__global__ void radix_compact_kernel(int64_t N, const uint8_t* __restrict__ state,
-                                     const uint8_t* __restrict__ depth, const double* __restrict__ sig,
-                                     int max_depth, PlanScalars* __restrict__ ps,
-                                     unsigned long long* __restrict__ ckey, int32_t* __restrict__ cidx) {
-    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+__global__ void __launch_bounds__(256) radix_compact_kernel(
+    int64_t N, PlanScalars* __restrict__ ps, unsigned long long* __restrict__ ckey,
+    int32_t* __restrict__ cidx, const unsigned long long* __restrict__ nkey) {
     const RadixState rs = ps->sig_rs;
-    bool take = false;
-    unsigned long long key = 0;
-    if (i < N && ps->k > 0) {
-        key = sample_key(i, state, depth, sig, max_depth);
-        take = key != 0ull && (key & rs.mask) == rs.prefix;
-    }
-    const unsigned m = __ballot_sync(0xffffffffu, take);
-    if (!m) return;
+    if (ps->k <= 0) return;
     const int lane = threadIdx.x & 31;
-    unsigned long long base = 0;
-    if (lane == __ffs(m) - 1) base = atomicAdd(&ps->n_cand, (unsigned long long)__popc(m));
-    base = __shfl_sync(0xffffffffu, base, __ffs(m) - 1);
-    if (take) {
-        const unsigned long long at = base + __popc(m & ((1u << lane) - 1u));
-        ckey[at] = key;
-        cidx[at] = int32_t(i);
+    const int64_t chunks = (N + 15) / 16;
+    const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+    // uniform trip count per warp (warp-collective scan below)
+    const int64_t c0 = int64_t(blockIdx.x) * blockDim.x + (threadIdx.x & ~31);
+    for (int64_t cb = c0; cb < chunks; cb += stride) {
+        const int64_t c = cb + lane;
+        unsigned long long v[16];
+        load16_keys(nkey, 16 * c, c < chunks ? N : 0, v);
+        unsigned m = 0;
+#pragma unroll
+        for (int k = 0; k < 16; ++k)
+            if (v[k] != 0ull && (v[k] & rs.mask) == rs.prefix) m |= 1u << k;
+        const unsigned cnt = __popc(m);
+        unsigned incl = cnt;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const unsigned y = __shfl_up_sync(0xffffffffu, incl, off);
+            if (lane >= off) incl += y;
+        }
+        const unsigned tot = __shfl_sync(0xffffffffu, incl, 31);
+        unsigned long long base = 0;
+        if (lane == 31 && tot) base = atomicAdd(&ps->n_cand, (unsigned long long)tot);
+        base = __shfl_sync(0xffffffffu, base, 31);
+        unsigned long long at = base + incl - cnt;
+        while (m) {
+            const int k = __ffs(m) - 1;
+            m &= m - 1;
+            ckey[at] = v[k];
+            cidx[at] = int32_t(16 * c + k);
+            ++at;
+        }
     }
 }
 
+// Pick the next radix digit: the largest bin b with sum(hist[b..255]) >=
+// remaining (one warp: 8 bins per lane, suffix sums by shuffles), then clear
+// the histogram for the next pass.
 __global__ void radix_pick_kernel(PlanScalars* ps, int mode, unsigned int* hist, int shift) {
-    if (threadIdx.x != 0) return;
+    const int lane = threadIdx.x & 31;
     RadixState& rs = mode == 0 ? ps->sig_rs : ps->tie_rs;
     const bool skip = mode == 0 ? ps->k <= 0 : (ps->k <= 0 || ps->sig_rs.remaining == ps->sig_rs.eq_count);
-    if (!skip) {
-        if (mode == 1 && shift == 24) rs.remaining = ps->sig_rs.remaining;
-        long long rem = rs.remaining;
-        int digit = 0;
-        for (int b = 255; b >= 0; --b) {
-            const long long c = hist[b];
-            if (rem <= c) {
-                digit = b;
-                rs.eq_count = c;
-                break;
-            }
-            rem -= c;
-        }
-        rs.remaining = rem;
-        rs.prefix |= (unsigned long long)digit << shift;
-        rs.mask |= 0xFFull << shift;
+    // lane l owns bins [8 l, 8 l + 8)
+    unsigned h[8];
+    long long own = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        h[k] = hist[8 * lane + k];
+        own += h[k];
     }
-    for (int b = 0; b < 256; ++b) hist[b] = 0;
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < 8; ++k) hist[8 * lane + k] = 0;
+    if (skip) return;
+    // suffix sum over lanes: above = sum of bins of lanes > lane
+    long long incl = own;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const long long v = __shfl_down_sync(0xffffffffu, incl, off);
+        if (lane + off < 32) incl += v;
+    }
+    const long long above = incl - own;
+    long long rem = (mode == 1 && shift == 24) ? ps->sig_rs.remaining : rs.remaining;
+    // the digit lies in this lane's bins iff above < rem <= above + own
+    const bool mine = above < rem && rem <= above + own;
+    const unsigned who = __ballot_sync(0xffffffffu, mine);
+    if (!mine) return;
+    (void)who;
+    rem -= above;
+    int digit = 8 * lane;
+    long long eq = 0;
+    for (int k = 7; k >= 0; --k) {
+        const long long c = h[k];
+        if (rem <= c) {
+            digit = 8 * lane + k;
+            eq = c;
+            break;
+        }
+        rem -= c;
+    }
+    rs.remaining = rem;
+    rs.eq_count = eq;
+    rs.prefix |= (unsigned long long)digit << shift;
+    rs.mask |= 0xFFull << shift;
 }
 
 // Mark the sample selection: key > K*, plus ties (key == K*) whose tie key
 // >= T* (i.e. pool id <= the m-th smallest), or threshold mode.
-__global__ void mark_split_kernel(int64_t N, int mode, uint8_t* __restrict__ state,
-                                  const uint8_t* __restrict__ depth, const double* __restrict__ sig,
-                                  int max_depth, const int32_t* __restrict__ pool_id, double thr,
-                                  PlanScalars* __restrict__ ps) {
-    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    bool sel = false;
-    if (i < N) {
-        const unsigned long long key = sample_key(i, state, depth, sig, max_depth);
+// Top-k mode of mark_split over the key array, 16 nodes per thread.
+__global__ void __launch_bounds__(256) mark_split_keys_kernel(
+    int64_t N, uint8_t* __restrict__ state, const int32_t* __restrict__ pool_id,
+    PlanScalars* __restrict__ ps, const unsigned long long* __restrict__ nkey) {
+    unsigned nsel = 0;
+    if (ps->k > 0) {
+        const unsigned long long kstar = ps->sig_rs.prefix;
+        const bool all = ps->sig_rs.remaining == ps->sig_rs.eq_count;
+        const unsigned long long tie = ps->tie_rs.prefix;
+        const int64_t chunks = (N + 15) / 16;
+        const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+        for (int64_t c = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; c < chunks; c += stride) {
+            const int64_t i0 = 16 * c;
+            unsigned long long v[16];
+            load16_keys(nkey, i0, N, v);
+            unsigned m = 0;
+#pragma unroll
+            for (int k = 0; k < 16; ++k) {
+                bool sel = v[k] != 0ull && v[k] > kstar;
+                if (v[k] != 0ull && v[k] == kstar)
+                    sel = all || 0xFFFFFFFFull - (unsigned long long)(uint32_t)pid_of(pool_id, i0 + k) >= tie;
+                if (sel) m |= 1u << k;
+            }
+            if (m) {
+                nsel += __popc(m);
+                if (i0 + 16 <= N) {
+                    uint4 w = *reinterpret_cast<const uint4*>(state + i0);
+                    uint8_t* b = reinterpret_cast<uint8_t*>(&w);
+#pragma unroll
+                    for (int k = 0; k < 16; ++k)
+                        if (m & (1u << k)) b[k] |= ST_SPLIT;
+                    *reinterpret_cast<uint4*>(state + i0) = w;
+                } else {
+                    for (int k = 0; k < 16; ++k)
+                        if (m & (1u << k)) state[i0 + k] |= ST_SPLIT;
+                }
+            }
+        }
+    }
+    block_add(&ps->splits, nsel);
+}
+
+__global__ void __launch_bounds__(256) mark_split_kernel(
+    int64_t N, int mode, uint8_t* __restrict__ state, const uint8_t* __restrict__ depth,
+    const double* __restrict__ sig, int max_depth, const int32_t* __restrict__ pool_id, double thr,
+    PlanScalars* __restrict__ ps, const unsigned long long* __restrict__ nkey) {
+    unsigned nsel = 0;
+    const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+#pragma unroll 4
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < N; i += stride) {
+        bool sel = false;
+        const unsigned long long key = nkey ? nkey[i] : sample_key(i, state, depth, sig, max_depth);
         if (key != 0ull) {
             if (mode == 2) {
                 sel = sig[i] > thr;
@@ -483,10 +679,12 @@ __global__ void mark_split_kernel(int64_t N, int mode, uint8_t* __restrict__ sta
                 }
             }
         }
-        if (sel) state[i] |= ST_SPLIT;
+        if (sel) {
+            state[i] |= ST_SPLIT;
+            ++nsel;
+        }
     }
-    const int cnt = __syncthreads_count(sel);
-    if (threadIdx.x == 0 && cnt) atomicAdd(&ps->splits, (unsigned long long)cnt);
+    block_add(&ps->splits, nsel);
 }
 
 // Ordered compaction flags for the on-demand event lists.
@@ -767,8 +965,10 @@ int dot_refine_plan_create(const dot_tree_view* tree, const int32_t* pool_id, co
     unsigned int* d_hist = nullptr;
     PlanScalars* d_ps = nullptr;
     unsigned long long* d_ckey = nullptr;
+    unsigned long long* d_nkey = nullptr;
     int32_t* d_cidx = nullptr;
     auto cleanup_tmp = [&]() {
+        cudaFreeAsync(d_nkey, s);
         cudaFreeAsync(d_ckey, s);
         cudaFreeAsync(d_cidx, s);
         cudaFreeAsync(d_list, s);
@@ -791,7 +991,7 @@ int dot_refine_plan_create(const dot_tree_view* tree, const int32_t* pool_id, co
     TRY(check_cuda(cudaMemsetAsync(d_hist, 0, 256 * sizeof(unsigned int), s), "memset"));
     TRY(check_cuda(cudaMemcpyToSymbolAsync(c_level_off, off.data(), off.size() * sizeof(int64_t), 0,
                                            cudaMemcpyHostToDevice, s), "memcpy"));
-    init_nodes_kernel<<<grid_for(N), kTB, 0, s>>>(T, N, n_levels, acc, use_sigma, p->state, p->depth, p->sig,
+    init_nodes_kernel<<<persistent_blocks(), kTB, 0, s>>>(T, N, n_levels, acc, use_sigma, p->state, p->depth, p->sig,
                                                   p->slot, p->mround, d_ps);
     TRY(check_launch("init_nodes_kernel"));
 
@@ -821,34 +1021,42 @@ int dot_refine_plan_create(const dot_tree_view* tree, const int32_t* pool_id, co
     }
 
     // --- sample selection, all decisions on the device
-    count_leaves_kernel<<<grid_for(N), kTB, 0, s>>>(N, p->state, p->depth, p->sig, tree->max_depth, d_ps);
-    TRY(check_launch("count_leaves_kernel"));
     const bool do_sample = use_threshold || gamma > 0.0;
+    const bool topk = do_sample && !use_threshold;
+    if (topk) {
+        TRY(dalloc(&d_nkey, N, s));
+        sample_keys_kernel<<<pb, kTB, 0, s>>>(N, p->state, p->depth, p->sig, tree->max_depth, d_nkey, d_hist, d_ps);
+        TRY(check_launch("sample_keys_kernel"));
+    } else {
+        count_leaves_kernel<<<pb, kTB, 0, s>>>(N, p->state, p->depth, p->sig, tree->max_depth, d_ps);
+        TRY(check_launch("count_leaves_kernel"));
+    }
     if (do_sample) {
         if (use_threshold) {
-            mark_split_kernel<<<grid_for(N), kTB, 0, s>>>(N, 2, p->state, p->depth, p->sig, tree->max_depth,
-                                                          pool_id, threshold, d_ps);
+            mark_split_kernel<<<pb, kTB, 0, s>>>(N, 2, p->state, p->depth, p->sig, tree->max_depth, pool_id,
+                                                 threshold, d_ps, nullptr);
         } else {
             sample_k_kernel<<<1, 1, 0, s>>>(d_ps, gamma);
             TRY(dalloc(&d_ckey, N, s));
             TRY(dalloc(&d_cidx, N, s));
             for (int shift = 56; shift >= 0; shift -= 8) {
-                const bool cand = shift < 48;  // after two full passes: candidates only
+                // pass 56's histogram came with the keys; after two passes over
+                // all nodes only the candidates matching the prefix remain
+                const bool cand = shift < 48;
                 if (shift == 40)
-                    radix_compact_kernel<<<grid_for(N), kTB, 0, s>>>(N, p->state, p->depth, p->sig,
-                                                                     tree->max_depth, d_ps, d_ckey, d_cidx);
-                radix_hist_kernel<<<pb, kTB, 0, s>>>(N, 0, p->state, p->depth, p->sig, tree->max_depth, pool_id,
-                                                     d_ps, shift, d_hist, cand ? d_ckey : nullptr,
-                                                     cand ? d_cidx : nullptr);
+                    radix_compact_kernel<<<pb, kTB, 0, s>>>(N, d_ps, d_ckey, d_cidx, d_nkey);
+                if (shift < 56)
+                    radix_hist_kernel<<<pb, kTB, 0, s>>>(N, 0, p->state, p->depth, p->sig, tree->max_depth,
+                                                         pool_id, d_ps, shift, d_hist, cand ? d_ckey : nullptr,
+                                                         cand ? d_cidx : nullptr, d_nkey);
                 radix_pick_kernel<<<1, 32, 0, s>>>(d_ps, 0, d_hist, shift);
             }
             for (int shift = 24; shift >= 0; shift -= 8) {  // ties: all keys equal the k-th, all candidates
                 radix_hist_kernel<<<pb, kTB, 0, s>>>(N, 1, p->state, p->depth, p->sig, tree->max_depth, pool_id,
-                                                     d_ps, shift, d_hist, d_ckey, d_cidx);
+                                                     d_ps, shift, d_hist, d_ckey, d_cidx, d_nkey);
                 radix_pick_kernel<<<1, 32, 0, s>>>(d_ps, 1, d_hist, shift);
             }
-            mark_split_kernel<<<grid_for(N), kTB, 0, s>>>(N, 0, p->state, p->depth, p->sig, tree->max_depth,
-                                                          pool_id, 0.0, d_ps);
+            mark_split_keys_kernel<<<pb, kTB, 0, s>>>(N, p->state, pool_id, d_ps, d_nkey);
         }
         TRY(check_launch("sample selection"));
     }
