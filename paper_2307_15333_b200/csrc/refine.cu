@@ -22,6 +22,7 @@
 // only canonicalises on save; topologies are compared after canonicalisation.
 #include <cub/block/block_reduce.cuh>
 #include <cub/block/block_scan.cuh>
+#include <cub/device/device_scan.cuh>
 #include <algorithm>
 #include <cmath>
 #include <vector>
@@ -104,13 +105,28 @@ __global__ void scan_apply_kernel(const int32_t* __restrict__ in, int64_t n,
     }
 }
 
+__global__ void scan_total_kernel(const int32_t* __restrict__ in, const int64_t* __restrict__ out, int64_t n,
+                                  int64_t* __restrict__ total) {
+    *total = n ? out[n - 1] + in[n - 1] : 0;
+}
+
+// Exclusive prefix sum of 0/1 int32 flags into int64 (single-pass decoupled
+// look-back scan, cub::DeviceScan) plus the total.  `sums` is unused (kept
+// for the call sites' buffer layout).
 static int exclusive_scan(const int32_t* in, int64_t n, int64_t* out, int64_t* sums, int64_t* d_total,
                           cudaStream_t s) {
-    const int64_t nb = (n + kScanTile - 1) / kScanTile;
-    if (nb == 0) return check_cuda(cudaMemsetAsync(d_total, 0, sizeof(int64_t), s), "memset");
-    scan_reduce_kernel<<<unsigned(nb), kTB, 0, s>>>(in, n, sums);
-    scan_sums_kernel<<<1, kTB, 0, s>>>(sums, nb, d_total);
-    scan_apply_kernel<<<unsigned(nb), kTB, 0, s>>>(in, n, sums, out);
+    (void)sums;
+    if (n == 0) return check_cuda(cudaMemsetAsync(d_total, 0, sizeof(int64_t), s), "memset");
+    size_t bytes = 0;
+    cub::DeviceScan::ExclusiveScan(nullptr, bytes, in, out, cub::Sum(), int64_t(0), n, s);
+    void* tmp = nullptr;
+    int st = check_cuda(cudaMallocAsync(&tmp, bytes, s), "cudaMallocAsync");
+    if (st == DOT_OK)
+        st = check_cuda(cub::DeviceScan::ExclusiveScan(tmp, bytes, in, out, cub::Sum(), int64_t(0), n, s),
+                        "DeviceScan");
+    cudaFreeAsync(tmp, s);
+    if (st != DOT_OK) return st;
+    scan_total_kernel<<<1, 1, 0, s>>>(in, out, n, d_total);
     return check_launch("exclusive_scan");
 }
 
