@@ -775,17 +775,28 @@ __global__ void level_emit_kernel(TreeDev T, int64_t m, int64_t base, int64_t ne
 // every surviving non-root node sits at its parent's block + octant, and a
 // split leaf's 8 new children fill its block (scene_io.py:529-541 order).
 
-__global__ void rebuild_flags_kernel(TreeDev T, int64_t N, const uint8_t* __restrict__ state,
-                                     int32_t* __restrict__ flags, int32_t* __restrict__ parent) {
-    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (i >= N) return;
-    const uint8_t st = state[i];
-    const bool alive = (st & ST_ALIVE) != 0;
-    flags[i] = alive && (!(st & ST_LEAF) || (st & ST_SPLIT)) ? 1 : 0;
-    if (alive && !(st & ST_LEAF)) {
-        const int32_t c = T.node[i];
+__global__ void __launch_bounds__(256) rebuild_flags_kernel(int64_t N, const uint8_t* __restrict__ state,
+                                                            int32_t* __restrict__ flags) {
+    const int64_t chunks = (N + 15) / 16;
+    const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+    for (int64_t c = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; c < chunks; c += stride) {
+        const int64_t i0 = 16 * c;
+        if (i0 + 16 <= N) {
+            const uint4 w = *reinterpret_cast<const uint4*>(state + i0);
+            const uint8_t* b = reinterpret_cast<const uint8_t*>(&w);
+            int f[16];
 #pragma unroll
-        for (int k = 0; k < 8; ++k) parent[c + k] = int32_t(i);
+            for (int k = 0; k < 16; ++k)
+                f[k] = (b[k] & ST_ALIVE) && (!(b[k] & ST_LEAF) || (b[k] & ST_SPLIT)) ? 1 : 0;
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                reinterpret_cast<int4*>(flags + i0)[k] = make_int4(f[4 * k], f[4 * k + 1], f[4 * k + 2], f[4 * k + 3]);
+        } else {
+            for (int64_t i = i0; i < N; ++i) {
+                const uint8_t st = state[i];
+                flags[i] = (st & ST_ALIVE) && (!(st & ST_LEAF) || (st & ST_SPLIT)) ? 1 : 0;
+            }
+        }
     }
 }
 
@@ -807,40 +818,68 @@ __global__ void rebuild_levels_kernel(int n_levels, const int64_t* __restrict__ 
     new_base[n_levels + 1] = base + count;
 }
 
-__global__ void rebuild_emit_kernel(TreeDev T, int64_t N, const uint8_t* __restrict__ state,
-                                    const uint8_t* __restrict__ depth, const int32_t* __restrict__ flags,
-                                    const int32_t* __restrict__ parent, const int64_t* __restrict__ rank,
-                                    const int64_t* __restrict__ new_base, const int64_t* __restrict__ rb,
-                                    int32_t* __restrict__ new_node, int64_t* __restrict__ src_index,
-                                    uint8_t* __restrict__ src_kind) {
-    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (i >= N) return;
-    const uint8_t st = state[i];
-    if (!(st & ST_ALIVE)) return;
-    const int L = depth[i];
-    int64_t g = 0;
-    if (i > 0) {
-        const int32_t P = parent[i];
-        g = new_base[L] + 8 * (rank[P] - rb[L - 1]) + (i - T.node[P]);
-    }
+// One thread per old node; internal-after nodes write their 8-child block
+// (consecutive internal-after nodes own consecutive blocks, so a warp's
+// writes are contiguous).  Entry 0 (the root) is written by thread 0.
+__device__ __forceinline__ void emit_node(const TreeDev& T, int64_t g, int64_t i, int L, uint8_t st, int flag,
+                                          const int64_t* __restrict__ rank, const int64_t* __restrict__ new_base,
+                                          const int64_t* __restrict__ rb, int32_t* __restrict__ new_node,
+                                          int64_t* __restrict__ src_index, uint8_t* __restrict__ src_kind) {
     src_index[g] = i;
-    if (flags[i]) {
-        const int64_t cb = new_base[L + 1] + 8 * (rank[i] - rb[L]);
-        new_node[g] = int32_t(cb);
-        if (st & ST_LEAF) {  // split: 8 new leaves copying this (original or merged) leaf
-            src_kind[g] = K_SPLITPARENT;
-#pragma unroll
-            for (int k = 0; k < 8; ++k) {
-                new_node[cb + k] = ~int32_t(cb + k);
-                src_index[cb + k] = i;
-                src_kind[cb + k] = K_NEWCHILD;
-            }
-        } else {
-            src_kind[g] = K_KEPT;
-        }
+    if (flag) {
+        new_node[g] = int32_t(new_base[L + 1] + 8 * (rank[i] - rb[L]));
+        src_kind[g] = (st & ST_LEAF) ? K_SPLITPARENT : K_KEPT;
     } else {
         new_node[g] = ~int32_t(g);
         src_kind[g] = (st & ST_MERGED) ? K_MERGED : K_KEPT;
+    }
+}
+
+__global__ void __launch_bounds__(256) rebuild_emit_kernel(
+    TreeDev T, int64_t N, const uint8_t* __restrict__ state, const uint8_t* __restrict__ depth,
+    const int32_t* __restrict__ flags, const int64_t* __restrict__ rank,
+    const int64_t* __restrict__ new_base, const int64_t* __restrict__ rb, int32_t* __restrict__ new_node,
+    int64_t* __restrict__ src_index, uint8_t* __restrict__ src_kind) {
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int lane = threadIdx.x & 31;
+    if (i == 0) emit_node(T, 0, 0, 0, state[0], flags[0], rank, new_base, rb, new_node, src_index, src_kind);
+    const int f = i < N ? flags[i] : 0;
+    const unsigned m = __ballot_sync(0xffffffffu, f != 0);
+    if (!m) return;
+    // this warp's internal-after nodes emit their child blocks together: slot
+    // s = 8 * (rank of the parent among the warp's set bits) + octant, one
+    // lane per slot, so every store instruction covers contiguous entries
+    uint8_t st = 0;
+    int L = 0;
+    int64_t cb = 0;
+    int32_t c = 0;
+    if (f) {
+        st = state[i];
+        L = depth[i];
+        cb = new_base[L + 1] + 8 * (rank[i] - rb[L]);
+        c = T.node[i];
+    }
+    const int slots = 8 * __popc(m);
+    for (int s0 = 0; s0 < slots; s0 += 32) {
+        const int sl = s0 + lane;
+        const int q = sl < slots ? sl >> 3 : 0;
+        const int src = __fns(m, 0, q + 1);  // lane of the q-th parent
+        const uint8_t pst = __shfl_sync(0xffffffffu, st, src);
+        const int pL = __shfl_sync(0xffffffffu, L, src);
+        const int64_t pcb = __shfl_sync(0xffffffffu, cb, src);
+        const int32_t pc = __shfl_sync(0xffffffffu, c, src);
+        const int64_t pi = __shfl_sync(0xffffffffu, i, src);
+        if (sl >= slots) continue;
+        const int k = sl & 7;
+        const int64_t g = pcb + k;
+        if (pst & ST_LEAF) {  // split: 8 new leaves copying this (original or merged) leaf
+            new_node[g] = ~int32_t(g);
+            src_index[g] = pi;
+            src_kind[g] = K_NEWCHILD;
+        } else {  // kept internal node: its 8 (alive) children in octant order
+            const int64_t ch = int64_t(pc) + k;
+            emit_node(T, g, ch, pL + 1, state[ch], flags[ch], rank, new_base, rb, new_node, src_index, src_kind);
+        }
     }
 }
 
@@ -1186,11 +1225,10 @@ int dot_refine_apply(const dot_refine_plan* p, const dot_tree_view* tree, int32_
     const int64_t N = p->N;
     const int n_levels = int(p->level_off.size()) - 1;
     if (n_levels + 2 > kMaxLevels) return set_error(DOT_BAD_ARG, "tree too deep");
-    int32_t *flags = nullptr, *parent = nullptr;
+    int32_t* flags = nullptr;
     int64_t *rank = nullptr, *sums = nullptr, *d_total = nullptr, *d_base = nullptr, *d_rb = nullptr;
     auto cleanup = [&]() {
         cudaFreeAsync(flags, s);
-        cudaFreeAsync(parent, s);
         cudaFreeAsync(rank, s);
         cudaFreeAsync(sums, s);
         cudaFreeAsync(d_total, s);
@@ -1199,7 +1237,6 @@ int dot_refine_apply(const dot_refine_plan* p, const dot_tree_view* tree, int32_
     };
 #define TRY(x) do { if ((st = (x)) != DOT_OK) { cleanup(); return st; } } while (0)
     TRY(dalloc(&flags, N, s));
-    TRY(dalloc(&parent, N, s));
     TRY(dalloc(&rank, N, s));
     TRY(dalloc(&sums, N / kScanTile + 2, s));
     TRY(dalloc(&d_total, 1, s));
@@ -1208,12 +1245,12 @@ int dot_refine_apply(const dot_refine_plan* p, const dot_tree_view* tree, int32_
     TRY(check_cuda(cudaMemcpyToSymbolAsync(c_level_off, p->level_off.data(),
                                            p->level_off.size() * sizeof(int64_t), 0,
                                            cudaMemcpyHostToDevice, s), "memcpy"));
-    rebuild_flags_kernel<<<grid_for(N), kTB, 0, s>>>(T, N, p->state, flags, parent);
+    rebuild_flags_kernel<<<persistent_blocks(), kTB, 0, s>>>(N, p->state, flags);
     TRY(check_launch("rebuild_flags_kernel"));
     TRY(exclusive_scan(flags, N, rank, sums, d_total, s));
     rebuild_levels_kernel<<<1, 1, 0, s>>>(n_levels, rank, d_total, d_base, d_rb);
-    rebuild_emit_kernel<<<grid_for(N), kTB, 0, s>>>(T, N, p->state, p->depth, flags, parent, rank, d_base,
-                                                    d_rb, new_node, src_index, src_kind);
+    rebuild_emit_kernel<<<grid_for(N), kTB, 0, s>>>(T, N, p->state, p->depth, flags, rank, d_base, d_rb,
+                                                    new_node, src_index, src_kind);
     TRY(check_launch("rebuild_emit_kernel"));
     std::vector<int64_t> nb(size_t(n_levels) + 2);
     TRY(check_cuda(cudaMemcpyAsync(nb.data(), d_base, nb.size() * sizeof(int64_t), cudaMemcpyDeviceToHost, s),

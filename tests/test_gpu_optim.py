@@ -108,7 +108,7 @@ def test_train_step_equals_unfused_step():
         rmsprop_step(a, g, sa)
         ba.accumulate(sig, sl.numel())
         loss_b = train_step(b, o, d, t, sb, bb, sws, 0.5, ray_index=sl)
-        assert float(loss_b) == pytest.approx(float(loss_a), rel=1e-9)
+        assert float(loss_b) == pytest.approx(float(loss_a), rel=1e-6)  # step 2: fp32-atomic noise
     torch.testing.assert_close(b.sigma, a.sigma, atol=1e-5, rtol=1e-4)
     torch.testing.assert_close(b.sh, a.sh, atol=1e-5, rtol=1e-4)
     torch.testing.assert_close(sb.v_sh, sa.v_sh, atol=1e-9, rtol=1e-3)
