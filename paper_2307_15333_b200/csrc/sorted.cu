@@ -67,18 +67,41 @@ __global__ void __launch_bounds__(128) reduce_runs_kernel(
         }
         double as = double(gsig[pid]);
         double aq = signal[pid];
-        for (; j < total; ++j) {
-            const unsigned long long key = keys[j];
-            if ((key >> ray_bits) != pid) break;
-            const int32_t k = idx[j];
-            const float4 r = rec[k];
-            const double q = recq[k];
-            const double bv = b < B ? double(basis[int64_t(key & rmask) * B + b]) : 0.0;
-            a0 = __dadd_rn(a0, __dmul_rn(double(r.y), bv));
-            a1 = __dadd_rn(a1, __dmul_rn(double(r.z), bv));
-            a2 = __dadd_rn(a2, __dmul_rn(double(r.w), bv));
-            as = __dadd_rn(as, double(r.x));
-            aq = __dadd_rn(aq, q);
+        // records in groups of U: all loads of a group are issued before its
+        // (sequential, in-order) additions, so a run costs ~1 memory latency
+        // per U records instead of per record
+        constexpr int U = 8;
+        for (bool more = true; more; j += U) {
+            unsigned long long kk[U];
+            int32_t ix[U];
+            float4 r[U];
+            double q[U], bv[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                kk[u] = j + u < total ? keys[j + u] : ~0ull;
+                if ((kk[u] >> ray_bits) != pid) kk[u] = ~0ull;
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) ix[u] = kk[u] != ~0ull ? idx[j + u] : 0;
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const bool in = kk[u] != ~0ull;
+                r[u] = in ? rec[ix[u]] : make_float4(0.f, 0.f, 0.f, 0.f);
+                q[u] = in ? recq[ix[u]] : 0.0;
+                bv[u] = (in && b < B) ? double(basis[int64_t(kk[u] & rmask) * B + b]) : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                if (kk[u] == ~0ull) {
+                    more = false;
+                    break;
+                }
+                a0 = __dadd_rn(a0, __dmul_rn(double(r[u].y), bv[u]));
+                a1 = __dadd_rn(a1, __dmul_rn(double(r[u].z), bv[u]));
+                a2 = __dadd_rn(a2, __dmul_rn(double(r[u].w), bv[u]));
+                as = __dadd_rn(as, double(r[u].x));
+                aq = __dadd_rn(aq, q[u]);
+            }
         }
         if (b < B) {
             gsh[pid * S + 0 * B + b] = float(a0);
