@@ -99,7 +99,7 @@ int dot_locate_build(const dot_tree_view* tree, int32_t level, int32_t* table, v
     if (!locate_dyadic(*tree))
         return set_error(DOT_BAD_ARG, "locate table needs a dyadic root (half_extent a power of two, "
                                       "centre a multiple of half * 2^-20, max_depth <= 21, capacity < 2^26)");
-    if (level < 1 || level > 9 || false)
+    if (level < 1 || level > 9)
         return set_error(DOT_BAD_ARG, "locate level must be in 1..9, got %d", level);
     if (!table) return set_error(DOT_BAD_ARG, "locate table is NULL");
     return launch_locate_build(make_tree(*tree), level, table, static_cast<cudaStream_t>(stream));
