@@ -276,6 +276,11 @@ def run_ours(args, rank, world, local_rank):
         allreduce_grads_overlapped(ws.dsigma, ws.dsh_store, ws.touched, update,
                                    chunks=args.ar_chunks)
 
+    if world > 1 and args.exchange == "peer":
+        # reduce-scatter + RMSProp + all-gather fused over symmetric (peer) memory
+        from paper_2307_15333_b200.parallel import PeerExchange
+        exchange = PeerExchange(tree, state, sws)
+
     def step(k, timed_kernel=True):
         # the batch is read in place from the resident pool (ray_index): no gather
         return train_step(tree, origins, dirs, targets, state, buf, sws, BG, EPS,
@@ -421,6 +426,7 @@ def run_ours(args, rank, world, local_rank):
             "segments_per_ray": seg / per_rank, "composited_per_ray": comp / per_rank,
             "l2": wl.l2,
             "parallelism": f"rays sharded dp{world}, tree replicated",
+            "exchange": args.exchange if world > 1 else "none",
             "batch_order": args.order, "bwd_flags": args.bwd_flags,
         },
         # per step: dot_ray_keys32 + render_bwd_buffered + one rmsprop per
@@ -669,6 +675,9 @@ def main():
                     help="batch ray order handed to the kernel (same ray set)")
     ap.add_argument("--ar-chunks", type=int, default=4,
                     help="row chunks of the overlapped gradient all-reduce (N > 1)")
+    ap.add_argument("--exchange", choices=["nccl", "peer"], default="nccl",
+                    help="N > 1 gradient exchange: chunked NCCL all-reduce + RMSProp, or the fused "
+                         "peer-memory update (dot_rmsprop_step_peers)")
     ap.add_argument("--bwd-flags", type=int, default=0,
                     help="dot_render_bwd flags (2 = legacy one-ray-per-thread kernel)")
     args = ap.parse_args()

@@ -227,6 +227,32 @@ int dot_rmsprop_step(float* sigma, float* sh, int32_t sh_stride, int32_t n_sh,
                      int64_t capacity, double beta, double eps, double lr_sigma,
                      double lr_sh, int32_t flags, void* stream);
 
+/* --- multi-GPU update fused with its collective (one node, peer memory
+ *     over NVLink/NVSwitch; replaces all-reduce + rmsprop_step of the
+ *     data-parallel step).  Rank `rank` of `world` calls it for the rows it
+ *     owns, [row_lo, row_hi), once every rank's backward has finished: the
+ *     kernel sums the W partial gradient rows (rank order, f64), applies
+ *     RMSProp with the local v_* (capacity-sized; only owned rows are
+ *     current), stores the updated row into every rank's payload replica and
+ *     (flags bit 0) zeroes the W consumed gradient rows.  All pointers are
+ *     device addresses valid on the calling GPU (peer-mapped for r != rank,
+ *     e.g. torch symmetric memory); a second barrier must separate it from
+ *     the next backward. */
+#define DOT_MAX_PEERS 8
+typedef struct dot_peer_rows {
+    float* sigma[DOT_MAX_PEERS];
+    float* sh[DOT_MAX_PEERS];
+    float* grad_sigma[DOT_MAX_PEERS];
+    float* grad_sh[DOT_MAX_PEERS];
+    const uint8_t* touched[DOT_MAX_PEERS];
+    int32_t world;
+    int32_t rank;
+} dot_peer_rows;
+int dot_rmsprop_step_peers(const dot_peer_rows* peers, int32_t sh_stride, int32_t n_sh,
+                           int32_t gsh_stride, double* v_sigma, double* v_sh, int64_t row_lo,
+                           int64_t row_hi, double beta, double eps, double lr_sigma, double lr_sh,
+                           int32_t flags, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -33,6 +33,17 @@ class DotTreeView(ctypes.Structure):
     ]
 
 
+MAX_PEERS = 8
+
+
+class DotPeerRows(ctypes.Structure):
+    _fields_ = [
+        ("sigma", c_void_p * MAX_PEERS), ("sh", c_void_p * MAX_PEERS),
+        ("grad_sigma", c_void_p * MAX_PEERS), ("grad_sh", c_void_p * MAX_PEERS),
+        ("touched", c_void_p * MAX_PEERS), ("world", c_i32), ("rank", c_i32),
+    ]
+
+
 class DotRefineStats(ctypes.Structure):
     _fields_ = [
         ("leaves_before", c_i64), ("leaves_after", c_i64), ("merges_applied", c_i64),
@@ -73,6 +84,8 @@ _SIGNATURES = {
                                  c_void_p, c_i32, c_void_p, c_void_p]),
     "dot_refine_plan_merge_rounds": (c_i32, [c_void_p, c_void_p, c_void_p]),
     "dot_refine_plan_destroy": (None, [c_void_p]),
+    "dot_rmsprop_step_peers": (c_i32, [c_void_p, c_i32, c_i32, c_i32, c_void_p, c_void_p, c_i64, c_i64, c_f64,
+                                       c_f64, c_f64, c_f64, c_i32, c_void_p]),
     "dot_rmsprop_step": (c_i32, [c_void_p, c_void_p, c_i32, c_i32, c_void_p, c_void_p, c_void_p,
                                  c_void_p, c_i32, c_void_p, c_i64, c_f64, c_f64, c_f64, c_f64,
                                  c_i32, c_void_p]),
@@ -139,5 +152,5 @@ def stream_ptr(stream=None) -> int:
     return int(s.cuda_stream)
 
 
-__all__ = ["DotTreeView", "DotRefineStats", "ExtensionError", "load", "check", "call", "ptr",
+__all__ = ["DotTreeView", "DotPeerRows", "DotRefineStats", "ExtensionError", "load", "check", "call", "ptr",
            "stream_ptr", "symbols", "LIB_PATH", "ConfigError"]

@@ -12,6 +12,8 @@
 
 namespace dot {
 
+constexpr int kMaxPeers = DOT_MAX_PEERS;
+
 __device__ __forceinline__ float rms_update(float theta, double& v, double g, double beta,
                                             double omb, double eps, double lr, bool clamp) {
     v = __dadd_rn(__dmul_rn(beta, v), __dmul_rn(__dmul_rn(omb, g), g));
@@ -73,9 +75,109 @@ __global__ void __launch_bounds__(256, MINB) rmsprop_kernel(float* __restrict__ 
     }
 }
 
+// ---------------------------------------------------------------------------
+// Multi-GPU update fused with its collective (one node, NVLink/NVSwitch peer
+// memory).  Every rank holds a replica of the payload and its own partial
+// gradients; rank k owns rows [lo_k, hi_k).  After all ranks' backward
+// kernels have finished, each rank runs this kernel over its own rows: it
+// reads the W partial gradient rows (local + W-1 peer loads) and sums them in
+// rank order (f64), applies RMSProp with its local second moments, writes the
+// updated row into EVERY rank's payload (peer stores: the all-gather), and
+// zeroes the W consumed gradient rows (consume).  Reduce-scatter + update +
+// all-gather in one pass, only over rows some rank touched; no NCCL call.
+
+struct PeerRows {
+    float* sigma[kMaxPeers];
+    float* sh[kMaxPeers];
+    float* gsig[kMaxPeers];
+    float* gsh[kMaxPeers];
+    const uint8_t* touched[kMaxPeers];
+    int world, rank;
+};
+
+__global__ void __launch_bounds__(256) rmsprop_peer_kernel(PeerRows P, int sh_stride, int n_sh, int gsh_stride,
+                                                           double* __restrict__ v_sigma,
+                                                           double* __restrict__ v_sh, int64_t lo, int64_t hi,
+                                                           int quads, double beta, double eps, double lr_sigma,
+                                                           double lr_sh, bool consume) {
+    const int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (t >= (hi - lo) * quads) return;
+    const int64_t row = lo + t / quads;
+    const int j = int(t - (row - lo) * quads);
+    bool touched = false;
+    for (int r = 0; r < P.world; ++r) touched |= P.touched[r][row] != 0;
+    if (!touched) return;
+    const double omb = __dsub_rn(1.0, beta);
+    if (j == 0) {
+        double g = 0.0;
+        for (int r = 0; r < P.world; ++r) g += double(P.gsig[r][row]);
+        double v = v_sigma[row];
+        const float th = rms_update(P.sigma[P.rank][row], v, g, beta, omb, eps, lr_sigma, true);
+        v_sigma[row] = v;
+        for (int r = 0; r < P.world; ++r) {
+            P.sigma[r][row] = th;
+            if (consume) P.gsig[r][row] = 0.f;
+        }
+    }
+    const int k0 = 4 * j;
+    double g[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int r = 0; r < P.world; ++r) {
+        const float* gp = P.gsh[r] + row * gsh_stride + k0;
+        for (int u = 0; u < 4 && k0 + u < n_sh; ++u) g[u] += double(gp[u]);
+    }
+    const float* th0 = P.sh[P.rank] + row * sh_stride + k0;
+    float th[4];
+    double* v = v_sh + row * n_sh + k0;
+    for (int u = 0; u < 4 && k0 + u < n_sh; ++u) {
+        double vv = v[u];
+        th[u] = rms_update(th0[u], vv, g[u], beta, omb, eps, lr_sh, false);
+        v[u] = vv;
+    }
+    for (int r = 0; r < P.world; ++r) {
+        float* p = P.sh[r] + row * sh_stride + k0;
+        float* gp = P.gsh[r] + row * gsh_stride + k0;
+        for (int u = 0; u < 4 && k0 + u < n_sh; ++u) {
+            p[u] = th[u];
+            if (consume) gp[u] = 0.f;
+        }
+    }
+}
+
 }  // namespace dot
 
 using namespace dot;
+
+extern "C" int dot_rmsprop_step_peers(const dot_peer_rows* peers, int32_t sh_stride, int32_t n_sh,
+                                      int32_t gsh_stride, double* v_sigma, double* v_sh, int64_t row_lo,
+                                      int64_t row_hi, double beta, double eps, double lr_sigma, double lr_sh,
+                                      int32_t flags, void* stream) {
+    if (!peers || !v_sigma || !v_sh) return set_error(DOT_BAD_ARG, "rmsprop_peers: NULL argument");
+    if (peers->world < 1 || peers->world > kMaxPeers || peers->rank < 0 || peers->rank >= peers->world)
+        return set_error(DOT_BAD_ARG, "rmsprop_peers: world must be 1..%d and rank < world", kMaxPeers);
+    if (!(beta > 0.0 && beta < 1.0)) return set_error(DOT_BAD_ARG, "beta must be in (0, 1), got %g", beta);
+    if (n_sh < 1 || sh_stride < n_sh || gsh_stride < n_sh) return set_error(DOT_BAD_ARG, "rmsprop_peers: bad strides");
+    PeerRows P;
+    P.world = peers->world;
+    P.rank = peers->rank;
+    for (int r = 0; r < kMaxPeers; ++r) {
+        const bool in = r < P.world;
+        if (in && (!peers->sigma[r] || !peers->sh[r] || !peers->grad_sigma[r] || !peers->grad_sh[r] ||
+                   !peers->touched[r]))
+            return set_error(DOT_BAD_ARG, "rmsprop_peers: NULL pointer for rank %d", r);
+        P.sigma[r] = in ? peers->sigma[r] : nullptr;
+        P.sh[r] = in ? peers->sh[r] : nullptr;
+        P.gsig[r] = in ? peers->grad_sigma[r] : nullptr;
+        P.gsh[r] = in ? peers->grad_sh[r] : nullptr;
+        P.touched[r] = in ? peers->touched[r] : nullptr;
+    }
+    if (row_hi <= row_lo) return DOT_OK;
+    const int quads = (n_sh + 3) / 4;
+    const int64_t total = (row_hi - row_lo) * quads;
+    rmsprop_peer_kernel<<<unsigned((total + 255) / 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+        P, sh_stride, n_sh, gsh_stride, v_sigma, v_sh, row_lo, row_hi, quads, beta, eps, lr_sigma, lr_sh,
+        (flags & 1) != 0);
+    return check_launch("rmsprop_peer_kernel");
+}
 
 extern "C" int dot_rmsprop_step(float* sigma, float* sh, int32_t sh_stride, int32_t n_sh, double* v_sigma,
                                 double* v_sh, float* grad_sigma, float* grad_sh,
