@@ -62,3 +62,19 @@ def test_peer_update_equals_summed_update(oracle, world):
         lo, hi = owned_rows(cap, r, world)
         np.testing.assert_array_equal(states[r].v_sigma.cpu().numpy()[lo:hi], e_vs[lo:hi])
         np.testing.assert_array_equal(states[r].v_sh.cpu().numpy()[lo:hi], e_vh[lo:hi])
+
+
+def test_peer_exchange_end_to_end_under_torchrun():
+    """PeerExchange (torch symmetric memory + device barriers + the fused
+    kernel) through train_step under torchrun on the GPUs of this box (one
+    here), against the same steps without an exchange."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    n = max(1, min(torch.cuda.device_count(), 8))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", "29541", os.path.join(root, "tools", "peer_smoke.py")]
+    res = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=root)
+    assert res.returncode == 0, res.stdout[-2000:] + res.stderr[-2000:]
+    assert res.stdout.count("PEER_OK") == n, res.stdout[-2000:]
