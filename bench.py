@@ -477,23 +477,29 @@ def bench_render(tree, dev, args, world):
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms = float(tt.item())
     rays = W * H * n_views * world
-    # the same views through render_view: rays generated in-kernel, 8x4 warp tiles
-    from paper_2307_15333_b200.render import render_view
+    # the same views with rays generated in-kernel (8x4 warp tiles): one
+    # launch for all of this rank's views (render_views), and one per view
+    from paper_2307_15333_b200.render import render_view, render_views
     from paper_2307_15333_b200.scene_io import Camera
     cams = [Camera(W, H, focal, poses[(rank * n_views + i) % 200]) for i in range(n_views)]
-    for i in range(min(3, n_views)):
-        render_view(tree, cams[i], BG, EPS)
-    torch.cuda.synchronize()
-    a.record()
-    for cam in cams:
-        render_view(tree, cam, BG, EPS)
-    b.record()
-    torch.cuda.synchronize()
-    ms_cam = a.elapsed_time(b)
-    if world > 1:
-        tt = torch.tensor([ms_cam], device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        ms_cam = float(tt.item())
+
+    def timed(fn, warm=3):
+        for _ in range(warm):
+            fn()
+        torch.cuda.synchronize()
+        a.record()
+        fn()
+        b.record()
+        torch.cuda.synchronize()
+        t = a.elapsed_time(b)
+        if world > 1:
+            tt = torch.tensor([t], device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            t = float(tt.item())
+        return t
+
+    ms_cam = timed(lambda: render_views(tree, cams, BG, EPS))
+    ms_per_view_launch = timed(lambda: [render_view(tree, c, BG, EPS) for c in cams])
     # roofline of render_camera_kernel: per view 12 B/pixel rgb out (rays are
     # generated in-kernel: 0 B in) + per composited segment sigma 4 B + the
     # 192 B SH row when q > 0; counts from dot_ray_stats
@@ -515,7 +521,10 @@ def bench_render(tree, dev, args, world):
                          "composited_per_ray": comp / (W * H * n_views),
                          "segments_per_ray": seg / (W * H * n_views)},
             "ms_per_view": ms_cam / n_views, "views": n_views * world, "eps": EPS,
-            "workload": "configs[2]: 800x800 random hemisphere views, render_view (in-kernel rays)",
+            "workload": "configs[2]: 800x800 random hemisphere views, render_views (in-kernel rays, "
+                        "all views of a rank in one launch)",
+            "one_launch_per_view": {"rays_per_s": rays / (ms_per_view_launch / 1e3),
+                                    "ms_per_view": ms_per_view_launch / n_views},
             "rays_resident": {"rays_per_s": rays / (ms / 1e3), "ms_per_view": ms / n_views,
                               "workload": "same views through render_rays, f64 rays resident in HBM"}}
 

@@ -104,6 +104,15 @@ int dot_render_camera(const dot_tree_view* tree, const double* cam_to_world, dou
                       double early_stop_eps, float* rgb, float* t_final, float* depth,
                       void* stream);
 
+/* --- many views in one launch (render_image over a camera list): n_views
+ *     host 4x4 cam_to_world matrices (row-major, [n_views][16]) and focal
+ *     lengths, one shared width/height; rgb is [n_views][height][width][3]
+ *     f32, t_final / depth [n_views][height][width] or NULL.  One launch
+ *     drains one wave tail instead of one per view. */
+int dot_render_cameras(const dot_tree_view* tree, const double* cam_to_world, const double* focal,
+                       int32_t n_views, int32_t width, int32_t height, const double* background,
+                       double early_stop_eps, float* rgb, float* t_final, float* depth, void* stream);
+
 /* --- fused forward + backward + signal (replaces segment_batch + grad_kernel
  *     + scatter_kernel, _kernels.py:227-346, as called by
  *     render.render_and_backprop render.py:175-225).

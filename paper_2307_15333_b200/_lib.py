@@ -16,7 +16,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libdot_b200.so")
 
 DOT_OK, DOT_BAD_ARG, DOT_OOM, DOT_CUDA_ERR, DOT_NO_DEVICE = range(5)
-ABI_VERSION = 4
+ABI_VERSION = 5
 
 c_void_p = ctypes.c_void_p
 c_i64 = ctypes.c_int64
@@ -67,6 +67,8 @@ _SIGNATURES = {
                                c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
     "dot_render_camera": (c_i32, [c_void_p, c_void_p, c_f64, c_i32, c_i32, c_void_p, c_f64, c_void_p,
                                   c_void_p, c_void_p, c_void_p]),
+    "dot_render_cameras": (c_i32, [c_void_p, c_void_p, c_void_p, c_i32, c_i32, c_i32, c_void_p, c_f64, c_void_p,
+                                   c_void_p, c_void_p, c_void_p]),
     "dot_render_bwd":(c_i32, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_i64, c_void_p, c_f64, c_f64,
                                c_f64, c_f64, c_void_p, c_void_p, c_i32, c_void_p, c_void_p, c_void_p,
                                c_void_p, c_i32, c_void_p]),

@@ -65,7 +65,7 @@ using namespace dot;
 
 extern "C" {
 
-int dot_abi_version(void) { return 4; }
+int dot_abi_version(void) { return 5; }
 
 const char* dot_last_error(void) { return g_err; }
 
@@ -182,6 +182,18 @@ int dot_render_camera(const dot_tree_view* tree, const double* cam_to_world, dou
         return set_error(DOT_BAD_ARG, "bad camera arguments");
     return launch_render_camera(make_tree(*tree), cam_to_world, focal, width, height, background, early_stop_eps,
                                 rgb, t_final, depth, static_cast<cudaStream_t>(stream));
+}
+
+int dot_render_cameras(const dot_tree_view* tree, const double* cam_to_world, const double* focal,
+                       int32_t n_views, int32_t width, int32_t height, const double* background,
+                       double early_stop_eps, float* rgb, float* t_final, float* depth, void* stream) {
+    if (int st = validate_tree_view(tree)) return st;
+    if (n_views < 0 || (n_views && (!cam_to_world || !focal || !rgb)) || !background || width < 0 || height < 0)
+        return set_error(DOT_BAD_ARG, "bad camera arguments");
+    for (int v = 0; v < n_views; ++v)
+        if (!(focal[v] > 0.0)) return set_error(DOT_BAD_ARG, "focal[%d] must be positive", v);
+    return launch_render_cameras(make_tree(*tree), cam_to_world, focal, n_views, width, height, background,
+                                 early_stop_eps, rgb, t_final, depth, static_cast<cudaStream_t>(stream));
 }
 
 int dot_ray_stats(const dot_tree_view* tree, const double* origins, const double* dirs, int64_t n_rays,

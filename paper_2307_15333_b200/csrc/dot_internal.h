@@ -42,6 +42,9 @@ int launch_ray_keys(const TreeDev& T, const double* o, const double* d, int64_t 
                     cudaStream_t s);
 int launch_ray_keys32(const TreeDev& T, const double* o, const double* d, const int64_t* ray_idx,
                       int64_t n, int32_t* keys, cudaStream_t s);
+int launch_render_cameras(const TreeDev& T, const double* cam_to_world, const double* focal, int n_views,
+                          int width, int height, const double* bg, double eps, float* rgb, float* tfin,
+                          float* depth, cudaStream_t s);
 int launch_render_camera(const TreeDev& T, const double* cam_to_world, double focal, int width, int height,
                          const double* bg, double eps, float* rgb, float* tfin, float* depth, cudaStream_t s);
 int launch_render_bwd_emit(const TreeDev& T, const double* o, const double* d, const double* tgt,

@@ -9,6 +9,7 @@
 // and signal with vector REDs (REDG.E.ADD.F32x4) issued warp-cooperatively
 // (CoopSink), or -- deterministic mode -- emits per-segment records for the
 // sorted reduction of sorted.cu.
+#include <vector>
 #include "dot_tree.cuh"
 #include "dot_internal.h"
 
@@ -564,14 +565,22 @@ struct CameraDev {
     int32_t width, height;
 };
 
+// Many views per launch: block b renders tile b % tiles of view b / tiles,
+// so one launch drains one tail instead of one per view.
 template <int B>
 __global__ void __launch_bounds__(kBlock, kFwdMinBlocks) render_camera_kernel(
-    TreeDev T, CameraDev cam, double bg0, double bg1, double bg2, double eps, float* __restrict__ rgb,
-    float* __restrict__ tfin_out, float* __restrict__ depth_out) {
+    TreeDev T, const CameraDev* __restrict__ cams, int tiles, double bg0, double bg1, double bg2,
+    double eps, float* __restrict__ rgb_all, float* __restrict__ tfin_all, float* __restrict__ depth_all) {
     constexpr int S = pad4(3 * B);
+    const int v = blockIdx.x / tiles, tile = blockIdx.x - v * tiles;
+    const CameraDev& cam = cams[v];
+    const int64_t pix = int64_t(cam.width) * cam.height;
+    float* __restrict__ rgb = rgb_all + 3 * pix * v;
+    float* __restrict__ tfin_out = tfin_all ? tfin_all + pix * v : nullptr;
+    float* __restrict__ depth_out = depth_all ? depth_all + pix * v : nullptr;
     // block = 4 warps = 16x8 pixels; warp w covers an 8x4 tile
     const int tiles_x = (cam.width + 15) / 16;
-    const int bx = blockIdx.x % tiles_x, by = blockIdx.x / tiles_x;
+    const int bx = tile % tiles_x, by = tile / tiles_x;
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int x = bx * 16 + (w & 1) * 8 + (lane & 7);
     const int y = by * 8 + (w >> 1) * 4 + (lane >> 3);
@@ -619,26 +628,48 @@ __global__ void __launch_bounds__(kBlock, kFwdMinBlocks) render_camera_kernel(
     if (depth_out) depth_out[p] = float(dep);
 }
 
+int launch_render_cameras(const TreeDev& T, const double* cam_to_world, const double* focal, int n_views,
+                          int width, int height, const double* bg, double eps, float* rgb, float* tfin,
+                          float* depth, cudaStream_t s) {
+    if (width <= 0 || height <= 0 || n_views <= 0) return DOT_OK;
+    std::vector<CameraDev> cams(static_cast<size_t>(n_views));
+    for (int v = 0; v < n_views; ++v) {
+        CameraDev& cam = cams[size_t(v)];
+        const double* m = cam_to_world + 16 * v;
+        for (int i = 0; i < 3; ++i) {
+            for (int j = 0; j < 3; ++j) cam.r[3 * i + j] = m[4 * i + j];
+            cam.t[i] = m[4 * i + 3];
+        }
+        cam.focal = focal[v];
+        cam.width = width;
+        cam.height = height;
+    }
+    retain_pool_memory();
+    CameraDev* d_cams = nullptr;
+    if (int st = check_cuda(cudaMallocAsync(reinterpret_cast<void**>(&d_cams), cams.size() * sizeof(CameraDev), s),
+                            "cudaMallocAsync"))
+        return st;
+    // pageable source: the copy is staged before cudaMemcpyAsync returns
+    if (int st = check_cuda(cudaMemcpyAsync(d_cams, cams.data(), cams.size() * sizeof(CameraDev),
+                                            cudaMemcpyHostToDevice, s), "memcpy")) {
+        cudaFreeAsync(d_cams, s);
+        return st;
+    }
+    const int tiles = ((width + 15) / 16) * ((height + 7) / 8);
+    const unsigned blocks = unsigned(int64_t(tiles) * n_views);
+#define DOT_CAM(BB)                                                                                  \
+    render_camera_kernel<BB><<<blocks, kBlock, 0, s>>>(T, d_cams, tiles, bg[0], bg[1], bg[2], eps, rgb, tfin, \
+                                                       depth);
+    DOT_DISPATCH_B(DOT_CAM)
+#undef DOT_CAM
+    const int st = check_launch("render_camera_kernel");
+    cudaFreeAsync(d_cams, s);
+    return st;
+}
+
 int launch_render_camera(const TreeDev& T, const double* cam_to_world, double focal, int width, int height,
                          const double* bg, double eps, float* rgb, float* tfin, float* depth, cudaStream_t s) {
-    if (width <= 0 || height <= 0) return DOT_OK;
-    CameraDev cam;
-    for (int i = 0; i < 3; ++i) {
-        for (int j = 0; j < 3; ++j) cam.r[3 * i + j] = cam_to_world[4 * i + j];
-        cam.t[i] = cam_to_world[4 * i + 3];
-    }
-    cam.focal = focal;
-    cam.width = width;
-    cam.height = height;
-    const unsigned blocks = unsigned(((width + 15) / 16) * ((height + 7) / 8));
-    switch (T.basis_count) {
-        case 1: render_camera_kernel<1><<<blocks, kBlock, 0, s>>>(T, cam, bg[0], bg[1], bg[2], eps, rgb, tfin, depth); break;
-        case 4: render_camera_kernel<4><<<blocks, kBlock, 0, s>>>(T, cam, bg[0], bg[1], bg[2], eps, rgb, tfin, depth); break;
-        case 9: render_camera_kernel<9><<<blocks, kBlock, 0, s>>>(T, cam, bg[0], bg[1], bg[2], eps, rgb, tfin, depth); break;
-        case 16: render_camera_kernel<16><<<blocks, kBlock, 0, s>>>(T, cam, bg[0], bg[1], bg[2], eps, rgb, tfin, depth); break;
-        default: return set_error(DOT_BAD_ARG, "basis_count must be 1, 4, 9 or 16");
-    }
-    return check_launch("render_camera_kernel");
+    return launch_render_cameras(T, cam_to_world, &focal, 1, width, height, bg, eps, rgb, tfin, depth, s);
 }
 
 // ---------------------------------------------------------------------------

@@ -373,6 +373,34 @@ def render_view(tree: SparseOctree, camera, background, early_stop_eps: float = 
     return (rgb, tfin, depth) if return_aux else rgb
 
 
+def render_views(tree: SparseOctree, cameras, background, early_stop_eps: float = EPS_T,
+                 return_aux: bool = False):
+    """Render many pinhole cameras of one resolution in a single launch
+    (in-kernel rays, 8x4-pixel warp tiles); returns [V, H, W, 3] f32 on the
+    device (+ (T_final, depth) [V, H, W] with return_aux).  Same pixels as
+    ``render_view`` per camera."""
+    cams = list(cameras)
+    dev = tree.device
+    V = len(cams)
+    if V == 0:
+        raise InputError("no cameras")
+    H, W = int(cams[0].height), int(cams[0].width)
+    if any(int(c.height) != H or int(c.width) != W for c in cams):
+        raise InputError("render_views needs cameras of one resolution")
+    rgb = torch.empty(V, H, W, 3, dtype=torch.float32, device=dev)
+    tfin = torch.empty(V, H, W, dtype=torch.float32, device=dev) if return_aux else None
+    depth = torch.empty(V, H, W, dtype=torch.float32, device=dev) if return_aux else None
+    m = np.ascontiguousarray(np.stack([np.asarray(c.cam_to_world, dtype=np.float64).reshape(4, 4)
+                                       for c in cams]))
+    f = np.ascontiguousarray([float(c.focal) for c in cams], dtype=np.float64)
+    bg = _background(background)
+    view, _topo = tree.tree_view()
+    _lib.call("dot_render_cameras", _lib.ctypes.byref(view), m.ctypes.data_as(_lib.c_void_p),
+              f.ctypes.data_as(_lib.c_void_p), V, W, H, _bg_ptr(bg), float(early_stop_eps),
+              _lib.ptr(rgb), _lib.ptr(tfin), _lib.ptr(depth), _lib.stream_ptr())
+    return (rgb, tfin, depth) if return_aux else rgb
+
+
 def render_image(tree: SparseOctree, camera, background, worker_count: int | None = None,
                  early_stop_eps: float = EPS_T, chunk: int = 65536,
                  exact_rays: bool = False) -> np.ndarray:

@@ -246,3 +246,20 @@ def test_long_rays_resume_past_the_record_buffer(oracle):
         np.testing.assert_allclose(g.dsh, r_g.dsh, atol=ATOL, rtol=RTOL)
         np.testing.assert_array_equal(g.touched, r_g.touched)
         np.testing.assert_allclose(sig, r_sig, atol=ATOL, rtol=RTOL)
+
+
+def test_render_views_equals_per_view():
+    """render_views (all views in one launch) == render_view per camera, bit
+    for bit (same per-pixel code)."""
+    import torch
+    from paper_2307_15333_b200 import scenes
+    from paper_2307_15333_b200.render import render_view, render_views
+    from paper_2307_15333_b200.scene_io import Camera
+    from helpers import irregular_tree
+    tree = irregular_tree(8, 9, depth=3, splits=40, max_depth=6, device="cuda")
+    focal, poses = scenes.hemisphere_cameras(5, 96, 72, 4.0, seed=2)
+    cams = [Camera(96, 72, focal * (1.0 + 0.1 * i), p) for i, p in enumerate(poses)]
+    rgb, tf, dep = render_views(tree, cams, (0.2, 0.3, 0.4), return_aux=True)
+    for i, c in enumerate(cams):
+        r1, t1, d1 = render_view(tree, c, (0.2, 0.3, 0.4), return_aux=True)
+        assert torch.equal(rgb[i], r1) and torch.equal(tf[i], t1) and torch.equal(dep[i], d1)
