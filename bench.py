@@ -513,9 +513,14 @@ def bench_render(tree, dev, args, world):
     alg = W * H * n_views * 12 + comp * 4 + qpos * 12 * B_SH
     hbm, peak_kind = peaks()
     achieved = alg / n_views / (ms_cam / n_views / 1e3) / 1e9
+    traffic, traffic_src = measured_traffic("render_camera_kernel")
     return {"rays_per_s": rays / (ms_cam / 1e3), "fps_800x800": n_views * world / (ms_cam / 1e3),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                          "frac": achieved / hbm, "peak_kind": peak_kind,
+                         "traffic": traffic, "traffic_source": traffic_src,
+                         "traffic_note": "DRAM bytes of one 20-view launch (ncu); the algorithmic "
+                                         "gathers are mostly L2/L1 hits for coherent camera rays, "
+                                         "so frac can exceed 1",
                          "kernel": "render_camera_kernel<16>", "alg_bytes_per_view": alg / n_views,
                          "bytes_model": "12 B/pixel + 4 B/composited segment + 192 B/segment with q>0",
                          "composited_per_ray": comp / (W * H * n_views),

@@ -12,4 +12,7 @@ DOT_PROFILE_RANGE=1 timeout 600 ncu --profile-from-start off --metrics gpu__time
     --csv --log-file $OUT/launches.csv $CMD > $OUT/ncu_list.log 2>&1
 DOT_PROFILE_RANGE=1 timeout 900 ncu --profile-from-start off --set full --clock-control none --import-source on \
     -k regex:"render_bwd_buffered|rmsprop_kernel" -c 2 -o $OUT/full -f $CMD > $OUT/ncu_full.log 2>&1
+timeout 600 python bench.py --steps 3 --warmup 3 --skip-cpu --skip-refine > $OUT/plain_render.log 2>&1 && \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:render_camera_kernel -s 3 -c 1 \
+    -o $OUT/render_full -f python bench.py --steps 3 --warmup 3 --skip-cpu --skip-refine > $OUT/ncu_render.log 2>&1
 ls -la $OUT

@@ -85,6 +85,8 @@ def main():
     text, agg, cnt = launch_shares(os.path.join(src, "launches.csv"))
     open(os.path.join(prof, f"{tag}_launch_shares.txt"), "w").write(text)
     full = full_metrics(os.path.join(src, "full.ncu-rep"))
+    if os.path.exists(os.path.join(src, "render_full.ncu-rep")):
+        full += full_metrics(os.path.join(src, "render_full.ncu-rep"))
     lines = [f"# ncu --set full --clock-control none, first timed launch of each kernel ({tag})"]
     traffic_path = os.path.join(prof, "traffic.json")
     traffic = json.load(open(traffic_path)) if os.path.exists(traffic_path) else {}
@@ -99,8 +101,12 @@ def main():
         rd = to_bytes(*m["dram__bytes_read.sum"])
         wr = to_bytes(*m["dram__bytes_write.sum"])
         key = "render_bwd_buffered" if "render_bwd_buffered" in short else short.split("<")[0].split("::")[-1]
+        if "lts__t_sector_hit_rate.pct" in m:
+            traffic_hit = float(m["lts__t_sector_hit_rate.pct"][0])
+        else:
+            traffic_hit = None
         traffic[key] = {"dram_bytes_per_launch": rd + wr, "dram_read": rd, "dram_write": wr,
-                        "capture": f"profiles/{tag}_ncu_full.txt", "kernel": short}
+                        "l2_hit_pct": traffic_hit, "capture": f"profiles/{tag}_ncu_full.txt", "kernel": short}
     open(os.path.join(prof, f"{tag}_ncu_full.txt"), "w").write("\n".join(lines) + "\n")
     json.dump(traffic, open(traffic_path, "w"), indent=1)
     print(text)
