@@ -115,6 +115,16 @@ __global__ void __launch_bounds__(128) reduce_runs_kernel(
     }
 }
 
+// ray_index must be a permutation of 0..n-1 (it indexes the per-ray arrays
+// and orders the reduction): flag out-of-range or repeated entries.
+__global__ void check_perm_kernel(const int64_t* __restrict__ idx, int64_t n, unsigned* __restrict__ seen,
+                                  unsigned long long* __restrict__ bad) {
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int64_t r = idx[i];
+    if (r < 0 || r >= n || atomicExch(seen + r, 1u) != 0u) atomicAdd(bad, 1ull);
+}
+
 static int bits_for(int64_t v) {  // smallest k with v < 2^k (k >= 1)
     int k = 1;
     while (k < 62 && (int64_t(1) << k) <= v) ++k;
@@ -169,6 +179,17 @@ static int run_sorted(const TreeDev& T, int64_t capacity, const double* o, const
     ALLOC(basis, size_t(n) * B * sizeof(float));
     ALLOC(loss_ray, size_t(n) * sizeof(double));
     unsigned long long h_ctr[2] = {0, 0};
+    if (ray_id) {
+        unsigned* seen = nullptr;
+        ALLOC(seen, size_t(n) * sizeof(unsigned));
+        TRY(check_cuda(cudaMemsetAsync(seen, 0, size_t(n) * sizeof(unsigned), s), "memset"));
+        TRY(check_cuda(cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), s), "memset"));
+        check_perm_kernel<<<unsigned((n + 255) / 256), 256, 0, s>>>(ray_id, n, seen, ctr);
+        cudaFreeAsync(seen, s);
+        TRY(check_cuda(cudaMemcpyAsync(h_ctr, ctr, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s), "memcpy"));
+        TRY(check_cuda(cudaStreamSynchronize(s), "cudaStreamSynchronize"));
+        if (h_ctr[0] != 0) TRY(set_error(DOT_BAD_ARG, "ray_index is not a permutation of 0..n-1"));
+    }
     for (int attempt = 0; attempt < 3; ++attempt) {
         ALLOC(keys, size_t(cap) * sizeof(unsigned long long));
         ALLOC(rec, size_t(cap) * sizeof(float4));

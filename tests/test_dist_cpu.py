@@ -141,3 +141,13 @@ def test_two_rank_allreduce_equals_full_batch(tmp_path, oracle):
     np.testing.assert_array_equal(np.nonzero(got["touched"])[0], g.touched)
     np.testing.assert_allclose(got["signal"], sig, rtol=1e-12, atol=1e-15)
     assert float(got["loss"][0]) == pytest.approx(loss, rel=1e-12)
+
+
+def test_owned_rows_partition():
+    from paper_2307_15333_b200.parallel import owned_rows
+    for cap in (1, 63, 64, 1000, 123457):
+        for world in (1, 2, 3, 8):
+            parts = [owned_rows(cap, r, world) for r in range(world)]
+            assert parts[0][0] == 0 and parts[-1][1] == cap
+            for (a, b), (c, d) in zip(parts, parts[1:]):
+                assert b == c and a <= b

@@ -94,3 +94,26 @@ def test_accumulate_and_empty():
     np.testing.assert_allclose(sig, sig2, atol=1e-12, rtol=1e-12)
     loss, g, sig = render_and_backprop(tree, o[:0], d[:0], tg[:0], 0.5, deterministic=True)
     assert loss == 0.0 and not g.touched_mask.any()
+
+
+def test_sorted_rejects_bad_ray_index():
+    import ctypes
+    import torch
+    from helpers import irregular_tree, ray_batch
+    from paper_2307_15333_b200 import _lib
+    from paper_2307_15333_b200.errors import InputError
+    from paper_2307_15333_b200.render import BackpropWorkspace
+    tree = irregular_tree(9, 1, depth=2, device="cuda")
+    o, d = ray_batch(1, 100)
+    o, d = torch.from_numpy(o).cuda(), torch.from_numpy(d).cuda()
+    t = torch.zeros_like(o)
+    ws = BackpropWorkspace.for_tree(tree)
+    bad = torch.arange(100, device="cuda")
+    bad[7] = 3  # repeated index
+    view, _ = tree.tree_view()
+    bg = np.ones(3)
+    with pytest.raises(InputError):
+        _lib.call("dot_render_bwd_sorted", ctypes.byref(view), _lib.ptr(o), _lib.ptr(d), _lib.ptr(t),
+                  _lib.ptr(bad), 100, bg.ctypes.data_as(ctypes.c_void_p), 1e-4, 0.0, float("inf"), 0.02,
+                  _lib.ptr(ws.dsigma), _lib.ptr(ws.dsh_store), tree.sh_stride, _lib.ptr(ws.signal),
+                  _lib.ptr(ws.touched), _lib.ptr(ws.loss), _lib.stream_ptr())
