@@ -125,13 +125,18 @@ int dot_render_cameras(const dot_tree_view* tree, const double* cam_to_world, co
  *     the batch is origins/dirs/targets[ray_index[r]], read in place (a
  *     caller passes a coherence-sorted order, or a batch drawn from a larger
  *     resident ray pool, without gathering); rgb_out (f32, indexed like the
- *     arrays) may be NULL.  flags: bit 0 = skip post-cut touched marking
+ *     arrays) may be NULL.  warp_order (may be NULL): block b processes
+ *     batch rays [32 w, 32 w + 32) with w = warp_order[b], a permutation of
+ *     0..ceil(n/32)-1 (dot_sched_order); results do not depend on it.
+ *     ray_used (may be NULL) receives each batch ray's composited-segment
+ *     count (u16, saturating) for dot_sched_update.
+ *     flags: bit 0 = skip post-cut touched marking
  *     (not reference semantics); bit 15 = per-lane REDs instead of the
  *     warp-cooperative SH-row scatter; bits 13 / 14 = timing diagnostics
  *     (pass 1 only / no reductions: results are incomplete). */
 int dot_render_bwd(const dot_tree_view* tree, const double* origins, const double* dirs,
-                   const double* targets, const int64_t* ray_index, int64_t n_rays,
-                   const double* background,
+                   const double* targets, const int64_t* ray_index, const int32_t* warp_order,
+                   uint16_t* ray_used, int64_t n_rays, const double* background,
                    double early_stop_eps, double t_near, double t_far, double grad_scale,
                    float* grad_sigma, float* grad_sh, int32_t gsh_stride, double* signal,
                    uint8_t* touched, double* loss_sum, float* rgb_out, int32_t flags,
@@ -154,6 +159,19 @@ int dot_render_bwd_sorted(const dot_tree_view* tree, const double* origins, cons
                           double t_far, double grad_scale, float* grad_sigma, float* grad_sh,
                           int32_t gsh_stride, double* signal, uint8_t* touched, double* loss_sum,
                           void* stream);
+
+/* --- warp scheduling from a learned cost table (no reference
+ *     counterpart): table is u16 [2^24], indexed by the top 24 bits of the
+ *     31-bit coherence key (dot_ray_keys32) of a warp's first ray, holding an
+ *     average of the per-warp max composited-segment count seen there.
+ *     dot_sched_order writes warp_order[ceil(n/32)]: chunks of consecutive
+ *     warps of the key-sorted batch (16 warps, doubled until at most 2048
+ *     chunks), costliest predicted chunk first; dot_sched_update folds a
+ *     finished batch's ray_used into the table.  Order only: results are identical for any order. */
+int dot_sched_order(const int32_t* sorted_keys, int64_t n_rays, const uint16_t* table, int32_t* warp_order,
+                    void* stream);
+int dot_sched_update(const int32_t* sorted_keys, const uint16_t* ray_used, int64_t n_rays, uint16_t* table,
+                     void* stream);
 
 /* --- coherence keys (no reference counterpart): keys[i] = (origin Morton
  *     << 32) | octahedral-direction Morton; sorting a batch by them puts rays

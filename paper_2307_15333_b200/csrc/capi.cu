@@ -65,7 +65,7 @@ using namespace dot;
 
 extern "C" {
 
-int dot_abi_version(void) { return 5; }
+int dot_abi_version(void) { return 6; }
 
 const char* dot_last_error(void) { return g_err; }
 
@@ -87,6 +87,18 @@ void dot_exp_ref_host(const double* x, double* y, int64_t n) {
 int dot_exp_ref_device(const double* x, double* y, int64_t n, void* stream) {
     if (n < 0 || (n && (!x || !y))) return set_error(DOT_BAD_ARG, "bad arrays");
     return launch_exp_ref(x, y, n, static_cast<cudaStream_t>(stream));
+}
+
+int dot_sched_order(const int32_t* sorted_keys, int64_t n_rays, const uint16_t* table, int32_t* warp_order,
+                    void* stream) {
+    if (n_rays < 0 || (n_rays && (!sorted_keys || !table || !warp_order))) return set_error(DOT_BAD_ARG, "bad arrays");
+    return launch_sched_order(sorted_keys, n_rays, table, warp_order, static_cast<cudaStream_t>(stream));
+}
+
+int dot_sched_update(const int32_t* sorted_keys, const uint16_t* ray_used, int64_t n_rays, uint16_t* table,
+                     void* stream) {
+    if (n_rays < 0 || (n_rays && (!sorted_keys || !ray_used || !table))) return set_error(DOT_BAD_ARG, "bad arrays");
+    return launch_sched_update(sorted_keys, ray_used, n_rays, table, static_cast<cudaStream_t>(stream));
 }
 
 int dot_locate_supported(const dot_tree_view* tree) {
@@ -137,8 +149,8 @@ int dot_render_fwd(const dot_tree_view* tree, const double* origins, const doubl
 }
 
 int dot_render_bwd(const dot_tree_view* tree, const double* origins, const double* dirs,
-                   const double* targets, const int64_t* ray_index, int64_t n_rays,
-                   const double* background,
+                   const double* targets, const int64_t* ray_index, const int32_t* warp_order,
+                   uint16_t* ray_used, int64_t n_rays, const double* background,
                    double early_stop_eps, double t_near, double t_far, double grad_scale,
                    float* grad_sigma, float* grad_sh, int32_t gsh_stride, double* signal,
                    uint8_t* touched, double* loss_sum, float* rgb_out, int32_t flags,
@@ -152,7 +164,8 @@ int dot_render_bwd(const dot_tree_view* tree, const double* origins, const doubl
         return set_error(DOT_BAD_ARG, "gsh_stride must equal sh_stride (%d)", tree->sh_stride);
     if ((reinterpret_cast<uintptr_t>(grad_sh) & 15) != 0)
         return set_error(DOT_BAD_ARG, "grad_sh must be 16-byte aligned");
-    return launch_render_bwd(make_tree(*tree), origins, dirs, targets, ray_index, n_rays, background,
+    return launch_render_bwd(make_tree(*tree), origins, dirs, targets, ray_index, warp_order, ray_used, n_rays,
+                             background,
                              early_stop_eps, t_near, t_far, grad_scale, grad_sigma, grad_sh,
                              signal, touched, loss_sum, rgb_out, flags,
                              static_cast<cudaStream_t>(stream));

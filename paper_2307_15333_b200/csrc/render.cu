@@ -284,11 +284,15 @@ __global__ void __launch_bounds__(32, 32) render_bwd_buffered_kernel(
     TreeDev T, const double* __restrict__ o, const double* __restrict__ d,
     const double* __restrict__ tgt, const int64_t* __restrict__ ray_idx, int64_t n, double bg0,
     double bg1, double bg2, double eps, double t_near, double t_far, double grad_scale,
-    uint8_t* __restrict__ touched, float* __restrict__ rgb_out, int flags, Sink sink) {
+    uint8_t* __restrict__ touched, float* __restrict__ rgb_out, int flags, Sink sink,
+    const int32_t* __restrict__ warp_order, uint16_t* __restrict__ ray_used) {
     constexpr int S = pad4(3 * B);
     constexpr int K = kBwdRecords;
     double loss = 0.0;
-    const int64_t slot = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    // warp_order: launch order of the 32-ray warps (costliest first, from the
+    // learned cost table -- see sched_order_kernel); slot = batch position
+    const int64_t wb = warp_order ? int64_t(__ldg(warp_order + blockIdx.x)) : int64_t(blockIdx.x);
+    const int64_t slot = wb * 32 + threadIdx.x;
     const bool valid = slot < n;
     const int64_t r = valid ? ray_index(ray_idx, slot) : 0;
     Tracer tr;
@@ -360,6 +364,7 @@ __global__ void __launch_bounds__(32, 32) render_bwd_buffered_kernel(
         g0 = grad_scale * r0;
         g1 = grad_scale * r1;
         g2 = grad_scale * r2;
+        if (ray_used) ray_used[slot] = uint16_t(used < 65535 ? used : 65535);
         if (flags & 8192) used = 0;
     }
     __syncwarp();
@@ -433,9 +438,10 @@ __global__ void __launch_bounds__(32, 32) render_bwd_buffered_kernel(
 }
 
 int launch_render_bwd(const TreeDev& T, const double* o, const double* d, const double* tgt,
-                      const int64_t* ray_idx, int64_t n, const double* bg, double eps, double tn,
-                      double tf, double gs, float* gsig, float* gsh, double* signal,
-                      uint8_t* touched, double* loss, float* rgb_out, int flags, cudaStream_t s) {
+                      const int64_t* ray_idx, const int32_t* warp_order, uint16_t* ray_used, int64_t n,
+                      const double* bg, double eps, double tn, double tf, double gs, float* gsig,
+                      float* gsh, double* signal, uint8_t* touched, double* loss, float* rgb_out,
+                      int flags, cudaStream_t s) {
     if (n == 0) return DOT_OK;
     const unsigned grid = unsigned((n + 31) / 32);
     // default: warp-cooperative SH scatter; flag bit 15: per-lane REDs
@@ -448,10 +454,12 @@ int launch_render_bwd(const TreeDev& T, const double* o, const double* d, const 
 #define DOT_BWD(BB)                                                                                  \
     if (coop)                                                                                        \
         render_bwd_buffered_kernel<BB, CoopSink><<<grid, 32, 0, s>>>(                                \
-            T, o, d, tgt, ray_idx, n, bg[0], bg[1], bg[2], eps, tn, tf, gs, touched, rgb_out, flags, cs); \
+            T, o, d, tgt, ray_idx, n, bg[0], bg[1], bg[2], eps, tn, tf, gs, touched, rgb_out, flags, cs, \
+            warp_order, ray_used);                                                                   \
     else                                                                                             \
         render_bwd_buffered_kernel<BB, AtomicSink><<<grid, 32, 0, s>>>(                              \
-            T, o, d, tgt, ray_idx, n, bg[0], bg[1], bg[2], eps, tn, tf, gs, touched, rgb_out, flags, as);
+            T, o, d, tgt, ray_idx, n, bg[0], bg[1], bg[2], eps, tn, tf, gs, touched, rgb_out, flags, as, \
+            warp_order, ray_used);
     DOT_DISPATCH_B(DOT_BWD)
 #undef DOT_BWD
     return check_launch("render_bwd_buffered_kernel");
@@ -517,7 +525,8 @@ int launch_render_bwd_emit(const TreeDev& T, const double* o, const double* d, c
     sink.orig = 0;
 #define DOT_EMIT(BB)                                                                                 \
     render_bwd_buffered_kernel<BB, EmitSink><<<unsigned((n + 31) / 32), 32, 0, s>>>(                 \
-        T, o, d, tgt, ray_idx, n, bg[0], bg[1], bg[2], eps, tn, tf, gs, touched, nullptr, 0, sink);
+        T, o, d, tgt, ray_idx, n, bg[0], bg[1], bg[2], eps, tn, tf, gs, touched, nullptr, 0, sink,   \
+        nullptr, nullptr);
     DOT_DISPATCH_B(DOT_EMIT)
 #undef DOT_EMIT
     return check_launch("render_bwd_buffered_kernel<emit>");
@@ -816,6 +825,100 @@ int launch_ray_stats(const TreeDev& T, const double* o, const double* d, int64_t
     if (n == 0) return DOT_OK;
     ray_stats_kernel<<<unsigned((n + kBlock - 1) / kBlock), kBlock, 0, s>>>(T, o, d, n, eps, out);
     return check_launch("ray_stats_kernel");
+}
+
+// ---------------------------------------------------------------------------
+// Warp scheduling from a learned cost table.  A backward warp's duration is
+// set by its rays' composited-segment counts (ncu/globaltimer: correlation
+// 0.95), and neighbouring rays in coherence-key order cost alike: the count
+// of the warp that started at key bucket k (top 24 bits of the 31-bit key:
+// origin cell + a ~12x12-pixel direction cell) predicts the next batch's
+// warps in that bucket with Spearman 0.93.  sched_update keeps a decaying
+// max of the per-warp max count per bucket (u16, 2^24 entries); sched_order ranks
+// chunks of 64 consecutive warps (coherence kept inside a chunk) by their
+// costliest predicted warp, descending, so the long rays start first
+// instead of forming the wave tail.  Results never depend on the order.
+
+constexpr int kSchedBits = 24;
+constexpr int kSchedSort = 2048;    // chunks ranked per launch (one block, bitonic in shared memory)
+constexpr int kSchedMinChunk = 16;  // warps per chunk (coherence kept inside a chunk)
+
+__device__ __forceinline__ uint32_t sched_bucket(int32_t key) {
+    return uint32_t(key) >> (31 - kSchedBits);
+}
+
+__global__ void __launch_bounds__(256) sched_update_kernel(const int32_t* __restrict__ keys,
+                                                           const uint16_t* __restrict__ ray_used, int64_t n,
+                                                           uint16_t* __restrict__ table) {
+    const int64_t w = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    const int64_t r = w * 32 + lane;
+    unsigned u = r < n ? ray_used[r] : 0u;
+    u = __reduce_max_sync(0xffffffffu, u);
+    if (lane == 0 && w * 32 < n) {
+        uint16_t* t = table + sched_bucket(keys[w * 32]);
+        // decaying max: a bucket keeps its costliest recent warp (several
+        // consecutive warps can share a bucket; the chunk cost is their max)
+        const unsigned old = *t;
+        *t = uint16_t(max(u, (old * 7u) >> 3));
+    }
+}
+
+__global__ void __launch_bounds__(1024) sched_order_kernel(const int32_t* __restrict__ keys, int64_t n, int chunk,
+                                                           const uint16_t* __restrict__ table,
+                                                           int32_t* __restrict__ warp_order) {
+    __shared__ unsigned long long s[kSchedSort];
+    const int64_t nw = (n + 31) / 32;
+    const int nc = int((nw + chunk - 1) / chunk);  // <= kSchedSort (host checks)
+    for (int c = threadIdx.x; c < kSchedSort; c += blockDim.x) {
+        unsigned cost = 0;
+        // a partial last chunk keeps cost 0 and the largest id: it sorts
+        // last, so every other position maps to a full chunk
+        const bool partial_last = c == nc - 1 && nw % chunk != 0;
+        if (c < nc && !partial_last) {
+            const int64_t w1 = min(nw, int64_t(c + 1) * chunk);
+            for (int64_t w = int64_t(c) * chunk; w < w1; ++w)
+                cost = max(cost, unsigned(table[sched_bucket(keys[w * 32])]));
+        }
+        // ascending sort of (~cost, chunk): costliest first, ties by chunk
+        s[c] = c < nc ? ((unsigned long long)(0xFFFFu - cost) << 32) | unsigned(c) : ~0ull;
+    }
+    __syncthreads();
+    for (int k = 2; k <= kSchedSort; k <<= 1) {
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int t = threadIdx.x; t < kSchedSort / 2; t += blockDim.x) {
+                const int i = (t / j) * 2 * j + (t % j), p = i + j;
+                const bool up = (i & k) == 0;
+                const unsigned long long a = s[i], b = s[p];
+                if ((a > b) == up) {
+                    s[i] = b;
+                    s[p] = a;
+                }
+            }
+            __syncthreads();
+        }
+    }
+    for (int64_t i = threadIdx.x; i < nw; i += blockDim.x) {
+        const int64_t q = i / chunk, off = i - q * chunk;
+        warp_order[i] = int32_t(int64_t(unsigned(s[q] & 0xFFFFFFFFu)) * chunk + off);
+    }
+}
+
+int launch_sched_order(const int32_t* keys, int64_t n, const uint16_t* table, int32_t* warp_order, cudaStream_t s) {
+    const int64_t nw = (n + 31) / 32;
+    if (nw == 0) return DOT_OK;
+    int64_t chunk = kSchedMinChunk;
+    while ((nw + chunk - 1) / chunk > kSchedSort) chunk *= 2;
+    if (chunk > (1 << 20)) return set_error(DOT_BAD_ARG, "batch too large to schedule");
+    sched_order_kernel<<<1, 1024, 0, s>>>(keys, n, int(chunk), table, warp_order);
+    return check_launch("sched_order_kernel");
+}
+
+int launch_sched_update(const int32_t* keys, const uint16_t* ray_used, int64_t n, uint16_t* table, cudaStream_t s) {
+    if (n == 0) return DOT_OK;
+    const int64_t threads = ((n + 31) / 32) * 32;
+    sched_update_kernel<<<unsigned((threads + 255) / 256), 256, 0, s>>>(keys, ray_used, n, table);
+    return check_launch("sched_update_kernel");
 }
 
 // ---------------------------------------------------------------------------

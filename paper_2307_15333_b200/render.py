@@ -19,6 +19,7 @@ and gradients, float64 signal); host torch tensors are copied with
 from __future__ import annotations
 
 import math
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -31,6 +32,18 @@ from .octree import SparseOctree
 EPS_T = 1e-4  # early-termination transmittance threshold (render.py:23)
 UNIT_TOL = 1e-6
 COHERENT_MIN_RAYS = 1 << 14  # below this a key sort costs more than it saves
+WARP_SCHED = os.environ.get("DOT_WARP_SCHED", "1") == "1"
+SCHED_MAX_RAYS = 1 << 30
+
+
+def _sched_table(tree) -> torch.Tensor:
+    """Learned per-key-bucket warp cost table of this tree object (u16,
+    2^24 entries, survives refines: it only orders launches)."""
+    t = getattr(tree, "_sched_table", None)
+    if t is None or t.device != tree.device:
+        t = torch.zeros(1 << 24, dtype=torch.int16, device=tree.device)
+        tree._sched_table = t
+    return t
 
 
 @dataclass
@@ -305,6 +318,7 @@ def render_and_backprop(tree: SparseOctree, origins, dirs, targets, background,
     if return_rgb and idx is not None:
         raise InputError("return_rgb is not available with ray_index")
     rgb = torch.empty(n, 3, dtype=torch.float32, device=tree.device) if return_rgb else None
+    warp_order = ray_used = None
     if n:
         gs = 2.0 / n if grad_scale is None else float(grad_scale)
         bg = _background(background)
@@ -315,8 +329,15 @@ def render_and_backprop(tree: SparseOctree, origins, dirs, targets, background,
             keys = torch.empty(n, dtype=torch.int32, device=tree.device)
             _lib.call("dot_ray_keys32", _lib.ctypes.byref(view), _lib.ptr(o), _lib.ptr(d),
                       _lib.ptr(idx), n, _lib.ptr(keys), _lib.stream_ptr())
-            perm = torch.argsort(keys)
+            sorted_keys, perm = torch.sort(keys)
             idx = perm if idx is None else idx[perm]
+            if WARP_SCHED and not deterministic and n <= SCHED_MAX_RAYS:
+                # launch the warps whose key buckets were costliest last time first
+                table = _sched_table(tree)
+                warp_order = torch.empty((n + 31) // 32, dtype=torch.int32, device=tree.device)
+                _lib.call("dot_sched_order", _lib.ptr(sorted_keys), n, _lib.ptr(table),
+                          _lib.ptr(warp_order), _lib.stream_ptr())
+                ray_used = torch.empty(n, dtype=torch.int16, device=tree.device)
         if kernel_events is not None:
             kernel_events[0].record()
         if deterministic:
@@ -329,10 +350,13 @@ def render_and_backprop(tree: SparseOctree, origins, dirs, targets, background,
                       _lib.stream_ptr())
         else:
             _lib.call("dot_render_bwd", _lib.ctypes.byref(view), _lib.ptr(o), _lib.ptr(d), _lib.ptr(t),
-                      _lib.ptr(idx), n, _bg_ptr(bg), float(early_stop_eps), float(t_near),
-                      float(t_far), gs, _lib.ptr(ws.dsigma), _lib.ptr(ws.dsh_store),
-                      tree.sh_stride, _lib.ptr(ws.signal), _lib.ptr(ws.touched),
+                      _lib.ptr(idx), _lib.ptr(warp_order), _lib.ptr(ray_used), n, _bg_ptr(bg),
+                      float(early_stop_eps), float(t_near), float(t_far), gs, _lib.ptr(ws.dsigma),
+                      _lib.ptr(ws.dsh_store), tree.sh_stride, _lib.ptr(ws.signal), _lib.ptr(ws.touched),
                       _lib.ptr(ws.loss), _lib.ptr(rgb), int(kernel_flags), _lib.stream_ptr())
+            if ray_used is not None:
+                _lib.call("dot_sched_update", _lib.ptr(sorted_keys), _lib.ptr(ray_used), n,
+                          _lib.ptr(_sched_table(tree)), _lib.stream_ptr())
         if kernel_events is not None:
             kernel_events[1].record()
     nsh = 3 * tree.basis_count
