@@ -281,13 +281,23 @@ def run_ours(args, rank, world, local_rank):
         from paper_2307_15333_b200.parallel import PeerExchange
         exchange = PeerExchange(tree, state, sws)
 
+    from paper_2307_15333_b200.render import plan_batch
+    plan_stream = torch.cuda.Stream(dev)
+    plans = {}
+
     def step(k, timed_kernel=True):
-        # the batch is read in place from the resident pool (ray_index): no gather
+        # the batch is read in place from the resident pool (ray_index): no
+        # gather; its coherence order was sorted on a side stream during the
+        # previous step (plan_batch), and the next one is queued now
+        idx = batch_index(k)
+        plan = plans.pop(k, None)
+        if k + 1 < total_steps + 2:
+            plans[k + 1] = plan_batch(tree, origins, dirs, batch_index(k + 1), stream=plan_stream)
         return train_step(tree, origins, dirs, targets, state, buf, sws, BG, EPS,
-                          ray_index=batch_index(k), grad_scale=gs,
+                          ray_index=idx, grad_scale=gs,
                           exchange=exchange if world > 1 else None,
                           kernel_events=kev[k] if timed_kernel else None,
-                          kernel_flags=args.bwd_flags)
+                          kernel_flags=args.bwd_flags, plan=plan)
 
     for k in range(args.warmup):
         step(k)
@@ -358,17 +368,17 @@ def run_ours(args, rank, world, local_rank):
                               exchange=ex)
             float(loss.item())
 
-    stager = RayBatchStager(dev, max_rays=per_rank)
+    stager = RayBatchStager(dev, max_rays=per_rank, plan_tree=tree)
 
     def staged_loop(steps):
         reader = LossReader()
         stager.stage(*host[0])
         for k in range(steps):
-            o_d, d_d, t_d = stager.take()
+            o_d, d_d, t_d, plan = stager.take_with_plan()
             if k + 1 < steps:
                 stager.stage(*host[(k + 1) % 2])
             loss = train_step(tree, o_d, d_d, t_d, state, buf, sws, BG, EPS, grad_scale=gs,
-                              exchange=ex)
+                              exchange=ex, plan=plan)
             stager.release()
             reader.push(loss)
         reader.flush()
@@ -442,7 +452,7 @@ def run_ours(args, rank, world, local_rank):
         },
         "e2e": {"value": e2e_value, "unit": "rays/s", "h2d_bytes_per_step": per_rank * 72,
                 "d2h_bytes_per_step": 8, "ms_per_step": e2e_ms / args.steps,
-                "api": "RayBatchStager (H2D of step k+1 overlaps step k) + optim.train_step "
+                "api": "RayBatchStager (H2D + coherence sort of step k+1 overlap step k) + optim.train_step "
                        "(render_and_backprop + rmsprop_step) + LossReader (loss read one step late)",
                 "serial_ms_per_step": e2e_serial_ms / args.steps},
         "clocks": clk,

@@ -267,12 +267,59 @@ class BackpropWorkspace:
             t.zero_()
 
 
+@dataclass
+class RayPlan:
+    """A batch's coherence order: the kernel's ray index (the caller's
+    ray_index composed with the key sort) and the sorted 31-bit keys (which
+    also index the warp-schedule table)."""
+
+    n: int
+    idx: torch.Tensor
+    sorted_keys: torch.Tensor
+    event: "torch.cuda.Event | None" = None
+
+    def wait(self, stream=None) -> None:
+        if self.event is not None:
+            (stream or torch.cuda.current_stream()).wait_event(self.event)
+
+
+def plan_batch(tree: SparseOctree, origins: torch.Tensor, dirs: torch.Tensor, ray_index=None,
+               stream=None, wait_current: bool = True) -> RayPlan:
+    """Coherence order of a batch (origin / octahedral-direction Morton keys,
+    dot_ray_keys32 + a radix sort).  Depends only on the rays, so it can run
+    on a side stream (``stream``) ahead of the step that consumes it; the
+    returned plan carries an event the consumer waits on.  ``wait_current``
+    orders the side stream after the work queued so far on the current stream
+    (off when the rays were produced on ``stream`` itself)."""
+    idx = None if ray_index is None else torch.as_tensor(ray_index, device=tree.device).reshape(-1).to(torch.int64)
+    n = int(idx.shape[0]) if idx is not None else int(origins.shape[0])
+    view, _topo = tree.tree_view()
+    cur = torch.cuda.current_stream(tree.device)
+    s = stream or cur
+    if s is not cur and wait_current:
+        s.wait_stream(cur)  # inputs produced on the current stream
+    with torch.cuda.stream(s):
+        keys = torch.empty(n, dtype=torch.int32, device=tree.device)
+        _lib.call("dot_ray_keys32", _lib.ctypes.byref(view), _lib.ptr(origins), _lib.ptr(dirs),
+                  _lib.ptr(idx), n, _lib.ptr(keys), _lib.stream_ptr(s))
+        sorted_keys, perm = torch.sort(keys)
+        idx = perm if idx is None else idx[perm]
+        ev = None
+        if s is not cur:
+            ev = torch.cuda.Event()
+            ev.record(s)
+            for t in (idx, sorted_keys):
+                t.record_stream(cur)
+    return RayPlan(n, idx, sorted_keys, ev)
+
+
 def render_and_backprop(tree: SparseOctree, origins, dirs, targets, background,
                         early_stop_eps: float = EPS_T, t_near: float = 0.0,
                         t_far: float = math.inf, grad_scale: float | None = None,
                         workspace: BackpropWorkspace | None = None, accumulate: bool = False,
                         return_rgb: bool = False, kernel_events=None, kernel_flags: int = 0,
-                        coherent: bool = True, deterministic: bool = False, ray_index=None):
+                        coherent: bool = True, deterministic: bool = False, ray_index=None,
+                        plan: "RayPlan | None" = None):
     """Batch MSE loss, analytic leaf gradients and per-leaf signal (render.py:175-225).
 
     Returns (loss, GradBuffer, signal).  ``grad_scale`` defaults to the
@@ -286,6 +333,9 @@ def render_and_backprop(tree: SparseOctree, origins, dirs, targets, background,
     resident ray pool -- read in place by the kernel instead of gathered.
     ``coherent`` reorders the batch internally (origin / direction Morton
     keys) so each warp walks neighbouring cells; results are sums over rays.
+
+    ``plan`` (``plan_batch``, optional): the batch's coherence order computed
+    ahead of time -- e.g. on a side stream while the previous step runs.
 
     ``deterministic=True`` reduces every leaf's contributions in the
     reference's order (scatter_kernel: rays in batch order, f64 sums) via
@@ -318,19 +368,20 @@ def render_and_backprop(tree: SparseOctree, origins, dirs, targets, background,
     if return_rgb and idx is not None:
         raise InputError("return_rgb is not available with ray_index")
     rgb = torch.empty(n, 3, dtype=torch.float32, device=tree.device) if return_rgb else None
-    warp_order = ray_used = None
+    warp_order = ray_used = sorted_keys = None
     if n:
         gs = 2.0 / n if grad_scale is None else float(grad_scale)
         bg = _background(background)
         view, _topo = tree.tree_view()
-        if coherent and n >= COHERENT_MIN_RAYS:
-            # visit the batch in coherence order: sort 31-bit (origin, direction)
-            # Morton keys and hand the kernel the permuted index (no gathers)
-            keys = torch.empty(n, dtype=torch.int32, device=tree.device)
-            _lib.call("dot_ray_keys32", _lib.ctypes.byref(view), _lib.ptr(o), _lib.ptr(d),
-                      _lib.ptr(idx), n, _lib.ptr(keys), _lib.stream_ptr())
-            sorted_keys, perm = torch.sort(keys)
-            idx = perm if idx is None else idx[perm]
+        if plan is not None:
+            if plan.n != n:
+                raise InputError(f"ray plan is for {plan.n} rays, batch has {n}")
+            plan.wait()
+            idx, sorted_keys = plan.idx, plan.sorted_keys
+        elif coherent and n >= COHERENT_MIN_RAYS:
+            p = plan_batch(tree, o, d, idx)
+            idx, sorted_keys = p.idx, p.sorted_keys
+        if sorted_keys is not None:
             if WARP_SCHED and not deterministic and n <= SCHED_MAX_RAYS:
                 # launch the warps whose key buckets were costliest last time first
                 table = _sched_table(tree)

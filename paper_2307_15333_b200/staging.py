@@ -35,10 +35,11 @@ from .errors import InputError
 
 
 class _Slot:
-    __slots__ = ("bufs", "n", "ready", "free", "busy")
+    __slots__ = ("bufs", "n", "ready", "free", "busy", "plan")
 
     def __init__(self):
         self.bufs = None
+        self.plan = None
         self.n = 0
         self.ready = torch.cuda.Event()
         self.free = None
@@ -48,10 +49,14 @@ class _Slot:
 class RayBatchStager:
     """Double-buffered (``depth`` slots) host->HBM staging of ray batches."""
 
-    def __init__(self, device, max_rays: int = 0, depth: int = 2):
+    def __init__(self, device, max_rays: int = 0, depth: int = 2, plan_tree=None):
+        """``plan_tree``: also compute each staged batch's coherence order
+        (render.plan_batch) on the copy stream right after its copy, so the
+        step that takes it skips the key sort (``take_with_plan``)."""
         if depth < 2:
             raise InputError("depth must be >= 2 for copy/compute overlap")
         self.device = torch.device(device)
+        self.plan_tree = plan_tree
         self.copy_stream = torch.cuda.Stream(self.device)
         self.slots = [_Slot() for _ in range(depth)]
         self.pending: deque[int] = deque()
@@ -95,6 +100,11 @@ class RayBatchStager:
                 self.copy_stream.wait_event(slot.free)  # the last step reading this slot is done
             for dst, src in zip(slot.bufs, (o, d, t)):
                 dst[:n].copy_(src, non_blocking=True)
+            slot.plan = None
+            if self.plan_tree is not None:
+                from .render import plan_batch
+                slot.plan = plan_batch(self.plan_tree, slot.bufs[0][:n], slot.bufs[1][:n],
+                                       stream=self.copy_stream, wait_current=False)
             slot.ready.record(self.copy_stream)
         slot.n = n
         slot.busy = True
@@ -112,6 +122,12 @@ class RayBatchStager:
         torch.cuda.current_stream(self.device).wait_event(slot.ready)
         self.in_use.append(i)
         return tuple(b[:slot.n] for b in slot.bufs)
+
+    def take_with_plan(self):
+        """``take()`` plus the batch's coherence plan (None without plan_tree)."""
+        i = self.pending[0] if self.pending else None
+        out = self.take()
+        return out + (self.slots[i].plan,)
 
     def release(self) -> None:
         """Mark the oldest taken batch consumed by the work queued so far."""

@@ -89,3 +89,29 @@ def test_stager_rejects_misuse():
         RayBatchStager("cuda").stage(b[0][0], b[0][1], b[0][2][:10])
     with pytest.raises(InputError):
         RayBatchStager("cuda", depth=1)
+
+
+def test_stager_plans_match_in_stream_plans():
+    """RayBatchStager(plan_tree=...) sorts each staged batch on the copy
+    stream; the plan equals plan_batch on the same rays and the step it
+    drives equals the step that sorts internally."""
+    import numpy as np
+    import torch
+    from helpers import irregular_tree, ray_batch
+    from paper_2307_15333_b200.render import BackpropWorkspace, plan_batch, render_and_backprop
+    from paper_2307_15333_b200.staging import RayBatchStager
+    tree = irregular_tree(41, 4, depth=3, splits=30, max_depth=6, device="cuda")
+    o, d = ray_batch(42, 40000)
+    t = np.random.default_rng(43).uniform(0, 1, o.shape)
+    st = RayBatchStager("cuda", max_rays=40000, plan_tree=tree)
+    st.stage(torch.from_numpy(o), torch.from_numpy(d), torch.from_numpy(t))
+    od, dd, td, plan = st.take_with_plan()
+    ref = plan_batch(tree, od, dd)
+    assert torch.equal(plan.idx, ref.idx) and torch.equal(plan.sorted_keys, ref.sorted_keys)
+    ws1, ws2 = BackpropWorkspace.for_tree(tree), BackpropWorkspace.for_tree(tree)
+    l1, g1, s1 = render_and_backprop(tree, od, dd, td, 0.5, workspace=ws1, plan=plan)
+    l2, g2, s2 = render_and_backprop(tree, od, dd, td, 0.5, workspace=ws2)
+    st.release()
+    assert float(l1) == pytest.approx(float(l2), rel=1e-12)  # f64 atomic order
+    torch.testing.assert_close(g1.dsh, g2.dsh, atol=1e-7, rtol=1e-5)
+    assert torch.equal(g1.touched_mask, g2.touched_mask)
