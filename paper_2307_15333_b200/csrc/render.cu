@@ -864,43 +864,70 @@ __global__ void __launch_bounds__(256) sched_update_kernel(const int32_t* __rest
     }
 }
 
-__global__ void __launch_bounds__(1024) sched_order_kernel(const int32_t* __restrict__ keys, int64_t n, int chunk,
-                                                           const uint16_t* __restrict__ table,
-                                                           int32_t* __restrict__ warp_order) {
-    __shared__ unsigned long long s[kSchedSort];
+// Predicted cost of every chunk (one thread per chunk, many blocks: the
+// table lookups are scattered).
+__global__ void __launch_bounds__(256) sched_cost_kernel(const int32_t* __restrict__ keys, int64_t n, int chunk,
+                                                         const uint16_t* __restrict__ table,
+                                                         unsigned* __restrict__ cost_out) {
+    const int c = int(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int64_t nw = (n + 31) / 32;
+    const int nc = int((nw + chunk - 1) / chunk);
+    if (c >= nc) return;
+    unsigned cost = 0;
+    // a partial last chunk keeps cost 0 and the largest id: it sorts last,
+    // so every other position maps to a full chunk
+    if (!(c == nc - 1 && nw % chunk != 0)) {
+        const int64_t w1 = min(nw, int64_t(c + 1) * chunk);
+        for (int64_t w = int64_t(c) * chunk; w < w1; ++w)
+            cost = max(cost, unsigned(__ldg(table + sched_bucket(__ldg(keys + w * 32)))));
+    }
+    cost_out[c] = cost;
+}
+
+// Chunks ordered by descending predicted cost with a counting sort over
+// the (capped) cost values -- the order within a cost value is whatever the
+// shared-memory atomics give: launch order only, results never depend on it.
+__global__ void __launch_bounds__(1024) sched_order_kernel(const unsigned* __restrict__ chunk_cost, int64_t n,
+                                                           int chunk, int32_t* __restrict__ warp_order) {
+    constexpr int kBins = 1024;
+    __shared__ int hist[kBins];
+    __shared__ int start[kBins];
+    __shared__ int sorted[kSchedSort];
     const int64_t nw = (n + 31) / 32;
     const int nc = int((nw + chunk - 1) / chunk);  // <= kSchedSort (host checks)
-    for (int c = threadIdx.x; c < kSchedSort; c += blockDim.x) {
-        unsigned cost = 0;
-        // a partial last chunk keeps cost 0 and the largest id: it sorts
-        // last, so every other position maps to a full chunk
-        const bool partial_last = c == nc - 1 && nw % chunk != 0;
-        if (c < nc && !partial_last) {
-            const int64_t w1 = min(nw, int64_t(c + 1) * chunk);
-            for (int64_t w = int64_t(c) * chunk; w < w1; ++w)
-                cost = max(cost, unsigned(table[sched_bucket(keys[w * 32])]));
-        }
-        // ascending sort of (~cost, chunk): costliest first, ties by chunk
-        s[c] = c < nc ? ((unsigned long long)(0xFFFFu - cost) << 32) | unsigned(c) : ~0ull;
+    const int t = threadIdx.x;
+    hist[t] = 0;
+    __syncthreads();
+    int bin[kSchedSort / 1024];
+#pragma unroll
+    for (int k = 0; k < kSchedSort / 1024; ++k) {
+        const int c = t + 1024 * k;
+        // descending cost; the partial last chunk (cost 0) must come last: bin kBins-1
+        bin[k] = c < nc ? (kBins - 1) - int(min(chunk_cost[c], unsigned(kBins - 2))) - (c == nc - 1 && nw % chunk ? 0 : 1) : -1;
+        if (c == nc - 1 && nw % chunk) bin[k] = kBins - 1;
+        if (bin[k] >= 0) atomicAdd(&hist[bin[k]], 1);
     }
     __syncthreads();
-    for (int k = 2; k <= kSchedSort; k <<= 1) {
-        for (int j = k >> 1; j > 0; j >>= 1) {
-            for (int t = threadIdx.x; t < kSchedSort / 2; t += blockDim.x) {
-                const int i = (t / j) * 2 * j + (t % j), p = i + j;
-                const bool up = (i & k) == 0;
-                const unsigned long long a = s[i], b = s[p];
-                if ((a > b) == up) {
-                    s[i] = b;
-                    s[p] = a;
-                }
-            }
-            __syncthreads();
-        }
+    // exclusive scan of hist (1024 bins, one per thread)
+    int v = hist[t];
+    for (int off = 1; off < kBins; off <<= 1) {
+        __syncthreads();
+        const int u = t >= off ? hist[t - off] : 0;
+        __syncthreads();
+        hist[t] += u;
     }
-    for (int64_t i = threadIdx.x; i < nw; i += blockDim.x) {
+    __syncthreads();
+    start[t] = hist[t] - v;
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < kSchedSort / 1024; ++k) {
+        const int c = t + 1024 * k;
+        if (bin[k] >= 0) sorted[atomicAdd(&start[bin[k]], 1)] = c;
+    }
+    __syncthreads();
+    for (int64_t i = t; i < nw; i += blockDim.x) {
         const int64_t q = i / chunk, off = i - q * chunk;
-        warp_order[i] = int32_t(int64_t(unsigned(s[q] & 0xFFFFFFFFu)) * chunk + off);
+        warp_order[i] = int32_t(int64_t(sorted[q]) * chunk + off);
     }
 }
 
@@ -910,7 +937,14 @@ int launch_sched_order(const int32_t* keys, int64_t n, const uint16_t* table, in
     int64_t chunk = kSchedMinChunk;
     while ((nw + chunk - 1) / chunk > kSchedSort) chunk *= 2;
     if (chunk > (1 << 20)) return set_error(DOT_BAD_ARG, "batch too large to schedule");
-    sched_order_kernel<<<1, 1024, 0, s>>>(keys, n, int(chunk), table, warp_order);
+    const int nc = int((nw + chunk - 1) / chunk);
+    retain_pool_memory();
+    unsigned* cost = nullptr;
+    if (int st = check_cuda(cudaMallocAsync(reinterpret_cast<void**>(&cost), sizeof(unsigned) * nc, s), "cudaMallocAsync"))
+        return st;
+    sched_cost_kernel<<<unsigned((nc + 255) / 256), 256, 0, s>>>(keys, n, int(chunk), table, cost);
+    sched_order_kernel<<<1, 1024, 0, s>>>(cost, n, int(chunk), warp_order);
+    cudaFreeAsync(cost, s);
     return check_launch("sched_order_kernel");
 }
 
