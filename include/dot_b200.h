@@ -161,9 +161,11 @@ int dot_render_bwd_sorted(const dot_tree_view* tree, const double* origins, cons
                           void* stream);
 
 /* --- warp scheduling from a learned cost table (no reference
- *     counterpart): table is u16 [2^24], indexed by the top 24 bits of the
- *     31-bit coherence key (dot_ray_keys32) of a warp's first ray, holding an
- *     average of the per-warp max composited-segment count seen there.
+ *     counterpart): table is u16 [2^24 + 2^27]: a coarse part indexed by the
+ *     top 24 bits and a fine part by the top 27 bits of the 31-bit coherence
+ *     key (dot_ray_keys32) of a warp's first ray, each holding a decaying
+ *     max of the per-warp max composited-segment count seen there (the fine
+ *     entry is used when populated).
  *     dot_sched_order writes warp_order[ceil(n/32)]: chunks of consecutive
  *     warps of the key-sorted batch (16 warps, doubled until at most 2048
  *     chunks), costliest predicted chunk first; dot_sched_update folds a

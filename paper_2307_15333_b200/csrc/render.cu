@@ -843,8 +843,18 @@ constexpr int kSchedBits = 24;
 constexpr int kSchedSort = 2048;    // chunks ranked per launch (one block, bitonic in shared memory)
 constexpr int kSchedMinChunk = 16;  // warps per chunk (coherence kept inside a chunk)
 
+constexpr int kSchedFineBits = 27;  // second, finer table (fallback to the coarse one when empty)
+
 __device__ __forceinline__ uint32_t sched_bucket(int32_t key) {
     return uint32_t(key) >> (31 - kSchedBits);
+}
+__device__ __forceinline__ uint32_t sched_fine(int32_t key) {
+    return uint32_t(key) >> (31 - kSchedFineBits);
+}
+// table layout: [2^kSchedBits coarse | 2^kSchedFineBits fine] u16
+__device__ __forceinline__ unsigned sched_lookup(const uint16_t* __restrict__ table, int32_t key) {
+    const unsigned f = __ldg(table + (1u << kSchedBits) + sched_fine(key));
+    return f ? f : unsigned(__ldg(table + sched_bucket(key)));
 }
 
 __global__ void __launch_bounds__(256) sched_update_kernel(const int32_t* __restrict__ keys,
@@ -856,10 +866,14 @@ __global__ void __launch_bounds__(256) sched_update_kernel(const int32_t* __rest
     unsigned u = r < n ? ray_used[r] : 0u;
     u = __reduce_max_sync(0xffffffffu, u);
     if (lane == 0 && w * 32 < n) {
-        uint16_t* t = table + sched_bucket(keys[w * 32]);
+        const int32_t k = keys[w * 32];
         // decaying max: a bucket keeps its costliest recent warp (several
         // consecutive warps can share a bucket; the chunk cost is their max)
-        const unsigned old = *t;
+        uint16_t* t = table + sched_bucket(k);
+        unsigned old = *t;
+        *t = uint16_t(max(u, (old * 7u) >> 3));
+        t = table + (1u << kSchedBits) + sched_fine(k);
+        old = *t;
         *t = uint16_t(max(u, (old * 7u) >> 3));
     }
 }
@@ -879,7 +893,7 @@ __global__ void __launch_bounds__(256) sched_cost_kernel(const int32_t* __restri
     if (!(c == nc - 1 && nw % chunk != 0)) {
         const int64_t w1 = min(nw, int64_t(c + 1) * chunk);
         for (int64_t w = int64_t(c) * chunk; w < w1; ++w)
-            cost = max(cost, unsigned(__ldg(table + sched_bucket(__ldg(keys + w * 32)))));
+            cost = max(cost, sched_lookup(table, __ldg(keys + w * 32)));
     }
     cost_out[c] = cost;
 }

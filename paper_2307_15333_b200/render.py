@@ -38,10 +38,11 @@ SCHED_MAX_RAYS = 1 << 30
 
 def _sched_table(tree) -> torch.Tensor:
     """Learned per-key-bucket warp cost table of this tree object (u16,
-    2^24 entries, survives refines: it only orders launches)."""
+    2^24 coarse + 2^27 fine entries = 288 MB, survives refines: it only
+    orders launches)."""
     t = getattr(tree, "_sched_table", None)
     if t is None or t.device != tree.device:
-        t = torch.zeros(1 << 24, dtype=torch.int16, device=tree.device)
+        t = torch.zeros((1 << 24) + (1 << 27), dtype=torch.int16, device=tree.device)
         tree._sched_table = t
     return t
 
