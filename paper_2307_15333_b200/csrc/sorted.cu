@@ -10,9 +10,10 @@
 //      segment, keyed (pool id << ray_bits | original ray index);
 //   2. a CUB radix sort over the key bits orders the records by leaf, and
 //      within a leaf by original ray index -- exactly scatter_kernel's order;
-//   3. reduce_runs_kernel sums each leaf's run sequentially in f64 (half a
-//      warp per run: lane b owns basis column b of the three channels) and
-//      adds the result to the f32 gradients / f64 signal;
+//   3. the runs of equal leaf are listed longest first and
+//      reduce_runs_kernel sums each run sequentially in f64 (half a warp per
+//      run: lane b owns basis column b of the three channels), adding the
+//      result to the f32 gradients / f64 signal;
 //   4. the per-ray squared errors are summed by cub::DeviceReduce (fixed
 //      order).
 // Everything is a pure function of the inputs: results are bit-identical
@@ -21,6 +22,8 @@
 // bit-exact traversal; exp may differ from glibc's by an ulp).
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_reduce.cuh>
+#include <cub/device/device_select.cuh>
+#include <cub/iterator/counting_input_iterator.cuh>
 #include "dot_tree.cuh"
 #include "dot_internal.h"
 
@@ -29,89 +32,92 @@ namespace dot {
 int launch_iota(int32_t* p, int64_t n, cudaStream_t s);
 int launch_add_f64(double* dst, const double* src, cudaStream_t s);
 
+// Per leaf, the run of its records in sorted (= the reference's ray-major)
+// order.  run_heads_kernel flags run starts; the runs are then listed
+// longest first (a leaf hit by thousands of rays is a long serial f64 sum:
+// started first it overlaps the bulk instead of forming the kernel's tail).
+
+__global__ void run_heads_kernel(const unsigned long long* __restrict__ keys, int64_t total, int ray_bits,
+                                 int32_t* __restrict__ flag) {
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= total) return;
+    flag[i] = i == 0 || (keys[i - 1] >> ray_bits) != (keys[i] >> ray_bits);
+}
+
+// key = ~length (descending sort), value = run start
+__global__ void run_lengths_kernel(const int32_t* __restrict__ head, const int32_t* __restrict__ n_runs,
+                                   int64_t total, uint32_t* __restrict__ len_key) {
+    const int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int64_t m = *n_runs;
+    if (j >= m) return;
+    const int64_t end = j + 1 < m ? head[j + 1] : total;
+    len_key[j] = ~uint32_t(end - head[j]);
+}
+
 template <int B>
 __global__ void __launch_bounds__(128) reduce_runs_kernel(
-    const unsigned long long* __restrict__ keys, const int32_t* __restrict__ idx, int64_t total,
-    int ray_bits, const float4* __restrict__ rec, const double* __restrict__ recq,
-    const float* __restrict__ basis, float* __restrict__ gsig, float* __restrict__ gsh,
-    double* __restrict__ signal) {
+    const unsigned long long* __restrict__ keys, const int32_t* __restrict__ idx,
+    const int32_t* __restrict__ run_start, const uint32_t* __restrict__ run_len_key,
+    const int32_t* __restrict__ n_runs, int ray_bits, const float4* __restrict__ rec,
+    const double* __restrict__ recq, const float* __restrict__ basis, float* __restrict__ gsig,
+    float* __restrict__ gsh, double* __restrict__ signal) {
     constexpr int S = pad4(3 * B);
-    const int lane = threadIdx.x & 31;
-    const int64_t w0 = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-    const int64_t pos = w0 * 32 + lane;
+    // half a warp per run: lane b owns basis column b of the three channels
+    const int64_t h = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 4;
+    const int b = threadIdx.x & 15;
+    if (h >= *n_runs) return;
     const unsigned long long rmask = (1ull << ray_bits) - 1ull;
-    bool head = false;
-    if (pos < total) {
-        const unsigned long long k = keys[pos] >> ray_bits;
-        head = pos == 0 || (keys[pos - 1] >> ray_bits) != k;
+    int64_t j = run_start[h];
+    const int64_t end = j + int64_t(~run_len_key[h]);
+    const unsigned long long pid = keys[j] >> ray_bits;
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+    if (b < B) {
+        a0 = double(gsh[pid * S + 0 * B + b]);
+        a1 = double(gsh[pid * S + 1 * B + b]);
+        a2 = double(gsh[pid * S + 2 * B + b]);
     }
-    unsigned heads = __ballot_sync(0xffffffffu, head);
-    const int half = lane >> 4, b = lane & 15;
-    while (heads) {
-        const int h0 = __ffs(heads) - 1;
-        heads &= heads - 1;
-        int h1 = -1;
-        if (heads) {
-            h1 = __ffs(heads) - 1;
-            heads &= heads - 1;
-        }
-        const int h = half ? h1 : h0;
-        if (h < 0) continue;
-        int64_t j = w0 * 32 + h;
-        const unsigned long long pid = keys[j] >> ray_bits;
-        double a0 = 0.0, a1 = 0.0, a2 = 0.0;
-        if (b < B) {
-            a0 = double(gsh[pid * S + 0 * B + b]);
-            a1 = double(gsh[pid * S + 1 * B + b]);
-            a2 = double(gsh[pid * S + 2 * B + b]);
-        }
-        double as = double(gsig[pid]);
-        double aq = signal[pid];
-        // records in groups of U: all loads of a group are issued before its
-        // (sequential, in-order) additions, so a run costs ~1 memory latency
-        // per U records instead of per record
-        constexpr int U = 8;
-        for (bool more = true; more; j += U) {
-            unsigned long long kk[U];
-            int32_t ix[U];
-            float4 r[U];
-            double q[U], bv[U];
+    double as = double(gsig[pid]);
+    double aq = signal[pid];
+    // records in groups of U: all loads of a group are issued before its
+    // (sequential, in-order) additions, so a run costs ~1 memory latency per
+    // U records instead of per record
+    constexpr int U = 8;
+    for (; j < end; j += U) {
+        int32_t ix[U];
+        unsigned long long kk[U];
+        float4 r[U];
+        double q[U], bv[U];
 #pragma unroll
-            for (int u = 0; u < U; ++u) {
-                kk[u] = j + u < total ? keys[j + u] : ~0ull;
-                if ((kk[u] >> ray_bits) != pid) kk[u] = ~0ull;
-            }
-#pragma unroll
-            for (int u = 0; u < U; ++u) ix[u] = kk[u] != ~0ull ? idx[j + u] : 0;
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-                const bool in = kk[u] != ~0ull;
-                r[u] = in ? rec[ix[u]] : make_float4(0.f, 0.f, 0.f, 0.f);
-                q[u] = in ? recq[ix[u]] : 0.0;
-                bv[u] = (in && b < B) ? double(basis[int64_t(kk[u] & rmask) * B + b]) : 0.0;
-            }
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-                if (kk[u] == ~0ull) {
-                    more = false;
-                    break;
-                }
-                a0 = __dadd_rn(a0, __dmul_rn(double(r[u].y), bv[u]));
-                a1 = __dadd_rn(a1, __dmul_rn(double(r[u].z), bv[u]));
-                a2 = __dadd_rn(a2, __dmul_rn(double(r[u].w), bv[u]));
-                as = __dadd_rn(as, double(r[u].x));
-                aq = __dadd_rn(aq, q[u]);
-            }
+        for (int u = 0; u < U; ++u) {
+            const bool in = j + u < end;
+            kk[u] = in ? keys[j + u] : 0ull;
+            ix[u] = in ? idx[j + u] : 0;
         }
-        if (b < B) {
-            gsh[pid * S + 0 * B + b] = float(a0);
-            gsh[pid * S + 1 * B + b] = float(a1);
-            gsh[pid * S + 2 * B + b] = float(a2);
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const bool in = j + u < end;
+            r[u] = in ? rec[ix[u]] : make_float4(0.f, 0.f, 0.f, 0.f);
+            q[u] = in ? recq[ix[u]] : 0.0;
+            bv[u] = (in && b < B) ? double(basis[int64_t(kk[u] & rmask) * B + b]) : 0.0;
         }
-        if (b == 0) {
-            gsig[pid] = float(as);
-            signal[pid] = aq;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if (j + u >= end) break;
+            a0 = __dadd_rn(a0, __dmul_rn(double(r[u].y), bv[u]));
+            a1 = __dadd_rn(a1, __dmul_rn(double(r[u].z), bv[u]));
+            a2 = __dadd_rn(a2, __dmul_rn(double(r[u].w), bv[u]));
+            as = __dadd_rn(as, double(r[u].x));
+            aq = __dadd_rn(aq, q[u]);
         }
+    }
+    if (b < B) {
+        gsh[pid * S + 0 * B + b] = float(a0);
+        gsh[pid * S + 1 * B + b] = float(a1);
+        gsh[pid * S + 2 * B + b] = float(a2);
+    }
+    if (b == 0) {
+        gsig[pid] = float(as);
+        signal[pid] = aq;
     }
 }
 
@@ -221,10 +227,51 @@ static int run_sorted(const TreeDev& T, int64_t capacity, const double* o, const
         ALLOC(tmp, tmp_bytes);
         TRY(check_cuda(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, keys, keys2, idx, idx2, int(total), 0,
                                                        ray_bits + pid_bits, s), "DeviceRadixSort"));
-        const int64_t warps = (total + 31) / 32;
-        reduce_runs_kernel<B><<<unsigned((warps * 32 + 127) / 128), 128, 0, s>>>(
-            keys2, idx2, total, ray_bits, rec, recq, basis, gsig, gsh, signal);
-        TRY(check_launch("reduce_runs_kernel"));
+        // runs of equal leaf, longest first
+        int32_t *flag = nullptr, *heads = nullptr, *heads2 = nullptr, *d_nruns = nullptr;
+        uint32_t *lkey = nullptr, *lkey2 = nullptr;
+        void* tmp2 = nullptr;
+        auto free_runs = [&]() {
+            cudaFreeAsync(flag, s);
+            cudaFreeAsync(heads, s);
+            cudaFreeAsync(heads2, s);
+            cudaFreeAsync(d_nruns, s);
+            cudaFreeAsync(lkey, s);
+            cudaFreeAsync(lkey2, s);
+            cudaFreeAsync(tmp2, s);
+        };
+#define TRY2(x) do { if ((st = (x)) != DOT_OK) { free_runs(); cleanup(); return st; } } while (0)
+#define ALLOC2(p, bytes) TRY2(check_cuda(cudaMallocAsync(reinterpret_cast<void**>(&(p)), (bytes), s), "cudaMallocAsync"))
+        ALLOC2(flag, size_t(total) * sizeof(int32_t));
+        ALLOC2(heads, size_t(total) * sizeof(int32_t));
+        ALLOC2(heads2, size_t(total) * sizeof(int32_t));
+        ALLOC2(d_nruns, sizeof(int32_t));
+        ALLOC2(lkey, size_t(total) * sizeof(uint32_t));
+        ALLOC2(lkey2, size_t(total) * sizeof(uint32_t));
+        run_heads_kernel<<<unsigned((total + 255) / 256), 256, 0, s>>>(keys2, total, ray_bits, flag);
+        size_t b1 = 0, b2 = 0;
+        cub::CountingInputIterator<int32_t> pos(0);
+        cub::DeviceSelect::Flagged(nullptr, b1, pos, flag, heads, d_nruns, int(total), s);
+        cub::DeviceRadixSort::SortPairs(nullptr, b2, lkey, lkey2, heads, heads2, int(total), 0, 32, s);
+        ALLOC2(tmp2, b1 > b2 ? b1 : b2);
+        TRY2(check_cuda(cub::DeviceSelect::Flagged(tmp2, b1, pos, flag, heads, d_nruns, int(total), s),
+                        "DeviceSelect"));
+        int32_t n_runs = 0;
+        TRY2(check_cuda(cudaMemcpyAsync(&n_runs, d_nruns, sizeof(n_runs), cudaMemcpyDeviceToHost, s), "memcpy"));
+        TRY2(check_cuda(cudaStreamSynchronize(s), "sync"));
+        run_lengths_kernel<<<unsigned((n_runs + 255) / 256), 256, 0, s>>>(heads, d_nruns, total, lkey);
+        TRY2(check_cuda(cub::DeviceRadixSort::SortPairs(tmp2, b2, lkey, lkey2, heads, heads2, n_runs, 0, 32, s),
+                        "DeviceRadixSort"));
+        reduce_runs_kernel<B><<<unsigned((int64_t(n_runs) * 16 + 127) / 128), 128, 0, s>>>(
+            keys2, idx2, heads2, lkey2, d_nruns, ray_bits, rec, recq, basis, gsig, gsh, signal);
+        st = check_launch("reduce_runs_kernel");
+        free_runs();
+        if (st != DOT_OK) {
+            cleanup();
+            return st;
+        }
+#undef TRY2
+#undef ALLOC2
     }
     {
         // loss_sum += sum of per-ray squared errors (fixed reduction order)
