@@ -151,10 +151,12 @@ int dot_render_bwd(const dot_tree_view* tree, const double* origins, const doubl
  *     Results are bit-identical across runs.  ray_index (may be NULL) must
  *     be a permutation of 0..n-1: rays are read at ray_index[r] and the
  *     reduction order is the order of the caller's arrays, so the batch may
- *     be processed in any (e.g. coherence-sorted) order.  Synchronises the
- *     stream (the record count sizes the sort). */
+ *     be processed in any (e.g. coherence-sorted) order.  warp_order and
+ *     ray_used as in dot_render_bwd (may be NULL).  Synchronises the stream
+ *     (the record count sizes the sort). */
 int dot_render_bwd_sorted(const dot_tree_view* tree, const double* origins, const double* dirs,
-                          const double* targets, const int64_t* ray_index, int64_t n_rays,
+                          const double* targets, const int64_t* ray_index,
+                          const int32_t* warp_order, uint16_t* ray_used, int64_t n_rays,
                           const double* background, double early_stop_eps, double t_near,
                           double t_far, double grad_scale, float* grad_sigma, float* grad_sh,
                           int32_t gsh_stride, double* signal, uint8_t* touched, double* loss_sum,

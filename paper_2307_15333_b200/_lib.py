@@ -16,7 +16,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libdot_b200.so")
 
 DOT_OK, DOT_BAD_ARG, DOT_OOM, DOT_CUDA_ERR, DOT_NO_DEVICE = range(5)
-ABI_VERSION = 6
+ABI_VERSION = 7
 
 c_void_p = ctypes.c_void_p
 c_i64 = ctypes.c_int64
@@ -73,7 +73,8 @@ _SIGNATURES = {
                                c_f64, c_f64,
                                c_f64, c_f64, c_void_p, c_void_p, c_i32, c_void_p, c_void_p, c_void_p,
                                c_void_p, c_i32, c_void_p]),
-    "dot_render_bwd_sorted": (c_i32, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_i64, c_void_p,
+    "dot_render_bwd_sorted": (c_i32, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
+                                      c_i64, c_void_p,
                                       c_f64, c_f64, c_f64, c_f64, c_void_p, c_void_p, c_i32, c_void_p,
                                       c_void_p, c_void_p, c_void_p]),
     "dot_sched_order": (c_i32, [c_void_p, c_i64, c_void_p, c_void_p, c_void_p]),

@@ -65,7 +65,7 @@ using namespace dot;
 
 extern "C" {
 
-int dot_abi_version(void) { return 6; }
+int dot_abi_version(void) { return 7; }
 
 const char* dot_last_error(void) { return g_err; }
 

@@ -51,8 +51,9 @@ int launch_render_cameras(const TreeDev& T, const double* cam_to_world, const do
 int launch_render_camera(const TreeDev& T, const double* cam_to_world, double focal, int width, int height,
                          const double* bg, double eps, float* rgb, float* tfin, float* depth, cudaStream_t s);
 int launch_render_bwd_emit(const TreeDev& T, const double* o, const double* d, const double* tgt,
-                           const int64_t* ray_idx, int64_t n, const double* bg, double eps, double tn,
-                           double tf, double gs, uint8_t* touched, const EmitArgs& ea, cudaStream_t s);
+                           const int64_t* ray_idx, const int32_t* warp_order, uint16_t* ray_used, int64_t n,
+                           const double* bg, double eps, double tn, double tf, double gs, uint8_t* touched,
+                           const EmitArgs& ea, cudaStream_t s);
 int launch_exp_ref(const double* x, double* y, int64_t n, cudaStream_t s);
 int launch_locate_build(const TreeDev& T, int level, int32_t* table, cudaStream_t s);
 int launch_ray_stats(const TreeDev& T, const double* o, const double* d, int64_t n, double eps,

@@ -516,8 +516,9 @@ struct EmitSink {
 };
 
 int launch_render_bwd_emit(const TreeDev& T, const double* o, const double* d, const double* tgt,
-                           const int64_t* ray_idx, int64_t n, const double* bg, double eps, double tn,
-                           double tf, double gs, uint8_t* touched, const EmitArgs& ea, cudaStream_t s) {
+                           const int64_t* ray_idx, const int32_t* warp_order, uint16_t* ray_used, int64_t n,
+                           const double* bg, double eps, double tn, double tf, double gs, uint8_t* touched,
+                           const EmitArgs& ea, cudaStream_t s) {
     if (n == 0) return DOT_OK;
     EmitSink sink;
     sink.a = ea;
@@ -526,7 +527,7 @@ int launch_render_bwd_emit(const TreeDev& T, const double* o, const double* d, c
 #define DOT_EMIT(BB)                                                                                 \
     render_bwd_buffered_kernel<BB, EmitSink><<<unsigned((n + 31) / 32), 32, 0, s>>>(                 \
         T, o, d, tgt, ray_idx, n, bg[0], bg[1], bg[2], eps, tn, tf, gs, touched, nullptr, 0, sink,   \
-        nullptr, nullptr);
+        warp_order, ray_used);
     DOT_DISPATCH_B(DOT_EMIT)
 #undef DOT_EMIT
     return check_launch("render_bwd_buffered_kernel<emit>");

@@ -141,7 +141,7 @@ static int64_t g_rec_hint = 0;  // records needed by the last call (grows only)
 
 template <int B>
 static int run_sorted(const TreeDev& T, int64_t capacity, const double* o, const double* d, const double* tgt,
-                      const int64_t* ray_id, int64_t n, const double* bg, double eps, double tn,
+                      const int64_t* ray_id, const int32_t* warp_order, uint16_t* ray_used, int64_t n, const double* bg, double eps, double tn,
                       double tf, double gs, float* gsig, float* gsh, double* signal,
                       uint8_t* touched, double* loss_sum, cudaStream_t s) {
     retain_pool_memory();
@@ -202,7 +202,8 @@ static int run_sorted(const TreeDev& T, int64_t capacity, const double* o, const
         ALLOC(recq, size_t(cap) * sizeof(double));
         TRY(check_cuda(cudaMemsetAsync(ctr, 0, 2 * sizeof(unsigned long long), s), "memset"));
         EmitArgs ea{ctr, cap, keys, rec, recq, basis, loss_ray, ray_bits};
-        TRY(launch_render_bwd_emit(T, o, d, tgt, ray_id, n, bg, eps, tn, tf, gs, touched, ea, s));
+        TRY(launch_render_bwd_emit(T, o, d, tgt, ray_id, warp_order, ray_used, n, bg, eps, tn, tf, gs, touched,
+                                   ea, s));
         TRY(check_cuda(cudaMemcpyAsync(h_ctr, ctr, sizeof(h_ctr), cudaMemcpyDeviceToHost, s), "memcpy"));
         TRY(check_cuda(cudaStreamSynchronize(s), "cudaStreamSynchronize"));
         if (int64_t(h_ctr[0]) > g_rec_hint) g_rec_hint = int64_t(h_ctr[0]);
@@ -319,7 +320,8 @@ int launch_add_f64(double* dst, const double* src, cudaStream_t s) {
 using namespace dot;
 
 extern "C" int dot_render_bwd_sorted(const dot_tree_view* tree, const double* origins, const double* dirs,
-                                     const double* targets, const int64_t* ray_index, int64_t n_rays,
+                                     const double* targets, const int64_t* ray_index,
+                                     const int32_t* warp_order, uint16_t* ray_used, int64_t n_rays,
                                      const double* background, double early_stop_eps, double t_near,
                                      double t_far, double grad_scale, float* grad_sigma, float* grad_sh,
                                      int32_t gsh_stride, double* signal, uint8_t* touched,
@@ -335,10 +337,10 @@ extern "C" int dot_render_bwd_sorted(const dot_tree_view* tree, const double* or
     const TreeDev T = make_tree(*tree);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     switch (T.basis_count) {
-        case 1: return run_sorted<1>(T, tree->capacity, origins, dirs, targets, ray_index, n_rays, background, early_stop_eps, t_near, t_far, grad_scale, grad_sigma, grad_sh, signal, touched, loss_sum, s);
-        case 4: return run_sorted<4>(T, tree->capacity, origins, dirs, targets, ray_index, n_rays, background, early_stop_eps, t_near, t_far, grad_scale, grad_sigma, grad_sh, signal, touched, loss_sum, s);
-        case 9: return run_sorted<9>(T, tree->capacity, origins, dirs, targets, ray_index, n_rays, background, early_stop_eps, t_near, t_far, grad_scale, grad_sigma, grad_sh, signal, touched, loss_sum, s);
-        case 16: return run_sorted<16>(T, tree->capacity, origins, dirs, targets, ray_index, n_rays, background, early_stop_eps, t_near, t_far, grad_scale, grad_sigma, grad_sh, signal, touched, loss_sum, s);
+        case 1: return run_sorted<1>(T, tree->capacity, origins, dirs, targets, ray_index, warp_order, ray_used, n_rays, background, early_stop_eps, t_near, t_far, grad_scale, grad_sigma, grad_sh, signal, touched, loss_sum, s);
+        case 4: return run_sorted<4>(T, tree->capacity, origins, dirs, targets, ray_index, warp_order, ray_used, n_rays, background, early_stop_eps, t_near, t_far, grad_scale, grad_sigma, grad_sh, signal, touched, loss_sum, s);
+        case 9: return run_sorted<9>(T, tree->capacity, origins, dirs, targets, ray_index, warp_order, ray_used, n_rays, background, early_stop_eps, t_near, t_far, grad_scale, grad_sigma, grad_sh, signal, touched, loss_sum, s);
+        case 16: return run_sorted<16>(T, tree->capacity, origins, dirs, targets, ray_index, warp_order, ray_used, n_rays, background, early_stop_eps, t_near, t_far, grad_scale, grad_sigma, grad_sh, signal, touched, loss_sum, s);
         default: return set_error(DOT_BAD_ARG, "basis_count must be 1, 4, 9 or 16");
     }
 }

@@ -383,7 +383,7 @@ def render_and_backprop(tree: SparseOctree, origins, dirs, targets, background,
             p = plan_batch(tree, o, d, idx)
             idx, sorted_keys = p.idx, p.sorted_keys
         if sorted_keys is not None:
-            if WARP_SCHED and not deterministic and n <= SCHED_MAX_RAYS:
+            if WARP_SCHED and n <= SCHED_MAX_RAYS:
                 # launch the warps whose key buckets were costliest last time first
                 table = _sched_table(tree)
                 warp_order = torch.empty((n + 31) // 32, dtype=torch.int32, device=tree.device)
@@ -396,7 +396,8 @@ def render_and_backprop(tree: SparseOctree, origins, dirs, targets, background,
             if rgb is not None:
                 raise InputError("return_rgb is not available with deterministic=True")
             _lib.call("dot_render_bwd_sorted", _lib.ctypes.byref(view), _lib.ptr(o), _lib.ptr(d),
-                      _lib.ptr(t), _lib.ptr(idx), n, _bg_ptr(bg), float(early_stop_eps),
+                      _lib.ptr(t), _lib.ptr(idx), _lib.ptr(warp_order), _lib.ptr(ray_used), n,
+                      _bg_ptr(bg), float(early_stop_eps),
                       float(t_near), float(t_far), gs, _lib.ptr(ws.dsigma), _lib.ptr(ws.dsh_store),
                       tree.sh_stride, _lib.ptr(ws.signal), _lib.ptr(ws.touched), _lib.ptr(ws.loss),
                       _lib.stream_ptr())
@@ -406,9 +407,9 @@ def render_and_backprop(tree: SparseOctree, origins, dirs, targets, background,
                       float(early_stop_eps), float(t_near), float(t_far), gs, _lib.ptr(ws.dsigma),
                       _lib.ptr(ws.dsh_store), tree.sh_stride, _lib.ptr(ws.signal), _lib.ptr(ws.touched),
                       _lib.ptr(ws.loss), _lib.ptr(rgb), int(kernel_flags), _lib.stream_ptr())
-            if ray_used is not None:
-                _lib.call("dot_sched_update", _lib.ptr(sorted_keys), _lib.ptr(ray_used), n,
-                          _lib.ptr(_sched_table(tree)), _lib.stream_ptr())
+        if ray_used is not None:
+            _lib.call("dot_sched_update", _lib.ptr(sorted_keys), _lib.ptr(ray_used), n,
+                      _lib.ptr(_sched_table(tree)), _lib.stream_ptr())
         if kernel_events is not None:
             kernel_events[1].record()
     nsh = 3 * tree.basis_count

@@ -114,6 +114,6 @@ def test_sorted_rejects_bad_ray_index():
     bg = np.ones(3)
     with pytest.raises(InputError):
         _lib.call("dot_render_bwd_sorted", ctypes.byref(view), _lib.ptr(o), _lib.ptr(d), _lib.ptr(t),
-                  _lib.ptr(bad), 100, bg.ctypes.data_as(ctypes.c_void_p), 1e-4, 0.0, float("inf"), 0.02,
+                  _lib.ptr(bad), None, None, 100, bg.ctypes.data_as(ctypes.c_void_p), 1e-4, 0.0, float("inf"), 0.02,
                   _lib.ptr(ws.dsigma), _lib.ptr(ws.dsh_store), tree.sh_stride, _lib.ptr(ws.signal),
                   _lib.ptr(ws.touched), _lib.ptr(ws.loss), _lib.stream_ptr())
