@@ -161,17 +161,42 @@ struct BufSeg {
     float pad;
 };
 
+// 24-byte record of the atomic sinks: alpha rounded to f32 (pass 2 only
+// rebuilds T_i and q_i for gradients and the atomic signal, both within the
+// float tolerance); the deterministic sink keeps the exact f64 alpha so its
+// signal stays bit-identical to the reference's.
+struct BufSegCompact {
+    int32_t pid;
+    float delta;
+    float a;
+    float k0, k1, k2;
+};
+
+template <bool EXACT>
+struct RecordOf {
+    using type = BufSegCompact;
+};
+template <>
+struct RecordOf<true> {
+    using type = BufSeg;
+};
+
 // Where pass 2 sends each composited segment's gradient contribution.
 // AtomicSink: vector REDs straight into the per-leaf buffers (default).
 // EmitSink (sorted.cu): one record per segment, reduced per leaf afterwards
 // in ray-major order (deterministic mode).
 struct AtomicSink {
     static constexpr bool kSmem = false;
+    static constexpr bool kExactAlpha = false;
     float* __restrict__ gsig;
     float* __restrict__ gsh;
     double* __restrict__ signal;
     double* __restrict__ loss_sum;
     __device__ __forceinline__ void bind(float*, float4*) {}
+    // pass 1, per composited segment: the signal needs only the exact q
+    __device__ __forceinline__ void pass1(int64_t pid, double q) {
+        if (q != 0.0) red_add_f64(signal + pid, q);
+    }
     // warp-collective, all 32 lanes (no-op here)
     __device__ __forceinline__ void reserve(int, bool) {}
     template <int B>
@@ -195,7 +220,6 @@ struct AtomicSink {
                 red_add_v4(row + 4 * j, v[0], v[1], v[2], v[3]);
             }
         }
-        if (q != 0.0) red_add_f64(signal + pid, q);
     }
     template <int B>
     __device__ __forceinline__ void ray_done(int64_t, const float*, double) {}
@@ -234,10 +258,7 @@ struct CoopSink : AtomicSink {
                                         const float*, double q) {
         constexpr int S = pad4(3 * B), CH = S / 4;
         const int lane = threadIdx.x & 31;
-        if (act) {
-            red_add_f32(gsig + pid, ds);
-            if (q != 0.0) red_add_f64(signal + pid, q);
-        }
+        if (act) red_add_f32(gsig + pid, ds);
         const bool has = act && (w0 != 0.f || w1 != 0.f || w2 != 0.f);
         const unsigned m = __ballot_sync(0xffffffffu, has);
         if (m == 0) return;
@@ -297,7 +318,8 @@ __global__ void __launch_bounds__(32, 32) render_bwd_buffered_kernel(
     const int64_t r = valid ? ray_index(ray_idx, slot) : 0;
     Tracer tr;
     float basis[B];
-    BufSeg buf[K];
+    using Rec = typename RecordOf<Sink::kExactAlpha>::type;
+    Rec buf[K];
     int used = 0;
     double resume_t = 0.0, resume_nudge = 0.0;
     double R0 = 0.0, R1 = 0.0, R2 = 0.0, g0 = 0.0, g1 = 0.0, g2 = 0.0;
@@ -314,6 +336,7 @@ __global__ void __launch_bounds__(32, 32) render_bwd_buffered_kernel(
                 if (cut) continue;  // post-cut: touched only
                 const double a = exp_ref(-double(__ldg(T.sigma + L.pid)) * dl);
                 const double q = 1.0 - a;
+                if (!(flags & 16384)) sink.pass1(L.pid, q);
                 float k0 = __int_as_float(0x7fc00000), k1 = k0, k2 = k0;
                 if (q > 0.0) {
                     float e0, e1, e2;
@@ -327,14 +350,13 @@ __global__ void __launch_bounds__(32, 32) render_bwd_buffered_kernel(
                     c2 += tq * double(k2);
                 }
                 if (used < K) {
-                    BufSeg e;
+                    Rec e;
                     e.pid = L.pid;
                     e.delta = float(dl);
                     e.a = a;
                     e.k0 = k0;
                     e.k1 = k1;
                     e.k2 = k2;
-                    e.pad = 0.f;
                     buf[used] = e;
                 } else if (used == K) {  // buffer full: remember where pass 2 resumes
                     resume_t = te;
@@ -384,7 +406,7 @@ __global__ void __launch_bounds__(32, 32) render_bwd_buffered_kernel(
         tr.t = resume_t;
         tr.nudge = resume_nudge;
     }
-    BufSeg nxt;
+    Rec nxt;
     if (used > 0) nxt = buf[0];
     for (int i = 0; i < maxu; ++i) {
         const bool act = valid && i < used;
@@ -393,7 +415,7 @@ __global__ void __launch_bounds__(32, 32) render_bwd_buffered_kernel(
         float k0 = 0.f, k1 = 0.f, k2 = 0.f;
         if (act) {
             if (i < K) {  // software pipeline: entry i+1 is in flight while i is scattered
-                const BufSeg e = nxt;
+                const Rec e = nxt;
                 if (i + 1 < used && i + 1 < K) nxt = buf[i + 1];
                 pid = e.pid;
                 a = e.a;
@@ -473,6 +495,8 @@ int launch_render_bwd(const TreeDev& T, const double* o, const double* d, const 
 // counted in ctr[1] and writes nothing (the host retries with more room).
 struct EmitSink {
     static constexpr bool kSmem = false;
+    static constexpr bool kExactAlpha = true;
+    __device__ __forceinline__ void pass1(int64_t, double) {}
     __device__ __forceinline__ void bind(float*, float4*) {}
     EmitArgs a;
     int64_t base;
