@@ -54,9 +54,22 @@ __global__ void __launch_bounds__(256, MINB) rmsprop_kernel(float* __restrict__ 
     float* g = gsh + row * gsh_stride + k0;
     double* v = v_sh + row * n_sh + k0;
     if (VEC) {  // n_sh % 4 == 0: all quads full and 16/32-byte aligned
-        float4 th = *reinterpret_cast<float4*>(p);
         const float4 gg = *reinterpret_cast<const float4*>(g);
         double2 va = reinterpret_cast<double2*>(v)[0], vb = reinterpret_cast<double2*>(v)[1];
+        if (gg.x == 0.f && gg.y == 0.f && gg.z == 0.f && gg.w == 0.f) {
+            // zero gradient quad (e.g. a leaf touched only past the cut): v
+            // decays, theta - lr*0/(sqrt(v)+eps) == theta exactly and the
+            // gradients are already (+-)0 -- skip the payload and the zeroing
+            const double4 nv = {__dmul_rn(beta, va.x), __dmul_rn(beta, va.y), __dmul_rn(beta, vb.x),
+                                __dmul_rn(beta, vb.y)};
+            const double lim = 1.7976931348623157e308;
+            if (nv.x <= lim && nv.y <= lim && nv.z <= lim && nv.w <= lim) {
+                reinterpret_cast<double2*>(v)[0] = make_double2(nv.x, nv.y);
+                reinterpret_cast<double2*>(v)[1] = make_double2(nv.z, nv.w);
+                return;
+            }
+        }
+        float4 th = *reinterpret_cast<float4*>(p);
         th.x = rms_update(th.x, va.x, double(gg.x), beta, omb, eps, lr_sh, false);
         th.y = rms_update(th.y, va.y, double(gg.y), beta, omb, eps, lr_sh, false);
         th.z = rms_update(th.z, vb.x, double(gg.z), beta, omb, eps, lr_sh, false);
