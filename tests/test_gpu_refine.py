@@ -235,3 +235,38 @@ def test_config1_end_to_end_deterministic_refine_bytes_identical():
     assert rep.merges_applied == int(z["calib_merges"])
     assert rep.splits_applied == int(z["calib_splits"])
     assert hashlib.sha256(tree_bytes(tree)).hexdigest() == str(z["calib_sha256"])
+
+
+def test_rmsprop_zero_gradient_rows_bit_exact(oracle):
+    """Touched rows whose gradients are exactly zero (leaves touched only past
+    the early-termination cut) take the kernel's shortcut paths; v must still
+    decay and theta stay put, bit for bit like the reference update."""
+    from paper_2307_15333_b200.optim import RmsPropState, rmsprop_step
+    from paper_2307_15333_b200.render import GradBuffer
+    from helpers import irregular_tree
+    rng = np.random.default_rng(8)
+    tree = irregular_tree(56, 16, depth=2, splits=4, max_depth=4, device="cuda")
+    cap, nsh = tree.capacity, 48
+    st = RmsPropState(tree)
+    v0s = rng.uniform(0, 1e-3, cap)
+    v0h = rng.uniform(0, 1e-3, (cap, nsh))
+    st.v_sigma.copy_(torch.from_numpy(v0s))
+    st.v_sh.copy_(torch.from_numpy(v0h))
+    gs = rng.normal(0, 1e-2, cap).astype(np.float32)
+    gh = rng.normal(0, 1e-2, (cap, nsh)).astype(np.float32)
+    rows = np.arange(cap)
+    gs[rows % 3 == 0] = 0.0
+    gh[rows % 3 == 0] = 0.0                   # whole rows zero
+    gh[rows % 3 == 1, 4:8] = 0.0              # single zero quads
+    gh[rows % 5 == 0, 12] = -0.0
+    mask = np.zeros(cap, np.uint8)
+    mask[tree.leaf_ids()] = 1
+    sig0 = tree.sigma.cpu().numpy().copy()
+    sh0 = tree.sh.cpu().numpy().copy()
+    rmsprop_step(tree, GradBuffer(gs.astype(np.float64), gh.astype(np.float64), mask, tree.generation), st)
+    vs, vh = v0s.copy(), v0h.copy()
+    oracle.rmsprop_step(sig0, sh0, vs, vh, gs.astype(np.float64), gh.astype(np.float64), np.nonzero(mask)[0])
+    np.testing.assert_array_equal(tree.sigma.cpu().numpy(), sig0)
+    np.testing.assert_array_equal(tree.sh.cpu().numpy(), sh0)
+    np.testing.assert_array_equal(st.v_sigma.cpu().numpy(), vs)
+    np.testing.assert_array_equal(st.v_sh.cpu().numpy(), vh)
