@@ -439,9 +439,9 @@ def run_ours(args, rank, world, local_rank):
             "exchange": args.exchange if world > 1 else "none",
             "batch_order": args.order, "bwd_flags": args.bwd_flags,
         },
-        # per step: dot_ray_keys32 + render_bwd_buffered + one rmsprop per
-        # all-reduce chunk (a single update at N = 1)
-        "gpu_launches": (2 + (1 if world == 1 else len(chunk_bounds(tree.capacity, args.ar_chunks)))) * args.steps,
+        # per step: ray_keys32 (plan) + sched_cost + sched_order + render_bwd_buffered
+        # + sched_update + one rmsprop per all-reduce chunk (a single update at N = 1)
+        "gpu_launches": (5 + (1 if world == 1 else len(chunk_bounds(tree.capacity, args.ar_chunks)))) * args.steps,
         "roofline": {
             "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
             "frac": achieved / hbm, "traffic": traffic, "traffic_source": traffic_src,
