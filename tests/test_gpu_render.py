@@ -263,3 +263,42 @@ def test_render_views_equals_per_view():
     for i, c in enumerate(cams):
         r1, t1, d1 = render_view(tree, c, (0.2, 0.3, 0.4), return_aux=True)
         assert torch.equal(rgb[i], r1) and torch.equal(tf[i], t1) and torch.equal(dep[i], d1)
+
+
+@pytest.mark.parametrize("n", [1, 31, 32, 33, 1000, 1 << 16, (1 << 20) + 5, 3 << 20])
+def test_sched_order_is_a_permutation(n):
+    """dot_sched_order must launch every warp exactly once whatever the table
+    holds (a duplicate or missing warp would silently drop rays)."""
+    import torch
+    from paper_2307_15333_b200 import _lib
+    g = torch.Generator(device="cuda")
+    g.manual_seed(n)
+    keys = torch.sort(torch.randint(0, 2 ** 31 - 1, (n,), generator=g, device="cuda", dtype=torch.int64)
+                      .to(torch.int32)).values
+    table = torch.randint(0, 3000, ((1 << 24) + (1 << 27),), generator=g, device="cuda",
+                          dtype=torch.int64).to(torch.int16)
+    nw = (n + 31) // 32
+    order = torch.full((nw,), -1, dtype=torch.int32, device="cuda")
+    _lib.call("dot_sched_order", _lib.ptr(keys), n, _lib.ptr(table), _lib.ptr(order), _lib.stream_ptr())
+    assert torch.equal(torch.sort(order.to(torch.int64)).values, torch.arange(nw, device="cuda"))
+
+
+def test_large_batch_with_schedule_vs_oracle(oracle):
+    """A batch large enough for the coherence sort and the learned warp
+    schedule (several steps, so the table is warm) against the oracle."""
+    import torch
+    from helpers import irregular_tree, ray_batch
+    from paper_2307_15333_b200.render import render_and_backprop
+    tree = irregular_tree(90, 4, depth=3, splits=60, merges=4, max_depth=6, device="cuda")
+    o, d = ray_batch(91, 100_000)
+    tg = np.random.default_rng(92).uniform(0, 1, (o.shape[0], 3))
+    for _ in range(3):  # warm the cost table
+        render_and_backprop(tree, torch.from_numpy(o).cuda(), torch.from_numpy(d).cuda(),
+                            torch.from_numpy(tg).cuda(), 0.4)
+    loss, g, sig = render_and_backprop(tree, o, d, tg, 0.4)
+    r_loss, r_g, r_sig = oracle.render_and_backprop(tree, o, d, tg, 0.4)
+    assert loss == pytest.approx(r_loss, rel=RTOL, abs=ATOL)
+    np.testing.assert_allclose(g.dsigma, r_g.dsigma, atol=ATOL, rtol=RTOL)
+    np.testing.assert_allclose(g.dsh, r_g.dsh, atol=ATOL, rtol=RTOL)
+    np.testing.assert_array_equal(g.touched, r_g.touched)
+    np.testing.assert_allclose(sig, r_sig, atol=ATOL, rtol=RTOL)
