@@ -19,7 +19,6 @@ from __future__ import annotations
 
 import ctypes
 import json
-import math
 from dataclasses import dataclass, field
 
 import numpy as np

@@ -31,7 +31,7 @@ from .errors import (
     StructureError,
     TreeFileError,
 )
-from .octree import VALID_BASIS_COUNTS, level_order
+from .octree import VALID_BASIS_COUNTS
 
 TREE_MAGIC = b"DOT1"
 TREE_VERSION = 1
