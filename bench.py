@@ -613,7 +613,7 @@ def bench_refine(dev, args):
                         "gamma 0.1, prune+sample+canonical compaction"}
 
 
-def cpu_baseline(tree, args, n_rays=1 << 16):
+def cpu_baseline(tree, args, n_rays=1 << 19):
     """The C oracle port of the reference kernels, all host threads, on a
     bounded sample of the same training workload."""
     import torch
