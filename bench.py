@@ -613,7 +613,7 @@ def bench_refine(dev, args):
                         "gamma 0.1, prune+sample+canonical compaction"}
 
 
-def cpu_baseline(tree, args, n_rays=1 << 19):
+def cpu_baseline(tree, args, n_rays=1 << 20):
     """The C oracle port of the reference kernels, all host threads, on a
     bounded sample of the same training workload."""
     import torch
@@ -701,7 +701,7 @@ def main():
     ap.add_argument("--skip-render", action="store_true")
     ap.add_argument("--skip-refine", action="store_true")
     ap.add_argument("--skip-cpu", action="store_true")
-    ap.add_argument("--ref-sample", type=int, default=1 << 14)
+    ap.add_argument("--ref-sample", type=int, default=1 << 18)
     ap.add_argument("--workload", choices=["c2", "c4"], default="c2",
                     help="c2 = configs[1] (the headline line), c4 = configs[3] (8.5M leaves, 1080p)")
     ap.add_argument("--order", choices=["random", "raster", "morton"], default="random",
