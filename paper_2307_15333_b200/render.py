@@ -480,14 +480,16 @@ def render_views(tree: SparseOctree, cameras, background, early_stop_eps: float 
 
 def render_image(tree: SparseOctree, camera, background, worker_count: int | None = None,
                  early_stop_eps: float = EPS_T, chunk: int = 65536,
-                 exact_rays: bool = False) -> np.ndarray:
+                 exact_rays: bool = True) -> np.ndarray:
     """H x W x 3 float64 image (render.py:228-241).
 
-    Pinhole cameras (``cam_to_world``/``focal``) are rendered with in-kernel
-    rays (``render_view``); ``exact_rays=True`` -- or any other camera
-    object with ``rays()`` -- renders ``camera.rays()`` instead, i.e. the very
-    same f64 rays as the reference.  ``worker_count`` and ``chunk`` are
-    accepted for API compatibility; results never depend on them."""
+    By default renders ``camera.rays()`` -- the very same f64 rays as the
+    reference, so images (and ``heldout_psnr``) match it within the float
+    tolerance.  ``exact_rays=False`` renders pinhole cameras
+    (``cam_to_world``/``focal``) with in-kernel rays (``render_view``): no
+    host ray build or copy, but directions can differ from numpy's matmul in
+    the last ulp.  ``worker_count`` and ``chunk`` are accepted for API
+    compatibility; results never depend on them."""
     if not exact_rays and all(hasattr(camera, a) for a in ("cam_to_world", "focal")):
         return render_view(tree, camera, background, early_stop_eps).double().cpu().numpy()
     origins, dirs = camera.rays()
