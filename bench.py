@@ -60,9 +60,9 @@ def measured_traffic(kernel):
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
             t = json.load(fh)[kernel]
-        return float(t["dram_bytes_per_launch"]), t["capture"]
+        return float(t["dram_bytes_per_launch"]), t["capture"], t.get("l2_hit_pct")
     except Exception:
-        return None, None
+        return None, None, None
 
 
 def peaks():
@@ -341,7 +341,7 @@ def run_ours(args, rank, world, local_rank):
     alg_bytes = per_rank * RAY_BYTES + comp * SEG_BYTES
     hbm, peak_kind = peaks()
     achieved = alg_bytes / (kern_ms_avg / 1e3) / 1e9
-    traffic, traffic_src = measured_traffic("render_bwd_buffered")
+    traffic, traffic_src, l2_hit = measured_traffic("render_bwd_buffered")
     # REDs per launch: dsigma for every composited segment, 12 x F32x4 SH rows
     # and one f64 signal add for every segment with q > 0
     reds = comp + 13 * qpos
@@ -444,7 +444,8 @@ def run_ours(args, rank, world, local_rank):
         "roofline": {
             "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
             "frac": achieved / hbm, "traffic": traffic, "traffic_source": traffic_src,
-            "kernel": "render_bwd_buffered_kernel<16,48>",
+            "l2_hit_pct": l2_hit,
+            "kernel": "render_bwd_buffered_kernel<16, CoopSink> (K = 128 records)",
             "kernel_ms": kern_ms_avg, "alg_bytes_per_launch": alg_bytes, "peak_kind": peak_kind,
             "bytes_model": f"{RAY_BYTES} B/ray + {SEG_BYTES} B/composited segment",
             "atomics_per_launch": reds, "atomics_per_s": reds / (kern_ms_avg / 1e3),
@@ -528,13 +529,13 @@ def bench_render(tree, dev, args, world):
     alg_view = W * H * 12 + (comp * 4 + qpos * 12 * B_SH) / n_res
     hbm, peak_kind = peaks()
     achieved = alg_view / (ms_cam / n_views / 1e3) / 1e9
-    traffic, traffic_src = measured_traffic("render_camera_kernel")
+    traffic, traffic_src, l2_hit = measured_traffic("render_camera_kernel")
     if traffic is not None:
         traffic /= 200.0  # the capture is the timed 200-view launch: DRAM bytes per view
     return {"rays_per_s": rays / (ms_cam / 1e3), "fps_800x800": 200 / (ms_cam / 1e3),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                          "frac": achieved / hbm, "peak_kind": peak_kind,
-                         "traffic": traffic, "traffic_source": traffic_src,
+                         "traffic": traffic, "traffic_source": traffic_src, "l2_hit_pct": l2_hit,
                          "traffic_note": "DRAM bytes per view (ncu of the 200-view launch / 200); "
                                          "the algorithmic gathers are mostly L2/L1 hits for "
                                          "coherent camera rays, so frac can exceed 1",
