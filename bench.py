@@ -713,7 +713,8 @@ def main():
                     help="N > 1 gradient exchange: chunked NCCL all-reduce + RMSProp, or the fused "
                          "peer-memory update (dot_rmsprop_step_peers)")
     ap.add_argument("--bwd-flags", type=int, default=0,
-                    help="dot_render_bwd flags (2 = legacy one-ray-per-thread kernel)")
+                    help="dot_render_bwd flags (diagnostics: 1 skip post-cut marks, 8192 pass 1 only, "
+                         "16384 no reductions, 32768 per-lane REDs)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     world = int(os.environ.get("WORLD_SIZE", "1"))
