@@ -650,21 +650,22 @@ def run_reference(args):
     from oracle import oracle as O
     from paper_2307_15333_b200 import scenes
     O.build()
-    tree = scenes.config2_scene(device="cpu")
+    wl = workloads()[args.workload]  # the same workload as our arm's line
+    tree = wl.scene("cpu")
     tree._host()
-    focal, poses = scenes.hemisphere_cameras(N_VIEWS, W, H, RADIUS, seed=3)
+    focal, poses = wl.cameras()
     sample = args.ref_sample
     rng = np.random.default_rng(11)
     batches = []
     for k in range(args.warmup + args.steps):
-        v = rng.integers(N_VIEWS)
-        o, d = scenes.pinhole_rays(W, H, focal, poses[v])
+        v = rng.integers(wl.views)
+        o, d = scenes.pinhole_rays(wl.W, wl.H, focal, poses[v])
         pick = rng.choice(o.shape[0], sample, replace=False)
         batches.append((o[pick], d[pick], rng.uniform(0.0, 1.0, (sample, 3))))
     sig = tree.sigma.numpy()
     sh = tree.sh.numpy()
     vs = np.zeros(tree.capacity)
-    vh = np.zeros((tree.capacity, 48))
+    vh = np.zeros((tree.capacity, 3 * tree.basis_count))
 
     def step(b):
         o, d, tg = b
@@ -680,12 +681,12 @@ def run_reference(args):
     dt = time.perf_counter() - t
     value = sample * args.steps / dt
     return {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": "rays/s", "n_gpus": 0,
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "rays/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": wl.scaling, "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
-        "config": {"workload": "configs[1] training step (bounded sample per step)",
-                   "leaves": int(tree.leaf_count), "sample_rays_per_step": sample},
+        "config": {"workload": wl.desc, "leaves": int(tree.leaf_count), "sample_rays_per_step": sample,
+                   "host": "CPU only (the reference path is CPU code); N GPUs of the line are unused"},
         "cpu_baseline": {"value": value, "unit": "rays/s", "cores": O.num_threads(), "kind": "port",
                          "sample": f"{sample} rays per step from one random training view, "
                                    "fwd+bwd (count+fill+grad+serial scatter) + RMSProp"},
