@@ -132,7 +132,8 @@ int dot_render_cameras(const dot_tree_view* tree, const double* cam_to_world, co
  *     count (u16, saturating) for dot_sched_update.
  *     flags: bit 0 = skip post-cut touched marking
  *     (not reference semantics); bit 15 = per-lane REDs instead of the
- *     warp-cooperative SH-row scatter; bits 13 / 14 = timing diagnostics
+ *     warp-cooperative SH-row scatter (implied for capacity > 2^27);
+ *     bits 13 / 14 = timing diagnostics
  *     (pass 1 only / no reductions: results are incomplete). */
 int dot_render_bwd(const dot_tree_view* tree, const double* origins, const double* dirs,
                    const double* targets, const int64_t* ray_index, const int32_t* warp_order,

@@ -164,6 +164,9 @@ int dot_render_bwd(const dot_tree_view* tree, const double* origins, const doubl
         return set_error(DOT_BAD_ARG, "gsh_stride must equal sh_stride (%d)", tree->sh_stride);
     if ((reinterpret_cast<uintptr_t>(grad_sh) & 15) != 0)
         return set_error(DOT_BAD_ARG, "grad_sh must be 16-byte aligned");
+    // the warp-cooperative sink packs (pool id, lane) into 32 bits: pool ids
+    // need 27 bits, larger pools take the per-lane REDs
+    if (tree->capacity > (int64_t(1) << 27)) flags |= 32768;
     return launch_render_bwd(make_tree(*tree), origins, dirs, targets, ray_index, warp_order, ray_used, n_rays,
                              background,
                              early_stop_eps, t_near, t_far, grad_scale, grad_sigma, grad_sh,
