@@ -47,6 +47,9 @@ int validate_tree_view(const dot_tree_view* v) {
     if (!v) return set_error(DOT_BAD_ARG, "tree view is NULL");
     if (!v->node || v->n_nodes < 1) return set_error(DOT_BAD_ARG, "tree has no nodes");
     if (!v->sigma || !v->sh) return set_error(DOT_BAD_ARG, "tree payload is NULL");
+    // node words are int32: child indices and ~pool id must fit
+    if (v->n_nodes > INT32_MAX || v->capacity < 1 || v->capacity > INT32_MAX)
+        return set_error(DOT_BAD_ARG, "n_nodes / capacity must be in [1, 2^31)");
     const int B = v->basis_count;
     if (B != 1 && B != 4 && B != 9 && B != 16)
         return set_error(DOT_BAD_ARG, "basis_count must be 1, 4, 9 or 16, got %d", B);

@@ -244,6 +244,9 @@ def test_locate_dyadic_predicate():
     assert view((0, 0, 0), 0.75) == 0
     assert view((0, 0, 0), 1.0, max_depth=22) == 0
     assert view((0, 0, 0), 1.0, capacity=1 << 26) == 0
+    # invalid views are rejected by the shared validator (int32 node words)
+    assert view((0, 0, 0), 1.0, capacity=0) == 0
+    assert view((0, 0, 0), 1.0, capacity=1 << 31) == 0
 
 
 def _exp_args(n, seed=0):
