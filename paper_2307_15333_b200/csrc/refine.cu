@@ -47,63 +47,7 @@ static unsigned persistent_blocks() {
 }
 
 // ---------------------------------------------------------------------------
-// Exclusive scan of int32 values (3 phases, cub block scans).
-
-constexpr int kScanItems = 4;
-constexpr int kScanTile = kTB * kScanItems;
-
-__global__ void scan_reduce_kernel(const int32_t* __restrict__ in, int64_t n, int64_t* __restrict__ sums) {
-    using BR = cub::BlockReduce<int64_t, kTB>;
-    __shared__ typename BR::TempStorage tmp;
-    const int64_t base = int64_t(blockIdx.x) * kScanTile;
-    int64_t v = 0;
-#pragma unroll
-    for (int i = 0; i < kScanItems; ++i) {
-        const int64_t idx = base + threadIdx.x * kScanItems + i;
-        if (idx < n) v += in[idx];
-    }
-    const int64_t s = BR(tmp).Sum(v);
-    if (threadIdx.x == 0) sums[blockIdx.x] = s;
-}
-
-__global__ void scan_sums_kernel(int64_t* __restrict__ sums, int64_t nb, int64_t* __restrict__ total) {
-    using BS = cub::BlockScan<int64_t, kTB>;
-    __shared__ typename BS::TempStorage tmp;
-    __shared__ int64_t carry;
-    if (threadIdx.x == 0) carry = 0;
-    __syncthreads();
-    for (int64_t b = 0; b < nb; b += kTB) {
-        const int64_t idx = b + threadIdx.x;
-        int64_t v = idx < nb ? sums[idx] : 0, agg;
-        int64_t ex;
-        BS(tmp).ExclusiveSum(v, ex, agg);
-        if (idx < nb) sums[idx] = ex + carry;
-        __syncthreads();
-        if (threadIdx.x == 0) carry += agg;
-        __syncthreads();
-    }
-    if (threadIdx.x == 0) *total = carry;
-}
-
-__global__ void scan_apply_kernel(const int32_t* __restrict__ in, int64_t n,
-                                  const int64_t* __restrict__ sums, int64_t* __restrict__ out) {
-    using BS = cub::BlockScan<int64_t, kTB>;
-    __shared__ typename BS::TempStorage tmp;
-    const int64_t base = int64_t(blockIdx.x) * kScanTile;
-    int64_t v[kScanItems];
-#pragma unroll
-    for (int i = 0; i < kScanItems; ++i) {
-        const int64_t idx = base + threadIdx.x * kScanItems + i;
-        v[i] = idx < n ? in[idx] : 0;
-    }
-    BS(tmp).ExclusiveSum(v, v);
-    const int64_t off = sums[blockIdx.x];
-#pragma unroll
-    for (int i = 0; i < kScanItems; ++i) {
-        const int64_t idx = base + threadIdx.x * kScanItems + i;
-        if (idx < n) out[idx] = v[i] + off;
-    }
-}
+// Exclusive scan of int32 flags.
 
 __global__ void scan_total_kernel(const int32_t* __restrict__ in, const int64_t* __restrict__ out, int64_t n,
                                   int64_t* __restrict__ total) {
@@ -111,11 +55,8 @@ __global__ void scan_total_kernel(const int32_t* __restrict__ in, const int64_t*
 }
 
 // Exclusive prefix sum of 0/1 int32 flags into int64 (single-pass decoupled
-// look-back scan, cub::DeviceScan) plus the total.  `sums` is unused (kept
-// for the call sites' buffer layout).
-static int exclusive_scan(const int32_t* in, int64_t n, int64_t* out, int64_t* sums, int64_t* d_total,
-                          cudaStream_t s) {
-    (void)sums;
+// look-back scan, cub::DeviceScan) plus the total.
+static int exclusive_scan(const int32_t* in, int64_t n, int64_t* out, int64_t* d_total, cudaStream_t s) {
     if (n == 0) return check_cuda(cudaMemsetAsync(d_total, 0, sizeof(int64_t), s), "memset");
     size_t bytes = 0;
     cub::DeviceScan::ExclusiveScan(nullptr, bytes, in, out, cub::Sum(), int64_t(0), n, s);
@@ -718,53 +659,6 @@ __global__ void compact_kernel(int64_t N, const int32_t* __restrict__ flags, con
 }
 
 // ---------------------------------------------------------------------------
-// Apply: level-synchronous canonical rebuild.
-
-__global__ void level_flags_kernel(int64_t m, const int32_t* __restrict__ ent_old,
-                                   const uint8_t* __restrict__ ent_kind, const uint8_t* __restrict__ state,
-                                   int32_t* __restrict__ flags) {
-    const int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (e >= m) return;
-    int internal = 0;
-    if (ent_kind[e] != K_NEWCHILD) {
-        const uint8_t st = state[ent_old[e]];
-        internal = (!(st & ST_LEAF)) || (st & ST_SPLIT) ? 1 : 0;
-    }
-    flags[e] = internal;
-}
-
-__global__ void level_emit_kernel(TreeDev T, int64_t m, int64_t base, int64_t next_base,
-                                  const int32_t* __restrict__ ent_old, const uint8_t* __restrict__ ent_kind,
-                                  const int32_t* __restrict__ flags, const int64_t* __restrict__ rank,
-                                  const uint8_t* __restrict__ state, int32_t* __restrict__ new_node,
-                                  int64_t* __restrict__ src_index, uint8_t* __restrict__ src_kind,
-                                  int32_t* __restrict__ nxt_old, uint8_t* __restrict__ nxt_kind) {
-    const int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (e >= m) return;
-    const int64_t gi = base + e;
-    const int32_t o = ent_old[e];
-    const uint8_t kind = ent_kind[e];
-    src_index[gi] = o;
-    if (flags[e]) {
-        const int64_t r = rank[e];
-        new_node[gi] = int32_t(next_base + 8 * r);
-        const uint8_t st = state[o];
-        const bool from_leaf = (st & ST_LEAF) != 0;  // split of an (original or merged) leaf
-        src_kind[gi] = from_leaf ? K_SPLITPARENT : K_KEPT;
-        const int32_t c = T.node[o];
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-            nxt_old[8 * r + k] = from_leaf ? o : c + k;
-            nxt_kind[8 * r + k] = from_leaf ? K_NEWCHILD : K_KEPT;
-        }
-    } else {
-        new_node[gi] = ~int32_t(gi);
-        if (kind == K_NEWCHILD) src_kind[gi] = K_NEWCHILD;
-        else src_kind[gi] = (state[o] & ST_MERGED) ? K_MERGED : K_KEPT;
-    }
-}
-
-// ---------------------------------------------------------------------------
 // Canonical rebuild in one scan.  The new tree's BFS order keeps the relative
 // order of surviving nodes inside a level, so with
 //   f(i) = 1 if old node i is internal after the refine (alive internal and
@@ -1148,20 +1042,18 @@ int dot_refine_plan_lists(dot_refine_plan* p, const int64_t** merge_parents, int
         cudaStream_t s = static_cast<cudaStream_t>(stream);
         const int64_t N = p->N;
         int32_t* flags = nullptr;
-        int64_t *rank = nullptr, *sums = nullptr, *total = nullptr, *list = nullptr;
+        int64_t *rank = nullptr, *total = nullptr, *list = nullptr;
         int32_t* rounds = nullptr;
         int st = DOT_OK;
         auto cleanup = [&]() {
             cudaFreeAsync(flags, s);
             cudaFreeAsync(rank, s);
-            cudaFreeAsync(sums, s);
             cudaFreeAsync(total, s);
             cudaFreeAsync(list, s);
         };
 #define TRY(x) do { if ((st = (x)) != DOT_OK) { cleanup(); return st; } } while (0)
         TRY(dalloc(&flags, N, s));
         TRY(dalloc(&rank, N, s));
-        TRY(dalloc(&sums, N / kScanTile + 2, s));
         TRY(dalloc(&total, 1, s));
         TRY(dalloc(&list, std::max<int64_t>(p->M, p->K) + 1, s));
         for (int which = 0; which < 2; ++which) {
@@ -1170,7 +1062,7 @@ int dot_refine_plan_lists(dot_refine_plan* p, const int64_t** merge_parents, int
             dst.resize(size_t(cnt));
             if (cnt == 0) continue;
             flag_kernel<<<grid_for(N), kTB, 0, s>>>(N, p->state, p->mround, which, flags);
-            TRY(exclusive_scan(flags, N, rank, sums, total, s));
+            TRY(exclusive_scan(flags, N, rank, total, s));
             compact_kernel<<<grid_for(N), kTB, 0, s>>>(N, flags, rank, list);
             TRY(check_launch("compact_kernel"));
             TRY(check_cuda(cudaMemcpyAsync(dst.data(), list, cnt * sizeof(int64_t), cudaMemcpyDeviceToHost, s),
@@ -1226,11 +1118,10 @@ int dot_refine_apply(const dot_refine_plan* p, const dot_tree_view* tree, int32_
     const int n_levels = int(p->level_off.size()) - 1;
     if (n_levels + 2 > kMaxLevels) return set_error(DOT_BAD_ARG, "tree too deep");
     int32_t* flags = nullptr;
-    int64_t *rank = nullptr, *sums = nullptr, *d_total = nullptr, *d_base = nullptr, *d_rb = nullptr;
+    int64_t *rank = nullptr, *d_total = nullptr, *d_base = nullptr, *d_rb = nullptr;
     auto cleanup = [&]() {
         cudaFreeAsync(flags, s);
         cudaFreeAsync(rank, s);
-        cudaFreeAsync(sums, s);
         cudaFreeAsync(d_total, s);
         cudaFreeAsync(d_base, s);
         cudaFreeAsync(d_rb, s);
@@ -1238,7 +1129,6 @@ int dot_refine_apply(const dot_refine_plan* p, const dot_tree_view* tree, int32_
 #define TRY(x) do { if ((st = (x)) != DOT_OK) { cleanup(); return st; } } while (0)
     TRY(dalloc(&flags, N, s));
     TRY(dalloc(&rank, N, s));
-    TRY(dalloc(&sums, N / kScanTile + 2, s));
     TRY(dalloc(&d_total, 1, s));
     TRY(dalloc(&d_base, kMaxLevels + 2, s));
     TRY(dalloc(&d_rb, kMaxLevels + 2, s));
@@ -1247,7 +1137,7 @@ int dot_refine_apply(const dot_refine_plan* p, const dot_tree_view* tree, int32_
                                            cudaMemcpyHostToDevice, s), "memcpy"));
     rebuild_flags_kernel<<<persistent_blocks(), kTB, 0, s>>>(N, p->state, flags);
     TRY(check_launch("rebuild_flags_kernel"));
-    TRY(exclusive_scan(flags, N, rank, sums, d_total, s));
+    TRY(exclusive_scan(flags, N, rank, d_total, s));
     rebuild_levels_kernel<<<1, 1, 0, s>>>(n_levels, rank, d_total, d_base, d_rb);
     rebuild_emit_kernel<<<grid_for(N), kTB, 0, s>>>(T, N, p->state, p->depth, flags, rank, d_base, d_rb,
                                                     new_node, src_index, src_kind);
