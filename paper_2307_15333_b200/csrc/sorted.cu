@@ -23,7 +23,7 @@
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_reduce.cuh>
 #include <cub/device/device_select.cuh>
-#include <cub/iterator/counting_input_iterator.cuh>
+#include <thrust/iterator/counting_iterator.h>
 #include "dot_tree.cuh"
 #include "dot_internal.h"
 
@@ -251,7 +251,7 @@ static int run_sorted(const TreeDev& T, int64_t capacity, const double* o, const
         ALLOC2(lkey2, size_t(total) * sizeof(uint32_t));
         run_heads_kernel<<<unsigned((total + 255) / 256), 256, 0, s>>>(keys2, total, ray_bits, flag);
         size_t b1 = 0, b2 = 0;
-        cub::CountingInputIterator<int32_t> pos(0);
+        thrust::counting_iterator<int32_t> pos(0);
         cub::DeviceSelect::Flagged(nullptr, b1, pos, flag, heads, d_nruns, int(total), s);
         cub::DeviceRadixSort::SortPairs(nullptr, b2, lkey, lkey2, heads, heads2, int(total), 0, 32, s);
         ALLOC2(tmp2, b1 > b2 ? b1 : b2);
