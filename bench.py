@@ -280,9 +280,12 @@ def run_ours(args, rank, world, local_rank):
         from paper_2307_15333_b200.parallel import PeerExchange
         exchange = PeerExchange(tree, state, sws)
 
-    from paper_2307_15333_b200.render import plan_batch
+    from paper_2307_15333_b200.render import plan_batch, pool_keys
     plan_stream = torch.cuda.Stream(dev)
     plans = {}
+    # the resident pool's coherence keys, once (like the pool itself): each
+    # step's plan gathers 4 B per ray instead of re-reading 48 B at random
+    pkeys = pool_keys(tree, origins, dirs)
 
     def step(k, timed_kernel=True):
         # the batch is read in place from the resident pool (ray_index): no
@@ -291,7 +294,7 @@ def run_ours(args, rank, world, local_rank):
         idx = batch_index(k)
         plan = plans.pop(k, None)
         if k + 1 < total_steps + 2:
-            plans[k + 1] = plan_batch(tree, origins, dirs, batch_index(k + 1), stream=plan_stream)
+            plans[k + 1] = plan_batch(tree, origins, dirs, batch_index(k + 1), stream=plan_stream, keys=pkeys)
         return train_step(tree, origins, dirs, targets, state, buf, sws, BG, EPS,
                           ray_index=idx, grad_scale=gs,
                           exchange=exchange if world > 1 else None,
@@ -437,10 +440,14 @@ def run_ours(args, rank, world, local_rank):
             "parallelism": f"rays sharded dp{world}, tree replicated",
             "exchange": args.exchange if world > 1 else "none",
             "batch_order": args.order, "bwd_flags": args.bwd_flags,
+            "plan": "coherence order of step k+1 sorted on a side stream during step k; the "
+                    "resident pool's 31-bit ray keys computed once at setup (render.pool_keys)",
         },
-        # per step: ray_keys32 (plan) + sched_cost + sched_order + render_bwd_buffered
-        # + sched_update + one rmsprop per all-reduce chunk (a single update at N = 1)
-        "gpu_launches": (5 + (1 if world == 1 else len(chunk_bounds(tree.capacity, args.ar_chunks)))) * args.steps,
+        # per step (profiles/r1j_launch_shares.txt): the plan's radix sort in
+        # dot_plan_sort (histogram + exclusive sum + 4 onesweep passes) +
+        # sched_cost + sched_order + render_bwd_buffered + sched_update + one
+        # rmsprop per all-reduce chunk (a single update at N = 1)
+        "gpu_launches": (10 + (1 if world == 1 else len(chunk_bounds(tree.capacity, args.ar_chunks)))) * args.steps,
         "roofline": {
             "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
             "frac": achieved / hbm, "traffic": traffic, "traffic_source": traffic_src,

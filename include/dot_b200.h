@@ -189,6 +189,14 @@ int dot_ray_keys(const dot_tree_view* tree, const double* origins, const double*
 int dot_ray_keys32(const dot_tree_view* tree, const double* origins, const double* dirs,
                    const int64_t* ray_index, int64_t n_rays, int32_t* keys, void* stream);
 
+/* The batch's coherence order: radix sort of keys (dot_ray_keys32) by bits
+ * [begin_bit, 31) carrying ray_index (NULL: the batch positions) as the
+ * value, so sorted_index is directly the ray_index of dot_render_bwd and
+ * sorted_keys feeds dot_sched_order / dot_sched_update.  Ties keep the
+ * batch order (stable). */
+int dot_plan_sort(const int32_t* keys, const int64_t* ray_index, int64_t n_rays, int32_t begin_bit,
+                  int32_t* sorted_keys, int64_t* sorted_index, void* stream);
+
 /* --- workload statistics (measurement helper, no reference counterpart):
  *     totals[0] += traversed segments, totals[1] += composited (pre-cut)
  *     segments, totals[2] += composited segments with q > 0. */

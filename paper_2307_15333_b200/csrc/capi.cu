@@ -68,7 +68,7 @@ using namespace dot;
 
 extern "C" {
 
-int dot_abi_version(void) { return 7; }
+int dot_abi_version(void) { return 8; }
 
 const char* dot_last_error(void) { return g_err; }
 
@@ -183,6 +183,15 @@ int dot_ray_keys(const dot_tree_view* tree, const double* origins, const double*
     if (n_rays < 0 || (n_rays && (!origins || !dirs || !keys))) return set_error(DOT_BAD_ARG, "bad arrays");
     return launch_ray_keys(make_tree(*tree), origins, dirs, n_rays, reinterpret_cast<unsigned long long*>(keys),
                            static_cast<cudaStream_t>(stream));
+}
+
+int dot_plan_sort(const int32_t* keys, const int64_t* ray_index, int64_t n_rays, int32_t begin_bit,
+                  int32_t* sorted_keys, int64_t* sorted_index, void* stream) {
+    if (n_rays < 0 || (n_rays && (!keys || !sorted_keys || !sorted_index)))
+        return set_error(DOT_BAD_ARG, "bad plan_sort arrays");
+    if (begin_bit < 0 || begin_bit > 30) return set_error(DOT_BAD_ARG, "begin_bit must be in 0..30");
+    return run_plan_sort(keys, ray_index, n_rays, begin_bit, sorted_keys, sorted_index,
+                         static_cast<cudaStream_t>(stream));
 }
 
 int dot_ray_keys32(const dot_tree_view* tree, const double* origins, const double* dirs,

@@ -43,6 +43,8 @@ int launch_sched_order(const int32_t* keys, int64_t n, const uint16_t* table, in
 int launch_sched_update(const int32_t* keys, const uint16_t* ray_used, int64_t n, uint16_t* table, cudaStream_t s);
 int launch_ray_keys(const TreeDev& T, const double* o, const double* d, int64_t n, unsigned long long* keys,
                     cudaStream_t s);
+int run_plan_sort(const int32_t* keys, const int64_t* ray_index, int64_t n, int begin_bit,
+                  int32_t* sorted_keys, int64_t* sorted_index, cudaStream_t s);
 int launch_ray_keys32(const TreeDev& T, const double* o, const double* d, const int64_t* ray_idx,
                       int64_t n, int32_t* keys, cudaStream_t s);
 int launch_render_cameras(const TreeDev& T, const double* cam_to_world, const double* focal, int n_views,

@@ -315,6 +315,43 @@ int launch_add_f64(double* dst, const double* src, cudaStream_t s) {
     return check_launch("add_f64_kernel");
 }
 
+// ---------------------------------------------------------------------------
+// Batch coherence order: one radix sort of the 31-bit keys (dot_ray_keys32)
+// carrying the caller's ray index (or the batch position) as the value, so
+// the sorted values are directly the kernel's ray_index (no gather after).
+
+__global__ void iota64_kernel(int64_t* __restrict__ v, int64_t n) {
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < n) v[i] = i;
+}
+
+int run_plan_sort(const int32_t* keys, const int64_t* ray_index, int64_t n, int begin_bit,
+                  int32_t* sorted_keys, int64_t* sorted_index, cudaStream_t s) {
+    if (n == 0) return DOT_OK;
+    retain_pool_memory();
+    int64_t* iota = nullptr;
+    const int64_t* vin = ray_index;
+    int st = DOT_OK;
+    if (!vin) {
+        if ((st = check_cuda(cudaMallocAsync(reinterpret_cast<void**>(&iota), size_t(n) * 8, s), "cudaMallocAsync")))
+            return st;
+        iota64_kernel<<<unsigned((n + 255) / 256), 256, 0, s>>>(iota, n);
+        vin = iota;
+    }
+    size_t bytes = 0;
+    void* tmp = nullptr;
+    st = check_cuda(cub::DeviceRadixSort::SortPairs(nullptr, bytes, keys, sorted_keys, vin, sorted_index, n,
+                                                    begin_bit, 31, s), "SortPairs");
+    if (st == DOT_OK) st = check_cuda(cudaMallocAsync(&tmp, bytes, s), "cudaMallocAsync");
+    if (st == DOT_OK)
+        st = check_cuda(cub::DeviceRadixSort::SortPairs(tmp, bytes, keys, sorted_keys, vin, sorted_index, n,
+                                                        begin_bit, 31, s), "SortPairs");
+    if (tmp) cudaFreeAsync(tmp, s);
+    if (iota) cudaFreeAsync(iota, s);
+    if (st != DOT_OK) return st;
+    return check_launch("plan_sort");
+}
+
 }  // namespace dot
 
 using namespace dot;
