@@ -44,7 +44,26 @@ def _sched_table(tree) -> torch.Tensor:
     if t is None or t.device != tree.device:
         t = torch.zeros((1 << 24) + (1 << 27), dtype=torch.int16, device=tree.device)
         tree._sched_table = t
+        tree._sched_written = None  # event after the last dot_sched_update
+        tree._sched_read = None     # event after the last side-stream dot_sched_order
     return t
+
+
+def _sched_order(tree, sorted_keys: torch.Tensor, n: int, stream) -> torch.Tensor:
+    """dot_sched_order on ``stream``; ordered after the table's last update
+    and recorded as its latest reader (see render_and_backprop's update)."""
+    table = _sched_table(tree)
+    cur = torch.cuda.current_stream(tree.device)
+    if stream is not cur and tree._sched_written is not None:
+        stream.wait_event(tree._sched_written)
+    warp_order = torch.empty((n + 31) // 32, dtype=torch.int32, device=tree.device)
+    _lib.call("dot_sched_order", _lib.ptr(sorted_keys), n, _lib.ptr(table), _lib.ptr(warp_order),
+              _lib.stream_ptr(stream))
+    if stream is not cur:
+        ev = torch.cuda.Event()
+        ev.record(stream)
+        tree._sched_read = ev
+    return warp_order
 
 
 @dataclass
@@ -278,6 +297,7 @@ class RayPlan:
     idx: torch.Tensor
     sorted_keys: torch.Tensor
     event: "torch.cuda.Event | None" = None
+    warp_order: "torch.Tensor | None" = None  # learned launch order, when computed with the plan
 
     def wait(self, stream=None) -> None:
         if self.event is not None:
@@ -331,13 +351,17 @@ def plan_batch(tree: SparseOctree, origins: torch.Tensor, dirs: torch.Tensor, ra
         _lib.call("dot_plan_sort", _lib.ptr(keys), _lib.ptr(idx), n, PLAN_SORT_BEGIN_BIT,
                   _lib.ptr(sorted_keys), _lib.ptr(order), _lib.stream_ptr(s))
         idx = order
+        # the warp launch order too, off the critical path (it reads the
+        # learned table as of the previous completed update)
+        warp_order = _sched_order(tree, sorted_keys, n, s) if WARP_SCHED and 0 < n <= SCHED_MAX_RAYS else None
         ev = None
         if s is not cur:
             ev = torch.cuda.Event()
             ev.record(s)
-            for t in (idx, sorted_keys):
-                t.record_stream(cur)
-    return RayPlan(n, idx, sorted_keys, ev)
+            for t in (idx, sorted_keys, warp_order):
+                if t is not None:
+                    t.record_stream(cur)
+    return RayPlan(n, idx, sorted_keys, ev, warp_order)
 
 
 def render_and_backprop(tree: SparseOctree, origins, dirs, targets, background,
@@ -404,18 +428,15 @@ def render_and_backprop(tree: SparseOctree, origins, dirs, targets, background,
             if plan.n != n:
                 raise InputError(f"ray plan is for {plan.n} rays, batch has {n}")
             plan.wait()
-            idx, sorted_keys = plan.idx, plan.sorted_keys
+            idx, sorted_keys, warp_order = plan.idx, plan.sorted_keys, plan.warp_order
         elif coherent and n >= COHERENT_MIN_RAYS:
             p = plan_batch(tree, o, d, idx)
-            idx, sorted_keys = p.idx, p.sorted_keys
-        if sorted_keys is not None:
-            if WARP_SCHED and n <= SCHED_MAX_RAYS:
-                # launch the warps whose key buckets were costliest last time first
-                table = _sched_table(tree)
-                warp_order = torch.empty((n + 31) // 32, dtype=torch.int32, device=tree.device)
-                _lib.call("dot_sched_order", _lib.ptr(sorted_keys), n, _lib.ptr(table),
-                          _lib.ptr(warp_order), _lib.stream_ptr())
-                ray_used = torch.empty(n, dtype=torch.int16, device=tree.device)
+            idx, sorted_keys, warp_order = p.idx, p.sorted_keys, p.warp_order
+        if sorted_keys is not None and WARP_SCHED and n <= SCHED_MAX_RAYS:
+            # launch the warps whose key buckets were costliest last time first
+            if warp_order is None:
+                warp_order = _sched_order(tree, sorted_keys, n, torch.cuda.current_stream(tree.device))
+            ray_used = torch.empty(n, dtype=torch.int16, device=tree.device)
         if kernel_events is not None:
             kernel_events[0].record()
         if deterministic:
@@ -433,11 +454,19 @@ def render_and_backprop(tree: SparseOctree, origins, dirs, targets, background,
                       float(early_stop_eps), float(t_near), float(t_far), gs, _lib.ptr(ws.dsigma),
                       _lib.ptr(ws.dsh_store), tree.sh_stride, _lib.ptr(ws.signal), _lib.ptr(ws.touched),
                       _lib.ptr(ws.loss), _lib.ptr(rgb), int(kernel_flags), _lib.stream_ptr())
-        if ray_used is not None:
-            _lib.call("dot_sched_update", _lib.ptr(sorted_keys), _lib.ptr(ray_used), n,
-                      _lib.ptr(_sched_table(tree)), _lib.stream_ptr())
         if kernel_events is not None:
             kernel_events[1].record()
+        if ray_used is not None:
+            # write the table only after every side-stream reader queued so far
+            table = _sched_table(tree)
+            cur = torch.cuda.current_stream(tree.device)
+            if tree._sched_read is not None:
+                cur.wait_event(tree._sched_read)
+            _lib.call("dot_sched_update", _lib.ptr(sorted_keys), _lib.ptr(ray_used), n,
+                      _lib.ptr(table), _lib.stream_ptr())
+            ev = torch.cuda.Event()
+            ev.record(cur)
+            tree._sched_written = ev
     nsh = 3 * tree.basis_count
     dsh = ws.dsh_store if nsh == tree.sh_stride else ws.dsh_store[:, :nsh]
     if io.numpy:
