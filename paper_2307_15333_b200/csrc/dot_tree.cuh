@@ -308,11 +308,12 @@ __device__ __forceinline__ void sh_dot(const float* __restrict__ row, const floa
     e2 = e[2];
 }
 
-// Branch-stable logistic (_kernels.py:22-27) in fp32.
+// Stable logistic (_kernels.py:22-27) in fp32, branch-free: with
+// e = exp(-|x|) <= 1, 1 / (1 + e) for x >= 0 and e / (1 + e) otherwise.
 __device__ __forceinline__ float sigmoidf(float x) {
-    if (x >= 0.f) return __frcp_rn(1.f + __expf(-x));
-    const float e = __expf(x);
-    return __fdividef(e, 1.f + e);
+    const float e = __expf(-fabsf(x));
+    const float r = __fdividef(1.f, 1.f + e);
+    return x >= 0.f ? r : e * r;
 }
 
 // Vector reduction into global memory (REDG.E.ADD.F32x4, sm_90+).
