@@ -122,7 +122,7 @@ __global__ void __launch_bounds__(kBlock, kFwdMinBlocks) render_fwd_kernel(
                 c1 += tq * double(sigmoidf(e1));
                 c2 += tq * double(sigmoidf(e2));
                 ws += tq;
-                dep += tq * (te + 0.5 * dl);
+                if (depth_out) dep += tq * (te + 0.5 * dl);
             }
             trans *= a;
             if (eps > 0.0 && trans < eps) break;
@@ -648,7 +648,7 @@ __global__ void __launch_bounds__(kBlock, kFwdMinBlocks) render_camera_kernel(
                 c0 += tq * double(sigmoidf(e0));
                 c1 += tq * double(sigmoidf(e1));
                 c2 += tq * double(sigmoidf(e2));
-                dep += tq * (te + 0.5 * dl);
+                if (depth_out) dep += tq * (te + 0.5 * dl);
             }
             trans *= a;
             if (eps > 0.0 && trans < eps) break;
