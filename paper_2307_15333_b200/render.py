@@ -312,7 +312,9 @@ PLAN_SORT_BEGIN_BIT = 0
 def pool_keys(tree: SparseOctree, origins: torch.Tensor, dirs: torch.Tensor) -> torch.Tensor:
     """31-bit coherence keys of every ray of a resident pool (dot_ray_keys32),
     computed once so that ``plan_batch(..., keys=)`` gathers 4 B per ray
-    instead of re-reading each ray's 48 bytes at random."""
+    instead of re-reading each ray's 48 bytes at random.  Keys only order
+    the work: stale keys (rays edited afterwards) cost speed, never
+    correctness."""
     n = int(origins.shape[0])
     keys = torch.empty(n, dtype=torch.int32, device=tree.device)
     view, _topo = tree.tree_view()
