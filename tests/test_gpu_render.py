@@ -283,6 +283,30 @@ def test_sched_order_is_a_permutation(n):
     assert torch.equal(torch.sort(order.to(torch.int64)).values, torch.arange(nw, device="cuda"))
 
 
+def test_plan_sort_and_pool_keys():
+    """dot_plan_sort is a stable key sort carrying the ray index (== torch's
+    stable sort + gather), and a plan from precomputed pool keys equals the
+    plan computed from the rays; the schedule is a permutation of the warps."""
+    import torch
+    from helpers import irregular_tree, ray_batch
+    from paper_2307_15333_b200.render import plan_batch, pool_keys
+    tree = irregular_tree(31, 4, depth=2, splits=10, max_depth=4, device="cuda")
+    o, d = ray_batch(32, 50000)
+    o, d = torch.from_numpy(o).cuda(), torch.from_numpy(d).cuda()
+    g = torch.Generator(device="cuda")
+    g.manual_seed(3)
+    idx = torch.randperm(50000, generator=g, device="cuda")[:40000]
+    p1 = plan_batch(tree, o, d, idx)
+    keys = pool_keys(tree, o, d)
+    p2 = plan_batch(tree, o, d, idx, keys=keys)
+    ks, perm = torch.sort(keys[idx], stable=True)
+    assert torch.equal(p1.sorted_keys, ks) and torch.equal(p2.sorted_keys, ks)
+    assert torch.equal(p1.idx, idx[perm]) and torch.equal(p2.idx, idx[perm])
+    nw = (40000 + 31) // 32
+    for p in (p1, p2):
+        assert torch.equal(torch.sort(p.warp_order.to(torch.int64)).values, torch.arange(nw, device="cuda"))
+
+
 def test_large_batch_with_schedule_vs_oracle(oracle):
     """A batch large enough for the coherence sort and the learned warp
     schedule (several steps, so the table is warm) against the oracle."""
