@@ -75,9 +75,15 @@ def peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """nvidia-smi clocks / throttle reasons during the timed region.
 
-    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+    The recipe's query, started BEFORE the warm-up (nvidia-smi's own start-up
+    is CPU-heavy and would otherwise delay the first timed launches) and
+    stopped after; ``mark(t0, t1)`` gives the host wall-clock window of the
+    timed region and only samples stamped inside it (widened to the nearest
+    samples when the region is shorter than the sampling period) count."""
+
+    FIELDS = ("timestamp,index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
@@ -85,12 +91,13 @@ class ClockSampler:
         self.index = index
         self.rows = []
         self.proc = None
+        self.window = None
 
     def start(self):
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "50"],
+                 "--format=csv,noheader,nounits", "-lms", "20"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             threading.Thread(target=self._read, daemon=True).start()
         except Exception:
@@ -101,21 +108,45 @@ class ClockSampler:
         for line in self.proc.stdout:
             self.rows.append([x.strip() for x in line.split(",")])
 
+    def mark(self, t0: float, t1: float) -> None:
+        self.window = (t0, t1)
+
+    @staticmethod
+    def _stamp(text: str):
+        import datetime
+        try:
+            return datetime.datetime.strptime(text, "%Y/%m/%d %H:%M:%S.%f").timestamp()
+        except Exception:
+            return None
+
     def stop(self):
+        time.sleep(0.1)  # let the samples bracketing the region arrive
         if self.proc is not None:
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=2)
             except Exception:
                 self.proc.kill()
+        rows = [(self._stamp(r[0]), r) for r in self.rows if len(r) >= 10]
+        rows = [(t, r) for t, r in rows if t is not None]
+        if self.window is not None and rows:
+            a, b = self.window
+            inside = [r for t, r in rows if a <= t <= b]
+            if not inside:  # region shorter than the period: the samples around it
+                before = [r for t, r in rows if t < a][-1:]
+                after = [r for t, r in rows if t > b][:1]
+                inside = before + after
+            picked = inside
+        else:
+            picked = [r for _, r in rows]
         sm, mx, reasons = [], 0.0, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for r in self.rows:
+        for r in picked:
             try:
-                sm.append(float(r[1]))
-                mx = max(mx, float(r[2]))
+                sm.append(float(r[2]))
+                mx = max(mx, float(r[3]))
                 for k, nm in enumerate(names):
-                    if r[5 + k].lower().startswith("active"):
+                    if r[6 + k].lower().startswith("active"):
                         reasons.add(nm)
             except Exception:
                 continue
@@ -301,24 +332,26 @@ def run_ours(args, rank, world, local_rank):
                           kernel_events=kev[k] if timed_kernel else None,
                           kernel_flags=args.bwd_flags, plan=plan)
 
+    clocks = ClockSampler(local_rank).start()  # before the warm-up: its start-up is CPU-heavy
     for k in range(args.warmup):
         step(k)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     setup_s = time.time() - t_setup
-    clocks = ClockSampler(local_rank).start()
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
     # ncu --profile-from-start off captures exactly the timed steps
     profile_range = bool(os.environ.get("DOT_PROFILE_RANGE"))
     if profile_range:
         torch.cuda.profiler.start()
+    h0 = time.time()
     t0.record()
     for k in range(args.warmup, total_steps):
         step(k)
     t1.record()
     torch.cuda.synchronize()
+    clocks.mark(h0, time.time())
     if profile_range:
         torch.cuda.profiler.stop()
     clk = clocks.stop()

@@ -27,7 +27,7 @@ import torch
 
 from . import _lib
 from .errors import InputError
-from .octree import SparseOctree
+from .octree import SparseOctree, locate_level_train
 
 EPS_T = 1e-4  # early-termination transmittance threshold (render.py:23)
 UNIT_TOL = 1e-6
@@ -425,7 +425,7 @@ def render_and_backprop(tree: SparseOctree, origins, dirs, targets, background,
     if n:
         gs = 2.0 / n if grad_scale is None else float(grad_scale)
         bg = _background(background)
-        view, _topo = tree.tree_view()
+        view, _topo = tree.tree_view(locate_level=locate_level_train())
         if plan is not None:
             if plan.n != n:
                 raise InputError(f"ray plan is for {plan.n} rays, batch has {n}")
