@@ -279,8 +279,11 @@ def run_ours(args, rank, world, local_rank):
     gen = torch.Generator(device=dev)
     gen.manual_seed(1234 + rank)
     total_steps = args.warmup + args.steps
-    # an epoch-style permutation of the 64M-ray pool, one slice per step
-    perm = torch.randperm(n_pool, generator=gen, device=dev)[:(total_steps + 2) * per_rank]
+    # epoch-style permutations of the ray pool, one slice per step (a new
+    # permutation whenever the steps outrun the pool: train_epoch's order)
+    need = (total_steps + 2) * per_rank
+    perm = torch.cat([torch.randperm(n_pool, generator=gen, device=dev)
+                      for _ in range((need + n_pool - 1) // n_pool)])[:need]
     perm = perm.reshape(total_steps + 2, per_rank)
     kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
            for _ in range(total_steps)]
