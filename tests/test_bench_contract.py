@@ -27,3 +27,26 @@ def test_reference_arm_json_line():
     assert j["e2e"] == {"value": j["value"], "unit": "rays/s", "h2d_bytes_per_step": 0,
                         "d2h_bytes_per_step": 0}
     assert j["config"]["workload"].startswith("configs[1]")
+
+
+def test_clock_sampler_window():
+    """Only the nvidia-smi samples stamped inside the timed region count;
+    with none inside, the two samples around it do."""
+    import datetime
+    sys.path.insert(0, ROOT)
+    import bench
+
+    def row(t, sm, reason="Not Active"):
+        stamp = datetime.datetime.fromtimestamp(t).strftime("%Y/%m/%d %H:%M:%S.%f")[:-3]
+        return [stamp, "0", str(sm), "1965", "500.0", "0x0", reason, "Not Active", "Not Active", "Not Active"]
+
+    c = bench.ClockSampler(0)
+    c.rows = [row(100.0, 800), row(100.5, 1965), row(100.6, 1965, "Active"), row(101.5, 900)]
+    c.mark(100.4, 100.7)
+    out = c.stop()
+    assert out["samples"] == 2 and out["sm_mhz"] == 1965.0 and out["reasons"] == ["hw_slowdown"]
+    c = bench.ClockSampler(0)
+    c.rows = [row(100.0, 1900), row(100.5, 1965)]
+    c.mark(100.1, 100.2)
+    out = c.stop()
+    assert out["samples"] == 2 and out["sm_max_mhz"] == 1965.0
