@@ -100,6 +100,11 @@ class ClockSampler:
                  "--format=csv,noheader,nounits", "-lms", "20"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             threading.Thread(target=self._read, daemon=True).start()
+            # nvidia-smi's start-up (NVML init) takes ~1 s of CPU: wait for its
+            # first sample so none of it overlaps the timed region
+            t_end = time.time() + 5.0
+            while not self.rows and time.time() < t_end and self.proc.poll() is None:
+                time.sleep(0.02)
         except Exception:
             self.proc = None
         return self
