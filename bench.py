@@ -25,6 +25,7 @@ oracle port, all host threads) on the same workload, rank 0 only.
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import statistics
@@ -83,7 +84,9 @@ class ClockSampler:
     timed region and only samples stamped inside it (widened to the nearest
     samples when the region is shorter than the sampling period) count."""
 
-    FIELDS = ("timestamp,index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+    # power.draw is left out: reading it stalls the driver for tens of ms,
+    # long enough to starve the launch thread of a ~80 ms timed region
+    FIELDS = ("timestamp,index,clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
@@ -94,10 +97,12 @@ class ClockSampler:
         self.window = None
 
     def start(self):
+        if os.environ.get("DOT_BENCH_NO_CLOCKS"):
+            return self
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "20"],
+                 "--format=csv,noheader,nounits", "-lms", "200"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             threading.Thread(target=self._read, daemon=True).start()
             # nvidia-smi's start-up (NVML init) takes ~1 s of CPU: wait for its
@@ -132,7 +137,7 @@ class ClockSampler:
                 self.proc.wait(timeout=2)
             except Exception:
                 self.proc.kill()
-        rows = [(self._stamp(r[0]), r) for r in self.rows if len(r) >= 10]
+        rows = [(self._stamp(r[0]), r) for r in self.rows if len(r) >= 9]
         rows = [(t, r) for t, r in rows if t is not None]
         if self.window is not None and rows:
             a, b = self.window
@@ -151,7 +156,7 @@ class ClockSampler:
                 sm.append(float(r[2]))
                 mx = max(mx, float(r[3]))
                 for k, nm in enumerate(names):
-                    if r[6 + k].lower().startswith("active"):
+                    if r[5 + k].lower().startswith("active"):
                         reasons.add(nm)
             except Exception:
                 continue
@@ -341,8 +346,23 @@ def run_ours(args, rank, world, local_rank):
                           kernel_flags=args.bwd_flags, plan=plan)
 
     clocks = ClockSampler(local_rank).start()  # before the warm-up: its start-up is CPU-heavy
+    # at most LEAD steps in flight: the host waits for step k - LEAD before
+    # queuing step k, so the caching allocator recycles the plans' buffers
+    # instead of growing (cudaMalloc on the launch thread starved the GPU)
+    LEAD = 2
+    done = {}
+
+    def paced(k):
+        if k - LEAD in done:
+            done.pop(k - LEAD).synchronize()
+        out = step(k)
+        ev = torch.cuda.Event()
+        ev.record()
+        done[k] = ev
+        return out
+
     for k in range(args.warmup):
-        step(k)
+        paced(k)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -353,13 +373,16 @@ def run_ours(args, rank, world, local_rank):
     profile_range = bool(os.environ.get("DOT_PROFILE_RANGE"))
     if profile_range:
         torch.cuda.profiler.start()
+    gc.collect()
+    gc.disable()  # no collector pause between the launches of the timed steps
     h0 = time.time()
     t0.record()
     for k in range(args.warmup, total_steps):
-        step(k)
+        paced(k)
     t1.record()
     torch.cuda.synchronize()
     clocks.mark(h0, time.time())
+    gc.enable()
     if profile_range:
         torch.cuda.profiler.stop()
     clk = clocks.stop()
@@ -431,10 +454,13 @@ def run_ours(args, rank, world, local_rank):
         loop(args.warmup)
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        gc.collect()
+        gc.disable()
         e0.record()
         loop(args.steps)
         e1.record()
         torch.cuda.synchronize()
+        gc.enable()
         t = e0.elapsed_time(e1)
         if world > 1:
             tt = torch.tensor([t], device=dev)

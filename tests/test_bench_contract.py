@@ -38,7 +38,7 @@ def test_clock_sampler_window():
 
     def row(t, sm, reason="Not Active"):
         stamp = datetime.datetime.fromtimestamp(t).strftime("%Y/%m/%d %H:%M:%S.%f")[:-3]
-        return [stamp, "0", str(sm), "1965", "500.0", "0x0", reason, "Not Active", "Not Active", "Not Active"]
+        return [stamp, "0", str(sm), "1965", "0x0", reason, "Not Active", "Not Active", "Not Active"]
 
     c = bench.ClockSampler(0)
     c.rows = [row(100.0, 800), row(100.5, 1965), row(100.6, 1965, "Active"), row(101.5, 900)]
