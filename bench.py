@@ -42,6 +42,7 @@ sys.path.insert(0, ROOT)
 METRIC = ("rays/sec render & fwd+bwd per GPU (1/2/4/8 B200), 800x800 FPS, refine ms, "
           "%HBM roofline")
 BATCH = 1 << 20
+E2E_BATCHES = 8  # distinct pinned host batches the e2e loop cycles through
 N_VIEWS = 100
 W = H = 800
 RADIUS = 4.03
@@ -263,6 +264,16 @@ def build_training_pool(tree, device, wl=None):
     return origins, dirs, targets
 
 
+def workload_config(wl, tree, world):
+    """The line's ``config``: what defines the workload, identical on both
+    arms (``--impl reference`` prints the same dict)."""
+    return {"workload": wl.desc, "leaves": int(tree.leaf_count), "nodes": int(tree.topology().n_nodes),
+            "global_batch": wl.batch(world) * world, "views": wl.views, "resolution": [wl.W, wl.H],
+            "batch_draw": "uniform random rays of the resident training-view ray pool, a fresh "
+                          "epoch permutation slice per step",
+            "eps": EPS, "background": BG, "l2": wl.l2}
+
+
 # ---------------------------------------------------------------------------
 # our arm
 
@@ -342,8 +353,7 @@ def run_ours(args, rank, world, local_rank):
         return train_step(tree, origins, dirs, targets, state, buf, sws, BG, EPS,
                           ray_index=idx, grad_scale=gs,
                           exchange=exchange if world > 1 else None,
-                          kernel_events=kev[k] if timed_kernel else None,
-                          kernel_flags=args.bwd_flags, plan=plan)
+                          kernel_events=kev[k] if timed_kernel else None, plan=plan)
 
     clocks = ClockSampler(local_rank).start()  # before the warm-up: its start-up is CPU-heavy
     # at most LEAD steps in flight: the host waits for step k - LEAD before
@@ -420,8 +430,8 @@ def run_ours(args, rank, world, local_rank):
     # "serial_ms_per_step": the same loop with blocking copies + reads.
     from paper_2307_15333_b200.staging import LossReader, RayBatchStager
     host = []
-    for j in range(2):
-        idx = perm[j]
+    for j in range(E2E_BATCHES):  # distinct pinned host batches, cycled
+        idx = perm[j % perm.shape[0]]
         host.append(tuple(x[idx].cpu().pin_memory() for x in (origins, dirs, targets)))
     torch.cuda.synchronize()
 
@@ -429,7 +439,7 @@ def run_ours(args, rank, world, local_rank):
 
     def serial_loop(steps):
         for k in range(steps):
-            o_h, d_h, t_h = host[k % 2]
+            o_h, d_h, t_h = host[k % len(host)]
             loss = train_step(tree, o_h, d_h, t_h, state, buf, sws, BG, EPS, grad_scale=gs,
                               exchange=ex)
             float(loss.item())
@@ -442,7 +452,7 @@ def run_ours(args, rank, world, local_rank):
         for k in range(steps):
             o_d, d_d, t_d, plan = stager.take_with_plan()
             if k + 1 < steps:
-                stager.stage(*host[(k + 1) % 2])
+                stager.stage(*host[(k + 1) % len(host)])
             loss = train_step(tree, o_d, d_d, t_d, state, buf, sws, BG, EPS, grad_scale=gs,
                               exchange=ex, plan=plan)
             stager.release()
@@ -495,18 +505,17 @@ def run_ours(args, rank, world, local_rank):
         "higher_is_better": True,
         "scaling": wl.scaling,
         "vs_baseline": None,
-        "dtype": "f64",
-        "dtype_detail": "f64 traversal/transmittance/accumulation, f32 SH shading and leaf gradients",
+        "dtype": "mixed f64/f32",
+        "dtype_detail": "f64 traversal, transmittance, colour accumulation, loss and per-leaf signal; "
+                        "f32 SH dot products, sigmoid and leaf gradients (north star: fp32 tolerance "
+                        "1e-4 abs / 1e-3 rel)",
         "data": "synthetic (seeded blob-field scene, random-init SH, targets from a perturbed copy)",
-        "config": {
-            "workload": wl.desc,
-            "leaves": int(tree.leaf_count), "nodes": int(tree.topology().n_nodes),
-            "global_batch": n_global, "views": wl.views, "resolution": [wl.W, wl.H],
+        "config": workload_config(wl, tree, world),
+        "run": {
             "segments_per_ray": seg / per_rank, "composited_per_ray": comp / per_rank,
-            "l2": wl.l2,
             "parallelism": f"rays sharded dp{world}, tree replicated",
             "exchange": args.exchange if world > 1 else "none",
-            "batch_order": args.order, "bwd_flags": args.bwd_flags,
+            "batch_order": args.order,
             "plan": "coherence order of step k+1 sorted on a side stream during step k; the "
                     "resident pool's 31-bit ray keys computed once at setup (render.pool_keys)",
         },
@@ -528,6 +537,7 @@ def run_ours(args, rank, world, local_rank):
                 "d2h_bytes_per_step": 8, "ms_per_step": e2e_ms / args.steps,
                 "api": "RayBatchStager (H2D + coherence sort of step k+1 overlap step k) + optim.train_step "
                        "(render_and_backprop + rmsprop_step) + LossReader (loss read one step late)",
+                "host_batches": E2E_BATCHES,
                 "serial_ms_per_step": e2e_serial_ms / args.steps},
         "clocks": clk,
         "render": render,
@@ -689,82 +699,122 @@ def bench_refine(dev, args):
 
 
 def cpu_baseline(tree, args, n_rays=1 << 20):
-    """The C oracle port of the reference kernels, all host threads, on a
-    bounded sample of the same training workload."""
-    import torch
+    """The C oracle port of the reference kernels on this host's cores, on a
+    bounded sample of the same training workload (uniform random rays of the
+    100-view pool, like the timed batches): all threads on 2^20 rays, and
+    one thread on 2^16 rays."""
     from oracle import oracle as O
     from paper_2307_15333_b200 import scenes
     O.build()
     focal, poses = scenes.hemisphere_cameras(N_VIEWS, W, H, RADIUS, seed=3)
     rng = np.random.default_rng(9)
-    os_, ds_ = [], []
-    for v in rng.choice(N_VIEWS, 8, replace=False):
-        o, d = scenes.pinhole_rays(W, H, focal, poses[v])
-        pick = rng.choice(o.shape[0], n_rays // 8, replace=False)
-        os_.append(o[pick])
-        ds_.append(d[pick])
-    o, d = np.concatenate(os_), np.concatenate(ds_)
+    o, d = pool_rays_np(focal, poses, W, H, rng.integers(0, N_VIEWS * W * H, n_rays))
     tg = rng.uniform(0.0, 1.0, o.shape)
     tree._host()  # pool arrays for the oracle (outside the timing)
     O.render_and_backprop(tree, o[:256], d[:256], tg[:256], BG, EPS)
     t = time.perf_counter()
     O.render_and_backprop(tree, o, d, tg, BG, EPS)
     dt = time.perf_counter() - t
-    return {"value": o.shape[0] / dt, "unit": "rays/s", "cores": O.num_threads(), "kind": "port",
-            "sample": f"{o.shape[0]} rays (8 of the 100 training views) fwd+bwd through "
+    cores = O.num_threads()
+    m = 1 << 16
+    O.set_threads(1)
+    t1 = time.perf_counter()
+    O.render_and_backprop(tree, o[:m], d[:m], tg[:m], BG, EPS)
+    dt1 = time.perf_counter() - t1
+    O.set_threads(cores)
+    return {"value": o.shape[0] / dt, "unit": "rays/s", "cores": cores, "kind": "port",
+            "sample": f"{o.shape[0]} uniform random rays of the 100-view pool, fwd+bwd through "
                       "oracle/dot_oracle.c (count+fill+grad+serial scatter, OpenMP)",
-            "seconds": dt}
+            "seconds": dt,
+            "one_thread": {"value": m / dt1, "unit": "rays/s", "cores": 1,
+                           "sample": f"{m} of the same rays, one OpenMP thread"}}
 
 
 # ---------------------------------------------------------------------------
 # reference arm
 
+def pool_rays_np(focal, poses, W, H, flat):
+    """Rays of pool entries ``flat`` (view-major, row-major pixels) of a
+    pinhole camera rig -- the same pixel convention as scene_io.Camera.rays
+    (scene_io.py:77-91), for a random subset of the pool."""
+    view = flat // (W * H)
+    pix = flat - view * (W * H)
+    y = pix // W
+    x = pix - y * W
+    cam = np.stack([(x + 0.5 - 0.5 * W) / focal, -(y + 0.5 - 0.5 * H) / focal, -np.ones(flat.size)], axis=1)
+    P = np.asarray(poses, dtype=np.float64)[view]
+    world = np.einsum("nj,nij->ni", cam, P[:, :3, :3])
+    world /= np.linalg.norm(world, axis=1, keepdims=True)
+    return np.ascontiguousarray(P[:, :3, 3]), np.ascontiguousarray(world)
+
+
 def run_reference(args):
-    import torch
+    """The reference's algorithm on the host cores (the C oracle port of
+    octrf's Numba kernels, OpenMP over rays -- the reference package is Python
+    + Numba and does not travel to the GPU box): every step is the reference
+    train_epoch loop body (optim.py:146-152) on a 2^20-ray batch drawn like
+    our arm's -- uniform random rays of the 100-view pool --
+    render_and_backprop (count + fill + grad + serial scatter) -> rmsprop_step
+    over the touched leaves -> SignalBuffer.accumulate.  Rank 0 only."""
     from oracle import oracle as O
-    from paper_2307_15333_b200 import scenes
     O.build()
     wl = workloads()[args.workload]  # the same workload as our arm's line
     tree = wl.scene("cpu")
     tree._host()
     focal, poses = wl.cameras()
-    sample = args.ref_sample
+    n_pool = wl.views * wl.W * wl.H
+    sample = args.ref_sample or wl.batch(1)
     rng = np.random.default_rng(11)
-    batches = []
-    for k in range(args.warmup + args.steps):
-        v = rng.integers(wl.views)
-        o, d = scenes.pinhole_rays(wl.W, wl.H, focal, poses[v])
-        pick = rng.choice(o.shape[0], sample, replace=False)
-        batches.append((o[pick], d[pick], rng.uniform(0.0, 1.0, (sample, 3))))
+
+    def batch():
+        flat = rng.integers(0, n_pool, sample)
+        o, d = pool_rays_np(focal, poses, wl.W, wl.H, flat)
+        return o, d, rng.uniform(0.0, 1.0, (sample, 3))
+
     sig = tree.sigma.numpy()
     sh = tree.sh.numpy()
     vs = np.zeros(tree.capacity)
     vh = np.zeros((tree.capacity, 3 * tree.basis_count))
+    acc = np.zeros(tree.capacity)
 
     def step(b):
         o, d, tg = b
         loss, g, s = O.render_and_backprop(tree, o, d, tg, BG, EPS)
         O.rmsprop_step(sig, sh, vs, vh, g.dsigma, g.dsh, g.touched)
+        acc[:] += s
         return loss
 
+    batches = [batch() for _ in range(min(args.warmup + args.steps, 4))]  # drawn outside the timing
     for k in range(args.warmup):
-        step(batches[k])
+        step(batches[k % len(batches)])
     t = time.perf_counter()
-    for k in range(args.warmup, args.warmup + args.steps):
-        step(batches[k])
+    for k in range(args.steps):
+        step(batches[(args.warmup + k) % len(batches)])
     dt = time.perf_counter() - t
     value = sample * args.steps / dt
+    cores = O.num_threads()
+    # the scalar figure (BASELINE.md section 3): one thread, a 2^16-ray slice
+    o, d, tg = batches[0]
+    m = 1 << 16
+    O.set_threads(1)
+    t1 = time.perf_counter()
+    O.render_and_backprop(tree, o[:m], d[:m], tg[:m], BG, EPS)
+    dt1 = time.perf_counter() - t1
+    O.set_threads(cores)
     return {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "rays/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
         "higher_is_better": True, "scaling": wl.scaling, "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic",
-        "config": {"workload": wl.desc, "leaves": int(tree.leaf_count), "sample_rays_per_step": sample,
-                   "host": "CPU only (the reference path is CPU code); N GPUs of the line are unused"},
-        "cpu_baseline": {"value": value, "unit": "rays/s", "cores": O.num_threads(), "kind": "port",
-                         "sample": f"{sample} rays per step from one random training view, "
-                                   "fwd+bwd (count+fill+grad+serial scatter) + RMSProp"},
+        "data": "synthetic (seeded blob-field scene, random-init SH, uniform random targets)",
+        "config": workload_config(wl, tree, args.gpus),
+        "cpu_baseline": {"value": value, "unit": "rays/s", "cores": cores, "kind": "port",
+                         "sample": f"{sample} rays per step (uniform random rays of the {wl.views}-view pool; "
+                                   f"{len(batches)} pre-drawn batches cycled), fwd+bwd (count + fill + grad + "
+                                   "serial scatter) + RMSProp over the touched leaves + signal accumulate",
+                         "one_thread": {"value": m / dt1, "unit": "rays/s", "cores": 1,
+                                        "sample": f"{m} rays fwd+bwd, one OpenMP thread"}},
         "e2e": {"value": value, "unit": "rays/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "host": "CPU only (the reference path is CPU code); the line's GPUs are unused",
     }
 
 
@@ -777,7 +827,8 @@ def main():
     ap.add_argument("--skip-render", action="store_true")
     ap.add_argument("--skip-refine", action="store_true")
     ap.add_argument("--skip-cpu", action="store_true")
-    ap.add_argument("--ref-sample", type=int, default=1 << 18)
+    ap.add_argument("--ref-sample", type=int, default=0,
+                    help="rays per reference-arm step (default: our arm's per-GPU batch)")
     ap.add_argument("--workload", choices=["c2", "c4"], default="c2",
                     help="c2 = configs[1] (the headline line), c4 = configs[3] (8.5M leaves, 1080p)")
     ap.add_argument("--order", choices=["random", "raster", "morton"], default="random",
@@ -787,9 +838,6 @@ def main():
     ap.add_argument("--exchange", choices=["nccl", "peer"], default="nccl",
                     help="N > 1 gradient exchange: chunked NCCL all-reduce + RMSProp, or the fused "
                          "peer-memory update (dot_rmsprop_step_peers)")
-    ap.add_argument("--bwd-flags", type=int, default=0,
-                    help="dot_render_bwd flags (diagnostics: 1 skip post-cut marks, 8192 pass 1 only, "
-                         "16384 no reductions, 32768 per-lane REDs)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     world = int(os.environ.get("WORLD_SIZE", "1"))

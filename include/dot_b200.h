@@ -121,27 +121,44 @@ int dot_render_cameras(const dot_tree_view* tree, const double* cam_to_world, co
  *     error; the caller divides by n), and sets touched[capacity] u8 to 1 for
  *     every traversed leaf (post-cut segments included, like scatter_kernel).
  *     grad_scale is the reference's 2/n (2/n_global when rays are sharded).
- *     ray_index (may be NULL = 0..n-1) names the n rays to process: ray r of
- *     the batch is origins/dirs/targets[ray_index[r]], read in place (a
- *     caller passes a coherence-sorted order, or a batch drawn from a larger
- *     resident ray pool, without gathering); rgb_out (f32, indexed like the
- *     arrays) may be NULL.  warp_order (may be NULL): block b processes
- *     batch rays [32 w, 32 w + 32) with w = warp_order[b], a permutation of
- *     0..ceil(n/32)-1 (dot_sched_order); results do not depend on it.
- *     ray_used (may be NULL) receives each batch ray's composited-segment
- *     count (u16, saturating) for dot_sched_update.
- *     flags: bit 0 = skip post-cut touched marking
- *     (not reference semantics); bit 15 = per-lane REDs instead of the
- *     warp-cooperative SH-row scatter (implied for capacity > 2^27);
- *     bits 13 / 14 = timing diagnostics
- *     (pass 1 only / no reductions: results are incomplete). */
+ *     origins/dirs/targets hold n_pool rays; ray_index (may be NULL =
+ *     0..n_rays-1, then n_pool >= n_rays) names the n_rays rays to process:
+ *     ray r of the batch is origins/dirs/targets[ray_index[r]], read in place
+ *     (a coherence-sorted order, or a batch drawn from a larger resident ray
+ *     pool, without gathering).  An index outside [0, n_pool) skips that ray
+ *     and makes loss_sum NaN (kernels cannot raise).  rgb_out (f32, indexed
+ *     like the arrays) may be NULL.  warp_order (may be NULL): block b
+ *     processes batch rays [32 w, 32 w + 32) with w = warp_order[b], a
+ *     permutation of 0..ceil(n/32)-1 (dot_sched_order); results do not depend
+ *     on it.  ray_used (may be NULL) receives each batch ray's
+ *     composited-segment count (u16, saturating) for dot_sched_update.
+ *     weight_sum / weight_max (f64 [capacity], may be NULL; no reference
+ *     counterpart, defined by oracle_weights): per leaf += / max= the
+ *     compositing weight T_i Q_i of every composited segment.
+ *     flags: 0, or bit 15 = per-lane REDs instead of the warp-cooperative
+ *     SH-row scatter (implied for capacity > 2^27); other bits are rejected. */
 int dot_render_bwd(const dot_tree_view* tree, const double* origins, const double* dirs,
-                   const double* targets, const int64_t* ray_index, const int32_t* warp_order,
-                   uint16_t* ray_used, int64_t n_rays, const double* background,
-                   double early_stop_eps, double t_near, double t_far, double grad_scale,
-                   float* grad_sigma, float* grad_sh, int32_t gsh_stride, double* signal,
-                   uint8_t* touched, double* loss_sum, float* rgb_out, int32_t flags,
-                   void* stream);
+                   const double* targets, int64_t n_pool, const int64_t* ray_index,
+                   const int32_t* warp_order, uint16_t* ray_used, int64_t n_rays,
+                   const double* background, double early_stop_eps, double t_near, double t_far,
+                   double grad_scale, float* grad_sigma, float* grad_sh, int32_t gsh_stride,
+                   double* signal, uint8_t* touched, double* loss_sum, float* rgb_out,
+                   double* weight_sum, double* weight_max, int32_t flags, void* stream);
+
+/* --- signal-only forward (the training signal of grad_kernel +
+ *     scatter_kernel, _kernels.py:249-282, 337, without gradients; what
+ *     signals.SignalBuffer.accumulate, signals.py:58-69, consumes): per
+ *     composited (pre-cut) segment signal[leaf] += Q = 1 - exp(-sigma delta),
+ *     weight_sum[leaf] += T_i Q_i, weight_max[leaf] = max(., T_i Q_i) (f64
+ *     [capacity] each), touched[leaf] = 1 for every traversed leaf including
+ *     post-cut ones; every output may be NULL (at least one must be given).
+ *     Reads sigma only (no SH rows).  Rays as in dot_render_bwd; indices
+ *     outside [0, n_pool) are skipped and counted into *invalid_rays (u64,
+ *     device, may be NULL). */
+int dot_signal_fwd(const dot_tree_view* tree, const double* origins, const double* dirs, int64_t n_pool,
+                   const int64_t* ray_index, int64_t n_rays, double early_stop_eps, double t_near,
+                   double t_far, double* signal, double* weight_sum, double* weight_max,
+                   uint8_t* touched, uint64_t* invalid_rays, void* stream);
 
 /* --- deterministic fused forward + backward: same inputs and outputs as
  *     dot_render_bwd (accumulates into the same buffers; rgb not returned),
@@ -185,8 +202,9 @@ int dot_sched_update(const int32_t* sorted_keys, const uint16_t* ray_used, int64
 int dot_ray_keys(const dot_tree_view* tree, const double* origins, const double* dirs,
                  int64_t n_rays, uint64_t* keys, void* stream);
 /* 31-bit keys (origin 4 bits/axis, direction 10x9 bits): half the sort
- * passes.  ray_index (may be NULL) as in dot_render_bwd. */
-int dot_ray_keys32(const dot_tree_view* tree, const double* origins, const double* dirs,
+ * passes.  n_pool / ray_index (may be NULL) as in dot_render_bwd; an
+ * out-of-range index gets key 0. */
+int dot_ray_keys32(const dot_tree_view* tree, const double* origins, const double* dirs, int64_t n_pool,
                    const int64_t* ray_index, int64_t n_rays, int32_t* keys, void* stream);
 
 /* The batch's coherence order: radix sort of keys (dot_ray_keys32) by bits

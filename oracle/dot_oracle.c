@@ -317,6 +317,44 @@ void oracle_scatter(const int64_t* offsets, int64_t n_rays, const int64_t* seg_l
     }
 }
 
+/* North-star extras with no reference counterpart, DEFINED here on the
+ * reference's own segment lists (render.py:105-124) and compositing order
+ * (_kernels.py:189-224): per ray the expected termination depth
+ * sum_i T_i Q_i (t_i + delta_i / 2); per leaf the sum and the max over
+ * composited (pre-cut, crossing segment included) segments of the
+ * compositing weight T_i Q_i.  Serial in ray-major order (like the scatter).
+ * Any output may be NULL. */
+void oracle_weights(const float* sigma, const int64_t* offsets, int64_t n_rays, const int64_t* seg_leaf,
+                    const double* seg_t, const double* seg_delta, double eps, double* depth,
+                    double* weight_sum, double* weight_max) {
+    for (int64_t r = 0; r < n_rays; ++r) {
+        double trans = 1.0, dep = 0.0;
+        for (int64_t s = offsets[r]; s < offsets[r + 1]; ++s) {
+            double a = exp(-(double)sigma[seg_leaf[s]] * seg_delta[s]);
+            double q = 1.0 - a;
+            double w = trans * q;
+            if (q > 0.0) {
+                dep += w * (seg_t[s] + 0.5 * seg_delta[s]);
+                if (weight_sum) weight_sum[seg_leaf[s]] += w;
+                if (weight_max && w > weight_max[seg_leaf[s]]) weight_max[seg_leaf[s]] = w;
+            }
+            trans *= a;
+            if (eps > 0.0 && trans < eps) break;
+        }
+        if (depth) depth[r] = dep;
+    }
+}
+
+/* Thread count of the OpenMP loops (the CPU baseline's 1-thread figure). */
+void oracle_set_threads(int n) {
+#ifdef _OPENMP
+    extern void omp_set_num_threads(int);
+    omp_set_num_threads(n);
+#else
+    (void)n;
+#endif
+}
+
 int oracle_num_threads(void) {
 #ifdef _OPENMP
     extern int omp_get_max_threads(void);

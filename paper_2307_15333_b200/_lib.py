@@ -14,9 +14,11 @@ from .errors import ConfigError, InputError, OctrfError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libdot_b200.so")
+# experiment builds only (tools/): another in-tree build of the same ABI
+_LIB_OVERRIDE = os.environ.get("DOT_LIB_PATH")
 
 DOT_OK, DOT_BAD_ARG, DOT_OOM, DOT_CUDA_ERR, DOT_NO_DEVICE = range(5)
-ABI_VERSION = 8
+ABI_VERSION = 9
 
 c_void_p = ctypes.c_void_p
 c_i64 = ctypes.c_int64
@@ -69,10 +71,11 @@ _SIGNATURES = {
                                   c_void_p, c_void_p, c_void_p]),
     "dot_render_cameras": (c_i32, [c_void_p, c_void_p, c_void_p, c_i32, c_i32, c_i32, c_void_p, c_f64, c_void_p,
                                    c_void_p, c_void_p, c_void_p]),
-    "dot_render_bwd":(c_i32, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_i64, c_void_p,
-                               c_f64, c_f64,
-                               c_f64, c_f64, c_void_p, c_void_p, c_i32, c_void_p, c_void_p, c_void_p,
-                               c_void_p, c_i32, c_void_p]),
+    "dot_render_bwd": (c_i32, [c_void_p, c_void_p, c_void_p, c_void_p, c_i64, c_void_p, c_void_p, c_void_p, c_i64,
+                               c_void_p, c_f64, c_f64, c_f64, c_f64, c_void_p, c_void_p, c_i32, c_void_p,
+                               c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_i32, c_void_p]),
+    "dot_signal_fwd": (c_i32, [c_void_p, c_void_p, c_void_p, c_i64, c_void_p, c_i64, c_f64, c_f64, c_f64,
+                               c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
     "dot_render_bwd_sorted": (c_i32, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
                                       c_i64, c_void_p,
                                       c_f64, c_f64, c_f64, c_f64, c_void_p, c_void_p, c_i32, c_void_p,
@@ -80,7 +83,7 @@ _SIGNATURES = {
     "dot_sched_order": (c_i32, [c_void_p, c_i64, c_void_p, c_void_p, c_void_p]),
     "dot_sched_update": (c_i32, [c_void_p, c_void_p, c_i64, c_void_p, c_void_p]),
     "dot_ray_keys": (c_i32, [c_void_p, c_void_p, c_void_p, c_i64, c_void_p, c_void_p]),
-    "dot_ray_keys32": (c_i32, [c_void_p, c_void_p, c_void_p, c_void_p, c_i64, c_void_p, c_void_p]),
+    "dot_ray_keys32": (c_i32, [c_void_p, c_void_p, c_void_p, c_i64, c_void_p, c_i64, c_void_p, c_void_p]),
     "dot_plan_sort": (c_i32, [c_void_p, c_void_p, c_i64, c_i32, c_void_p, c_void_p, c_void_p]),
     "dot_ray_stats":(c_i32, [c_void_p, c_void_p, c_void_p, c_i64, c_f64, c_void_p, c_void_p]),
     "dot_refine_plan_create": (c_i32, [c_void_p, c_void_p, c_void_p, c_i32, c_f64, c_f64, c_i32, c_i32,
@@ -106,9 +109,10 @@ class ExtensionError(OctrfError):
     """The CUDA extension is missing, failed to load, or a CUDA call failed."""
 
 
-def load(path: str = LIB_PATH):
+def load(path: str | None = None):
     """Load libdot_b200.so (raises ExtensionError if absent -- no fallback)."""
     global _lib
+    path = path or _LIB_OVERRIDE or LIB_PATH
     with _lock:
         if _lib is not None:
             return _lib

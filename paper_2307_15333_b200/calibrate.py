@@ -19,7 +19,7 @@ from __future__ import annotations
 
 import ctypes
 import json
-from dataclasses import dataclass, field
+from dataclasses import dataclass
 
 import numpy as np
 import torch
@@ -62,15 +62,37 @@ class RefineRemap:
     rounds: int
 
 
-@dataclass
 class CalibrationReport:
-    leaves_before: int
-    leaves_after: int
-    merges_applied: int
-    splits_applied: int
-    recursion_rounds: int
-    events: list = field(default_factory=list)
-    remap: RefineRemap | None = None
+    """calibrate.py:45-68.  ``events`` is materialised on first access from
+    the device-side ``remap`` (merge rounds, split sources, the new node
+    table), so a report nobody reads the events of costs no host work."""
+
+    def __init__(self, leaves_before: int, leaves_after: int, merges_applied: int, splits_applied: int,
+                 recursion_rounds: int, events: list | None = None, remap: "RefineRemap | None" = None,
+                 new_node: torch.Tensor | None = None):
+        self.leaves_before = leaves_before
+        self.leaves_after = leaves_after
+        self.merges_applied = merges_applied
+        self.splits_applied = splits_applied
+        self.recursion_rounds = recursion_rounds
+        self.remap = remap
+        self._new_node = new_node
+        self._events = events
+
+    @property
+    def events(self) -> list:
+        if self._events is None:
+            self._events = _events_from_remap(self.remap, self._new_node)
+        return self._events
+
+    @events.setter
+    def events(self, value):
+        self._events = value
+
+    def __repr__(self) -> str:
+        return (f"CalibrationReport(leaves_before={self.leaves_before}, leaves_after={self.leaves_after}, "
+                f"merges_applied={self.merges_applied}, splits_applied={self.splits_applied}, "
+                f"recursion_rounds={self.recursion_rounds})")
 
     def to_json(self) -> str:
         return json.dumps({
@@ -174,28 +196,29 @@ def _acc_for(buffer: SignalBuffer, acc=None):
     return a, use_sigma
 
 
-def _events(plan: _Plan, remap: RefineRemap | None) -> list:
-    """Reference-style event list (lazy host work; see module docstring)."""
-    ev = []
-    node_old = plan.topo.node.cpu().numpy().astype(np.int64)
-    # the reference logs merges by (round, pool id) and splits by pool id
-    mp = plan.pool_ids(plan.merge_parents)
-    order = np.lexsort((mp, plan.merge_round))
-    for p in plan.merge_parents[order]:
-        kids = node_old[p] + np.arange(8)
-        ev.append(("merge", int(plan.pool_ids(np.array([p]))[0]),
-                   tuple(int(k) for k in plan.pool_ids(kids))))
-    if plan.split_leaves.size and remap is not None:
-        src = remap.src_index.cpu().numpy()
-        kind = remap.src_kind.cpu().numpy()
-        new_node = plan.tree.topology().node.cpu().numpy()
-        parents = np.nonzero(kind == K_SPLITPARENT)[0]
-        first = {int(src[i]): int(new_node[i]) for i in parents}
-        sp = plan.pool_ids(plan.split_leaves)
-        for leaf in plan.split_leaves[np.argsort(sp, kind="stable")]:
-            f = first[int(leaf)]
-            ev.append(("split", int(plan.pool_ids(np.array([leaf]))[0]),
-                       tuple(range(f, f + 8))))
+def _events_from_remap(remap: RefineRemap | None, new_node: torch.Tensor | None) -> list:
+    """Reference-style event list (calibrate.py:45-68), vectorised: merges
+    ("merge", parent, kids) by (round, pool id) with old pool ids, then splits
+    ("split", leaf, kids) by ascending pool id with the new canonical ids of
+    the 8 children (the refined tree is canonical, see module docstring)."""
+    if remap is None:
+        return []
+    node_old = remap.old_node.cpu().numpy().astype(np.int64)
+    pool = (remap.old_pool_id.cpu().numpy().astype(np.int64) if remap.old_pool_id is not None
+            else np.arange(node_old.size, dtype=np.int64))
+    mr = remap.merge_round.cpu().numpy()
+    p = np.nonzero(mr)[0]
+    p = p[np.lexsort((pool[p], mr[p]))]
+    mk = pool[node_old[p][:, None] + np.arange(8)]
+    ev = [("merge", a, tuple(b)) for a, b in zip(pool[p].tolist(), mk.tolist())]
+    kind = remap.src_kind.cpu().numpy()
+    sp = np.nonzero(kind == K_SPLITPARENT)[0]
+    if sp.size:
+        leaf = pool[remap.src_index.cpu().numpy()[sp]]
+        first = new_node.cpu().numpy().astype(np.int64)[sp]
+        o = np.argsort(leaf, kind="stable")
+        kids = first[o][:, None] + np.arange(8)
+        ev += [("split", a, tuple(b)) for a, b in zip(leaf[o].tolist(), kids.tolist())]
     return ev
 
 
@@ -205,14 +228,13 @@ def _run(tree, buffer, tau, gamma, recursive, threshold, apply=True, acc=None, e
     plan = _Plan(tree, a, use_sigma, tau, gamma, recursive, threshold)
     try:
         st = plan.stats
-        if lists or events:
+        if lists:
             plan._fetch_lists()  # before apply: the lists describe the old tree
         remap = plan.apply() if apply else None
+        new_node = tree.topology().node if apply else None
         report = CalibrationReport(int(st.leaves_before), int(st.leaves_after),
                                    int(st.merges_applied), int(st.splits_applied),
-                                   int(st.recursion_rounds), [], remap)
-        if events:
-            report.events = _events(plan, remap)
+                                   int(st.recursion_rounds), None if events else [], remap, new_node)
         return report, plan
     finally:
         plan.close()
@@ -257,7 +279,10 @@ def sample(tree, buffer: SignalBuffer, gamma: float, threshold=None) -> Calibrat
 
 def calibrate(tree, buffer: SignalBuffer, config: CalibrationConfig,
               events: bool = True) -> CalibrationReport:
-    """One calibration event: prune, sample on the post-prune topology, reset."""
+    """One calibration event: prune, sample on the post-prune topology, reset.
+
+    ``report.events`` is built lazily on first access (``events=False``
+    returns an empty list instead)."""
     buffer.check_fresh()
     gamma = config.gamma if (config.sample_threshold is not None or config.gamma > 0.0) else 0.0
     report, _ = _run(tree, buffer, config.tau, gamma, 1 if config.recursive else 0,

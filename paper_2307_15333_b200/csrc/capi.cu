@@ -68,7 +68,7 @@ using namespace dot;
 
 extern "C" {
 
-int dot_abi_version(void) { return 8; }
+int dot_abi_version(void) { return 9; }
 
 const char* dot_last_error(void) { return g_err; }
 
@@ -152,15 +152,21 @@ int dot_render_fwd(const dot_tree_view* tree, const double* origins, const doubl
 }
 
 int dot_render_bwd(const dot_tree_view* tree, const double* origins, const double* dirs,
-                   const double* targets, const int64_t* ray_index, const int32_t* warp_order,
-                   uint16_t* ray_used, int64_t n_rays, const double* background,
-                   double early_stop_eps, double t_near, double t_far, double grad_scale,
-                   float* grad_sigma, float* grad_sh, int32_t gsh_stride, double* signal,
-                   uint8_t* touched, double* loss_sum, float* rgb_out, int32_t flags,
-                   void* stream) {
+                   const double* targets, int64_t n_pool, const int64_t* ray_index,
+                   const int32_t* warp_order, uint16_t* ray_used, int64_t n_rays,
+                   const double* background, double early_stop_eps, double t_near, double t_far,
+                   double grad_scale, float* grad_sigma, float* grad_sh, int32_t gsh_stride,
+                   double* signal, uint8_t* touched, double* loss_sum, float* rgb_out,
+                   double* weight_sum, double* weight_max, int32_t flags, void* stream) {
     if (int st = validate_tree_view(tree)) return st;
     if (n_rays < 0 || (n_rays && (!origins || !dirs || !targets)) || !background)
         return set_error(DOT_BAD_ARG, "bad ray arrays");
+    if (!ray_index && n_pool < n_rays)
+        return set_error(DOT_BAD_ARG, "n_pool (%lld) < n_rays (%lld) without a ray_index", (long long)n_pool,
+                         (long long)n_rays);
+#ifndef DOT_DIAG_FLAGS
+    if (flags & ~32768) return set_error(DOT_BAD_ARG, "unknown dot_render_bwd flags 0x%x", flags);
+#endif
     if (!grad_sigma || !grad_sh || !signal || !touched || !loss_sum)
         return set_error(DOT_BAD_ARG, "gradient / signal outputs must not be NULL");
     if (gsh_stride != tree->sh_stride)
@@ -170,11 +176,26 @@ int dot_render_bwd(const dot_tree_view* tree, const double* origins, const doubl
     // the warp-cooperative sink packs (pool id, lane) into 32 bits: pool ids
     // need 27 bits, larger pools take the per-lane REDs
     if (tree->capacity > (int64_t(1) << 27)) flags |= 32768;
-    return launch_render_bwd(make_tree(*tree), origins, dirs, targets, ray_index, warp_order, ray_used, n_rays,
-                             background,
-                             early_stop_eps, t_near, t_far, grad_scale, grad_sigma, grad_sh,
-                             signal, touched, loss_sum, rgb_out, flags,
+    return launch_render_bwd(make_tree(*tree), origins, dirs, targets, ray_index, n_pool, warp_order, ray_used,
+                             n_rays, background, early_stop_eps, t_near, t_far, grad_scale, grad_sigma, grad_sh,
+                             signal, touched, loss_sum, rgb_out, weight_sum, weight_max, flags,
                              static_cast<cudaStream_t>(stream));
+}
+
+int dot_signal_fwd(const dot_tree_view* tree, const double* origins, const double* dirs, int64_t n_pool,
+                   const int64_t* ray_index, int64_t n_rays, double early_stop_eps, double t_near, double t_far,
+                   double* signal, double* weight_sum, double* weight_max, uint8_t* touched,
+                   uint64_t* invalid_rays, void* stream) {
+    if (int st = validate_tree_view(tree)) return st;
+    if (n_rays < 0 || (n_rays && (!origins || !dirs))) return set_error(DOT_BAD_ARG, "bad ray arrays");
+    if (!ray_index && n_pool < n_rays)
+        return set_error(DOT_BAD_ARG, "n_pool (%lld) < n_rays (%lld) without a ray_index", (long long)n_pool,
+                         (long long)n_rays);
+    if (!signal && !weight_sum && !weight_max && !touched)
+        return set_error(DOT_BAD_ARG, "dot_signal_fwd: no output requested");
+    return launch_signal_fwd(make_tree(*tree), origins, dirs, ray_index, n_pool, n_rays, early_stop_eps, t_near,
+                             t_far, signal, weight_sum, weight_max, touched,
+                             reinterpret_cast<unsigned long long*>(invalid_rays), static_cast<cudaStream_t>(stream));
 }
 
 int dot_ray_keys(const dot_tree_view* tree, const double* origins, const double* dirs, int64_t n_rays,
@@ -194,11 +215,12 @@ int dot_plan_sort(const int32_t* keys, const int64_t* ray_index, int64_t n_rays,
                          static_cast<cudaStream_t>(stream));
 }
 
-int dot_ray_keys32(const dot_tree_view* tree, const double* origins, const double* dirs,
+int dot_ray_keys32(const dot_tree_view* tree, const double* origins, const double* dirs, int64_t n_pool,
                    const int64_t* ray_index, int64_t n_rays, int32_t* keys, void* stream) {
     if (int st = validate_tree_view(tree)) return st;
     if (n_rays < 0 || (n_rays && (!origins || !dirs || !keys))) return set_error(DOT_BAD_ARG, "bad arrays");
-    return launch_ray_keys32(make_tree(*tree), origins, dirs, ray_index, n_rays, keys,
+    if (!ray_index && n_pool < n_rays) return set_error(DOT_BAD_ARG, "n_pool < n_rays without a ray_index");
+    return launch_ray_keys32(make_tree(*tree), origins, dirs, ray_index, n_pool, n_rays, keys,
                              static_cast<cudaStream_t>(stream));
 }
 

@@ -35,10 +35,13 @@ int launch_render_fwd(const TreeDev& T, const double* o, const double* d, int64_
                       const double* bg, double eps, double tn, double tf, float* rgb, float* tfin,
                       float* wsum, float* depth, cudaStream_t s);
 int launch_render_bwd(const TreeDev& T, const double* o, const double* d, const double* tgt,
-                      const int64_t* ray_idx, const int32_t* warp_order, uint16_t* ray_used, int64_t n,
-                      const double* bg, double eps, double tn, double tf, double gs, float* gsig,
+                      const int64_t* ray_idx, int64_t n_pool, const int32_t* warp_order, uint16_t* ray_used,
+                      int64_t n, const double* bg, double eps, double tn, double tf, double gs, float* gsig,
                       float* gsh, double* signal, uint8_t* touched, double* loss, float* rgb_out,
-                      int flags, cudaStream_t s);
+                      double* wsum, double* wmax, int flags, cudaStream_t s);
+int launch_signal_fwd(const TreeDev& T, const double* o, const double* d, const int64_t* ray_idx, int64_t n_pool,
+                      int64_t n, double eps, double tn, double tf, double* signal, double* wsum, double* wmax,
+                      uint8_t* touched, unsigned long long* invalid, cudaStream_t s);
 int launch_sched_order(const int32_t* keys, int64_t n, const uint16_t* table, int32_t* warp_order, cudaStream_t s);
 int launch_sched_update(const int32_t* keys, const uint16_t* ray_used, int64_t n, uint16_t* table, cudaStream_t s);
 int launch_ray_keys(const TreeDev& T, const double* o, const double* d, int64_t n, unsigned long long* keys,
@@ -46,7 +49,7 @@ int launch_ray_keys(const TreeDev& T, const double* o, const double* d, int64_t 
 int run_plan_sort(const int32_t* keys, const int64_t* ray_index, int64_t n, int begin_bit,
                   int32_t* sorted_keys, int64_t* sorted_index, cudaStream_t s);
 int launch_ray_keys32(const TreeDev& T, const double* o, const double* d, const int64_t* ray_idx,
-                      int64_t n, int32_t* keys, cudaStream_t s);
+                      int64_t n_pool, int64_t n, int32_t* keys, cudaStream_t s);
 int launch_render_cameras(const TreeDev& T, const double* cam_to_world, const double* focal, int n_views,
                           int width, int height, const double* bg, double eps, float* rgb, float* tfin,
                           float* depth, cudaStream_t s);

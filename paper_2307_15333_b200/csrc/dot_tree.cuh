@@ -330,4 +330,17 @@ __device__ __forceinline__ void red_add_f64(double* addr, double a) {
     asm volatile("red.global.add.f64 [%0], %1;" :: "l"(addr), "d"(a) : "memory");
 }
 
+// North-star training-signal extras (no reference counterpart; defined and
+// pinned by oracle/dot_oracle.c oracle_weights): per leaf the sum and the
+// max over composited segments of the compositing weight T_i Q_i.  The max
+// uses the u64 order of non-negative doubles, so it is exact and
+// order-independent.
+__device__ __forceinline__ void weight_extras(double* wsum, double* wmax, int64_t pid, double tq) {
+    if (tq > 0.0) {
+        if (wsum) red_add_f64(wsum + pid, tq);
+        if (wmax) atomicMax(reinterpret_cast<unsigned long long*>(wmax + pid),
+                            static_cast<unsigned long long>(__double_as_longlong(tq)));
+    }
+}
+
 }  // namespace dot

@@ -18,6 +18,22 @@ namespace dot {
 constexpr int kBlock = 128;
 constexpr int kFwdMinBlocks = 8;   // forward: 64 registers -> 8 blocks (32 warps) per SM
 constexpr int kBwdRecords = 128;   // composited segments buffered per ray (pass 1 -> pass 2); longer rays resume the walk
+// Warp-schedule cost of a ray (what dot_sched_update learns): 0 = composited
+// segments, 1 = all traversed segments, 2 = composited + post-cut / 2.  A
+// warp lasts as long as its longest ray, and the longest rays are mostly
+// post-cut walks (configs[1] batch: p99.9 of 240 traversed segments vs 101
+// composited), which the composited count alone does not see.  Measured
+// (tools/sweep_variants.sh, 2 runs each): backward 1.83 ms (0, 64 regs) ->
+// 1.75 (0, 80 regs) -> 1.71 (1, 80 regs) -> 1.69 ms (2, 80 regs).
+#ifndef DOT_SCHED_COST
+#define DOT_SCHED_COST 2
+#endif
+// Resident one-warp blocks per SM of the backward: 24 -> 80 registers (no
+// spills in the walk); 32 (64 registers, 192 B of spills) measured 3-4 %
+// slower, 20 (96 registers) equal.
+#ifndef DOT_BWD_MINB
+#define DOT_BWD_MINB 24
+#endif
 
 static unsigned blocks_for(int64_t n) { return unsigned((n + kBlock - 1) / kBlock); }
 
@@ -159,17 +175,37 @@ struct BufSeg {
     double a;          // alpha = exp(-sigma delta) exactly as pass 1 used it
     float k0, k1, k2;  // colour (NaN: not evaluated in pass 1, q == 0)
     float pad;
+    __device__ __forceinline__ void set_alpha(double a_, double) { a = a_; }
+    __device__ __forceinline__ void alpha(double& a_, double& q_) const {
+        a_ = a;
+        q_ = 1.0 - a;
+    }
 };
 
-// 24-byte record of the atomic sinks: alpha rounded to f32 (pass 2 only
-// rebuilds T_i and q_i for gradients and the atomic signal, both within the
-// float tolerance); the deterministic sink keeps the exact f64 alpha so its
-// signal stays bit-identical to the reference's.
+// 24-byte record of the atomic sinks (pass 2 only rebuilds T_i and q_i for
+// the gradients, within the float tolerance): one f32 holds whichever of
+// alpha and q = 1 - alpha is <= 1/2, sign bit set when it is q, so both
+// keep ~1e-7 relative precision -- rounding alpha itself would leave q of a
+// nearly transparent segment (alpha -> 1) with no significant bits.  The
+// deterministic sink keeps the exact f64 alpha so its signal stays
+// bit-identical to the reference's.
 struct BufSegCompact {
     int32_t pid;
     float delta;
-    float a;
+    float aq;
     float k0, k1, k2;
+    __device__ __forceinline__ void set_alpha(double a, double q) {
+        aq = a > 0.5 ? -float(q) : float(a);  // q == 0 -> -0.0f (sign bit set)
+    }
+    __device__ __forceinline__ void alpha(double& a, double& q) const {
+        if (signbit(aq)) {
+            q = -double(aq);
+            a = 1.0 - q;
+        } else {
+            a = double(aq);
+            q = 1.0 - a;
+        }
+    }
 };
 
 template <bool EXACT>
@@ -192,11 +228,17 @@ struct AtomicSink {
     float* __restrict__ gsh;
     double* __restrict__ signal;
     double* __restrict__ loss_sum;
+    double* __restrict__ wsum;  // optional per-leaf sum of T_i Q_i (may be NULL)
+    double* __restrict__ wmax;  // optional per-leaf max of T_i Q_i (may be NULL)
     __device__ __forceinline__ void bind(float*, float4*) {}
-    // pass 1, per composited segment: the signal needs only the exact q
-    __device__ __forceinline__ void pass1(int64_t pid, double q) {
+    // pass 1, per composited segment: the signal needs only the exact q (and
+    // the weight extras the exact T_i Q_i)
+    __device__ __forceinline__ void pass1(int64_t pid, double q, double tq) {
         if (q != 0.0) red_add_f64(signal + pid, q);
+        weight_extras(wsum, wmax, pid, tq);
     }
+    // an out-of-range ray index: the loss becomes NaN (the call cannot raise)
+    __device__ __forceinline__ void bad_ray() { red_add_f64(loss_sum, __longlong_as_double(0x7ff8000000000000ll)); }
     // warp-collective, all 32 lanes (no-op here)
     __device__ __forceinline__ void reserve(int, bool) {}
     template <int B>
@@ -298,12 +340,14 @@ struct CoopSink : AtomicSink {
 };
 
 
-// flags: bit 0 skip post-cut touched marks (not reference semantics);
-// bit 13 pass 1 only, bit 14 no reductions (diagnostics for timing splits).
+// flags: bit 15 = per-lane REDs (AtomicSink instead of CoopSink, chosen at
+// launch).  Timing-diagnostic bits exist only in experiment builds
+// (-DDOT_DIAG_FLAGS, tools/build_variants.py): bit 0 skip post-cut touched
+// marks, bit 13 pass 1 only, bit 14 no reductions -- never in the product.
 template <int B, class Sink>
-__global__ void __launch_bounds__(32, 32) render_bwd_buffered_kernel(
+__global__ void __launch_bounds__(32, DOT_BWD_MINB) render_bwd_buffered_kernel(
     TreeDev T, const double* __restrict__ o, const double* __restrict__ d,
-    const double* __restrict__ tgt, const int64_t* __restrict__ ray_idx, int64_t n, double bg0,
+    const double* __restrict__ tgt, const int64_t* __restrict__ ray_idx, int64_t n_pool, int64_t n, double bg0,
     double bg1, double bg2, double eps, double t_near, double t_far, double grad_scale,
     uint8_t* __restrict__ touched, float* __restrict__ rgb_out, int flags, Sink sink,
     const int32_t* __restrict__ warp_order, uint16_t* __restrict__ ray_used) {
@@ -314,13 +358,21 @@ __global__ void __launch_bounds__(32, 32) render_bwd_buffered_kernel(
     // learned cost table -- see sched_order_kernel); slot = batch position
     const int64_t wb = warp_order ? int64_t(__ldg(warp_order + blockIdx.x)) : int64_t(blockIdx.x);
     const int64_t slot = wb * 32 + threadIdx.x;
-    const bool valid = slot < n;
-    const int64_t r = valid ? ray_index(ray_idx, slot) : 0;
+    int64_t r = slot < n ? ray_index(ray_idx, slot) : 0;
+    bool valid = slot < n;
+    if (valid && (r < 0 || r >= n_pool)) {  // caller's index outside its arrays: skip the ray
+        sink.bad_ray();
+        valid = false;
+        r = 0;
+    }
     Tracer tr;
     float basis[B];
     using Rec = typename RecordOf<Sink::kExactAlpha>::type;
     Rec buf[K];
     int used = 0;
+#if DOT_SCHED_COST
+    int tail = 0;
+#endif
     double resume_t = 0.0, resume_nudge = 0.0;
     double R0 = 0.0, R1 = 0.0, R2 = 0.0, g0 = 0.0, g1 = 0.0, g2 = 0.0;
     if (valid) {
@@ -333,10 +385,19 @@ __global__ void __launch_bounds__(32, 32) render_bwd_buffered_kernel(
             bool cut = false;
             while (tr.next_prefetch(T, L, te, dl, !cut)) {
                 touched[L.pid] = 1;
-                if (cut) continue;  // post-cut: touched only
+                if (cut) {  // post-cut: touched only
+#if DOT_SCHED_COST
+                    ++tail;
+#endif
+                    continue;
+                }
                 const double a = exp_ref(-double(__ldg(T.sigma + L.pid)) * dl);
                 const double q = 1.0 - a;
-                if (!(flags & 16384)) sink.pass1(L.pid, q);
+                const double tq = trans * q;
+#ifdef DOT_DIAG_FLAGS
+                if (!(flags & 16384))
+#endif
+                sink.pass1(L.pid, q, tq);
                 float k0 = __int_as_float(0x7fc00000), k1 = k0, k2 = k0;
                 if (q > 0.0) {
                     float e0, e1, e2;
@@ -344,7 +405,6 @@ __global__ void __launch_bounds__(32, 32) render_bwd_buffered_kernel(
                     k0 = sigmoidf(e0);
                     k1 = sigmoidf(e1);
                     k2 = sigmoidf(e2);
-                    const double tq = trans * q;
                     c0 += tq * double(k0);
                     c1 += tq * double(k1);
                     c2 += tq * double(k2);
@@ -353,7 +413,7 @@ __global__ void __launch_bounds__(32, 32) render_bwd_buffered_kernel(
                     Rec e;
                     e.pid = L.pid;
                     e.delta = float(dl);
-                    e.a = a;
+                    e.set_alpha(a, q);
                     e.k0 = k0;
                     e.k1 = k1;
                     e.k2 = k2;
@@ -366,7 +426,9 @@ __global__ void __launch_bounds__(32, 32) render_bwd_buffered_kernel(
                 trans *= a;
                 if (eps > 0.0 && trans < eps) {
                     cut = true;
+#ifdef DOT_DIAG_FLAGS
                     if (flags & 1) break;
+#endif
                 }
             }
         }
@@ -386,8 +448,17 @@ __global__ void __launch_bounds__(32, 32) render_bwd_buffered_kernel(
         g0 = grad_scale * r0;
         g1 = grad_scale * r1;
         g2 = grad_scale * r2;
-        if (ray_used) ray_used[slot] = uint16_t(used < 65535 ? used : 65535);
+#if DOT_SCHED_COST == 1
+        const int cost = used + tail;
+#elif DOT_SCHED_COST == 2
+        const int cost = used + (tail >> 1);
+#else
+        const int cost = used;
+#endif
+        if (ray_used) ray_used[slot] = uint16_t(cost < 65535 ? cost : 65535);
+#ifdef DOT_DIAG_FLAGS
         if (flags & 8192) used = 0;
+#endif
     }
     __syncwarp();
     if constexpr (Sink::kSmem) {
@@ -411,14 +482,14 @@ __global__ void __launch_bounds__(32, 32) render_bwd_buffered_kernel(
     for (int i = 0; i < maxu; ++i) {
         const bool act = valid && i < used;
         int64_t pid = 0;
-        double a = 1.0, dl = 0.0;
+        double a = 1.0, q = 0.0, dl = 0.0;
         float k0 = 0.f, k1 = 0.f, k2 = 0.f;
         if (act) {
             if (i < K) {  // software pipeline: entry i+1 is in flight while i is scattered
                 const Rec e = nxt;
                 if (i + 1 < used && i + 1 < K) nxt = buf[i + 1];
                 pid = e.pid;
-                a = e.a;
+                e.alpha(a, q);
                 dl = e.delta;
                 k0 = e.k0;
                 k1 = e.k1;
@@ -429,6 +500,7 @@ __global__ void __launch_bounds__(32, 32) render_bwd_buffered_kernel(
                 tr.next(T, L, te, dl);
                 pid = L.pid;
                 a = exp_ref(-double(__ldg(T.sigma + pid)) * dl);
+                q = 1.0 - a;
                 k0 = __int_as_float(0x7fc00000);
             }
             if (k0 != k0) {  // q == 0 in pass 1: the colour is still needed for dsigma
@@ -439,7 +511,6 @@ __global__ void __launch_bounds__(32, 32) render_bwd_buffered_kernel(
                 k2 = sigmoidf(e2);
             }
         }
-        const double q = 1.0 - a;
         const double tq = Ti * q;
         s0 -= tq * double(k0);
         s1 -= tq * double(k1);
@@ -450,25 +521,27 @@ __global__ void __launch_bounds__(32, 32) render_bwd_buffered_kernel(
         const float w1 = float(g1 * tq) * k1 * (1.f - k1);
         const float w2 = float(g2 * tq) * k2 * (1.f - k2);
         Ti *= a;
+#ifdef DOT_DIAG_FLAGS
         if (flags & 16384) {  // keep the arithmetic alive without reducing
             if (ds == 12345.0 && w0 == 1.f) touched[0] = uint8_t(w1 + w2);
             continue;
         }
+#endif
         sink.template put<B>(act, i, pid, float(ds), w0, w1, w2, basis, q);
     }
     sink.loss(loss);
 }
 
 int launch_render_bwd(const TreeDev& T, const double* o, const double* d, const double* tgt,
-                      const int64_t* ray_idx, const int32_t* warp_order, uint16_t* ray_used, int64_t n,
-                      const double* bg, double eps, double tn, double tf, double gs, float* gsig,
+                      const int64_t* ray_idx, int64_t n_pool, const int32_t* warp_order, uint16_t* ray_used,
+                      int64_t n, const double* bg, double eps, double tn, double tf, double gs, float* gsig,
                       float* gsh, double* signal, uint8_t* touched, double* loss, float* rgb_out,
-                      int flags, cudaStream_t s) {
+                      double* wsum, double* wmax, int flags, cudaStream_t s) {
     if (n == 0) return DOT_OK;
     const unsigned grid = unsigned((n + 31) / 32);
     // default: warp-cooperative SH scatter; flag bit 15: per-lane REDs
     const bool coop = (flags & 32768) == 0;
-    AtomicSink as{gsig, gsh, signal, loss};
+    AtomicSink as{gsig, gsh, signal, loss, wsum, wmax};
     CoopSink cs;
     static_cast<AtomicSink&>(cs) = as;
     cs.sb = nullptr;
@@ -476,11 +549,11 @@ int launch_render_bwd(const TreeDev& T, const double* o, const double* d, const 
 #define DOT_BWD(BB)                                                                                  \
     if (coop)                                                                                        \
         render_bwd_buffered_kernel<BB, CoopSink><<<grid, 32, 0, s>>>(                                \
-            T, o, d, tgt, ray_idx, n, bg[0], bg[1], bg[2], eps, tn, tf, gs, touched, rgb_out, flags, cs, \
+            T, o, d, tgt, ray_idx, n_pool, n, bg[0], bg[1], bg[2], eps, tn, tf, gs, touched, rgb_out, flags, cs, \
             warp_order, ray_used);                                                                   \
     else                                                                                             \
         render_bwd_buffered_kernel<BB, AtomicSink><<<grid, 32, 0, s>>>(                              \
-            T, o, d, tgt, ray_idx, n, bg[0], bg[1], bg[2], eps, tn, tf, gs, touched, rgb_out, flags, as, \
+            T, o, d, tgt, ray_idx, n_pool, n, bg[0], bg[1], bg[2], eps, tn, tf, gs, touched, rgb_out, flags, as, \
             warp_order, ray_used);
     DOT_DISPATCH_B(DOT_BWD)
 #undef DOT_BWD
@@ -496,7 +569,8 @@ int launch_render_bwd(const TreeDev& T, const double* o, const double* d, const 
 struct EmitSink {
     static constexpr bool kSmem = false;
     static constexpr bool kExactAlpha = true;
-    __device__ __forceinline__ void pass1(int64_t, double) {}
+    __device__ __forceinline__ void pass1(int64_t, double, double) {}
+    __device__ __forceinline__ void bad_ray() {}  // ray_index validated as a permutation on the host
     __device__ __forceinline__ void bind(float*, float4*) {}
     EmitArgs a;
     int64_t base;
@@ -550,7 +624,7 @@ int launch_render_bwd_emit(const TreeDev& T, const double* o, const double* d, c
     sink.orig = 0;
 #define DOT_EMIT(BB)                                                                                 \
     render_bwd_buffered_kernel<BB, EmitSink><<<unsigned((n + 31) / 32), 32, 0, s>>>(                 \
-        T, o, d, tgt, ray_idx, n, bg[0], bg[1], bg[2], eps, tn, tf, gs, touched, nullptr, 0, sink,   \
+        T, o, d, tgt, ray_idx, n, n, bg[0], bg[1], bg[2], eps, tn, tf, gs, touched, nullptr, 0, sink,   \
         warp_order, ray_used);
     DOT_DISPATCH_B(DOT_EMIT)
 #undef DOT_EMIT
@@ -582,6 +656,58 @@ int launch_render_fwd(const TreeDev& T, const double* o, const double* d, int64_
     DOT_DISPATCH_B(DOT_FWD)
 #undef DOT_FWD
     return check_launch("render_fwd_kernel");
+}
+
+// ---------------------------------------------------------------------------
+// Signal-only forward (the signal half of grad_kernel + scatter_kernel,
+// _kernels.py:249-282 and 337, as SignalBuffer.accumulate consumes it,
+// signals.py:58-69): per composited segment signal[leaf] += Q (cut-aware),
+// plus the optional weight extras and touched marks.  No SH row is read and
+// no gradient reduced: calibration-only passes cost a traversal plus one
+// sigma gather per segment.  The walk stops at the cut unless touched marks
+// (which include post-cut leaves) are requested.
+
+__global__ void __launch_bounds__(kBlock, kFwdMinBlocks) signal_fwd_kernel(
+    TreeDev T, const double* __restrict__ o, const double* __restrict__ d, const int64_t* __restrict__ ray_idx,
+    int64_t n_pool, int64_t n, double eps, double t_near, double t_far, double* __restrict__ signal,
+    double* __restrict__ wsum, double* __restrict__ wmax, uint8_t* __restrict__ touched,
+    unsigned long long* __restrict__ invalid) {
+    const int64_t slot = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (slot >= n) return;
+    const int64_t r = ray_index(ray_idx, slot);
+    if (r < 0 || r >= n_pool) {
+        if (invalid) atomicAdd(invalid, 1ull);
+        return;
+    }
+    Tracer tr;
+    load_ray(o, d, r, tr);
+    if (!tr.init(T, t_near, t_far)) return;
+    double trans = 1.0;
+    bool cut = false;
+    Leaf L;
+    double te, dl;
+    while (tr.next(T, L, te, dl)) {
+        if (touched) touched[L.pid] = 1;
+        if (cut) continue;
+        const double a = exp_ref(-double(__ldg(T.sigma + L.pid)) * dl);
+        const double q = 1.0 - a;
+        if (signal && q != 0.0) red_add_f64(signal + L.pid, q);
+        weight_extras(wsum, wmax, L.pid, trans * q);
+        trans *= a;
+        if (eps > 0.0 && trans < eps) {
+            cut = true;
+            if (!touched) break;
+        }
+    }
+}
+
+int launch_signal_fwd(const TreeDev& T, const double* o, const double* d, const int64_t* ray_idx, int64_t n_pool,
+                      int64_t n, double eps, double tn, double tf, double* signal, double* wsum, double* wmax,
+                      uint8_t* touched, unsigned long long* invalid, cudaStream_t s) {
+    if (n == 0) return DOT_OK;
+    signal_fwd_kernel<<<blocks_for(n), kBlock, 0, s>>>(T, o, d, ray_idx, n_pool, n, eps, tn, tf, signal, wsum,
+                                                       wmax, touched, invalid);
+    return check_launch("signal_fwd_kernel");
 }
 
 // ---------------------------------------------------------------------------
@@ -730,11 +856,15 @@ __device__ __forceinline__ unsigned long long spread3_10(unsigned v) {
 // 31-bit variant (int32 keys sort in half the radix passes): origin 4 bits per
 // axis (12 bits), direction 10 x 9 bits (19 bits).
 __global__ void ray_keys32_kernel(TreeDev T, const double* __restrict__ o, const double* __restrict__ d,
-                                  const int64_t* __restrict__ ray_idx, int64_t n,
+                                  const int64_t* __restrict__ ray_idx, int64_t n_pool, int64_t n,
                                   int32_t* __restrict__ keys) {
     const int64_t slot = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (slot >= n) return;
     const int64_t r = ray_index(ray_idx, slot);
+    if (r < 0 || r >= n_pool) {  // out of range: the consumer rejects the ray; the key only orders
+        keys[slot] = 0;
+        return;
+    }
     unsigned q[3];
     const double c3[3] = {T.cx, T.cy, T.cz};
 #pragma unroll
@@ -760,10 +890,10 @@ __global__ void ray_keys32_kernel(TreeDev T, const double* __restrict__ o, const
     keys[slot] = int32_t((om << 19) | dm);
 }
 
-int launch_ray_keys32(const TreeDev& T, const double* o, const double* d, const int64_t* ray_idx, int64_t n,
-                      int32_t* keys, cudaStream_t s) {
+int launch_ray_keys32(const TreeDev& T, const double* o, const double* d, const int64_t* ray_idx, int64_t n_pool,
+                      int64_t n, int32_t* keys, cudaStream_t s) {
     if (n == 0) return DOT_OK;
-    ray_keys32_kernel<<<unsigned((n + 255) / 256), 256, 0, s>>>(T, o, d, ray_idx, n, keys);
+    ray_keys32_kernel<<<unsigned((n + 255) / 256), 256, 0, s>>>(T, o, d, ray_idx, n_pool, n, keys);
     return check_launch("ray_keys32_kernel");
 }
 

@@ -107,15 +107,44 @@ class GradBuffer:
     ``dsigma`` [capacity] and ``dsh`` [capacity, 3B] are dense by node id;
     ``touched`` lists the touched leaf ids ascending; ``touched_mask`` is the
     u8 mask the kernels write (kept on device for the optimizer).
+
+    For numpy callers (``host=True``) the device buffers are kept and the
+    float64 numpy views the reference returns are made on first attribute
+    access, so a caller that hands the gradients straight to
+    ``rmsprop_step`` (the reference's train_epoch pattern, optim.py:147-150)
+    never copies them to the host.
     """
 
-    def __init__(self, dsigma, dsh, touched_mask, generation, dsh_store=None):
-        self.dsigma = dsigma
-        self.dsh = dsh
-        self.touched_mask = touched_mask
+    def __init__(self, dsigma, dsh, touched_mask, generation, dsh_store=None, host=False):
         self.generation = generation
         self.dsh_store = dsh_store  # padded [capacity, pad4(3B)] device store
+        self._host = bool(host)
+        self._dev = {"dsigma": dsigma, "dsh": dsh, "touched_mask": touched_mask}
+        self._np = {}
         self._touched = None
+
+    def _get(self, name):
+        if not self._host:
+            return self._dev[name]
+        if name not in self._np:
+            t = self._dev[name]
+            a = t.detach().cpu().numpy()
+            self._np[name] = a if name == "touched_mask" else a.astype(np.float64)
+        return self._np[name]
+
+    def _set(self, name, value):
+        self._dev[name] = value
+        self._np.pop(name, None)
+
+    dsigma = property(lambda self: self._get("dsigma"), lambda self, v: self._set("dsigma", v))
+    dsh = property(lambda self: self._get("dsh"), lambda self, v: self._set("dsh", v))
+    touched_mask = property(lambda self: self._get("touched_mask"),
+                            lambda self, v: self._set("touched_mask", v))
+
+    def device_tensors(self):
+        """(dsigma, dsh, touched_mask) as they live on the device (torch
+        tensors; numpy arrays for a GradBuffer built from host data)."""
+        return self._dev["dsigma"], self._dev["dsh"], self._dev["touched_mask"]
 
     @property
     def touched(self):
@@ -318,7 +347,7 @@ def pool_keys(tree: SparseOctree, origins: torch.Tensor, dirs: torch.Tensor) -> 
     n = int(origins.shape[0])
     keys = torch.empty(n, dtype=torch.int32, device=tree.device)
     view, _topo = tree.tree_view()
-    _lib.call("dot_ray_keys32", _lib.ctypes.byref(view), _lib.ptr(origins), _lib.ptr(dirs), None, n,
+    _lib.call("dot_ray_keys32", _lib.ctypes.byref(view), _lib.ptr(origins), _lib.ptr(dirs), n, None, n,
               _lib.ptr(keys), _lib.stream_ptr())
     return keys
 
@@ -334,17 +363,24 @@ def plan_batch(tree: SparseOctree, origins: torch.Tensor, dirs: torch.Tensor, ra
     pool's precomputed keys (``pool_keys``), gathered by ``ray_index``."""
     idx = None if ray_index is None else torch.as_tensor(ray_index, device=tree.device).reshape(-1).to(torch.int64)
     n = int(idx.shape[0]) if idx is not None else int(origins.shape[0])
+    n_pool = int(origins.shape[0])
     view, _topo = tree.tree_view()
     cur = torch.cuda.current_stream(tree.device)
     s = stream or cur
-    if s is not cur and wait_current:
-        s.wait_stream(cur)  # inputs produced on the current stream
+    if s is not cur:
+        if wait_current:
+            s.wait_stream(cur)  # inputs produced on the current stream
+        # the inputs (and the index temporary made above) are read on the side
+        # stream: keep the allocator from recycling them before it is done
+        for t in (idx, origins, dirs, keys):
+            if t is not None:
+                t.record_stream(s)
     with torch.cuda.stream(s):
         if keys is not None:
             keys = keys if idx is None else keys.index_select(0, idx)
         else:
             keys = torch.empty(n, dtype=torch.int32, device=tree.device)
-            _lib.call("dot_ray_keys32", _lib.ctypes.byref(view), _lib.ptr(origins), _lib.ptr(dirs),
+            _lib.call("dot_ray_keys32", _lib.ctypes.byref(view), _lib.ptr(origins), _lib.ptr(dirs), n_pool,
                       _lib.ptr(idx), n, _lib.ptr(keys), _lib.stream_ptr(s))
         # one radix sort carrying the ray index: the sorted values are the
         # kernel's ray_index directly
@@ -372,7 +408,7 @@ def render_and_backprop(tree: SparseOctree, origins, dirs, targets, background,
                         workspace: BackpropWorkspace | None = None, accumulate: bool = False,
                         return_rgb: bool = False, kernel_events=None, kernel_flags: int = 0,
                         coherent: bool = True, deterministic: bool = False, ray_index=None,
-                        plan: "RayPlan | None" = None):
+                        plan: "RayPlan | None" = None, weight_sum=None, weight_max=None):
     """Batch MSE loss, analytic leaf gradients and per-leaf signal (render.py:175-225).
 
     Returns (loss, GradBuffer, signal).  ``grad_scale`` defaults to the
@@ -396,6 +432,12 @@ def render_and_backprop(tree: SparseOctree, origins, dirs, targets, background,
     are bit-identical from run to run and the signal equals the reference's
     bit for bit.  It synchronises once per call and is slower than the
     default (warp-cooperative atomic) reduction.
+
+    ``weight_sum`` / ``weight_max`` (device f64 [capacity] tensors, optional;
+    not in the reference): accumulate per leaf the sum / max of the
+    compositing weight T_i Q_i of its composited segments (the north star's
+    "max/sum compositing weight" signal; atomic path only).  An index in
+    ``ray_index`` outside the arrays skips that ray and makes the loss NaN.
     """
     io = _IO(tree, origins)
     o = io.rays(origins, "origins")
@@ -413,6 +455,13 @@ def render_and_backprop(tree: SparseOctree, origins, dirs, targets, background,
     if idx is None and (t.shape[0] != n or d.shape[0] != n):
         raise InputError(f"batch length mismatch: {n} origins, {d.shape[0]} dirs, "
                          f"{t.shape[0]} targets")
+    n_pool = int(o.shape[0])
+    for name, x in (("weight_sum", weight_sum), ("weight_max", weight_max)):
+        if x is not None and (not isinstance(x, torch.Tensor) or x.dtype != torch.float64
+                              or x.device != tree.device or x.numel() != tree.capacity or not x.is_contiguous()):
+            raise InputError(f"{name} must be a contiguous float64 [capacity] tensor on {tree.device}")
+    if deterministic and (weight_sum is not None or weight_max is not None):
+        raise InputError("weight_sum / weight_max are not available with deterministic=True")
     ws = workspace if workspace is not None else BackpropWorkspace.for_tree(tree)
     if ws.dsigma.shape[0] != tree.capacity:
         raise InputError("workspace capacity does not match the tree")
@@ -451,11 +500,12 @@ def render_and_backprop(tree: SparseOctree, origins, dirs, targets, background,
                       tree.sh_stride, _lib.ptr(ws.signal), _lib.ptr(ws.touched), _lib.ptr(ws.loss),
                       _lib.stream_ptr())
         else:
-            _lib.call("dot_render_bwd", _lib.ctypes.byref(view), _lib.ptr(o), _lib.ptr(d), _lib.ptr(t),
+            _lib.call("dot_render_bwd", _lib.ctypes.byref(view), _lib.ptr(o), _lib.ptr(d), _lib.ptr(t), n_pool,
                       _lib.ptr(idx), _lib.ptr(warp_order), _lib.ptr(ray_used), n, _bg_ptr(bg),
                       float(early_stop_eps), float(t_near), float(t_far), gs, _lib.ptr(ws.dsigma),
                       _lib.ptr(ws.dsh_store), tree.sh_stride, _lib.ptr(ws.signal), _lib.ptr(ws.touched),
-                      _lib.ptr(ws.loss), _lib.ptr(rgb), int(kernel_flags), _lib.stream_ptr())
+                      _lib.ptr(ws.loss), _lib.ptr(rgb), _lib.ptr(weight_sum), _lib.ptr(weight_max),
+                      int(kernel_flags), _lib.stream_ptr())
         if kernel_events is not None:
             kernel_events[1].record()
         if ray_used is not None:
@@ -473,9 +523,13 @@ def render_and_backprop(tree: SparseOctree, origins, dirs, targets, background,
     dsh = ws.dsh_store if nsh == tree.sh_stride else ws.dsh_store[:, :nsh]
     if io.numpy:
         loss = float(ws.loss.item()) / n if n else 0.0
-        grads = GradBuffer(ws.dsigma.cpu().numpy().astype(np.float64),
-                           dsh.cpu().numpy().astype(np.float64), ws.touched.cpu().numpy(),
-                           tree.generation)
+        # the float64 numpy gradients are made on first access (GradBuffer);
+        # a caller-owned workspace may be overwritten by its next call: copy now
+        grads = GradBuffer(ws.dsigma, dsh, ws.touched, tree.generation, ws.dsh_store, host=True)
+        if workspace is not None:
+            grads.dsigma, grads.dsh, grads.touched_mask  # noqa: B018 (materialise)
+            grads._dev = {"dsigma": grads.dsigma, "dsh": grads.dsh, "touched_mask": grads.touched_mask}
+            grads.dsh_store = None
         out = (loss, grads, ws.signal.cpu().numpy())
         if return_rgb:
             out = out + (rgb.cpu().numpy().astype(np.float64),)
@@ -486,6 +540,60 @@ def render_and_backprop(tree: SparseOctree, origins, dirs, targets, background,
     if return_rgb:
         out = out + (rgb,)
     return out
+
+
+def signal_pass(tree: SparseOctree, origins, dirs, early_stop_eps: float = EPS_T, t_near: float = 0.0,
+                t_far: float = math.inf, ray_index=None, buffer=None, signal=None, weight_sum=None,
+                weight_max=None, touched=None, coherent: bool = True):
+    """Training signal without gradients (``dot_signal_fwd``): per leaf the
+    sum over the batch's composited segments of Q = 1 - exp(-sigma delta) --
+    exactly the ``signal`` output of ``render_and_backprop`` (render.py:
+    175-225, _kernels.py:337) that ``SignalBuffer.accumulate`` consumes
+    (signals.py:58-69) -- at the cost of a traversal and one sigma gather
+    per segment (no SH rows, no gradient reductions), for calibration-only
+    passes.
+
+    Accumulates (+=) into ``buffer.accumulator`` (a ``SignalBuffer``; its
+    ray count is bumped like ``accumulate``) or into ``signal`` (device f64
+    [capacity]); with neither, a fresh zeroed array is returned.  Optional
+    ``weight_sum`` / ``weight_max`` (f64 [capacity]) collect the sum / max
+    of the compositing weight T_i Q_i, ``touched`` (u8 [capacity]) marks
+    every traversed leaf (post-cut included).  numpy inputs give a numpy
+    signal; torch inputs stay on the device (no synchronisation)."""
+    io = _IO(tree, origins)
+    o = io.rays(origins, "origins")
+    d = io.rays(dirs, "dirs")
+    n_pool = int(o.shape[0])
+    if d.shape[0] != n_pool:
+        raise InputError(f"batch length mismatch: {n_pool} origins, {d.shape[0]} dirs")
+    idx = None
+    if ray_index is not None:
+        idx = torch.as_tensor(ray_index, device=tree.device).reshape(-1).to(torch.int64)
+    n = int(idx.shape[0]) if idx is not None else n_pool
+    cap, dev = tree.capacity, tree.device
+    if buffer is not None:
+        buffer.check_fresh()
+        signal = buffer.accumulator
+    elif signal is None:
+        signal = torch.zeros(cap, dtype=torch.float64, device=dev)
+    for name, x, dt in (("signal", signal, torch.float64), ("weight_sum", weight_sum, torch.float64),
+                        ("weight_max", weight_max, torch.float64), ("touched", touched, torch.uint8)):
+        if x is not None and (not isinstance(x, torch.Tensor) or x.dtype != dt or x.device != dev
+                              or x.numel() != cap or not x.is_contiguous()):
+            raise InputError(f"{name} must be a contiguous {dt} [capacity] tensor on {dev}")
+    if n:
+        if coherent and n >= COHERENT_MIN_RAYS:
+            idx = plan_batch(tree, o, d, idx).idx
+        view, _topo = tree.tree_view(locate_level=locate_level_train())
+        invalid = torch.zeros(1, dtype=torch.int64, device=dev)
+        _lib.call("dot_signal_fwd", _lib.ctypes.byref(view), _lib.ptr(o), _lib.ptr(d), n_pool, _lib.ptr(idx), n,
+                  float(early_stop_eps), float(t_near), float(t_far), _lib.ptr(signal), _lib.ptr(weight_sum),
+                  _lib.ptr(weight_max), _lib.ptr(touched), _lib.ptr(invalid), _lib.stream_ptr())
+        if io.numpy and int(invalid.item()):
+            raise InputError(f"{int(invalid.item())} ray_index entries outside [0, {n_pool})")
+    if buffer is not None:
+        buffer.epoch_rays += n
+    return io.out(signal) if io.numpy else signal
 
 
 def render_view(tree: SparseOctree, camera, background, early_stop_eps: float = EPS_T,

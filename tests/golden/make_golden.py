@@ -346,5 +346,48 @@ def train_case():
     print("train", [round(h["loss"], 6) for h in hist], [h["leaf_count"] for h in hist])
 
 
+class _HeldoutBundle(_Bundle):
+    def __init__(self, origins, dirs, targets, heldout):
+        super().__init__(origins, dirs, targets)
+        self.heldout = heldout
+
+
+def train_heldout_case():
+    """train() with held-out views (optim.py:157-195): the per-epoch history
+    including heldout_psnr (render_image of each held-out camera vs its
+    image, metrics.psnr), and the held-out PSNR of the final tree."""
+    from octrf.optim import TrainConfig, heldout_psnr, train
+    from octrf.render import render_image
+    from octrf.sh import sh_from_rgb
+    sh_in = sh_from_rgb(np.array([0.2, 0.7, 0.4]), 4)
+
+    def ball(c):
+        inside = np.linalg.norm(c - np.array([0.1, -0.05, 0.0]), axis=1) <= 0.5
+        return np.where(inside, 6.0, 0.0), np.where(inside[:, None], sh_in, 0.0)
+
+    truth = build_dense(3, (0.0, 0.0, 0.0), 1.0, 4, ball, max_depth=5)
+    o, d = ray_set(701, 3000, specials=False, miss_fraction=0.05)
+    targets = render_rays(truth, o, d, 1.0, early_stop_eps=0.0)
+    f = scenes.focal_from_angle(24, scenes.FOV_40)
+    cams = [Camera(24, 20, f, scenes.orbit_pose(3.5, az, el)) for az, el in ((0.3, 0.4), (2.2, -0.2))]
+    heldout = [(c, render_image(truth, c, 1.0)) for c in cams]
+    trainee = build_dense(2, (0.0, 0.0, 0.0), 1.0, 4, LeafPayload(0.3, [0.0] * 12), max_depth=5)
+    cfg = TrainConfig(epochs=4, interval=2, tau=0.3, gamma=0.1, batch_size=600, seed=5)
+    _, hist = train(trainee, _HeldoutBundle(o, d, targets, heldout), cfg)
+    out = dict(origins=o, dirs=d, targets=targets,
+               cam_w=np.array([c.width for c in cams]), cam_h=np.array([c.height for c in cams]),
+               cam_f=np.array([c.focal for c in cams]), cam_pose=np.stack([c.cam_to_world for c in cams]),
+               heldout_images=np.stack([im for _, im in heldout]),
+               loss=np.array([h["loss"] for h in hist]), psnr=np.array([h["psnr"] for h in hist]),
+               leaf_count=np.array([h["leaf_count"] for h in hist]),
+               final_psnr=np.float64(heldout_psnr(trainee, _HeldoutBundle(o, d, targets, heldout), 1.0)),
+               final_dot1=np.frombuffer(dot1_bytes(trainee), dtype=np.uint8))
+    np.savez_compressed(os.path.join(HERE, "train_heldout.npz"), **out)
+    print("train_heldout", [round(h["psnr"], 4) for h in hist], [h["leaf_count"] for h in hist])
+
+
 if __name__ == "__main__":
-    main()
+    if sys.argv[1:] == ["train_heldout"]:
+        train_heldout_case()
+    else:
+        main()

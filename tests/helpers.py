@@ -51,3 +51,21 @@ def ray_batch(seed, n, center=(0.0, 0.0, 0.0), half=1.0, miss_fraction=0.1):
         dirs[:k] = rng.normal(0.0, 1.0, (k, 3))
     dirs /= np.linalg.norm(dirs, axis=1, keepdims=True)
     return origins, dirs
+
+
+def assert_grads_close(got, want, rtol=1e-3, atol_frac=1e-4, what="gradient"):
+    """Gradient parity at the north star's 1e-4 abs / 1e-3 rel, with the
+    absolute floor scaled to the gradient's own magnitude (leaf gradients
+    are ~1e-6 at 2/n scaling, far below a fixed 1e-4): elementwise
+    |got - want| <= atol_frac * max|want| + rtol * |want|, plus a relative L2
+    error below rtol.  A zeroed or 1 %-scaled gradient fails both."""
+    got = np.asarray(got, dtype=np.float64)
+    want = np.asarray(want, dtype=np.float64)
+    assert got.shape == want.shape, (got.shape, want.shape)
+    scale = float(np.abs(want).max()) if want.size else 0.0
+    if scale == 0.0:
+        assert not np.any(got), f"{what}: reference is zero, got nonzero"
+        return
+    np.testing.assert_allclose(got, want, rtol=rtol, atol=atol_frac * scale, err_msg=what)
+    rel = float(np.linalg.norm(got - want) / np.linalg.norm(want))
+    assert rel < rtol, f"{what}: relative L2 error {rel:.3e} >= {rtol}"

@@ -11,6 +11,8 @@ import pytest
 
 from conftest import GOLDEN
 
+from helpers import assert_grads_close  # noqa: E402
+
 pytestmark = pytest.mark.gpu
 
 ATOL, RTOL = 1e-4, 1e-3
@@ -27,8 +29,8 @@ def test_golden_deterministic(path, tag, eps):
     loss, g, sig = render_and_backprop(tree, z["origins"], z["dirs"], z["targets"], z["bg"], eps,
                                        float(z["t_near"]), float(z["t_far"]), deterministic=True)
     assert loss == pytest.approx(float(z[f"loss_{tag}"]), rel=RTOL, abs=ATOL)
-    np.testing.assert_allclose(g.dsigma, z[f"dsigma_{tag}"], atol=ATOL, rtol=RTOL)
-    np.testing.assert_allclose(g.dsh, z[f"dsh_{tag}"], atol=ATOL, rtol=RTOL)
+    assert_grads_close(g.dsigma, z[f"dsigma_{tag}"], what="dsigma")
+    assert_grads_close(g.dsh, z[f"dsh_{tag}"], what="dsh")
     np.testing.assert_array_equal(g.touched, z[f"touched_{tag}"])
     # same traversal (bit-exact), same exp (exp_ref == glibc), same order:
     # the signal is the reference's to the last bit

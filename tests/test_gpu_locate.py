@@ -7,6 +7,8 @@ start inside cells, or graze edges, and for every table level."""
 import numpy as np
 import pytest
 
+from helpers import assert_grads_close  # noqa: E402
+
 pytestmark = pytest.mark.gpu
 
 
@@ -71,7 +73,7 @@ def test_locate_matches_fp64_descent_and_oracle(oracle, monkeypatch, center, hal
     loss, g, sig = render_and_backprop(tree, o, d, tg, 0.5)
     r_loss, r_g, r_sig = oracle.render_and_backprop(tree, o, d, tg, 0.5)
     np.testing.assert_array_equal(g.touched, r_g.touched)
-    np.testing.assert_allclose(g.dsh, r_g.dsh, atol=1e-4, rtol=1e-3)
+    assert_grads_close(g.dsh, r_g.dsh, what="dsh")
 
 
 def test_non_dyadic_root_ignores_table(monkeypatch):

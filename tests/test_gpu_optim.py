@@ -116,3 +116,34 @@ def test_train_step_equals_unfused_step():
     torch.testing.assert_close(bb.accumulator, ba.accumulator, atol=1e-9, rtol=1e-4)
     assert bb.epoch_rays == ba.epoch_rays
     assert not bool(sws.ws.dsigma.any()) and not bool(sws.ws.dsh_store.any())
+
+
+class _HeldoutBundle(_Bundle):
+    def __init__(self, origins, dirs, targets, heldout):
+        super().__init__(origins, dirs, targets)
+        self.heldout = heldout
+
+
+def test_heldout_psnr_matches_reference():
+    """train() with held-out views (optim.py:157-195) against a reference run
+    (tests/golden/train_heldout.npz): leaf counts per epoch exact, losses
+    within 1e-3, the per-epoch held-out PSNR within 0.02 dB (the trained
+    payloads differ by fp32-atomic rounding), and the reference's own final
+    tree scored by our heldout_psnr within 1e-3 dB of its score."""
+    from paper_2307_15333_b200.octree import LeafPayload, build_dense
+    from paper_2307_15333_b200.optim import TrainConfig, heldout_psnr, train
+    from paper_2307_15333_b200.scene_io import Camera, load_tree_bytes
+    z = np.load(os.path.join(GOLDEN, "train_heldout.npz"))
+    cams = [Camera(int(w), int(h), float(f), p) for w, h, f, p in
+            zip(z["cam_w"], z["cam_h"], z["cam_f"], z["cam_pose"])]
+    bundle = _HeldoutBundle(z["origins"], z["dirs"], z["targets"], list(zip(cams, z["heldout_images"])))
+    trainee = build_dense(2, (0.0, 0.0, 0.0), 1.0, 4, LeafPayload(0.3, [0.0] * 12), max_depth=5, device="cuda")
+    cfg = TrainConfig(epochs=4, interval=2, tau=0.3, gamma=0.1, batch_size=600, seed=5)
+    _, hist = train(trainee, bundle, cfg)
+    np.testing.assert_array_equal([h["leaf_count"] for h in hist], z["leaf_count"])
+    np.testing.assert_allclose([h["loss"] for h in hist], z["loss"], rtol=1e-3)
+    got = np.array([h["psnr"] for h in hist])
+    assert np.all(np.isfinite(got))
+    np.testing.assert_allclose(got, z["psnr"], atol=0.02)
+    ref_tree = load_tree_bytes(z["final_dot1"].tobytes(), device="cuda")
+    assert heldout_psnr(ref_tree, bundle, 1.0) == pytest.approx(float(z["final_psnr"]), abs=1e-3)

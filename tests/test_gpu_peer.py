@@ -74,7 +74,7 @@ def test_peer_exchange_end_to_end_under_torchrun():
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     n = max(1, min(torch.cuda.device_count(), 8))
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
-           "--master-addr", "127.0.0.1", "--master-port", "29541", os.path.join(root, "tools", "peer_smoke.py")]
+           "--master-addr", "127.0.0.1", "--master-port", "29541", os.path.join(root, "tests", "peer_worker.py")]
     res = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=root)
     assert res.returncode == 0, res.stdout[-2000:] + res.stderr[-2000:]
     assert res.stdout.count("PEER_OK") == n, res.stdout[-2000:]

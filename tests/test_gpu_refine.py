@@ -51,7 +51,7 @@ def test_select_sample(case):
     np.testing.assert_array_equal(got, case["sel_sample_pre"])
 
 
-def test_calibrate_bytes_identical(case):
+def test_calibrate_bytes_identical(case, oracle):
     from paper_2307_15333_b200.calibrate import CalibrationConfig, calibrate
     from paper_2307_15333_b200.scene_io import tree_bytes
     tree, buf, thr = _setup(case)
@@ -65,11 +65,21 @@ def test_calibrate_bytes_identical(case):
     assert rep.leaves_before == int(case["leaves_before"])
     assert rep.leaves_after == int(case["leaves_after"]) == tree.leaf_count
     assert hashlib.sha256(tree_bytes(tree)).hexdigest() == str(case["after_dot1_sha256"])
-    # events: merges in the reference's (round, id) order with the same ids
+    # events (built lazily from the device remap): merges in the reference's
+    # (round, id) order with the reference's parent and kid pool ids; splits
+    # in its order; split kids are canonical ids of the refined tree, i.e. the
+    # reference's kid pool ids through the BFS renumbering of its own result
     merges = [(n, k) for kind, n, k in rep.events if kind == "merge"]
-    np.testing.assert_array_equal(sorted(m[0] for m in merges), sorted(case["merge_parents"]))
-    splits = [n for kind, n, k in rep.events if kind == "split"]
-    np.testing.assert_array_equal(splits, case["split_leaves"])
+    np.testing.assert_array_equal([m[0] for m in merges], case["merge_parents"])
+    if merges:
+        np.testing.assert_array_equal([m[1] for m in merges], case["child"][case["merge_parents"]])
+    splits = [(n, k) for kind, n, k in rep.events if kind == "split"]
+    np.testing.assert_array_equal([n for n, _ in splits], case["split_leaves"])
+    if splits:
+        after = {k[6:]: case[k] for k in case.files if k.startswith("after_")}
+        after["free"] = case["after_free"]
+        _, new_index = oracle.PoolTree.from_arrays(after).level_order()
+        np.testing.assert_array_equal([k for _, k in splits], new_index[case["split_kids"]])
     assert buf.is_fresh() and buf.epoch_rays == 0 and not bool(buf.accumulator.any())
 
 

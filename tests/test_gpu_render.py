@@ -15,6 +15,8 @@ import pytest
 
 from conftest import GOLDEN
 
+from helpers import assert_grads_close  # noqa: E402
+
 pytestmark = pytest.mark.gpu
 
 ATOL, RTOL = 1e-4, 1e-3
@@ -61,8 +63,8 @@ def test_backward_matches_reference(case, tag, eps):
                                               case["bg"], eps, float(case["t_near"]),
                                               float(case["t_far"]))
     assert loss == pytest.approx(float(case[f"loss_{tag}"]), rel=RTOL, abs=ATOL)
-    np.testing.assert_allclose(grads.dsigma, case[f"dsigma_{tag}"], atol=ATOL, rtol=RTOL)
-    np.testing.assert_allclose(grads.dsh, case[f"dsh_{tag}"], atol=ATOL, rtol=RTOL)
+    assert_grads_close(grads.dsigma, case[f"dsigma_{tag}"], what="dsigma")
+    assert_grads_close(grads.dsh, case[f"dsh_{tag}"], what="dsh")
     np.testing.assert_array_equal(grads.touched, case[f"touched_{tag}"])
     np.testing.assert_allclose(signal, case[f"signal_{tag}"], atol=ATOL, rtol=RTOL)
 
@@ -84,8 +86,8 @@ def test_config1_golden():
     loss, grads, signal = render_and_backprop(tree, z["origins"], z["dirs"], z["targets"], 1.0)
     assert loss == pytest.approx(float(z["loss"]), rel=RTOL, abs=ATOL)
     np.testing.assert_array_equal(grads.touched, z["touched"])
-    np.testing.assert_allclose(grads.dsigma[z["touched"]], z["dsigma_touched"], atol=ATOL, rtol=RTOL)
-    np.testing.assert_allclose(grads.dsh[z["touched"]], z["dsh_touched"], atol=ATOL, rtol=RTOL)
+    assert_grads_close(grads.dsigma[z["touched"]], z["dsigma_touched"], what="dsigma")
+    assert_grads_close(grads.dsh[z["touched"]], z["dsh_touched"], what="dsh")
     np.testing.assert_allclose(signal, z["signal"], atol=ATOL, rtol=RTOL)
 
 
@@ -110,8 +112,8 @@ def test_random_trees_vs_oracle(oracle, B):
         loss, g, sig = render_and_backprop(tree, o, d, tg, 0.3, eps)
         r_loss, r_g, r_sig = oracle.render_and_backprop(tree, o, d, tg, 0.3, eps)
         assert loss == pytest.approx(r_loss, rel=RTOL, abs=ATOL)
-        np.testing.assert_allclose(g.dsigma, r_g.dsigma, atol=ATOL, rtol=RTOL)
-        np.testing.assert_allclose(g.dsh, r_g.dsh, atol=ATOL, rtol=RTOL)
+        assert_grads_close(g.dsigma, r_g.dsigma, what="dsigma")
+        assert_grads_close(g.dsh, r_g.dsh, what="dsh")
         np.testing.assert_array_equal(g.touched, r_g.touched)
         np.testing.assert_allclose(sig, r_sig, atol=ATOL, rtol=RTOL)
 
@@ -242,8 +244,8 @@ def test_long_rays_resume_past_the_record_buffer(oracle):
         loss, g, sig = render_and_backprop(tree, o, d, tg, 0.5, 0.0, deterministic=det)
         r_loss, r_g, r_sig = oracle.render_and_backprop(tree, o, d, tg, 0.5, 0.0)
         assert loss == pytest.approx(r_loss, rel=RTOL, abs=ATOL)
-        np.testing.assert_allclose(g.dsigma, r_g.dsigma, atol=ATOL, rtol=RTOL)
-        np.testing.assert_allclose(g.dsh, r_g.dsh, atol=ATOL, rtol=RTOL)
+        assert_grads_close(g.dsigma, r_g.dsigma, what="dsigma")
+        assert_grads_close(g.dsh, r_g.dsh, what="dsh")
         np.testing.assert_array_equal(g.touched, r_g.touched)
         np.testing.assert_allclose(sig, r_sig, atol=ATOL, rtol=RTOL)
 
@@ -322,7 +324,7 @@ def test_large_batch_with_schedule_vs_oracle(oracle):
     loss, g, sig = render_and_backprop(tree, o, d, tg, 0.4)
     r_loss, r_g, r_sig = oracle.render_and_backprop(tree, o, d, tg, 0.4)
     assert loss == pytest.approx(r_loss, rel=RTOL, abs=ATOL)
-    np.testing.assert_allclose(g.dsigma, r_g.dsigma, atol=ATOL, rtol=RTOL)
-    np.testing.assert_allclose(g.dsh, r_g.dsh, atol=ATOL, rtol=RTOL)
+    assert_grads_close(g.dsigma, r_g.dsigma, what="dsigma")
+    assert_grads_close(g.dsh, r_g.dsh, what="dsh")
     np.testing.assert_array_equal(g.touched, r_g.touched)
     np.testing.assert_allclose(sig, r_sig, atol=ATOL, rtol=RTOL)

@@ -29,7 +29,20 @@ def test_library_exports_every_header_symbol():
     for s in syms:
         assert hasattr(lib, s), s
     assert set(syms) == set(_lib.symbols())
-    assert lib.dot_abi_version() == _lib.ABI_VERSION == 8
+    assert lib.dot_abi_version() == _lib.ABI_VERSION == 9
+
+
+def test_binding_arity_matches_header():
+    """Every ctypes signature in _lib has as many arguments as the header's
+    prototype (an ABI change must touch both)."""
+    from paper_2307_15333_b200 import _lib
+    text = open(os.path.join(ROOT, "include", "dot_b200.h")).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    protos = dict(re.findall(r"\b(dot_[a-z0-9_]+)\s*\(([^;{]*?)\)\s*;", text))
+    for name, (_, args) in _lib._SIGNATURES.items():
+        params = protos[name].strip()
+        n = 0 if params in ("", "void") else params.count(",") + 1
+        assert n == len(args), (name, n, len(args))
 
 
 def test_library_is_sm100a():
@@ -272,3 +285,17 @@ def test_exp_ref_matches_libm():
         np.array_equal(got, want, equal_nan=True)
     bad = np.nonzero(got.view(np.uint64) != want.view(np.uint64))[0]
     assert all(np.isnan(x[bad])), x[bad][:5]
+
+
+def test_grad_comparison_rejects_wrong_gradients():
+    """The scale-aware gradient check (helpers.assert_grads_close) fails for
+    zeroed and for 1 %-scaled gradients of realistic magnitude (~1e-6)."""
+    import pytest
+    from helpers import assert_grads_close
+    rng = np.random.default_rng(0)
+    want = rng.normal(0.0, 1e-6, (500, 48)) * (rng.uniform(size=(500, 1)) < 0.7)
+    assert_grads_close(want * (1 + 1e-6 * rng.normal(size=want.shape)), want)
+    with pytest.raises(AssertionError):
+        assert_grads_close(np.zeros_like(want), want)
+    with pytest.raises(AssertionError):
+        assert_grads_close(want * 1.01, want)

@@ -94,3 +94,90 @@ def test_oracle_remap_golden(oracle):
     np.testing.assert_array_equal(c["is_leaf"] == 1, leaf)
     np.testing.assert_array_equal(vs[c["order"]][leaf], z["canon_v_sigma"][leaf])
     np.testing.assert_array_equal(vh[c["order"]][leaf], z["canon_v_sh"][leaf])
+
+
+@pytest.mark.parametrize("path", CALIB, ids=lambda p: os.path.basename(p)[6:-4])
+def test_oracle_fast_calibrate_golden(oracle, path):
+    """The vectorised oracle (used at configs[4]'s 16M leaves) leaves the
+    reference's exact pool behind: slots, free list, payload, split ids."""
+    z = np.load(path)
+    t = oracle.PoolTree.from_arrays(z)
+    thr = float(z["threshold"])
+    thr = None if np.isnan(thr) else thr
+    r = oracle.calibrate(t, z["acc"], float(z["tau"]), float(z["gamma"]), bool(z["recursive"]),
+                         thr, str(z["target"]) == "sigma", fast=True)
+    assert (r.merges_applied, r.splits_applied, r.recursion_rounds, r.leaves_after) == (
+        int(z["merges_applied"]), int(z["splits_applied"]), int(z["recursion_rounds"]),
+        int(z["leaves_after"]))
+    for k in ("child", "parent", "depth", "leaf", "alive", "center"):
+        np.testing.assert_array_equal(getattr(t, "_" + k), z["after_" + k])
+    np.testing.assert_array_equal(t.sigma, z["after_sigma"])
+    np.testing.assert_array_equal(t.sh, z["after_sh"])
+    np.testing.assert_array_equal(np.asarray(t._free), z["after_free"])
+    np.testing.assert_array_equal(r.sample_selection, z["split_leaves"])
+    np.testing.assert_array_equal(r.split_kids, z["split_kids"])
+    if r.merge_rounds:
+        np.testing.assert_array_equal(np.concatenate([p for p, _ in r.merge_rounds]), z["merge_parents"])
+
+
+def test_oracle_fast_load_equals_sequential(oracle):
+    """from_canonical_words == from_canonical (load_tree's BFS split loop),
+    and a fast calibrate that grows the pool == the sequential one."""
+    rng = np.random.default_rng(5)
+    t = oracle.PoolTree((0.1, -0.2, 0.3), 1.5, 4, 5, 8)
+    t.sigma[0] = 1.0
+    for _ in range(60):
+        leaves = t.leaf_ids()
+        ok = leaves[t._depth[leaves] < 4]
+        kids = t.split_leaf(int(rng.choice(ok)))
+        t.sigma[kids] = rng.uniform(0, 3, 8)
+        t.sh[kids] = rng.normal(0, 1, (8, 12))
+    c = t.canonical()
+    node = np.where(c["is_leaf"] == 1, ~np.arange(c["is_leaf"].size), c["kids"][:, 0])
+    args = ((0.1, -0.2, 0.3), 1.5, 4, 5)
+    a = oracle.PoolTree.from_canonical(*args, c["kids"], c["is_leaf"], c["sigma"], c["sh"])
+    b = oracle.PoolTree.from_canonical_words(*args, node, c["sigma"], c["sh"])
+    for k in ("_child", "_parent", "_depth", "_leaf", "_alive", "_center", "sigma", "sh"):
+        np.testing.assert_array_equal(getattr(a, k), getattr(b, k))
+    assert a._free == b._free and a.leaf_count == b.leaf_count
+    acc = np.where(a._leaf == 1, rng.lognormal(-2, 2, a.capacity), 0.0)
+    ra = oracle.calibrate(a, acc, 0.05, 0.5)
+    rb = oracle.calibrate(b, acc, 0.05, 0.5, fast=True)
+    assert b.capacity > a.capacity // 2 and (ra.splits_applied, ra.merges_applied) == (rb.splits_applied, rb.merges_applied)
+    for k in ("_child", "_parent", "_depth", "_leaf", "_alive", "_center", "sigma", "sh"):
+        np.testing.assert_array_equal(getattr(a, k), getattr(b, k))
+    assert a._free == b._free
+
+
+@pytest.mark.parametrize("path", RENDER, ids=lambda p: os.path.basename(p)[7:-4])
+def test_oracle_weights_definition(oracle, path):
+    """oracle_weights (depth, per-leaf sum / max of T_i Q_i -- extras with no
+    reference counterpart) restated in Python over the reference's segment
+    lists, and tied to the reference's own outputs: summed over leaves the
+    weight sum equals sum_rays (weight sum - T_final) of render_rays."""
+    import math
+    z = np.load(path)
+    t = oracle.PoolTree.from_arrays(z)
+    tn, tf = float(z["t_near"]), float(z["t_far"])
+    for tag, eps in (("eps", 1e-4), ("noeps", 0.0)):
+        depth, wsum, wmax = oracle.render_weights(t, z["origins"], z["dirs"], eps, tn, tf)
+        off, leaf, st, sd = z["seg_offsets"], z["seg_leaf"], z["seg_t"], z["seg_delta"]
+        want_d = np.zeros(off.size - 1)
+        want_s = np.zeros(t.capacity)
+        want_m = np.zeros(t.capacity)
+        for r in range(off.size - 1):
+            trans = 1.0
+            for s in range(off[r], off[r + 1]):
+                a = math.exp(-float(t.sigma[leaf[s]]) * sd[s])
+                w = trans * (1.0 - a)
+                want_d[r] += w * (st[s] + 0.5 * sd[s])
+                want_s[leaf[s]] += w
+                want_m[leaf[s]] = max(want_m[leaf[s]], w)
+                trans *= a
+                if eps > 0.0 and trans < eps:
+                    break
+        np.testing.assert_allclose(depth, want_d, rtol=1e-12, atol=1e-15)
+        np.testing.assert_allclose(wsum, want_s, rtol=1e-12, atol=1e-15)
+        np.testing.assert_array_equal(wmax, want_m)
+        ref = (z[f"wsum_{tag}"] - z[f"tfin_{tag}"]).sum()
+        assert wsum.sum() == pytest.approx(ref, rel=1e-12, abs=1e-12)
