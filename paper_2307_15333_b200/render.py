@@ -194,6 +194,17 @@ class _IO:
         return t
 
 
+def _on_device(x: torch.Tensor, dev: torch.device) -> bool:
+    return x.device.type == dev.type and (dev.index is None or x.device.index == dev.index)
+
+
+def _check_out(name: str, x, dtype, tree) -> None:
+    """A caller-provided per-leaf output: contiguous [capacity] of ``dtype`` on the tree's device."""
+    if x is not None and (not isinstance(x, torch.Tensor) or x.dtype != dtype or not _on_device(x, tree.device)
+                          or x.numel() != tree.capacity or not x.is_contiguous()):
+        raise InputError(f"{name} must be a contiguous {dtype} [capacity] tensor on {tree.device}")
+
+
 def _background(bg) -> np.ndarray:
     b = np.asarray(bg, dtype=np.float64)
     if b.ndim == 0:
@@ -456,10 +467,8 @@ def render_and_backprop(tree: SparseOctree, origins, dirs, targets, background,
         raise InputError(f"batch length mismatch: {n} origins, {d.shape[0]} dirs, "
                          f"{t.shape[0]} targets")
     n_pool = int(o.shape[0])
-    for name, x in (("weight_sum", weight_sum), ("weight_max", weight_max)):
-        if x is not None and (not isinstance(x, torch.Tensor) or x.dtype != torch.float64
-                              or x.device != tree.device or x.numel() != tree.capacity or not x.is_contiguous()):
-            raise InputError(f"{name} must be a contiguous float64 [capacity] tensor on {tree.device}")
+    _check_out("weight_sum", weight_sum, torch.float64, tree)
+    _check_out("weight_max", weight_max, torch.float64, tree)
     if deterministic and (weight_sum is not None or weight_max is not None):
         raise InputError("weight_sum / weight_max are not available with deterministic=True")
     ws = workspace if workspace is not None else BackpropWorkspace.for_tree(tree)
@@ -578,9 +587,7 @@ def signal_pass(tree: SparseOctree, origins, dirs, early_stop_eps: float = EPS_T
         signal = torch.zeros(cap, dtype=torch.float64, device=dev)
     for name, x, dt in (("signal", signal, torch.float64), ("weight_sum", weight_sum, torch.float64),
                         ("weight_max", weight_max, torch.float64), ("touched", touched, torch.uint8)):
-        if x is not None and (not isinstance(x, torch.Tensor) or x.dtype != dt or x.device != dev
-                              or x.numel() != cap or not x.is_contiguous()):
-            raise InputError(f"{name} must be a contiguous {dt} [capacity] tensor on {dev}")
+        _check_out(name, x, dt, tree)
     if n:
         if coherent and n >= COHERENT_MIN_RAYS:
             idx = plan_batch(tree, o, d, idx).idx

@@ -27,6 +27,11 @@ def test_reference_arm_json_line():
     assert j["e2e"] == {"value": j["value"], "unit": "rays/s", "h2d_bytes_per_step": 0,
                         "d2h_bytes_per_step": 0}
     assert j["config"]["workload"].startswith("configs[1]")
+    # the reference arm prints our arm's workload config (bench.workload_config)
+    assert set(j["config"]) == {"workload", "leaves", "nodes", "global_batch", "views", "resolution",
+                                "batch_draw", "eps", "background", "l2"}
+    assert j["config"]["global_batch"] == 1 << 20 and j["config"]["leaves"] > 2_000_000
+    assert j["cpu_baseline"]["one_thread"]["cores"] == 1 and j["cpu_baseline"]["one_thread"]["value"] > 0
 
 
 def test_clock_sampler_window():

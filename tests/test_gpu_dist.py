@@ -116,7 +116,8 @@ def test_train_step_world2_equals_single_process(tmp_path):
     np.testing.assert_allclose(r0["sh"], one["sh"], rtol=1e-4, atol=1e-6)
     np.testing.assert_allclose(r0["v_sigma"], one["v_sigma"], rtol=1e-3, atol=1e-18)
     np.testing.assert_allclose(r0["v_sh"], one["v_sh"], rtol=1e-3, atol=1e-18)
-    np.testing.assert_allclose(r0["signal"], one["signal"], rtol=1e-9, atol=1e-12)
+    # steps 2-3 run on payloads that already differ by fp32-atomic rounding
+    np.testing.assert_allclose(r0["signal"], one["signal"], rtol=1e-5, atol=1e-12)
     assert int(r0["rays"]) + int(r1["rays"]) == int(one["rays"]) == STEPS * N_GLOBAL
     # the refine after the signal all-reduce: identical trees on both ranks
     assert str(r0["sha"]) == str(r1["sha"])

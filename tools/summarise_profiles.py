@@ -23,7 +23,13 @@ KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "sm__warps_active.avg.pct_of_peak_sustained_active",
         "smsp__thread_inst_executed_per_inst_executed.ratio", "launch__registers_per_thread",
         "smsp__inst_executed.sum", "lts__t_sectors_srcunit_tex_op_red.sum",
-        "smsp__inst_executed_op_global_red.sum", "launch__grid_size", "launch__block_size"]
+        "smsp__inst_executed_op_global_red.sum", "launch__grid_size", "launch__block_size",
+        "smsp__issue_active.avg.pct_of_peak_sustained_active",
+        "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
+        "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active",
+        "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active",
+        "sass__inst_executed_register_spilling",
+        "l1tex__t_sectors_pipe_lsu_mem_local_op_ld.sum", "l1tex__t_sectors_pipe_lsu_mem_local_op_st.sum"]
 
 
 def launch_shares(path):
@@ -70,6 +76,25 @@ def full_metrics(rep):
     return out
 
 
+def refine_totals(path):
+    rows = list(csv.reader(open(path)))
+    hi = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
+    h = rows[hi]
+    mi, vi, ui, idi = h.index("Metric Name"), h.index("Metric Value"), h.index("Metric Unit"), h.index("ID")
+    t = b = 0.0
+    ids = set()
+    for r in rows[hi + 1:]:
+        if len(r) <= vi:
+            continue
+        v = float(r[vi].replace(",", ""))
+        ids.add(r[idi])
+        if r[mi] == "gpu__time_duration.sum":
+            t += v * {"ns": 1e-9, "nsecond": 1e-9, "us": 1e-6, "usecond": 1e-6, "ms": 1e-3, "msecond": 1e-3}.get(r[ui], 1.0)
+        elif r[mi].startswith("dram__bytes_"):
+            b += to_bytes(r[vi], r[ui])
+    return t, b, len(ids)
+
+
 def to_bytes(v, unit):
     v = float(v.replace(",", ""))
     return v * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}.get(unit, 1)
@@ -105,8 +130,29 @@ def main():
             traffic_hit = float(m["lts__t_sector_hit_rate.pct"][0])
         else:
             traffic_hit = None
+        def pct(k):
+            return float(m[k][0].replace(",", "")) if k in m else None
+
         traffic[key] = {"dram_bytes_per_launch": rd + wr, "dram_read": rd, "dram_write": wr,
-                        "l2_hit_pct": traffic_hit, "capture": f"profiles/{tag}_ncu_full.txt", "kernel": short}
+                        "l2_hit_pct": traffic_hit, "capture": f"profiles/{tag}_ncu_full.txt", "kernel": short,
+                        "ncu_time_s": float(m["gpu__time_duration.sum"][0].replace(",", "")) *
+                        {"ns": 1e-9, "us": 1e-6, "usecond": 1e-6, "ms": 1e-3, "msecond": 1e-3,
+                         "nsecond": 1e-9}.get(m["gpu__time_duration.sum"][1], 1.0),
+                        "issue_active_pct": pct("smsp__issue_active.avg.pct_of_peak_sustained_active"),
+                        "fp64_pipe_pct": pct("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"),
+                        "xu_pipe_pct": pct("sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active"),
+                        "lsu_pipe_pct": pct("sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active"),
+                        "warps_active_pct": pct("sm__warps_active.avg.pct_of_peak_sustained_active")}
+    refine_csv = os.path.join(src, "refine_launches.csv")
+    if os.path.exists(refine_csv):  # one refine pass: every launch's time and DRAM bytes
+        res = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "refine_launches.py"), refine_csv],
+                             capture_output=True, text=True)
+        open(os.path.join(prof, f"{tag}_refine_launches.txt"), "w").write(res.stdout)
+        tot_t, tot_b, n = refine_totals(refine_csv)
+        traffic["refine_pass"] = {"dram_bytes_per_launch": tot_b, "ncu_time_s": tot_t, "launches": n,
+                                  "capture": f"profiles/{tag}_refine_launches.txt",
+                                  "kernel": "one configs[4] refine pass (all launches)"}
+        lines.append("\n## refine pass (configs[4])\n" + res.stdout)
     open(os.path.join(prof, f"{tag}_ncu_full.txt"), "w").write("\n".join(lines) + "\n")
     json.dump(traffic, open(traffic_path, "w"), indent=1)
     print(text)
