@@ -488,6 +488,32 @@ def run_ours(args, rank, world, local_rank):
     e2e_ms = timed(staged_loop)
     e2e_value = n_global * args.steps / (e2e_ms / 1e3)
 
+    # the optimizer update alone on one batch's gradients (consume=False so
+    # every repetition sees them): the reference's f64 state (the timed step
+    # above) and the opt-in f32 state
+    from paper_2307_15333_b200.optim import rmsprop_step
+    from paper_2307_15333_b200.render import BackpropWorkspace, render_and_backprop
+    rws = BackpropWorkspace.for_tree(tree)
+    _, rg, _ = render_and_backprop(tree, origins, dirs, targets, BG, EPS, ray_index=perm[total_steps],
+                                   grad_scale=gs, workspace=rws)
+    rms = {}
+    for name, dt in (("f64_state_ms", torch.float64), ("f32_state_ms", torch.float32)):
+        st = RmsPropState(tree, state_dtype=dt)
+        for _ in range(3):
+            rmsprop_step(tree, rg, st)
+        torch.cuda.synchronize()
+        r0, r1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        r0.record()
+        for _ in range(10):
+            rmsprop_step(tree, rg, st)
+        r1.record()
+        torch.cuda.synchronize()
+        rms[name] = r0.elapsed_time(r1) / 10
+    rms["touched_rows"] = int(rws.touched.sum())
+    rms["note"] = ("rmsprop_step alone on one batch's gradients; f64 = the reference's state dtype (bit-exact, "
+                   "the headline step), f32 = opt-in RmsPropState(state_dtype=torch.float32)")
+    del rws, rg
+
     # signal-only forward (dot_signal_fwd) on a training batch: the
     # calibration-only pass, same rays, no gradients
     from paper_2307_15333_b200.render import signal_pass
@@ -565,6 +591,7 @@ def run_ours(args, rank, world, local_rank):
                 "serial_ms_per_step": e2e_serial_ms / args.steps},
         "clocks": clk,
         "signal_fwd": signal_fwd,
+        "rmsprop": rms,
         "render": render,
         "refine": refine,
         "cpu_baseline": cpu,

@@ -285,6 +285,17 @@ int dot_rmsprop_step(float* sigma, float* sh, int32_t sh_stride, int32_t n_sh,
                      int64_t capacity, double beta, double eps, double lr_sigma,
                      double lr_sh, int32_t flags, void* stream);
 
+/* --- the same update with f32 second moments (opt-in, no reference
+ *     counterpart: octrf keeps f64 state, optim.py:70-72).  Arithmetic is
+ *     f64 with v widened on read and rounded once on store; results are
+ *     within float tolerance of dot_rmsprop_step and the state traffic is
+ *     halved.  sh, grad_sh and v_sh must be 16-byte aligned. */
+int dot_rmsprop_step_f32state(float* sigma, float* sh, int32_t sh_stride, int32_t n_sh,
+                              float* v_sigma, float* v_sh, float* grad_sigma, float* grad_sh,
+                              int32_t gsh_stride, const uint8_t* touched, int64_t capacity,
+                              double beta, double eps, double lr_sigma, double lr_sh,
+                              int32_t flags, void* stream);
+
 /* --- multi-GPU update fused with its collective (one node, peer memory
  *     over NVLink/NVSwitch; replaces all-reduce + rmsprop_step of the
  *     data-parallel step).  Rank `rank` of `world` calls it for the rows it

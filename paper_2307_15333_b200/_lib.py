@@ -99,6 +99,9 @@ _SIGNATURES = {
     "dot_rmsprop_step": (c_i32, [c_void_p, c_void_p, c_i32, c_i32, c_void_p, c_void_p, c_void_p,
                                  c_void_p, c_i32, c_void_p, c_i64, c_f64, c_f64, c_f64, c_f64,
                                  c_i32, c_void_p]),
+    "dot_rmsprop_step_f32state": (c_i32, [c_void_p, c_void_p, c_i32, c_i32, c_void_p, c_void_p, c_void_p,
+                                          c_void_p, c_i32, c_void_p, c_i64, c_f64, c_f64, c_f64, c_f64,
+                                          c_i32, c_void_p]),
 }
 
 _lib = None

@@ -133,14 +133,35 @@ __device__ __forceinline__ double pow2i(int e) {  // 2^e, |e| < 1000
     return __longlong_as_double(int64_t(1023 + e) << 52);
 }
 
-__device__ __forceinline__ Leaf descend_grid(const TreeDev& T, double px, double py, double pz) {
+// Integer cell coordinates (depth kLocBits) of a point, and its table entry.
+__device__ __forceinline__ void grid_coords(const TreeDev& T, double px, double py, double pz, int& ix, int& iy,
+                                            int& iz) {
     const double s = T.loc_scale, top = double((1 << kLocBits) - 1);
     const double fx = fmin(fmax(dsub(floor(dmul(px, s)), T.loc_lo[0]), 0.0), top);
     const double fy = fmin(fmax(dsub(floor(dmul(py, s)), T.loc_lo[1]), 0.0), top);
     const double fz = fmin(fmax(dsub(floor(dmul(pz, s)), T.loc_lo[2]), 0.0), top);
-    const int ix = __double2int_rz(fx), iy = __double2int_rz(fy), iz = __double2int_rz(fz);
+    ix = __double2int_rz(fx);
+    iy = __double2int_rz(fy);
+    iz = __double2int_rz(fz);
+}
+
+__device__ __forceinline__ int32_t grid_entry(const TreeDev& T, int ix, int iy, int iz) {
     const int Lv = T.loc_level, k = kLocBits - Lv;
-    const int32_t e = __ldg(T.loc + ((ix >> k) | ((iy >> k) << Lv) | ((iz >> k) << (2 * Lv))));
+    return __ldg(T.loc + ((ix >> k) | ((iy >> k) << Lv) | ((iz >> k) << (2 * Lv))));
+}
+
+__device__ __forceinline__ Leaf descend_from(const TreeDev& T, int ix, int iy, int iz, int32_t e);
+
+__device__ __forceinline__ Leaf descend_grid(const TreeDev& T, double px, double py, double pz) {
+    int ix, iy, iz;
+    grid_coords(T, px, py, pz, ix, iy, iz);
+    return descend_from(T, ix, iy, iz, grid_entry(T, ix, iy, iz));
+}
+
+// The rest of the descent below the table level from the entry e of cell
+// (ix, iy, iz), and the leaf centre.
+__device__ __forceinline__ Leaf descend_from(const TreeDev& T, int ix, int iy, int iz, int32_t e) {
+    const int Lv = T.loc_level;
     int dep, pid;
     if (e >= 0) {
         int32_t w = e;

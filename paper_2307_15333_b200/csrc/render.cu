@@ -34,6 +34,11 @@ constexpr int kBwdRecords = 128;   // composited segments buffered per ray (pass
 #ifndef DOT_BWD_MINB
 #define DOT_BWD_MINB 24
 #endif
+// Pass 2 reads its records two ahead (measured 1.69 -> 1.67 ms; at the
+// former 64-register cap it spilled and lost).
+#ifndef DOT_REC_PREFETCH2
+#define DOT_REC_PREFETCH2 1
+#endif
 
 static unsigned blocks_for(int64_t n) { return unsigned((n + kBlock - 1) / kBlock); }
 
@@ -479,6 +484,10 @@ __global__ void __launch_bounds__(32, DOT_BWD_MINB) render_bwd_buffered_kernel(
     }
     Rec nxt;
     if (used > 0) nxt = buf[0];
+#if DOT_REC_PREFETCH2
+    Rec nxt2;
+    if (used > 1) nxt2 = buf[1];
+#endif
     for (int i = 0; i < maxu; ++i) {
         const bool act = valid && i < used;
         int64_t pid = 0;
@@ -487,7 +496,12 @@ __global__ void __launch_bounds__(32, DOT_BWD_MINB) render_bwd_buffered_kernel(
         if (act) {
             if (i < K) {  // software pipeline: entry i+1 is in flight while i is scattered
                 const Rec e = nxt;
+#if DOT_REC_PREFETCH2
+                nxt = nxt2;
+                if (i + 2 < used && i + 2 < K) nxt2 = buf[i + 2];
+#else
                 if (i + 1 < used && i + 1 < K) nxt = buf[i + 1];
+#endif
                 pid = e.pid;
                 e.alpha(a, q);
                 dl = e.delta;
@@ -996,7 +1010,10 @@ int launch_ray_stats(const TreeDev& T, const double* o, const double* d, int64_t
 
 constexpr int kSchedBits = 24;
 constexpr int kSchedSort = 2048;    // chunks ranked per launch (one block, bitonic in shared memory)
-constexpr int kSchedMinChunk = 16;  // warps per chunk (coherence kept inside a chunk)
+#ifndef DOT_SCHED_CHUNK
+#define DOT_SCHED_CHUNK 16
+#endif
+constexpr int kSchedMinChunk = DOT_SCHED_CHUNK;  // warps per chunk (coherence kept inside a chunk)
 
 constexpr int kSchedFineBits = 27;  // second, finer table (fallback to the coarse one when empty)
 

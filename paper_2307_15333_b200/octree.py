@@ -104,11 +104,13 @@ def locate_level_default() -> int:
 
 
 def locate_level_train() -> int:
-    """Locate-table level of the training backward (env DOT_TRAIN_LOCATE_LEVEL):
-    one level deeper than the render's -- random training rays reuse table
-    entries less than camera rays, so resolving one more level per load pays
-    (backward -2.5 %) where the render prefers the 8x smaller table."""
-    return int(os.environ.get("DOT_TRAIN_LOCATE_LEVEL", "9"))
+    """Locate-table level of the training backward (env DOT_TRAIN_LOCATE_LEVEL).
+    The render's level 7 (2 MB, the same table): with the 80-register
+    backward, level 9 (512 MB, one load per depth-9 leaf) no longer pays --
+    step 2.43 ms with level 7 vs 2.44 with level 9 (the backward equal, the
+    optimizer faster without the 512 MB table churning L2) -- and it saves
+    512 MB per tree generation."""
+    return int(os.environ.get("DOT_TRAIN_LOCATE_LEVEL", "7"))
 
 
 class SparseOctree:

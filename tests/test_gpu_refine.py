@@ -280,3 +280,41 @@ def test_rmsprop_zero_gradient_rows_bit_exact(oracle):
     np.testing.assert_array_equal(tree.sh.cpu().numpy(), sh0)
     np.testing.assert_array_equal(st.v_sigma.cpu().numpy(), vs)
     np.testing.assert_array_equal(st.v_sh.cpu().numpy(), vh)
+
+
+@pytest.mark.parametrize("B", [16, 1])
+def test_rmsprop_f32_state_within_tolerance(oracle, B):
+    """The opt-in f32 second-moment update (state_dtype=float32) against the
+    reference's f64 update (oracle): payloads and state within 1e-6 relative,
+    zero-gradient rows still decay v only, untouched rows untouched."""
+    from paper_2307_15333_b200.optim import RmsPropState, rmsprop_step
+    from paper_2307_15333_b200.render import GradBuffer
+    from helpers import irregular_tree
+    rng = np.random.default_rng(9 + B)
+    tree = irregular_tree(57, B, depth=2, splits=4, max_depth=4, device="cuda")
+    cap, nsh = tree.capacity, 3 * B
+    st = RmsPropState(tree, state_dtype=torch.float32)
+    v0s = rng.uniform(0, 1e-3, cap).astype(np.float32)
+    v0h = rng.uniform(0, 1e-3, (cap, nsh)).astype(np.float32)
+    st.v_sigma.copy_(torch.from_numpy(v0s))
+    st.v_sh.copy_(torch.from_numpy(v0h))
+    gs = rng.normal(0, 1e-2, cap).astype(np.float32)
+    gh = rng.normal(0, 1e-2, (cap, nsh)).astype(np.float32)
+    gs[::3] = 0.0
+    gh[::3] = 0.0
+    mask = (rng.uniform(size=cap) < 0.7).astype(np.uint8)
+    sig0 = tree.sigma.cpu().numpy().copy()
+    sh0 = tree.sh.cpu().numpy().copy()
+    for _ in range(2):
+        rmsprop_step(tree, GradBuffer(gs, gh, mask, tree.generation), st)
+    vs, vh = v0s.astype(np.float64), v0h.astype(np.float64)
+    es, eh = sig0.copy(), sh0.copy()
+    for _ in range(2):
+        oracle.rmsprop_step(es, eh, vs, vh, gs.astype(np.float64), gh.astype(np.float64), np.nonzero(mask)[0])
+    np.testing.assert_allclose(tree.sigma.cpu().numpy(), es, rtol=1e-6, atol=1e-7)
+    np.testing.assert_allclose(tree.sh.cpu().numpy(), eh, rtol=1e-6, atol=1e-7)
+    np.testing.assert_allclose(st.v_sigma.cpu().numpy(), vs, rtol=1e-6, atol=0)
+    np.testing.assert_allclose(st.v_sh.cpu().numpy(), vh, rtol=1e-6, atol=0)
+    untouched = mask == 0
+    np.testing.assert_array_equal(st.v_sh.cpu().numpy()[untouched], v0h[untouched])
+    np.testing.assert_array_equal(tree.sh.cpu().numpy()[untouched], sh0[untouched])

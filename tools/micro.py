@@ -32,8 +32,8 @@ def timeit(fn, reps=5, warm=2):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--batch", type=int, default=20)
-    ap.add_argument("--order", default="morton")
-    ap.add_argument("--flags", default="0,32768,det")
+    ap.add_argument("--order", default="random")
+    ap.add_argument("--flags", default="0,1,32768,det")
     args = ap.parse_args()
     dev = torch.device("cuda")
     tree = scenes.config2_scene(device=dev)
