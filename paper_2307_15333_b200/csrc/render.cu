@@ -388,25 +388,27 @@ __global__ void __launch_bounds__(32, DOT_BWD_MINB) render_bwd_buffered_kernel(
             Leaf L;
             double te, dl;
             bool cut = false;
-            while (tr.next_prefetch(T, L, te, dl, !cut)) {
-                touched[L.pid] = 1;
+            // one segment of pass 1: touched mark; before the cut, alpha, the
+            // signal, shading, colour and the record for pass 2
+            auto segment = [&](const int32_t pid, const double te_c, const double dl_c) {
+                touched[pid] = 1;
                 if (cut) {  // post-cut: touched only
 #if DOT_SCHED_COST
                     ++tail;
 #endif
-                    continue;
+                    return;
                 }
-                const double a = exp_ref(-double(__ldg(T.sigma + L.pid)) * dl);
+                const double a = exp_ref(-double(__ldg(T.sigma + pid)) * dl_c);
                 const double q = 1.0 - a;
                 const double tq = trans * q;
 #ifdef DOT_DIAG_FLAGS
                 if (!(flags & 16384))
 #endif
-                sink.pass1(L.pid, q, tq);
+                sink.pass1(pid, q, tq);
                 float k0 = __int_as_float(0x7fc00000), k1 = k0, k2 = k0;
                 if (q > 0.0) {
                     float e0, e1, e2;
-                    sh_dot<B>(T.sh + int64_t(L.pid) * S, basis, e0, e1, e2);
+                    sh_dot<B>(T.sh + int64_t(pid) * S, basis, e0, e1, e2);
                     k0 = sigmoidf(e0);
                     k1 = sigmoidf(e1);
                     k2 = sigmoidf(e2);
@@ -416,26 +418,23 @@ __global__ void __launch_bounds__(32, DOT_BWD_MINB) render_bwd_buffered_kernel(
                 }
                 if (used < K) {
                     Rec e;
-                    e.pid = L.pid;
-                    e.delta = float(dl);
+                    e.pid = pid;
+                    e.delta = float(dl_c);
                     e.set_alpha(a, q);
                     e.k0 = k0;
                     e.k1 = k1;
                     e.k2 = k2;
                     buf[used] = e;
                 } else if (used == K) {  // buffer full: remember where pass 2 resumes
-                    resume_t = te;
+                    resume_t = te_c;
                     resume_nudge = tr.nudge0;
                 }
                 ++used;
                 trans *= a;
-                if (eps > 0.0 && trans < eps) {
-                    cut = true;
-#ifdef DOT_DIAG_FLAGS
-                    if (flags & 1) break;
-#endif
-                }
-            }
+                if (eps > 0.0 && trans < eps) cut = true;
+            };
+            while (tr.next_prefetch(T, L, te, dl, !cut)) segment(L.pid, te, dl);
+
         }
         const double tf = trans;
         R0 = c0 + tf * bg0;
@@ -557,12 +556,13 @@ int launch_render_bwd(const TreeDev& T, const double* o, const double* d, const 
     const bool coop = (flags & 32768) == 0;
     AtomicSink as{gsig, gsh, signal, loss, wsum, wmax};
     CoopSink cs;
+    using CoopT = CoopSink;
     static_cast<AtomicSink&>(cs) = as;
     cs.sb = nullptr;
     cs.sr = nullptr;
 #define DOT_BWD(BB)                                                                                  \
     if (coop)                                                                                        \
-        render_bwd_buffered_kernel<BB, CoopSink><<<grid, 32, 0, s>>>(                                \
+        render_bwd_buffered_kernel<BB, CoopT><<<grid, 32, 0, s>>>(                                   \
             T, o, d, tgt, ray_idx, n_pool, n, bg[0], bg[1], bg[2], eps, tn, tf, gs, touched, rgb_out, flags, cs, \
             warp_order, ray_used);                                                                   \
     else                                                                                             \
