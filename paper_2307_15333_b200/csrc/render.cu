@@ -36,6 +36,14 @@ constexpr int kBwdRecords = 128;   // composited segments buffered per ray (pass
 #endif
 // Pass 2 reads its records two ahead (measured 1.69 -> 1.67 ms; at the
 // former 64-register cap it spilled and lost).
+// Shared-memory carveout hint of the backward (percent of the unified
+// L1 / shared array): 25 % (57 KB of shared memory: 16 one-warp blocks of
+// 3.5 KB) leaves ~200 KB of L1 for the local-memory records and SH rows,
+// which matters more than the 8 warps it costs: step 2.430 -> 2.414 ms
+// (driver default = enough shared memory for 24 blocks).
+#ifndef DOT_BWD_CARVEOUT
+#define DOT_BWD_CARVEOUT 25
+#endif
 #ifndef DOT_REC_PREFETCH2
 #define DOT_REC_PREFETCH2 1
 #endif
@@ -561,6 +569,9 @@ int launch_render_bwd(const TreeDev& T, const double* o, const double* d, const 
     cs.sb = nullptr;
     cs.sr = nullptr;
 #define DOT_BWD(BB)                                                                                  \
+    if (DOT_BWD_CARVEOUT >= 0)                                                                       \
+        cudaFuncSetAttribute(render_bwd_buffered_kernel<BB, CoopT>,                                  \
+                             cudaFuncAttributePreferredSharedMemoryCarveout, DOT_BWD_CARVEOUT);      \
     if (coop)                                                                                        \
         render_bwd_buffered_kernel<BB, CoopT><<<grid, 32, 0, s>>>(                                   \
             T, o, d, tgt, ray_idx, n_pool, n, bg[0], bg[1], bg[2], eps, tn, tf, gs, touched, rgb_out, flags, cs, \
