@@ -188,6 +188,16 @@ struct BufSeg {
     double a;          // alpha = exp(-sigma delta) exactly as pass 1 used it
     float k0, k1, k2;  // colour (NaN: not evaluated in pass 1, q == 0)
     float pad;
+    __device__ __forceinline__ void set_colour(float a, float b, float c) {
+        k0 = a;
+        k1 = b;
+        k2 = c;
+    }
+    __device__ __forceinline__ void colour(float& a, float& b, float& c) const {
+        a = k0;
+        b = k1;
+        c = k2;
+    }
     __device__ __forceinline__ void set_alpha(double a_, double) { a = a_; }
     __device__ __forceinline__ void alpha(double& a_, double& q_) const {
         a_ = a;
@@ -207,6 +217,16 @@ struct BufSegCompact {
     float delta;
     float aq;
     float k0, k1, k2;
+    __device__ __forceinline__ void set_colour(float a, float b, float c) {
+        k0 = a;
+        k1 = b;
+        k2 = c;
+    }
+    __device__ __forceinline__ void colour(float& a, float& b, float& c) const {
+        a = k0;
+        b = k1;
+        c = k2;
+    }
     __device__ __forceinline__ void set_alpha(double a, double q) {
         aq = a > 0.5 ? -float(q) : float(a);  // q == 0 -> -0.0f (sign bit set)
     }
@@ -429,9 +449,7 @@ __global__ void __launch_bounds__(32, DOT_BWD_MINB) render_bwd_buffered_kernel(
                     e.pid = pid;
                     e.delta = float(dl_c);
                     e.set_alpha(a, q);
-                    e.k0 = k0;
-                    e.k1 = k1;
-                    e.k2 = k2;
+                    e.set_colour(k0, k1, k2);
                     buf[used] = e;
                 } else if (used == K) {  // buffer full: remember where pass 2 resumes
                     resume_t = te_c;
@@ -512,9 +530,7 @@ __global__ void __launch_bounds__(32, DOT_BWD_MINB) render_bwd_buffered_kernel(
                 pid = e.pid;
                 e.alpha(a, q);
                 dl = e.delta;
-                k0 = e.k0;
-                k1 = e.k1;
-                k2 = e.k2;
+                e.colour(k0, k1, k2);
             } else {
                 Leaf L;
                 double te;
