@@ -18,14 +18,16 @@ _EXPORTS = {
     "EPS_T": "render", "Ray": "render", "RaySegmentList": "render", "RenderOutput": "render",
     "GradBuffer": "render", "segment_batch": "render", "traverse": "render",
     "render_rays": "render", "render_ray": "render", "render_and_backprop": "render",
-    "render_image": "render", "BackpropWorkspace": "render",
+    "render_image": "render", "BackpropWorkspace": "render", "signal_pass": "render",
+    "render_view": "render", "render_views": "render", "plan_batch": "render",
     "SignalTarget": "signals", "SignalBuffer": "signals", "signal_value": "signals",
     "signal_values": "signals",
     "CalibrationConfig": "calibrate", "CalibrationReport": "calibrate", "calibrate": "calibrate",
     "prune": "calibrate", "sample": "calibrate", "select_prune": "calibrate",
     "select_sample": "calibrate",
     "RmsPropState": "optim", "rmsprop_step": "optim", "TrainConfig": "optim",
-    "train_epoch": "optim", "train": "optim",
+    "train_epoch": "optim", "train": "optim", "train_step": "optim", "StepWorkspace": "optim",
+    "heldout_psnr": "optim",
     "Camera": "scene_io", "look_at": "scene_io", "orbit_cameras": "scene_io",
     "save_tree": "scene_io", "load_tree": "scene_io",
     "RayBatchStager": "staging", "LossReader": "staging",
