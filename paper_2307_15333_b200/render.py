@@ -577,6 +577,10 @@ def signal_pass(tree: SparseOctree, origins, dirs, early_stop_eps: float = EPS_T
         raise InputError(f"batch length mismatch: {n_pool} origins, {d.shape[0]} dirs")
     idx = None
     if ray_index is not None:
+        if not isinstance(ray_index, torch.Tensor):  # host indices: reject bad ones before any work
+            ri = np.asarray(ray_index).reshape(-1)
+            if ri.size and (ri.min() < 0 or ri.max() >= n_pool):
+                raise InputError(f"ray_index entries outside [0, {n_pool})")
         idx = torch.as_tensor(ray_index, device=tree.device).reshape(-1).to(torch.int64)
     n = int(idx.shape[0]) if idx is not None else n_pool
     cap, dev = tree.capacity, tree.device
