@@ -544,8 +544,11 @@ def run_ours(args, rank, world, local_rank):
     torch.cuda.empty_cache()
     refine = None if (args.skip_refine or rank != 0 or not side) else bench_refine(dev, args)
     cpu = None
+    refine_c2 = None
     if rank == 0 and not args.skip_cpu and side:
         cpu = cpu_baseline(tree, args)
+        if not args.skip_refine:
+            refine_c2 = refine_vs_cpu(tree, dev)
 
     if rank != 0:
         return None
@@ -599,6 +602,7 @@ def run_ours(args, rank, world, local_rank):
         "rmsprop": rms,
         "render": render,
         "refine": refine,
+        "refine_vs_cpu": refine_c2,
         "cpu_baseline": cpu,
         "setup_s": setup_s,
     }
@@ -810,12 +814,68 @@ def cpu_baseline(tree, args, n_rays=1 << 20):
     O.render_and_backprop(tree, o[:m], d[:m], tg[:m], BG, EPS)
     dt1 = time.perf_counter() - t1
     O.set_threads(cores)
+    # render (configs[2]'s op): render_rays = count + fill + composite on 2^18 rays of one view
+    fo, fd = pool_rays_np(focal, poses, W, H, np.arange(1 << 18) + 3 * W * H)
+    t = time.perf_counter()
+    O.render_rays(tree, fo, fd, BG, EPS)
+    dt_r = time.perf_counter() - t
     return {"value": o.shape[0] / dt, "unit": "rays/s", "cores": cores, "kind": "port",
             "sample": f"{o.shape[0]} uniform random rays of the 100-view pool, fwd+bwd through "
                       "oracle/dot_oracle.c (count+fill+grad+serial scatter, OpenMP)",
             "seconds": dt,
             "one_thread": {"value": m / dt1, "unit": "rays/s", "cores": 1,
-                           "sample": f"{m} of the same rays, one OpenMP thread"}}
+                           "sample": f"{m} of the same rays, one OpenMP thread"},
+            "render": {"value": (1 << 18) / dt_r, "unit": "rays/s", "cores": cores,
+                       "sample": "262144 rays of one 800x800 training view, render_rays (count + fill + "
+                                 "composite)"}}
+
+
+def refine_vs_cpu(tree, dev):
+    """One DOT refine pass on the configs[1] scene (2.6M leaves, log-normal(-6, 2)
+    signals, tau 0.01, gamma 0.1): our calibrate() vs the reference's algorithm
+    on the host (oracle.calibrate -- the faithful restatement, LIFO splits one
+    by one like octree.split_leaf_many), same tree and signals."""
+    import torch
+    from oracle import oracle as O
+    from paper_2307_15333_b200.calibrate import CalibrationConfig, calibrate
+    from paper_2307_15333_b200.octree import from_canonical_tensors
+    from paper_2307_15333_b200.signals import SignalBuffer
+    topo = tree.topology()
+    node = topo.node
+    g = torch.Generator(device=dev)
+    g.manual_seed(77)
+    acc = torch.zeros(node.shape[0], dtype=torch.float64, device=dev)
+    leaf = node < 0
+    acc[leaf] = torch.exp(-6.0 + 2.0 * torch.randn(int(leaf.sum()), generator=g, device=dev, dtype=torch.float64))
+    times = []
+    for k in range(4):
+        t2 = from_canonical_tensors(tree.center, tree.half_extent, tree.basis_count, tree.max_depth, node.clone(),
+                                    tree._sigma.clone(), tree._sh_store.clone(), topo.level_offsets)
+        buf = SignalBuffer(t2)
+        buf.accumulator.copy_(acc)
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        rep = calibrate(t2, buf, CalibrationConfig(tau=0.01, gamma=0.10))
+        b.record()
+        torch.cuda.synchronize()
+        if k:
+            times.append(a.elapsed_time(b))
+        del t2, buf
+    pool = O.PoolTree.from_canonical_words(tree.center, tree.half_extent, tree.basis_count, tree.max_depth,
+                                          node.cpu().numpy(), tree.sigma.cpu().numpy(), tree.sh.cpu().numpy())
+    acc_h = acc.cpu().numpy()
+    t = time.perf_counter()
+    ref = O.calibrate(pool, acc_h, 0.01, 0.10)
+    cpu_s = time.perf_counter() - t
+    assert (ref.merges_applied, ref.splits_applied) == (rep.merges_applied, rep.splits_applied)
+    ms = sum(times) / len(times)
+    return {"ms_per_pass": ms, "leaves_before": rep.leaves_before, "merges": rep.merges_applied,
+            "splits": rep.splits_applied,
+            "cpu_baseline": {"ms_per_pass": cpu_s * 1e3, "kind": "port", "cores": 1,
+                             "sample": "the same pass through oracle.calibrate (numpy + the reference's "
+                                       "one-by-one LIFO split loop; single-threaded like the reference)"},
+            "workload": "configs[1] scene (2.6M leaves), log-normal(-6,2) signals, tau 0.01, gamma 0.1"}
 
 
 # ---------------------------------------------------------------------------
