@@ -694,6 +694,10 @@ def bench_render(tree, dev, args, world):
                          "segments_per_ray": seg / (W * H * n_res)},
             # the kernel is issue / latency bound, not HBM bound: its pipe
             # utilisations from the same ncu capture
+            "l2_gather": {"gbs": (prof["l2_bytes_per_launch"] / 200.0) / (ms_cam / n_views / 1e3) / 1e9
+                          if prof.get("l2_bytes_per_launch") else None,
+                          "note": "ncu lts__t_bytes per view / live ms per view (L2 traffic the gathers "
+                                  "generate; DRAM is the roofline above)"},
             "issue_roofline": {"bound": "issue", "issue_active_pct": prof.get("issue_active_pct"),
                                "fp64_pipe_pct": prof.get("fp64_pipe_pct"), "xu_pipe_pct": prof.get("xu_pipe_pct"),
                                "lsu_pipe_pct": prof.get("lsu_pipe_pct"),
