@@ -44,6 +44,12 @@ constexpr int kBwdRecords = 128;   // composited segments buffered per ray (pass
 #ifndef DOT_BWD_CARVEOUT
 #define DOT_BWD_CARVEOUT 25
 #endif
+// 20-byte records (colour as 21-bit fixed point): a warp's record lines
+// take L1 space for its longest ray, so smaller records buy L1 hits --
+// backward 1.747 -> 1.733 ms
+#ifndef DOT_REC_PACKED
+#define DOT_REC_PACKED 1
+#endif
 #ifndef DOT_REC_PREFETCH2
 #define DOT_REC_PREFETCH2 1
 #endif
@@ -216,6 +222,36 @@ struct BufSegCompact {
     int32_t pid;
     float delta;
     float aq;
+#if DOT_REC_PACKED
+    // colour as three 21-bit fixed-point fractions (|error| <= 2.4e-7, far
+    // inside the gradients' scale-aware tolerance) + a "not evaluated" bit:
+    // 20-byte records
+    uint32_t clo, chi;
+    __device__ __forceinline__ void set_colour(float a, float b, float c) {
+        if (a != a) {
+            clo = 0u;
+            chi = 0x80000000u;
+            return;
+        }
+        const float sc = 2097151.0f;
+        const unsigned long long u0 = __float2uint_rn(a * sc), u1 = __float2uint_rn(b * sc),
+                                 u2 = __float2uint_rn(c * sc);
+        const unsigned long long w = u0 | (u1 << 21) | (u2 << 42);
+        clo = uint32_t(w);
+        chi = uint32_t(w >> 32);
+    }
+    __device__ __forceinline__ void colour(float& a, float& b, float& c) const {
+        if (chi & 0x80000000u) {
+            a = b = c = __int_as_float(0x7fc00000);
+            return;
+        }
+        const unsigned long long w = (static_cast<unsigned long long>(chi) << 32) | clo;
+        const float inv = 1.0f / 2097151.0f;
+        a = float(unsigned(w & 0x1FFFFFull)) * inv;
+        b = float(unsigned((w >> 21) & 0x1FFFFFull)) * inv;
+        c = float(unsigned((w >> 42) & 0x1FFFFFull)) * inv;
+    }
+#else
     float k0, k1, k2;
     __device__ __forceinline__ void set_colour(float a, float b, float c) {
         k0 = a;
@@ -227,6 +263,7 @@ struct BufSegCompact {
         b = k1;
         c = k2;
     }
+#endif
     __device__ __forceinline__ void set_alpha(double a, double q) {
         aq = a > 0.5 ? -float(q) : float(a);  // q == 0 -> -0.0f (sign bit set)
     }
