@@ -28,7 +28,7 @@ KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
         "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active",
         "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active",
-        "sass__inst_executed_register_spilling", "lts__t_bytes.sum",
+        "sass__inst_executed_register_spilling", "lts__t_sectors.sum",
         "l1tex__t_sectors_pipe_lsu_mem_local_op_ld.sum", "l1tex__t_sectors_pipe_lsu_mem_local_op_st.sum"]
 
 
@@ -143,7 +143,8 @@ def main():
                         "xu_pipe_pct": pct("sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active"),
                         "lsu_pipe_pct": pct("sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active"),
                         "warps_active_pct": pct("sm__warps_active.avg.pct_of_peak_sustained_active"),
-                        "l2_bytes_per_launch": to_bytes(*m["lts__t_bytes.sum"]) if "lts__t_bytes.sum" in m else None}
+                        "l2_bytes_per_launch": 32.0 * float(m["lts__t_sectors.sum"][0].replace(",", ""))
+                        if "lts__t_sectors.sum" in m else None}
     refine_csv = os.path.join(src, "refine_launches.csv")
     if os.path.exists(refine_csv):  # one refine pass: every launch's time and DRAM bytes
         res = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "refine_launches.py"), refine_csv],
