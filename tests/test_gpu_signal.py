@@ -106,3 +106,21 @@ def test_numpy_gradients_are_lazy_and_optimizer_stays_on_device():
     assert isinstance(g.dsigma, np.ndarray) and g.dsigma.dtype == np.float64
     assert g.dsh.shape == (tree.capacity, 12) and isinstance(g.touched, np.ndarray)
     assert not torch.equal(before, tree.sigma)
+
+
+def test_diagnostic_flags_rejected_by_product_library():
+    """Timing-diagnostic flag bits exist only in experiment builds: the
+    product library rejects everything but bit 15 (per-lane REDs)."""
+    from helpers import irregular_tree, ray_batch
+    from paper_2307_15333_b200.errors import InputError
+    from paper_2307_15333_b200.render import render_and_backprop
+    tree = irregular_tree(71, 4, depth=2, splits=4, max_depth=4, device="cuda")
+    o, d = ray_batch(72, 500)
+    t = np.full((500, 3), 0.5)
+    for bad in (1, 8192, 16384):
+        with pytest.raises(InputError):
+            render_and_backprop(tree, o, d, t, 1.0, kernel_flags=bad)
+    l1, g1, _ = render_and_backprop(tree, o, d, t, 1.0)
+    l2, g2, _ = render_and_backprop(tree, o, d, t, 1.0, kernel_flags=32768)
+    assert l2 == pytest.approx(l1, rel=1e-9)
+    np.testing.assert_array_equal(g1.touched, g2.touched)
