@@ -299,3 +299,16 @@ def test_grad_comparison_rejects_wrong_gradients():
         assert_grads_close(np.zeros_like(want), want)
     with pytest.raises(AssertionError):
         assert_grads_close(want * 1.01, want)
+
+
+def test_write_history_format(tmp_path):
+    """optim.write_history writes the reference's CSV (optim.py:196-206)."""
+    from paper_2307_15333_b200.optim import write_history
+    hist = [{"epoch": 1, "loss": 0.1, "psnr": float("nan"), "leaf_count": 8, "event": ""},
+            {"epoch": 2, "loss": 1 / 3, "psnr": 20.5, "leaf_count": 15, "event": "calibrate merges=0 splits=1"}]
+    p = tmp_path / "h.csv"
+    write_history(hist, p)
+    lines = p.read_text().splitlines()
+    assert lines[0] == "epoch,loss,psnr,leaf_count,event"
+    assert lines[1] == "1,0.1,nan,8,"
+    assert lines[2] == f"2,{1 / 3!r},20.5,15,calibrate merges=0 splits=1"
