@@ -391,12 +391,19 @@ def run_ours(args, rank, world, local_rank):
         torch.cuda.profiler.start()
     gc.collect()
     gc.disable()  # no collector pause between the launches of the timed steps
+    trace = os.environ.get("DOT_TRACE")  # diagnostic (tools/step_gaps.py): never set for a bench line
+    if trace:
+        prof = torch.profiler.profile(activities=[torch.profiler.ProfilerActivity.CUDA])
+        prof.__enter__()
     h0 = time.time()
     t0.record()
     for k in range(args.warmup, total_steps):
         paced(k)
     t1.record()
     torch.cuda.synchronize()
+    if trace:
+        prof.__exit__(None, None, None)
+        prof.export_chrome_trace(trace)
     clocks.mark(h0, time.time())
     gc.enable()
     if profile_range:
