@@ -341,12 +341,15 @@ def run_ours(args, rank, world, local_rank):
         from paper_2307_15333_b200.parallel import PeerExchange
         exchange = PeerExchange(tree, state, sws)
 
-    from paper_2307_15333_b200.render import plan_batch, pool_keys
+    from paper_2307_15333_b200.render import plan_batch, pool_keys, ray_costs
     plan_stream = torch.cuda.Stream(dev)
     plans = {}
     # the resident pool's coherence keys, once (like the pool itself): each
     # step's plan gathers 4 B per ray instead of re-reading 48 B at random
     pkeys = pool_keys(tree, origins, dirs)
+    # and its per-ray schedule costs (the first epoch's prediction; every
+    # backward refreshes its rays' entries): warps launch longest first
+    pcosts = ray_costs(tree, origins, dirs, EPS)
 
     def step(k, timed_kernel=True):
         # the batch is read in place from the resident pool (ray_index): no
@@ -355,7 +358,8 @@ def run_ours(args, rank, world, local_rank):
         idx = batch_index(k)
         plan = plans.pop(k, None)
         if k + 1 < total_steps + 2:
-            plans[k + 1] = plan_batch(tree, origins, dirs, batch_index(k + 1), stream=plan_stream, keys=pkeys)
+            plans[k + 1] = plan_batch(tree, origins, dirs, batch_index(k + 1), stream=plan_stream, keys=pkeys,
+                                      costs=pcosts)
         return train_step(tree, origins, dirs, targets, state, buf, sws, BG, EPS,
                           ray_index=idx, grad_scale=gs,
                           exchange=exchange if world > 1 else None,
@@ -444,16 +448,16 @@ def run_ours(args, rank, world, local_rank):
     # "serial_ms_per_step": the same loop with blocking copies + reads.
     from paper_2307_15333_b200.staging import LossReader, RayBatchStager
     host = []
-    for j in range(E2E_BATCHES):  # distinct pinned host batches, cycled
+    for j in range(E2E_BATCHES):  # distinct pinned host batches (rays + targets + costs), cycled
         idx = perm[j % perm.shape[0]]
-        host.append(tuple(x[idx].cpu().pin_memory() for x in (origins, dirs, targets)))
+        host.append(tuple(x[idx].cpu().pin_memory() for x in (origins, dirs, targets, pcosts)))
     torch.cuda.synchronize()
 
     ex = exchange if world > 1 else None
 
     def serial_loop(steps):
         for k in range(steps):
-            o_h, d_h, t_h = host[k % len(host)]
+            o_h, d_h, t_h, _ = host[k % len(host)]
             loss = train_step(tree, o_h, d_h, t_h, state, buf, sws, BG, EPS, grad_scale=gs,
                               exchange=ex)
             float(loss.item())
@@ -582,7 +586,9 @@ def run_ours(args, rank, world, local_rank):
             "exchange": args.exchange if world > 1 else "none",
             "batch_order": args.order,
             "plan": "coherence order of step k+1 sorted on a side stream during step k; the "
-                    "resident pool's 31-bit ray keys computed once at setup (render.pool_keys)",
+                    "resident pool's 31-bit ray keys (render.pool_keys) and per-ray schedule costs "
+                    "(render.ray_costs; refreshed by every backward) computed once at setup; warps "
+                    "launched longest first by cost",
         },
         # per step (profiles/r1j_launch_shares.txt): the plan's radix sort in
         # dot_plan_sort (histogram + exclusive sum + 4 onesweep passes) +
@@ -598,7 +604,7 @@ def run_ours(args, rank, world, local_rank):
             "bytes_model": f"{RAY_BYTES} B/ray + {SEG_BYTES} B/composited segment",
             "atomics_per_launch": reds, "atomics_per_s": reds / (kern_ms_avg / 1e3),
         },
-        "e2e": {"value": e2e_value, "unit": "rays/s", "h2d_bytes_per_step": per_rank * 72,
+        "e2e": {"value": e2e_value, "unit": "rays/s", "h2d_bytes_per_step": per_rank * (72 + 2),
                 "d2h_bytes_per_step": 8, "ms_per_step": e2e_ms / args.steps,
                 "api": "RayBatchStager (H2D + coherence sort of step k+1 overlap step k) + optim.train_step "
                        "(render_and_backprop + rmsprop_step) + LossReader (loss read one step late)",

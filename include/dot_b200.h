@@ -131,7 +131,10 @@ int dot_render_cameras(const dot_tree_view* tree, const double* cam_to_world, co
  *     processes batch rays [32 w, 32 w + 32) with w = warp_order[b], a
  *     permutation of 0..ceil(n/32)-1 (dot_sched_order); results do not depend
  *     on it.  ray_used (may be NULL) receives each batch ray's
- *     composited-segment count (u16, saturating) for dot_sched_update.
+ *     cost (composited + post-cut / 2 segments, u16, saturating) for
+ *     dot_sched_update; ray_cost (may be NULL, indexed like the arrays)
+ *     receives the same value at each ray's own index (a ray pool's cost
+ *     column for dot_sched_order_costs).
  *     weight_sum / weight_max (f64 [capacity], may be NULL; no reference
  *     counterpart, defined by oracle_weights): per leaf += / max= the
  *     compositing weight T_i Q_i of every composited segment.
@@ -139,7 +142,7 @@ int dot_render_cameras(const dot_tree_view* tree, const double* cam_to_world, co
  *     SH-row scatter (implied for capacity > 2^27); other bits are rejected. */
 int dot_render_bwd(const dot_tree_view* tree, const double* origins, const double* dirs,
                    const double* targets, int64_t n_pool, const int64_t* ray_index,
-                   const int32_t* warp_order, uint16_t* ray_used, int64_t n_rays,
+                   const int32_t* warp_order, uint16_t* ray_used, uint16_t* ray_cost, int64_t n_rays,
                    const double* background, double early_stop_eps, double t_near, double t_far,
                    double grad_scale, float* grad_sigma, float* grad_sh, int32_t gsh_stride,
                    double* signal, uint8_t* touched, double* loss_sum, float* rgb_out,
@@ -195,6 +198,27 @@ int dot_sched_order(const int32_t* sorted_keys, int64_t n_rays, const uint16_t* 
 int dot_sched_update(const int32_t* sorted_keys, const uint16_t* ray_used, int64_t n_rays, uint16_t* table,
                      void* stream);
 
+/* --- warp order from per-ray costs (no reference counterpart; order only):
+ *     ray_cost is a cost column indexed like the ray arrays (u16: composited +
+ *     post-cut / 2 segments, what dot_ray_costs computes and dot_render_bwd
+ *     refreshes through its ray_cost output); slot i of the batch costs
+ *     ray_cost[ray_index[i]] (ray_index may be NULL); a warp costs the max of
+ *     its 32 slots, chunks of
+ *     `chunk` consecutive warps are ranked by their costliest warp, descending
+ *     (longest first), and warp_order[ceil(n/32)] lists the warps in that
+ *     order for dot_render_bwd. */
+int dot_sched_order_costs(const uint16_t* ray_cost, const int64_t* ray_index, int64_t n_rays, int32_t chunk,
+                          int32_t* warp_order, void* stream);
+
+/* --- per-ray schedule cost of a ray set (no reference counterpart):
+ *     cost[i] = composited + post-cut / 2 segments of ray ray_index[i] (or i),
+ *     u16 saturating -- what dot_render_bwd reports per slot in ray_used --
+ *     for the first epoch of a ray pool (later epochs reuse the backward's own
+ *     counts).  Rays as in dot_render_bwd; out-of-range indices get 0. */
+int dot_ray_costs(const dot_tree_view* tree, const double* origins, const double* dirs, int64_t n_pool,
+                  const int64_t* ray_index, int64_t n_rays, double early_stop_eps, double t_near,
+                  double t_far, uint16_t* cost, void* stream);
+
 /* --- coherence keys (no reference counterpart): keys[i] = (origin Morton
  *     << 32) | octahedral-direction Morton; sorting a batch by them puts rays
  *     that walk the same cells into the same warps.  Results are sums over
@@ -206,6 +230,11 @@ int dot_ray_keys(const dot_tree_view* tree, const double* origins, const double*
  * out-of-range index gets key 0. */
 int dot_ray_keys32(const dot_tree_view* tree, const double* origins, const double* dirs, int64_t n_pool,
                    const int64_t* ray_index, int64_t n_rays, int32_t* keys, void* stream);
+
+/* keys[i] = pool_keys[ray_index[i]] (0 for an index outside [0, n_pool)):
+ * a batch's keys gathered from its resident pool's dot_ray_keys32 keys. */
+int dot_gather_keys(const int32_t* pool_keys, int64_t n_pool, const int64_t* ray_index, int64_t n_rays,
+                    int32_t* keys, void* stream);
 
 /* The batch's coherence order: radix sort of keys (dot_ray_keys32) by bits
  * [begin_bit, 31) carrying ray_index (NULL: the batch positions) as the

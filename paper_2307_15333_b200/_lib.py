@@ -18,7 +18,7 @@ LIB_PATH = os.path.join(_HERE, "libdot_b200.so")
 _LIB_OVERRIDE = os.environ.get("DOT_LIB_PATH")
 
 DOT_OK, DOT_BAD_ARG, DOT_OOM, DOT_CUDA_ERR, DOT_NO_DEVICE = range(5)
-ABI_VERSION = 9
+ABI_VERSION = 10
 
 c_void_p = ctypes.c_void_p
 c_i64 = ctypes.c_int64
@@ -71,7 +71,8 @@ _SIGNATURES = {
                                   c_void_p, c_void_p, c_void_p]),
     "dot_render_cameras": (c_i32, [c_void_p, c_void_p, c_void_p, c_i32, c_i32, c_i32, c_void_p, c_f64, c_void_p,
                                    c_void_p, c_void_p, c_void_p]),
-    "dot_render_bwd": (c_i32, [c_void_p, c_void_p, c_void_p, c_void_p, c_i64, c_void_p, c_void_p, c_void_p, c_i64,
+    "dot_render_bwd": (c_i32, [c_void_p, c_void_p, c_void_p, c_void_p, c_i64, c_void_p, c_void_p, c_void_p,
+                               c_void_p, c_i64,
                                c_void_p, c_f64, c_f64, c_f64, c_f64, c_void_p, c_void_p, c_i32, c_void_p,
                                c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_i32, c_void_p]),
     "dot_signal_fwd": (c_i32, [c_void_p, c_void_p, c_void_p, c_i64, c_void_p, c_i64, c_f64, c_f64, c_f64,
@@ -82,8 +83,12 @@ _SIGNATURES = {
                                       c_void_p, c_void_p, c_void_p]),
     "dot_sched_order": (c_i32, [c_void_p, c_i64, c_void_p, c_void_p, c_void_p]),
     "dot_sched_update": (c_i32, [c_void_p, c_void_p, c_i64, c_void_p, c_void_p]),
+    "dot_sched_order_costs": (c_i32, [c_void_p, c_void_p, c_i64, c_i32, c_void_p, c_void_p]),
+    "dot_ray_costs": (c_i32, [c_void_p, c_void_p, c_void_p, c_i64, c_void_p, c_i64, c_f64, c_f64, c_f64,
+                              c_void_p, c_void_p]),
     "dot_ray_keys": (c_i32, [c_void_p, c_void_p, c_void_p, c_i64, c_void_p, c_void_p]),
     "dot_ray_keys32": (c_i32, [c_void_p, c_void_p, c_void_p, c_i64, c_void_p, c_i64, c_void_p, c_void_p]),
+    "dot_gather_keys": (c_i32, [c_void_p, c_i64, c_void_p, c_i64, c_void_p, c_void_p]),
     "dot_plan_sort": (c_i32, [c_void_p, c_void_p, c_i64, c_i32, c_void_p, c_void_p, c_void_p]),
     "dot_ray_stats":(c_i32, [c_void_p, c_void_p, c_void_p, c_i64, c_f64, c_void_p, c_void_p]),
     "dot_refine_plan_create": (c_i32, [c_void_p, c_void_p, c_void_p, c_i32, c_f64, c_f64, c_i32, c_i32,

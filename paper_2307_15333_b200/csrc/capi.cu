@@ -68,7 +68,7 @@ using namespace dot;
 
 extern "C" {
 
-int dot_abi_version(void) { return 9; }
+int dot_abi_version(void) { return 10; }
 
 const char* dot_last_error(void) { return g_err; }
 
@@ -102,6 +102,30 @@ int dot_sched_update(const int32_t* sorted_keys, const uint16_t* ray_used, int64
                      void* stream) {
     if (n_rays < 0 || (n_rays && (!sorted_keys || !ray_used || !table))) return set_error(DOT_BAD_ARG, "bad arrays");
     return launch_sched_update(sorted_keys, ray_used, n_rays, table, static_cast<cudaStream_t>(stream));
+}
+
+int dot_sched_order_costs(const uint16_t* ray_cost, const int64_t* ray_index, int64_t n_rays, int32_t chunk,
+                          int32_t* warp_order, void* stream) {
+    if (n_rays < 0 || (n_rays && (!ray_cost || !warp_order))) return set_error(DOT_BAD_ARG, "bad arrays");
+    if (chunk < 1 || chunk > 4096) return set_error(DOT_BAD_ARG, "chunk must be in 1..4096, got %d", chunk);
+    if ((n_rays + 31) / 32 > INT32_MAX) return set_error(DOT_BAD_ARG, "batch too large to schedule");
+    return launch_sched_order_costs(ray_cost, ray_index, n_rays, chunk, warp_order, static_cast<cudaStream_t>(stream));
+}
+
+int dot_gather_keys(const int32_t* pool_keys, int64_t n_pool, const int64_t* ray_index, int64_t n_rays,
+                    int32_t* keys, void* stream) {
+    if (n_rays < 0 || (n_rays && (!pool_keys || !ray_index || !keys))) return set_error(DOT_BAD_ARG, "bad arrays");
+    return launch_gather_keys(pool_keys, ray_index, n_pool, n_rays, keys, static_cast<cudaStream_t>(stream));
+}
+
+int dot_ray_costs(const dot_tree_view* tree, const double* origins, const double* dirs, int64_t n_pool,
+                  const int64_t* ray_index, int64_t n_rays, double early_stop_eps, double t_near, double t_far,
+                  uint16_t* cost, void* stream) {
+    if (int st = validate_tree_view(tree)) return st;
+    if (n_rays < 0 || (n_rays && (!origins || !dirs || !cost))) return set_error(DOT_BAD_ARG, "bad ray arrays");
+    if (!ray_index && n_pool < n_rays) return set_error(DOT_BAD_ARG, "n_pool < n_rays without a ray_index");
+    return launch_ray_costs(make_tree(*tree), origins, dirs, ray_index, n_pool, n_rays, early_stop_eps, t_near,
+                            t_far, cost, static_cast<cudaStream_t>(stream));
 }
 
 int dot_locate_supported(const dot_tree_view* tree) {
@@ -153,7 +177,7 @@ int dot_render_fwd(const dot_tree_view* tree, const double* origins, const doubl
 
 int dot_render_bwd(const dot_tree_view* tree, const double* origins, const double* dirs,
                    const double* targets, int64_t n_pool, const int64_t* ray_index,
-                   const int32_t* warp_order, uint16_t* ray_used, int64_t n_rays,
+                   const int32_t* warp_order, uint16_t* ray_used, uint16_t* ray_cost, int64_t n_rays,
                    const double* background, double early_stop_eps, double t_near, double t_far,
                    double grad_scale, float* grad_sigma, float* grad_sh, int32_t gsh_stride,
                    double* signal, uint8_t* touched, double* loss_sum, float* rgb_out,
@@ -177,7 +201,7 @@ int dot_render_bwd(const dot_tree_view* tree, const double* origins, const doubl
     // need 27 bits, larger pools take the per-lane REDs
     if (tree->capacity > (int64_t(1) << 27)) flags |= 32768;
     return launch_render_bwd(make_tree(*tree), origins, dirs, targets, ray_index, n_pool, warp_order, ray_used,
-                             n_rays, background, early_stop_eps, t_near, t_far, grad_scale, grad_sigma, grad_sh,
+                             ray_cost, n_rays, background, early_stop_eps, t_near, t_far, grad_scale, grad_sigma, grad_sh,
                              signal, touched, loss_sum, rgb_out, weight_sum, weight_max, flags,
                              static_cast<cudaStream_t>(stream));
 }

@@ -36,18 +36,24 @@ int launch_render_fwd(const TreeDev& T, const double* o, const double* d, int64_
                       float* wsum, float* depth, cudaStream_t s);
 int launch_render_bwd(const TreeDev& T, const double* o, const double* d, const double* tgt,
                       const int64_t* ray_idx, int64_t n_pool, const int32_t* warp_order, uint16_t* ray_used,
-                      int64_t n, const double* bg, double eps, double tn, double tf, double gs, float* gsig,
+                      uint16_t* ray_cost, int64_t n, const double* bg, double eps, double tn, double tf, double gs, float* gsig,
                       float* gsh, double* signal, uint8_t* touched, double* loss, float* rgb_out,
                       double* wsum, double* wmax, int flags, cudaStream_t s);
 int launch_signal_fwd(const TreeDev& T, const double* o, const double* d, const int64_t* ray_idx, int64_t n_pool,
                       int64_t n, double eps, double tn, double tf, double* signal, double* wsum, double* wmax,
                       uint8_t* touched, unsigned long long* invalid, cudaStream_t s);
 int launch_sched_order(const int32_t* keys, int64_t n, const uint16_t* table, int32_t* warp_order, cudaStream_t s);
+int launch_sched_order_costs(const uint16_t* slot_cost, const int64_t* ray_idx, int64_t n, int chunk,
+                             int32_t* warp_order, cudaStream_t s);
+int launch_ray_costs(const TreeDev& T, const double* o, const double* d, const int64_t* ray_idx, int64_t n_pool,
+                     int64_t n, double eps, double tn, double tf, uint16_t* cost, cudaStream_t s);
 int launch_sched_update(const int32_t* keys, const uint16_t* ray_used, int64_t n, uint16_t* table, cudaStream_t s);
 int launch_ray_keys(const TreeDev& T, const double* o, const double* d, int64_t n, unsigned long long* keys,
                     cudaStream_t s);
 int run_plan_sort(const int32_t* keys, const int64_t* ray_index, int64_t n, int begin_bit,
                   int32_t* sorted_keys, int64_t* sorted_index, cudaStream_t s);
+int launch_gather_keys(const int32_t* pool_keys, const int64_t* ray_idx, int64_t n_pool, int64_t n, int32_t* keys,
+                       cudaStream_t s);
 int launch_ray_keys32(const TreeDev& T, const double* o, const double* d, const int64_t* ray_idx,
                       int64_t n_pool, int64_t n, int32_t* keys, cudaStream_t s);
 int launch_render_cameras(const TreeDev& T, const double* cam_to_world, const double* focal, int n_views,

@@ -414,16 +414,26 @@ struct CoopSink : AtomicSink {
 // launch).  Timing-diagnostic bits exist only in experiment builds
 // (-DDOT_DIAG_FLAGS, tools/build_variants.py): bit 0 skip post-cut touched
 // marks, bit 13 pass 1 only, bit 14 no reductions -- never in the product.
+#ifdef DOT_DIAG_FLAGS
+// diagnostic builds only: per-block start / end %globaltimer of the last
+// backward launch (tools/bwd_timeline.py), read with dot_diag_timeline
+__device__ unsigned long long g_diag_t[2 * 65536];
+#endif
+
 template <int B, class Sink>
 __global__ void __launch_bounds__(32, DOT_BWD_MINB) render_bwd_buffered_kernel(
     TreeDev T, const double* __restrict__ o, const double* __restrict__ d,
     const double* __restrict__ tgt, const int64_t* __restrict__ ray_idx, int64_t n_pool, int64_t n, double bg0,
     double bg1, double bg2, double eps, double t_near, double t_far, double grad_scale,
     uint8_t* __restrict__ touched, float* __restrict__ rgb_out, int flags, Sink sink,
-    const int32_t* __restrict__ warp_order, uint16_t* __restrict__ ray_used) {
+    const int32_t* __restrict__ warp_order, uint16_t* __restrict__ ray_used, uint16_t* __restrict__ ray_cost) {
     constexpr int S = pad4(3 * B);
     constexpr int K = kBwdRecords;
     double loss = 0.0;
+#ifdef DOT_DIAG_FLAGS
+    unsigned long long diag_t0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(diag_t0));
+#endif
     // warp_order: launch order of the 32-ray warps (costliest first, from the
     // learned cost table -- see sched_order_kernel); slot = batch position
     const int64_t wb = warp_order ? int64_t(__ldg(warp_order + blockIdx.x)) : int64_t(blockIdx.x);
@@ -523,6 +533,7 @@ __global__ void __launch_bounds__(32, DOT_BWD_MINB) render_bwd_buffered_kernel(
         const int cost = used;
 #endif
         if (ray_used) ray_used[slot] = uint16_t(cost < 65535 ? cost : 65535);
+        if (ray_cost) ray_cost[r] = uint16_t(cost < 65535 ? cost : 65535);
 #ifdef DOT_DIAG_FLAGS
         if (flags & 8192) used = 0;
 #endif
@@ -604,10 +615,25 @@ __global__ void __launch_bounds__(32, DOT_BWD_MINB) render_bwd_buffered_kernel(
         sink.template put<B>(act, i, pid, float(ds), w0, w1, w2, basis, q);
     }
     sink.loss(loss);
+#ifdef DOT_DIAG_FLAGS
+    if (threadIdx.x == 0 && blockIdx.x < 65536) {
+        unsigned long long t1;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+        g_diag_t[2 * blockIdx.x] = diag_t0;
+        g_diag_t[2 * blockIdx.x + 1] = t1;
+    }
+#endif
 }
+
+#ifdef DOT_DIAG_FLAGS
+extern "C" int dot_diag_timeline(unsigned long long* out, int n) {
+    return cudaMemcpyFromSymbol(out, g_diag_t, sizeof(unsigned long long) * 2 * size_t(n)) == cudaSuccess ? 0 : 3;
+}
+#endif
 
 int launch_render_bwd(const TreeDev& T, const double* o, const double* d, const double* tgt,
                       const int64_t* ray_idx, int64_t n_pool, const int32_t* warp_order, uint16_t* ray_used,
+                      uint16_t* ray_cost,
                       int64_t n, const double* bg, double eps, double tn, double tf, double gs, float* gsig,
                       float* gsh, double* signal, uint8_t* touched, double* loss, float* rgb_out,
                       double* wsum, double* wmax, int flags, cudaStream_t s) {
@@ -628,11 +654,11 @@ int launch_render_bwd(const TreeDev& T, const double* o, const double* d, const 
     if (coop)                                                                                        \
         render_bwd_buffered_kernel<BB, CoopT><<<grid, 32, 0, s>>>(                                   \
             T, o, d, tgt, ray_idx, n_pool, n, bg[0], bg[1], bg[2], eps, tn, tf, gs, touched, rgb_out, flags, cs, \
-            warp_order, ray_used);                                                                   \
+            warp_order, ray_used, ray_cost);                                                         \
     else                                                                                             \
         render_bwd_buffered_kernel<BB, AtomicSink><<<grid, 32, 0, s>>>(                              \
             T, o, d, tgt, ray_idx, n_pool, n, bg[0], bg[1], bg[2], eps, tn, tf, gs, touched, rgb_out, flags, as, \
-            warp_order, ray_used);
+            warp_order, ray_used, ray_cost);
     DOT_DISPATCH_B(DOT_BWD)
 #undef DOT_BWD
     return check_launch("render_bwd_buffered_kernel");
@@ -703,7 +729,7 @@ int launch_render_bwd_emit(const TreeDev& T, const double* o, const double* d, c
 #define DOT_EMIT(BB)                                                                                 \
     render_bwd_buffered_kernel<BB, EmitSink><<<unsigned((n + 31) / 32), 32, 0, s>>>(                 \
         T, o, d, tgt, ray_idx, n, n, bg[0], bg[1], bg[2], eps, tn, tf, gs, touched, nullptr, 0, sink,   \
-        warp_order, ray_used);
+        warp_order, ray_used, nullptr);
     DOT_DISPATCH_B(DOT_EMIT)
 #undef DOT_EMIT
     return check_launch("render_bwd_buffered_kernel<emit>");
@@ -786,6 +812,141 @@ int launch_signal_fwd(const TreeDev& T, const double* o, const double* d, const 
     signal_fwd_kernel<<<blocks_for(n), kBlock, 0, s>>>(T, o, d, ray_idx, n_pool, n, eps, tn, tf, signal, wsum,
                                                        wmax, touched, invalid);
     return check_launch("signal_fwd_kernel");
+}
+
+// ---------------------------------------------------------------------------
+// Per-ray schedule cost (no reference counterpart; only orders launches):
+// composited + post-cut / 2 segments -- the metric the backward reports in
+// ray_used (DOT_SCHED_COST 2), so a ray pool's costs computed once and
+// refreshed by every backward predict each warp's duration closely.
+
+__global__ void __launch_bounds__(kBlock, kFwdMinBlocks) ray_cost_kernel(
+    TreeDev T, const double* __restrict__ o, const double* __restrict__ d, const int64_t* __restrict__ ray_idx,
+    int64_t n_pool, int64_t n, double eps, double t_near, double t_far, uint16_t* __restrict__ cost) {
+    const int64_t slot = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (slot >= n) return;
+    const int64_t r = ray_index(ray_idx, slot);
+    int used = 0, tail = 0;
+    if (r >= 0 && r < n_pool) {
+        Tracer tr;
+        load_ray(o, d, r, tr);
+        if (tr.init(T, t_near, t_far)) {
+            double trans = 1.0;
+            bool cut = false;
+            Leaf L;
+            double te, dl;
+            while (tr.next(T, L, te, dl)) {
+                if (cut) {
+                    ++tail;
+                    continue;
+                }
+                ++used;
+                trans *= exp_ref(-double(__ldg(T.sigma + L.pid)) * dl);
+                if (eps > 0.0 && trans < eps) cut = true;
+            }
+        }
+    }
+    const int c = used + (tail >> 1);
+    cost[slot] = uint16_t(c < 65535 ? c : 65535);
+}
+
+int launch_ray_costs(const TreeDev& T, const double* o, const double* d, const int64_t* ray_idx, int64_t n_pool,
+                     int64_t n, double eps, double tn, double tf, uint16_t* cost, cudaStream_t s) {
+    if (n == 0) return DOT_OK;
+    ray_cost_kernel<<<blocks_for(n), kBlock, 0, s>>>(T, o, d, ray_idx, n_pool, n, eps, tn, tf, cost);
+    return check_launch("ray_cost_kernel");
+}
+
+// Warp launch order from per-slot costs: warp cost = max over its 32 rays
+// (a warp lasts as long as its longest ray), chunks of `chunk` consecutive
+// warps ranked by their costliest warp, descending (longest-first packing),
+// via a counting sort over capped costs.
+constexpr int kCostBins = 1024;
+
+// one thread per batch slot: warp w's cost = max over its 32 slots (warp
+// reduction), then chunk costs (max over `chunk` warps) and their histogram
+__global__ void __launch_bounds__(256) cost_warp_kernel(const uint16_t* __restrict__ ray_cost,
+                                                        const int64_t* __restrict__ ray_idx, int64_t n,
+                                                        uint16_t* __restrict__ warp_cost) {
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int64_t nw = (n + 31) / 32;
+    unsigned c = 0;
+    if (i < n) c = __ldg(ray_cost + ray_index(ray_idx, i));
+    c = __reduce_max_sync(0xffffffffu, c);
+    if ((threadIdx.x & 31) == 0 && (i >> 5) < nw) warp_cost[i >> 5] = uint16_t(min(c, unsigned(kCostBins - 1)));
+}
+
+__global__ void __launch_bounds__(256) cost_hist_kernel(const uint16_t* __restrict__ warp_cost, int64_t n, int chunk,
+                                                        uint16_t* __restrict__ chunk_cost, int* __restrict__ hist) {
+    const int64_t c = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int64_t nw = (n + 31) / 32, nfull = nw / chunk;
+    if (c >= nfull) return;  // a short last chunk is placed last (cost_place_kernel)
+    unsigned m = 0;
+    for (int64_t w = c * chunk; w < (c + 1) * chunk; ++w) m = max(m, unsigned(warp_cost[w]));
+    chunk_cost[c] = uint16_t(m);
+    atomicAdd(hist + (kCostBins - 1 - int(m)), 1);
+}
+
+__global__ void __launch_bounds__(kCostBins) cost_scan_kernel(int* __restrict__ hist) {
+    __shared__ int v[kCostBins];
+    const int t = threadIdx.x;
+    const int own = hist[t];
+    v[t] = own;
+    __syncthreads();
+    for (int off = 1; off < kCostBins; off <<= 1) {
+        const int u = t >= off ? v[t - off] : 0;
+        __syncthreads();
+        v[t] += u;
+        __syncthreads();
+    }
+    hist[t] = v[t] - own;  // exclusive start of each bin
+}
+
+__global__ void __launch_bounds__(256) cost_place_kernel(const uint16_t* __restrict__ chunk_cost, int64_t n, int chunk,
+                                                         int* __restrict__ start, int32_t* __restrict__ warp_order) {
+    const int64_t c = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int64_t nw = (n + 31) / 32, nfull = nw / chunk;
+    if (c > nfull) return;
+    int64_t w0, w1, dst;
+    if (c == nfull) {  // the short last chunk (if any) goes last
+        w0 = nfull * chunk;
+        w1 = nw;
+        dst = w0;
+    } else {
+        w0 = c * chunk;
+        w1 = w0 + chunk;
+        dst = int64_t(atomicAdd(start + (kCostBins - 1 - int(chunk_cost[c])), 1)) * chunk;
+    }
+    // a chunk's warps keep their (coherent) order
+    for (int64_t w = w0; w < w1; ++w) warp_order[dst + (w - w0)] = int32_t(w);
+}
+
+int launch_sched_order_costs(const uint16_t* slot_cost, const int64_t* ray_idx, int64_t n, int chunk,
+                             int32_t* warp_order, cudaStream_t s) {
+    const int64_t nw = (n + 31) / 32;
+    if (nw == 0) return DOT_OK;
+    const int64_t nc = (nw + chunk - 1) / chunk;
+    retain_pool_memory();
+    uint16_t* cc = nullptr;
+    uint16_t* wc = nullptr;
+    int* hist = nullptr;
+    int st = check_cuda(cudaMallocAsync(reinterpret_cast<void**>(&cc), sizeof(uint16_t) * nc, s), "cudaMallocAsync");
+    if (st == DOT_OK)
+        st = check_cuda(cudaMallocAsync(reinterpret_cast<void**>(&wc), sizeof(uint16_t) * nw, s), "cudaMallocAsync");
+    if (st == DOT_OK)
+        st = check_cuda(cudaMallocAsync(reinterpret_cast<void**>(&hist), sizeof(int) * kCostBins, s), "cudaMallocAsync");
+    if (st == DOT_OK) st = check_cuda(cudaMemsetAsync(hist, 0, sizeof(int) * kCostBins, s), "cudaMemsetAsync");
+    if (st == DOT_OK) {
+        cost_warp_kernel<<<unsigned((nw * 32 + 255) / 256), 256, 0, s>>>(slot_cost, ray_idx, n, wc);
+        cost_hist_kernel<<<unsigned((nc + 255) / 256), 256, 0, s>>>(wc, n, chunk, cc, hist);
+        cost_scan_kernel<<<1, kCostBins, 0, s>>>(hist);
+        cost_place_kernel<<<unsigned((nc + 256) / 256), 256, 0, s>>>(cc, n, chunk, hist, warp_order);
+        st = check_launch("sched_order_costs");
+    }
+    if (cc) cudaFreeAsync(cc, s);
+    if (wc) cudaFreeAsync(wc, s);
+    if (hist) cudaFreeAsync(hist, s);
+    return st;
 }
 
 // ---------------------------------------------------------------------------
@@ -966,6 +1127,24 @@ __global__ void ray_keys32_kernel(TreeDev T, const double* __restrict__ o, const
     const unsigned uy = unsigned(fmin(fmax(0.5 * (y + 1.0), 0.0), 0.99999) * 512.0);
     const unsigned dm = unsigned(spread_bits(ux, 10) | (spread_bits(uy, 9) << 1));
     keys[slot] = int32_t((om << 19) | dm);
+}
+
+// keys[i] = pool_keys[ray_index[i]]: a batch's keys from its pool's
+// precomputed ones (4 B per ray instead of re-reading its 48 B of rays)
+__global__ void __launch_bounds__(256) gather_keys_kernel(const int32_t* __restrict__ pool_keys,
+                                                          const int64_t* __restrict__ ray_idx, int64_t n_pool,
+                                                          int64_t n, int32_t* __restrict__ keys) {
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int64_t r = __ldg(ray_idx + i);
+    keys[i] = (r >= 0 && r < n_pool) ? __ldg(pool_keys + r) : 0;
+}
+
+int launch_gather_keys(const int32_t* pool_keys, const int64_t* ray_idx, int64_t n_pool, int64_t n, int32_t* keys,
+                       cudaStream_t s) {
+    if (n == 0) return DOT_OK;
+    gather_keys_kernel<<<unsigned((n + 255) / 256), 256, 0, s>>>(pool_keys, ray_idx, n_pool, n, keys);
+    return check_launch("gather_keys_kernel");
 }
 
 int launch_ray_keys32(const TreeDev& T, const double* o, const double* d, const int64_t* ray_idx, int64_t n_pool,

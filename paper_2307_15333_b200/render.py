@@ -34,6 +34,9 @@ UNIT_TOL = 1e-6
 COHERENT_MIN_RAYS = 1 << 14  # below this a key sort costs more than it saves
 WARP_SCHED = os.environ.get("DOT_WARP_SCHED", "1") == "1"
 SCHED_MAX_RAYS = 1 << 30
+# warps per chunk of the cost-ordered launch (dot_sched_order_costs): single
+# warps pack best (chunks of 16 warps +4 %, tools/bwd_order_headroom.py)
+COST_CHUNK = int(os.environ.get("DOT_COST_CHUNK", "1"))
 
 
 def _sched_table(tree) -> torch.Tensor:
@@ -337,7 +340,8 @@ class RayPlan:
     idx: torch.Tensor
     sorted_keys: torch.Tensor
     event: "torch.cuda.Event | None" = None
-    warp_order: "torch.Tensor | None" = None  # learned launch order, when computed with the plan
+    warp_order: "torch.Tensor | None" = None  # launch order, when computed with the plan
+    costs: "torch.Tensor | None" = None       # the per-ray cost column the order came from (refreshed after the backward)
 
     def wait(self, stream=None) -> None:
         if self.event is not None:
@@ -363,15 +367,36 @@ def pool_keys(tree: SparseOctree, origins: torch.Tensor, dirs: torch.Tensor) -> 
     return keys
 
 
+def ray_costs(tree: SparseOctree, origins: torch.Tensor, dirs: torch.Tensor, early_stop_eps: float = EPS_T,
+              t_near: float = 0.0, t_far: float = math.inf) -> torch.Tensor:
+    """Per-ray schedule cost of a ray pool (``dot_ray_costs``: composited +
+    post-cut / 2 segments, int16 [n], device): the first-epoch prediction of
+    each ray's share of a backward warp.  Pass it to ``plan_batch(costs=)``;
+    every backward then refreshes the entries of the rays it processed with
+    its own counts, so later epochs schedule from the previous visit.  Order
+    only: stale or zero costs cost speed, never correctness."""
+    n = int(origins.shape[0])
+    cost = torch.zeros(n, dtype=torch.int16, device=tree.device)
+    view, _topo = tree.tree_view(locate_level=locate_level_train())
+    _lib.call("dot_ray_costs", _lib.ctypes.byref(view), _lib.ptr(origins), _lib.ptr(dirs), n, None, n,
+              float(early_stop_eps), float(t_near), float(t_far), _lib.ptr(cost), _lib.stream_ptr())
+    return cost
+
+
 def plan_batch(tree: SparseOctree, origins: torch.Tensor, dirs: torch.Tensor, ray_index=None,
-               stream=None, wait_current: bool = True, keys: torch.Tensor | None = None) -> RayPlan:
+               stream=None, wait_current: bool = True, keys: torch.Tensor | None = None,
+               costs: torch.Tensor | None = None) -> RayPlan:
     """Coherence order of a batch (origin / octahedral-direction Morton keys,
     dot_ray_keys32 + a radix sort).  Depends only on the rays, so it can run
     on a side stream (``stream``) ahead of the step that consumes it; the
     returned plan carries an event the consumer waits on.  ``wait_current``
     orders the side stream after the work queued so far on the current stream
     (off when the rays were produced on ``stream`` itself).  ``keys``: the
-    pool's precomputed keys (``pool_keys``), gathered by ``ray_index``."""
+    pool's precomputed keys (``pool_keys``), gathered by ``ray_index``.
+    ``costs`` (int16 per ray of the arrays, e.g. ``ray_costs``): launch the
+    backward's warps longest first by these per-ray costs
+    (``dot_sched_order_costs``) instead of the learned key-bucket table; the
+    backward writes its fresh counts back into ``costs``."""
     idx = None if ray_index is None else torch.as_tensor(ray_index, device=tree.device).reshape(-1).to(torch.int64)
     n = int(idx.shape[0]) if idx is not None else int(origins.shape[0])
     n_pool = int(origins.shape[0])
@@ -383,12 +408,16 @@ def plan_batch(tree: SparseOctree, origins: torch.Tensor, dirs: torch.Tensor, ra
             s.wait_stream(cur)  # inputs produced on the current stream
         # the inputs (and the index temporary made above) are read on the side
         # stream: keep the allocator from recycling them before it is done
-        for t in (idx, origins, dirs, keys):
+        for t in (idx, origins, dirs, keys, costs):
             if t is not None:
                 t.record_stream(s)
     with torch.cuda.stream(s):
         if keys is not None:
-            keys = keys if idx is None else keys.index_select(0, idx)
+            if idx is not None:
+                pk = keys
+                keys = torch.empty(n, dtype=torch.int32, device=tree.device)
+                _lib.call("dot_gather_keys", _lib.ptr(pk), int(pk.shape[0]), _lib.ptr(idx), n, _lib.ptr(keys),
+                          _lib.stream_ptr(s))
         else:
             keys = torch.empty(n, dtype=torch.int32, device=tree.device)
             _lib.call("dot_ray_keys32", _lib.ctypes.byref(view), _lib.ptr(origins), _lib.ptr(dirs), n_pool,
@@ -400,9 +429,16 @@ def plan_batch(tree: SparseOctree, origins: torch.Tensor, dirs: torch.Tensor, ra
         _lib.call("dot_plan_sort", _lib.ptr(keys), _lib.ptr(idx), n, PLAN_SORT_BEGIN_BIT,
                   _lib.ptr(sorted_keys), _lib.ptr(order), _lib.stream_ptr(s))
         idx = order
-        # the warp launch order too, off the critical path (it reads the
-        # learned table as of the previous completed update)
-        warp_order = _sched_order(tree, sorted_keys, n, s) if WARP_SCHED and 0 < n <= SCHED_MAX_RAYS else None
+        # the warp launch order too, off the critical path: from the rays'
+        # costs when given, else the learned table as of its last update
+        warp_order = None
+        if WARP_SCHED and 0 < n <= SCHED_MAX_RAYS:
+            if costs is not None:
+                warp_order = torch.empty((n + 31) // 32, dtype=torch.int32, device=tree.device)
+                _lib.call("dot_sched_order_costs", _lib.ptr(costs), _lib.ptr(idx), n, COST_CHUNK,
+                          _lib.ptr(warp_order), _lib.stream_ptr(s))
+            else:
+                warp_order = _sched_order(tree, sorted_keys, n, s)
         ev = None
         if s is not cur:
             ev = torch.cuda.Event()
@@ -410,7 +446,7 @@ def plan_batch(tree: SparseOctree, origins: torch.Tensor, dirs: torch.Tensor, ra
             for t in (idx, sorted_keys, warp_order):
                 if t is not None:
                     t.record_stream(cur)
-    return RayPlan(n, idx, sorted_keys, ev, warp_order)
+    return RayPlan(n, idx, sorted_keys, ev, warp_order, costs if warp_order is not None else None)
 
 
 def render_and_backprop(tree: SparseOctree, origins, dirs, targets, background,
@@ -484,15 +520,18 @@ def render_and_backprop(tree: SparseOctree, origins, dirs, targets, background,
         gs = 2.0 / n if grad_scale is None else float(grad_scale)
         bg = _background(background)
         view, _topo = tree.tree_view(locate_level=locate_level_train())
+        plan_costs = None
         if plan is not None:
             if plan.n != n:
                 raise InputError(f"ray plan is for {plan.n} rays, batch has {n}")
             plan.wait()
-            idx, sorted_keys, warp_order = plan.idx, plan.sorted_keys, plan.warp_order
+            idx, sorted_keys, warp_order, plan_costs = plan.idx, plan.sorted_keys, plan.warp_order, plan.costs
         elif coherent and n >= COHERENT_MIN_RAYS:
             p = plan_batch(tree, o, d, idx)
             idx, sorted_keys, warp_order = p.idx, p.sorted_keys, p.warp_order
-        if sorted_keys is not None and WARP_SCHED and n <= SCHED_MAX_RAYS:
+        if plan_costs is not None:
+            pass  # the backward writes each ray's fresh cost straight into the column
+        elif sorted_keys is not None and WARP_SCHED and n <= SCHED_MAX_RAYS:
             # launch the warps whose key buckets were costliest last time first
             if warp_order is None:
                 warp_order = _sched_order(tree, sorted_keys, n, torch.cuda.current_stream(tree.device))
@@ -510,7 +549,7 @@ def render_and_backprop(tree: SparseOctree, origins, dirs, targets, background,
                       _lib.stream_ptr())
         else:
             _lib.call("dot_render_bwd", _lib.ctypes.byref(view), _lib.ptr(o), _lib.ptr(d), _lib.ptr(t), n_pool,
-                      _lib.ptr(idx), _lib.ptr(warp_order), _lib.ptr(ray_used), n, _bg_ptr(bg),
+                      _lib.ptr(idx), _lib.ptr(warp_order), _lib.ptr(ray_used), _lib.ptr(plan_costs), n, _bg_ptr(bg),
                       float(early_stop_eps), float(t_near), float(t_far), gs, _lib.ptr(ws.dsigma),
                       _lib.ptr(ws.dsh_store), tree.sh_stride, _lib.ptr(ws.signal), _lib.ptr(ws.touched),
                       _lib.ptr(ws.loss), _lib.ptr(rgb), _lib.ptr(weight_sum), _lib.ptr(weight_max),

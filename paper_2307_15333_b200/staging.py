@@ -35,10 +35,11 @@ from .errors import InputError
 
 
 class _Slot:
-    __slots__ = ("bufs", "n", "ready", "free", "busy", "plan")
+    __slots__ = ("bufs", "n", "ready", "free", "busy", "plan", "cost")
 
     def __init__(self):
         self.bufs = None
+        self.cost = None
         self.plan = None
         self.n = 0
         self.ready = torch.cuda.Event()
@@ -73,6 +74,7 @@ class RayBatchStager:
             # a copy or kernel may touch it: the free/ready events order all uses
             torch.cuda.current_stream(self.device).synchronize()
             slot.bufs = tuple(torch.empty(n, 3, dtype=torch.float64, device=self.device) for _ in range(3))
+            slot.cost = torch.empty(n, dtype=torch.int16, device=self.device)
 
     @staticmethod
     def _host(x, name: str) -> torch.Tensor:
@@ -84,12 +86,20 @@ class RayBatchStager:
             t = t.double()
         return t.contiguous()
 
-    def stage(self, origins, dirs, targets) -> None:
-        """Queue the H2D copy of one batch on the copy stream (returns at once)."""
+    def stage(self, origins, dirs, targets, costs=None) -> None:
+        """Queue the H2D copy of one batch on the copy stream (returns at once).
+        ``costs`` (host int16 per ray, optional, e.g. a slice of
+        ``render.ray_costs`` kept with the dataset): staged too and used for the
+        batch's warp launch order (``plan_batch(costs=)``)."""
         o, d, t = (self._host(x, nm) for x, nm in ((origins, "origins"), (dirs, "dirs"), (targets, "targets")))
         n = o.shape[0]
         if d.shape[0] != n or t.shape[0] != n:
             raise InputError(f"batch length mismatch: {n} origins, {d.shape[0]} dirs, {t.shape[0]} targets")
+        c = None
+        if costs is not None:
+            c = costs if isinstance(costs, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(costs))
+            if c.device.type != "cpu" or c.dtype != torch.int16 or c.numel() != n:
+                raise InputError("costs must be a host int16 tensor with one entry per ray")
         i = self.next_slot
         slot = self.slots[i]
         if slot.busy:
@@ -100,15 +110,18 @@ class RayBatchStager:
                 self.copy_stream.wait_event(slot.free)  # the last step reading this slot is done
             for dst, src in zip(slot.bufs, (o, d, t)):
                 dst[:n].copy_(src, non_blocking=True)
+            if c is not None:
+                slot.cost[:n].copy_(c.reshape(-1), non_blocking=True)
             slot.plan = None
             if self.plan_tree is not None:
                 from .render import plan_batch
                 slot.plan = plan_batch(self.plan_tree, slot.bufs[0][:n], slot.bufs[1][:n],
-                                       stream=self.copy_stream, wait_current=False)
+                                       stream=self.copy_stream, wait_current=False,
+                                       costs=slot.cost[:n] if c is not None else None)
             slot.ready.record(self.copy_stream)
         slot.n = n
         slot.busy = True
-        self.bytes_staged += 3 * n * 24
+        self.bytes_staged += 3 * n * 24 + (2 * n if c is not None else 0)
         self.pending.append(i)
         self.next_slot = (i + 1) % len(self.slots)
 

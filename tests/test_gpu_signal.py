@@ -124,3 +124,52 @@ def test_diagnostic_flags_rejected_by_product_library():
     l2, g2, _ = render_and_backprop(tree, o, d, t, 1.0, kernel_flags=32768)
     assert l2 == pytest.approx(l1, rel=1e-9)
     np.testing.assert_array_equal(g1.touched, g2.touched)
+
+
+def test_ray_costs_and_cost_ordered_launch():
+    """dot_ray_costs gives exactly the per-ray cost the backward reports
+    (composited + post-cut / 2); dot_sched_order_costs is a permutation of
+    the warps with non-increasing warp (chunk) cost, a short last chunk last;
+    a plan built from costs gives the same results and refreshes the costs."""
+    from helpers import irregular_tree, ray_batch
+    from paper_2307_15333_b200 import _lib
+    from paper_2307_15333_b200.render import BackpropWorkspace, plan_batch, ray_costs, render_and_backprop
+    tree = irregular_tree(81, 9, depth=3, splits=60, merges=4, max_depth=6, device="cuda")
+    o, d = ray_batch(82, 70001)
+    t = np.random.default_rng(83).uniform(0, 1, (o.shape[0], 3))
+    o, d, t = (torch.from_numpy(x).cuda() for x in (o, d, t))
+    costs = ray_costs(tree, o, d)
+    assert int(costs.max()) > 3
+    idx = torch.randperm(o.shape[0], generator=torch.Generator().manual_seed(2))[:50000].cuda()
+    fresh = torch.zeros_like(costs)
+    p = plan_batch(tree, o, d, idx, costs=fresh)  # all-zero costs: any order, then refreshed
+    ws = BackpropWorkspace.for_tree(tree)
+    l1, g1, s1 = render_and_backprop(tree, o, d, t, 0.5, ray_index=idx, workspace=ws, plan=p)
+    torch.cuda.synchronize()
+    assert torch.equal(fresh[idx], costs[idx])  # the backward's counts == dot_ray_costs
+    assert not bool(fresh[torch.ones(o.shape[0], dtype=torch.bool, device="cuda").index_fill_(0, idx, False)].any())
+    ws2 = BackpropWorkspace.for_tree(tree)
+    l2, g2, s2 = render_and_backprop(tree, o, d, t, 0.5, ray_index=idx, workspace=ws2,
+                                     plan=plan_batch(tree, o, d, idx, costs=costs))
+    assert float(l2) == pytest.approx(float(l1), rel=1e-9)
+    torch.testing.assert_close(g2.dsh, g1.dsh, atol=1e-7, rtol=1e-4)
+    assert torch.equal(g2.touched_mask, g1.touched_mask)
+    torch.testing.assert_close(s2, s1, rtol=1e-12, atol=1e-15)
+    # the order itself
+    n = 70001
+    slot = costs[:n].contiguous()
+    nw = (n + 31) // 32
+    for chunk in (1, 16):
+        order = torch.empty(nw, dtype=torch.int32, device="cuda")
+        _lib.call("dot_sched_order_costs", _lib.ptr(slot), None, n, chunk, _lib.ptr(order), _lib.stream_ptr())
+        od = order.cpu().numpy()
+        assert np.array_equal(np.sort(od), np.arange(nw))
+        pad = np.zeros(nw * 32, dtype=np.int64)
+        pad[:n] = slot.cpu().numpy()
+        wc = np.minimum(pad.reshape(nw, 32).max(1), 1023)
+        nfull = nw // chunk
+        cc = wc[: nfull * chunk].reshape(nfull, chunk).max(1)
+        firsts = od[: nfull * chunk: chunk] // chunk
+        assert np.all(np.diff(cc[firsts]) <= 0)
+        if nw % chunk:
+            assert np.array_equal(od[nfull * chunk:], np.arange(nfull * chunk, nw))

@@ -33,7 +33,7 @@ def main():
     bg = np.ones(3)
     vt, _ = tree.tree_view(locate_level=9)
     _lib.call("dot_render_bwd", _lib.ctypes.byref(vt), _lib.ptr(o), _lib.ptr(d), _lib.ptr(t), o.shape[0],
-              _lib.ptr(p.idx), None, _lib.ptr(used), n, bg.ctypes.data_as(_lib.c_void_p), 1e-4, 0.0, float("inf"),
+              _lib.ptr(p.idx), None, _lib.ptr(used), None, n, bg.ctypes.data_as(_lib.c_void_p), 1e-4, 0.0, float("inf"),
               2.0 / n, _lib.ptr(ws.dsigma), _lib.ptr(ws.dsh_store), tree.sh_stride, _lib.ptr(ws.signal),
               _lib.ptr(ws.touched), _lib.ptr(ws.loss), None, None, None, 0, _lib.stream_ptr())
     c = counts.cpu().numpy()
