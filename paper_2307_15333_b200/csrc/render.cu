@@ -28,11 +28,13 @@ constexpr int kBwdRecords = 128;   // composited segments buffered per ray (pass
 #ifndef DOT_SCHED_COST
 #define DOT_SCHED_COST 2
 #endif
-// Resident one-warp blocks per SM of the backward: 24 -> 80 registers (no
-// spills in the walk); 32 (64 registers, 192 B of spills) measured 3-4 %
-// slower, 20 (96 registers) equal.
+// Register budget of the backward via its one-warp-block residency bound:
+// 20 -> 96 registers, no spills (the 25 % carveout keeps ~16-18 blocks per SM
+// anyway).  With the cost-ordered launch: 20 (96 registers) 1.451 ms, 24
+// (80) 1.508, 28 (72) 1.61-1.64, 16 (128) 1.56; without it 20 and 24 were
+// equal and 32 (64 registers, spills) 3-4 % slower.
 #ifndef DOT_BWD_MINB
-#define DOT_BWD_MINB 24
+#define DOT_BWD_MINB 20
 #endif
 // Pass 2 reads its records two ahead (measured 1.69 -> 1.67 ms; at the
 // former 64-register cap it spilled and lost).
