@@ -349,7 +349,7 @@ def run_ours(args, rank, world, local_rank):
     pkeys = pool_keys(tree, origins, dirs)
     # and its per-ray schedule costs (the first epoch's prediction; every
     # backward refreshes its rays' entries): warps launch longest first
-    pcosts = ray_costs(tree, origins, dirs, EPS)
+    pcosts = ray_costs(tree, origins, dirs, EPS) if os.environ.get("DOT_BENCH_COSTS", "1") == "1" else None
 
     def step(k, timed_kernel=True):
         # the batch is read in place from the resident pool (ray_index): no
@@ -450,7 +450,8 @@ def run_ours(args, rank, world, local_rank):
     host = []
     for j in range(E2E_BATCHES):  # distinct pinned host batches (rays + targets + costs), cycled
         idx = perm[j % perm.shape[0]]
-        host.append(tuple(x[idx].cpu().pin_memory() for x in (origins, dirs, targets, pcosts)))
+        host.append(tuple(x[idx].cpu().pin_memory() if x is not None else None
+                          for x in (origins, dirs, targets, pcosts)))
     torch.cuda.synchronize()
 
     ex = exchange if world > 1 else None

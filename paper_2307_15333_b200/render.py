@@ -34,9 +34,18 @@ UNIT_TOL = 1e-6
 COHERENT_MIN_RAYS = 1 << 14  # below this a key sort costs more than it saves
 WARP_SCHED = os.environ.get("DOT_WARP_SCHED", "1") == "1"
 SCHED_MAX_RAYS = 1 << 30
-# warps per chunk of the cost-ordered launch (dot_sched_order_costs): single
-# warps pack best (chunks of 16 warps +4 %, tools/bwd_order_headroom.py)
-COST_CHUNK = int(os.environ.get("DOT_COST_CHUNK", "1"))
+# warps per chunk of the cost-ordered launch (dot_sched_order_costs), env
+# DOT_COST_CHUNK overrides.  Measured: a 2^20-ray configs[1] batch packs best
+# with single warps (chunks of 2 / 4: +2 / +5 % backward); a 2^21-ray batch
+# of the larger configs[3] scene wants chunks of 16 warps (single warps +2 %:
+# neighbouring warps share L2 lines of the 1.9 GB payload).
+COST_CHUNK_ENV = os.environ.get("DOT_COST_CHUNK")
+
+
+def cost_chunk(n: int) -> int:
+    if COST_CHUNK_ENV:
+        return int(COST_CHUNK_ENV)
+    return 1 if n <= (1 << 20) else 16
 
 
 def _sched_table(tree) -> torch.Tensor:
@@ -435,7 +444,7 @@ def plan_batch(tree: SparseOctree, origins: torch.Tensor, dirs: torch.Tensor, ra
         if WARP_SCHED and 0 < n <= SCHED_MAX_RAYS:
             if costs is not None:
                 warp_order = torch.empty((n + 31) // 32, dtype=torch.int32, device=tree.device)
-                _lib.call("dot_sched_order_costs", _lib.ptr(costs), _lib.ptr(idx), n, COST_CHUNK,
+                _lib.call("dot_sched_order_costs", _lib.ptr(costs), _lib.ptr(idx), n, cost_chunk(n),
                           _lib.ptr(warp_order), _lib.stream_ptr(s))
             else:
                 warp_order = _sched_order(tree, sorted_keys, n, s)
