@@ -32,6 +32,15 @@ def main():
     busy += cur_e - cur_s
     print(f"kernels {len(k)}, window {t1 - t0:.0f} us, GPU busy {busy:.0f} us, idle {t1 - t0 - busy:.0f} us "
           f"({100 * (1 - busy / (t1 - t0)):.1f} %)")
+    # one step's timeline (the 5th backward launch onwards)
+    bw = [e for e in k if "render_bwd" in e["name"]]
+    if len(bw) > 6:
+        a, b = bw[5]["ts"], bw[6]["ts"]
+        print("one step (us from its backward's start): stream  start  end  kernel")
+        for e in k:
+            if a - 300 <= e["ts"] < b:
+                print(f"  {e.get('args', {}).get('stream', '?'):>4} {e['ts'] - a:8.0f} {e['ts'] + e['dur'] - a:8.0f}  "
+                      f"{e['name'].split('(')[0][:60]}")
     by = {}
     for e in k:
         n = e["name"].split("(")[0][:60]
