@@ -17,7 +17,10 @@ namespace dot {
 
 constexpr int kBlock = 128;
 constexpr int kFwdMinBlocks = 8;   // forward: 64 registers -> 8 blocks (32 warps) per SM
-constexpr int kBwdRecords = 128;   // composited segments buffered per ray (pass 1 -> pass 2); longer rays resume the walk
+#ifndef DOT_BWD_RECORDS
+#define DOT_BWD_RECORDS 128
+#endif
+constexpr int kBwdRecords = DOT_BWD_RECORDS;  // composited segments buffered per ray (pass 1 -> pass 2); longer rays resume the walk
 // Warp-schedule cost of a ray (what dot_sched_update learns): 0 = composited
 // segments, 1 = all traversed segments, 2 = composited + post-cut / 2.  A
 // warp lasts as long as its longest ray, and the longest rays are mostly
