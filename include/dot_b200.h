@@ -202,13 +202,14 @@ int dot_sched_update(const int32_t* sorted_keys, const uint16_t* ray_used, int64
  *     ray_cost is a cost column indexed like the ray arrays (u16: composited +
  *     post-cut / 2 segments, what dot_ray_costs computes and dot_render_bwd
  *     refreshes through its ray_cost output); slot i of the batch costs
- *     ray_cost[ray_index[i]] (ray_index may be NULL); a warp costs the max of
+ *     ray_cost[ray_index[i]] (ray_index may be NULL; an index outside
+ *     [0, n_costs) costs 0); a warp costs the max of
  *     its 32 slots, chunks of
  *     `chunk` consecutive warps are ranked by their costliest warp, descending
  *     (longest first), and warp_order[ceil(n/32)] lists the warps in that
  *     order for dot_render_bwd. */
-int dot_sched_order_costs(const uint16_t* ray_cost, const int64_t* ray_index, int64_t n_rays, int32_t chunk,
-                          int32_t* warp_order, void* stream);
+int dot_sched_order_costs(const uint16_t* ray_cost, int64_t n_costs, const int64_t* ray_index, int64_t n_rays,
+                          int32_t chunk, int32_t* warp_order, void* stream);
 
 /* --- per-ray schedule cost of a ray set (no reference counterpart):
  *     cost[i] = composited + post-cut / 2 segments of ray ray_index[i] (or i),

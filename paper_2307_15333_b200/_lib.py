@@ -83,7 +83,7 @@ _SIGNATURES = {
                                       c_void_p, c_void_p, c_void_p]),
     "dot_sched_order": (c_i32, [c_void_p, c_i64, c_void_p, c_void_p, c_void_p]),
     "dot_sched_update": (c_i32, [c_void_p, c_void_p, c_i64, c_void_p, c_void_p]),
-    "dot_sched_order_costs": (c_i32, [c_void_p, c_void_p, c_i64, c_i32, c_void_p, c_void_p]),
+    "dot_sched_order_costs": (c_i32, [c_void_p, c_i64, c_void_p, c_i64, c_i32, c_void_p, c_void_p]),
     "dot_ray_costs": (c_i32, [c_void_p, c_void_p, c_void_p, c_i64, c_void_p, c_i64, c_f64, c_f64, c_f64,
                               c_void_p, c_void_p]),
     "dot_ray_keys": (c_i32, [c_void_p, c_void_p, c_void_p, c_i64, c_void_p, c_void_p]),

@@ -104,12 +104,14 @@ int dot_sched_update(const int32_t* sorted_keys, const uint16_t* ray_used, int64
     return launch_sched_update(sorted_keys, ray_used, n_rays, table, static_cast<cudaStream_t>(stream));
 }
 
-int dot_sched_order_costs(const uint16_t* ray_cost, const int64_t* ray_index, int64_t n_rays, int32_t chunk,
-                          int32_t* warp_order, void* stream) {
+int dot_sched_order_costs(const uint16_t* ray_cost, int64_t n_costs, const int64_t* ray_index, int64_t n_rays,
+                          int32_t chunk, int32_t* warp_order, void* stream) {
     if (n_rays < 0 || (n_rays && (!ray_cost || !warp_order))) return set_error(DOT_BAD_ARG, "bad arrays");
     if (chunk < 1 || chunk > 4096) return set_error(DOT_BAD_ARG, "chunk must be in 1..4096, got %d", chunk);
     if ((n_rays + 31) / 32 > INT32_MAX) return set_error(DOT_BAD_ARG, "batch too large to schedule");
-    return launch_sched_order_costs(ray_cost, ray_index, n_rays, chunk, warp_order, static_cast<cudaStream_t>(stream));
+    if (!ray_index && n_costs < n_rays) return set_error(DOT_BAD_ARG, "n_costs < n_rays without a ray_index");
+    return launch_sched_order_costs(ray_cost, n_costs, ray_index, n_rays, chunk, warp_order,
+                                    static_cast<cudaStream_t>(stream));
 }
 
 int dot_gather_keys(const int32_t* pool_keys, int64_t n_pool, const int64_t* ray_index, int64_t n_rays,

@@ -43,8 +43,8 @@ int launch_signal_fwd(const TreeDev& T, const double* o, const double* d, const 
                       int64_t n, double eps, double tn, double tf, double* signal, double* wsum, double* wmax,
                       uint8_t* touched, unsigned long long* invalid, cudaStream_t s);
 int launch_sched_order(const int32_t* keys, int64_t n, const uint16_t* table, int32_t* warp_order, cudaStream_t s);
-int launch_sched_order_costs(const uint16_t* slot_cost, const int64_t* ray_idx, int64_t n, int chunk,
-                             int32_t* warp_order, cudaStream_t s);
+int launch_sched_order_costs(const uint16_t* slot_cost, int64_t n_costs, const int64_t* ray_idx, int64_t n,
+                             int chunk, int32_t* warp_order, cudaStream_t s);
 int launch_ray_costs(const TreeDev& T, const double* o, const double* d, const int64_t* ray_idx, int64_t n_pool,
                      int64_t n, double eps, double tn, double tf, uint16_t* cost, cudaStream_t s);
 int launch_sched_update(const int32_t* keys, const uint16_t* ray_used, int64_t n, uint16_t* table, cudaStream_t s);

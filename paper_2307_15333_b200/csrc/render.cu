@@ -870,13 +870,16 @@ constexpr int kCostBins = 1024;
 
 // one thread per batch slot: warp w's cost = max over its 32 slots (warp
 // reduction), then chunk costs (max over `chunk` warps) and their histogram
-__global__ void __launch_bounds__(256) cost_warp_kernel(const uint16_t* __restrict__ ray_cost,
+__global__ void __launch_bounds__(256) cost_warp_kernel(const uint16_t* __restrict__ ray_cost, int64_t n_costs,
                                                         const int64_t* __restrict__ ray_idx, int64_t n,
                                                         uint16_t* __restrict__ warp_cost) {
     const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     const int64_t nw = (n + 31) / 32;
     unsigned c = 0;
-    if (i < n) c = __ldg(ray_cost + ray_index(ray_idx, i));
+    if (i < n) {
+        const int64_t r = ray_index(ray_idx, i);
+        if (r >= 0 && r < n_costs) c = __ldg(ray_cost + r);
+    }
     c = __reduce_max_sync(0xffffffffu, c);
     if ((threadIdx.x & 31) == 0 && (i >> 5) < nw) warp_cost[i >> 5] = uint16_t(min(c, unsigned(kCostBins - 1)));
 }
@@ -926,8 +929,8 @@ __global__ void __launch_bounds__(256) cost_place_kernel(const uint16_t* __restr
     for (int64_t w = w0; w < w1; ++w) warp_order[dst + (w - w0)] = int32_t(w);
 }
 
-int launch_sched_order_costs(const uint16_t* slot_cost, const int64_t* ray_idx, int64_t n, int chunk,
-                             int32_t* warp_order, cudaStream_t s) {
+int launch_sched_order_costs(const uint16_t* slot_cost, int64_t n_costs, const int64_t* ray_idx, int64_t n,
+                             int chunk, int32_t* warp_order, cudaStream_t s) {
     const int64_t nw = (n + 31) / 32;
     if (nw == 0) return DOT_OK;
     const int64_t nc = (nw + chunk - 1) / chunk;
@@ -942,7 +945,7 @@ int launch_sched_order_costs(const uint16_t* slot_cost, const int64_t* ray_idx, 
         st = check_cuda(cudaMallocAsync(reinterpret_cast<void**>(&hist), sizeof(int) * kCostBins, s), "cudaMallocAsync");
     if (st == DOT_OK) st = check_cuda(cudaMemsetAsync(hist, 0, sizeof(int) * kCostBins, s), "cudaMemsetAsync");
     if (st == DOT_OK) {
-        cost_warp_kernel<<<unsigned((nw * 32 + 255) / 256), 256, 0, s>>>(slot_cost, ray_idx, n, wc);
+        cost_warp_kernel<<<unsigned((nw * 32 + 255) / 256), 256, 0, s>>>(slot_cost, n_costs, ray_idx, n, wc);
         cost_hist_kernel<<<unsigned((nc + 255) / 256), 256, 0, s>>>(wc, n, chunk, cc, hist);
         cost_scan_kernel<<<1, kCostBins, 0, s>>>(hist);
         cost_place_kernel<<<unsigned((nc + 256) / 256), 256, 0, s>>>(cc, n, chunk, hist, warp_order);

@@ -409,6 +409,11 @@ def plan_batch(tree: SparseOctree, origins: torch.Tensor, dirs: torch.Tensor, ra
     idx = None if ray_index is None else torch.as_tensor(ray_index, device=tree.device).reshape(-1).to(torch.int64)
     n = int(idx.shape[0]) if idx is not None else int(origins.shape[0])
     n_pool = int(origins.shape[0])
+    if costs is not None and (not isinstance(costs, torch.Tensor) or costs.dtype != torch.int16
+                              or not _on_device(costs, tree.device) or costs.numel() != n_pool
+                              or not costs.is_contiguous()):
+        raise InputError(f"costs must be a contiguous int16 tensor with one entry per ray ({n_pool}) "
+                         f"on {tree.device}")
     view, _topo = tree.tree_view()
     cur = torch.cuda.current_stream(tree.device)
     s = stream or cur
@@ -444,7 +449,7 @@ def plan_batch(tree: SparseOctree, origins: torch.Tensor, dirs: torch.Tensor, ra
         if WARP_SCHED and 0 < n <= SCHED_MAX_RAYS:
             if costs is not None:
                 warp_order = torch.empty((n + 31) // 32, dtype=torch.int32, device=tree.device)
-                _lib.call("dot_sched_order_costs", _lib.ptr(costs), _lib.ptr(idx), n, cost_chunk(n),
+                _lib.call("dot_sched_order_costs", _lib.ptr(costs), int(costs.shape[0]), _lib.ptr(idx), n, cost_chunk(n),
                           _lib.ptr(warp_order), _lib.stream_ptr(s))
             else:
                 warp_order = _sched_order(tree, sorted_keys, n, s)

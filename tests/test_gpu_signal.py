@@ -161,7 +161,7 @@ def test_ray_costs_and_cost_ordered_launch():
     nw = (n + 31) // 32
     for chunk in (1, 16):
         order = torch.empty(nw, dtype=torch.int32, device="cuda")
-        _lib.call("dot_sched_order_costs", _lib.ptr(slot), None, n, chunk, _lib.ptr(order), _lib.stream_ptr())
+        _lib.call("dot_sched_order_costs", _lib.ptr(slot), n, None, n, chunk, _lib.ptr(order), _lib.stream_ptr())
         od = order.cpu().numpy()
         assert np.array_equal(np.sort(od), np.arange(nw))
         pad = np.zeros(nw * 32, dtype=np.int64)
