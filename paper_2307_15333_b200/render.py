@@ -359,7 +359,7 @@ class RayPlan:
 
 # All 31 key bits are sorted: dropping the finest 7 (3 radix passes instead
 # of 4) made the backward 3.5 % slower (coarser coherence).
-PLAN_SORT_BEGIN_BIT = 0
+PLAN_SORT_BEGIN_BIT = int(os.environ.get("DOT_PLAN_SORT_BEGIN_BIT", "0"))
 
 
 def pool_keys(tree: SparseOctree, origins: torch.Tensor, dirs: torch.Tensor) -> torch.Tensor:
