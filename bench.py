@@ -341,12 +341,16 @@ def run_ours(args, rank, world, local_rank):
         from paper_2307_15333_b200.parallel import PeerExchange
         exchange = PeerExchange(tree, state, sws)
 
-    from paper_2307_15333_b200.render import plan_batch, pool_keys, ray_costs
+    from paper_2307_15333_b200.render import plan_batch, pool_keys, pool_rank, ray_costs
     plan_stream = torch.cuda.Stream(dev)
     plans = {}
-    # the resident pool's coherence keys, once (like the pool itself): each
-    # step's plan gathers 4 B per ray instead of re-reading 48 B at random
-    pkeys = pool_keys(tree, origins, dirs)
+    # the resident pool ranked once by its 62-bit coherence keys (like the
+    # pool itself): each step's plan is a counting sort of the batch over a
+    # pool-sized bitmap (dot_plan_ranked), no per-step key gather or radix
+    # sort.  DOT_BENCH_PLAN=keys: the 31-bit pool keys + radix sort instead.
+    plan_kind = os.environ.get("DOT_BENCH_PLAN", "rank")
+    pkeys = pool_keys(tree, origins, dirs) if plan_kind == "keys" else None
+    prank = pool_rank(tree, origins, dirs) if plan_kind == "rank" else None
     # and its per-ray schedule costs (the first epoch's prediction; every
     # backward refreshes its rays' entries): warps launch longest first
     pcosts = ray_costs(tree, origins, dirs, EPS) if os.environ.get("DOT_BENCH_COSTS", "1") == "1" else None
@@ -359,7 +363,7 @@ def run_ours(args, rank, world, local_rank):
         plan = plans.pop(k, None)
         if k + 1 < total_steps + 2:
             plans[k + 1] = plan_batch(tree, origins, dirs, batch_index(k + 1), stream=plan_stream, keys=pkeys,
-                                      costs=pcosts)
+                                      rank=prank, costs=pcosts)
         return train_step(tree, origins, dirs, targets, state, buf, sws, BG, EPS,
                           ray_index=idx, grad_scale=gs,
                           exchange=exchange if world > 1 else None,
@@ -586,16 +590,19 @@ def run_ours(args, rank, world, local_rank):
             "parallelism": f"rays sharded dp{world}, tree replicated",
             "exchange": args.exchange if world > 1 else "none",
             "batch_order": args.order,
-            "plan": "coherence order of step k+1 sorted on a side stream during step k; the "
-                    "resident pool's 31-bit ray keys (render.pool_keys) and per-ray schedule costs "
-                    "(render.ray_costs; refreshed by every backward) computed once at setup; warps "
-                    "launched longest first by cost",
+            "plan": ("coherence order of step k+1 computed on a side stream during step k: "
+                     + ("a counting sort over the resident pool's 62-bit key rank (render.pool_rank, "
+                        "dot_plan_ranked)" if plan_kind == "rank" else
+                        "the resident pool's 31-bit ray keys (render.pool_keys) gathered and radix sorted")
+                     + "; per-ray schedule costs (render.ray_costs; refreshed by every backward); the "
+                       "rank / keys and costs computed once at setup; warps launched longest first by cost"),
         },
-        # per step (profiles/r1j_launch_shares.txt): the plan's radix sort in
-        # dot_plan_sort (histogram + exclusive sum + 4 onesweep passes) +
-        # sched_cost + sched_order + render_bwd_buffered + sched_update + one
-        # rmsprop per all-reduce chunk (a single update at N = 1)
-        "gpu_launches": (10 + (1 if world == 1 else len(chunk_bounds(tree.capacity, args.ar_chunks)))) * args.steps,
+        # per step: the plan (rank: mark + count + scan + place; keys:
+        # gather + radix sort histogram + exclusive sum + 4 onesweep passes),
+        # the cost order (warp cost + histogram + scan + place), the backward
+        # and one rmsprop per all-reduce chunk (a single update at N = 1)
+        "gpu_launches": ((4 if plan_kind == "rank" else 7) + 4 + 1
+                         + (1 if world == 1 else len(chunk_bounds(tree.capacity, args.ar_chunks)))) * args.steps,
         "roofline": {
             "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
             "frac": achieved / hbm, "traffic": traffic, "traffic_source": traffic_src,

@@ -245,6 +245,21 @@ int dot_gather_keys(const int32_t* pool_keys, int64_t n_pool, const int64_t* ray
 int dot_plan_sort(const int32_t* keys, const int64_t* ray_index, int64_t n_rays, int32_t begin_bit,
                   int32_t* sorted_keys, int64_t* sorted_index, void* stream);
 
+/* Coherence order of a batch of a RANKED resident pool, without a sort (no
+ * reference counterpart; replaces dot_gather_keys + dot_plan_sort for pool
+ * batches).  rank[ray] is the ray's position in the pool's key order and
+ * order[position] the ray at that position (inverse permutations, built once
+ * per pool, e.g. from dot_ray_keys + a sort).  sorted_index receives the
+ * batch's rays in key order (a one-bit-per-position counting sort over a
+ * pool-sized bitmap); repeated rays and indices outside [0, n_pool) follow
+ * the placed rays, so sorted_index is always a permutation of ray_index.
+ * workspace: dot_plan_ranked_workspace(n_pool, n_rays) bytes, 256-byte
+ * aligned, ZEROED before its first use; every call leaves it reusable.
+ * Calls sharing a workspace must be stream-ordered.  n_pool, n_rays < 2^31. */
+int64_t dot_plan_ranked_workspace(int64_t n_pool, int64_t n_rays);
+int dot_plan_ranked(const int32_t* rank, const int32_t* order, int64_t n_pool, const int64_t* ray_index,
+                    int64_t n_rays, void* workspace, int64_t workspace_bytes, int64_t* sorted_index, void* stream);
+
 /* --- workload statistics (measurement helper, no reference counterpart):
  *     totals[0] += traversed segments, totals[1] += composited (pre-cut)
  *     segments, totals[2] += composited segments with q > 0. */

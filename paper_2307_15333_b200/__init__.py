@@ -20,6 +20,7 @@ _EXPORTS = {
     "render_rays": "render", "render_ray": "render", "render_and_backprop": "render",
     "render_image": "render", "BackpropWorkspace": "render", "signal_pass": "render",
     "render_view": "render", "render_views": "render", "plan_batch": "render",
+    "pool_keys": "render", "pool_rank": "render", "PoolRank": "render", "ray_costs": "render",
     "SignalTarget": "signals", "SignalBuffer": "signals", "signal_value": "signals",
     "signal_values": "signals",
     "CalibrationConfig": "calibrate", "CalibrationReport": "calibrate", "calibrate": "calibrate",

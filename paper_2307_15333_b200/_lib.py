@@ -18,7 +18,7 @@ LIB_PATH = os.path.join(_HERE, "libdot_b200.so")
 _LIB_OVERRIDE = os.environ.get("DOT_LIB_PATH")
 
 DOT_OK, DOT_BAD_ARG, DOT_OOM, DOT_CUDA_ERR, DOT_NO_DEVICE = range(5)
-ABI_VERSION = 10
+ABI_VERSION = 11
 
 c_void_p = ctypes.c_void_p
 c_i64 = ctypes.c_int64
@@ -90,6 +90,8 @@ _SIGNATURES = {
     "dot_ray_keys32": (c_i32, [c_void_p, c_void_p, c_void_p, c_i64, c_void_p, c_i64, c_void_p, c_void_p]),
     "dot_gather_keys": (c_i32, [c_void_p, c_i64, c_void_p, c_i64, c_void_p, c_void_p]),
     "dot_plan_sort": (c_i32, [c_void_p, c_void_p, c_i64, c_i32, c_void_p, c_void_p, c_void_p]),
+    "dot_plan_ranked_workspace": (c_i64, [c_i64, c_i64]),
+    "dot_plan_ranked": (c_i32, [c_void_p, c_void_p, c_i64, c_void_p, c_i64, c_void_p, c_i64, c_void_p, c_void_p]),
     "dot_ray_stats":(c_i32, [c_void_p, c_void_p, c_void_p, c_i64, c_f64, c_void_p, c_void_p]),
     "dot_refine_plan_create": (c_i32, [c_void_p, c_void_p, c_void_p, c_i32, c_f64, c_f64, c_i32, c_i32,
                                        c_f64, c_void_p, c_i32, c_void_p, c_void_p, c_void_p]),

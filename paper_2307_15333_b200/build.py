@@ -18,7 +18,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libdot_b200.so")
-SOURCES = ["capi.cu", "render.cu", "sorted.cu", "refine.cu", "optim.cu"]
+SOURCES = ["capi.cu", "render.cu", "sorted.cu", "refine.cu", "optim.cu", "plan.cu"]
 HEADERS = ["dot_tree.cuh", "dot_exp.cuh", "dot_internal.h"]
 
 NVCC_FLAGS = [

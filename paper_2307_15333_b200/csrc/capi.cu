@@ -68,7 +68,7 @@ using namespace dot;
 
 extern "C" {
 
-int dot_abi_version(void) { return 10; }
+int dot_abi_version(void) { return 11; }
 
 const char* dot_last_error(void) { return g_err; }
 
@@ -239,6 +239,26 @@ int dot_plan_sort(const int32_t* keys, const int64_t* ray_index, int64_t n_rays,
     if (begin_bit < 0 || begin_bit > 30) return set_error(DOT_BAD_ARG, "begin_bit must be in 0..30");
     return run_plan_sort(keys, ray_index, n_rays, begin_bit, sorted_keys, sorted_index,
                          static_cast<cudaStream_t>(stream));
+}
+
+int64_t dot_plan_ranked_workspace(int64_t n_pool, int64_t n_rays) {
+    if (n_pool < 0 || n_rays < 0) return -1;
+    return int64_t(plan_ranked_workspace(n_pool, n_rays));
+}
+
+int dot_plan_ranked(const int32_t* rank, const int32_t* order, int64_t n_pool, const int64_t* ray_index,
+                    int64_t n_rays, void* workspace, int64_t workspace_bytes, int64_t* sorted_index, void* stream) {
+    if (n_rays < 0 || n_pool < 0 || (n_rays && (!rank || !order || !ray_index || !workspace || !sorted_index)))
+        return set_error(DOT_BAD_ARG, "bad plan_ranked arrays");
+    if (n_pool > INT32_MAX || n_rays > INT32_MAX)
+        return set_error(DOT_BAD_ARG, "plan_ranked: pool and batch must have < 2^31 rays");
+    if (workspace_bytes < int64_t(plan_ranked_workspace(n_pool, n_rays)))
+        return set_error(DOT_BAD_ARG, "plan_ranked: workspace of %lld bytes, %lld needed",
+                         (long long)workspace_bytes, (long long)plan_ranked_workspace(n_pool, n_rays));
+    if (reinterpret_cast<uintptr_t>(workspace) & 255)
+        return set_error(DOT_BAD_ARG, "plan_ranked: workspace must be 256-byte aligned");
+    return run_plan_ranked(rank, order, n_pool, ray_index, n_rays, workspace, sorted_index,
+                           static_cast<cudaStream_t>(stream));
 }
 
 int dot_ray_keys32(const dot_tree_view* tree, const double* origins, const double* dirs, int64_t n_pool,

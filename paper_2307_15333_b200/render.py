@@ -343,11 +343,11 @@ class BackpropWorkspace:
 class RayPlan:
     """A batch's coherence order: the kernel's ray index (the caller's
     ray_index composed with the key sort) and the sorted 31-bit keys (which
-    also index the warp-schedule table)."""
+    also index the warp-schedule table; None for plans from a ``PoolRank``)."""
 
     n: int
     idx: torch.Tensor
-    sorted_keys: torch.Tensor
+    sorted_keys: "torch.Tensor | None"
     event: "torch.cuda.Event | None" = None
     warp_order: "torch.Tensor | None" = None  # launch order, when computed with the plan
     costs: "torch.Tensor | None" = None       # the per-ray cost column the order came from (refreshed after the backward)
@@ -376,6 +376,66 @@ def pool_keys(tree: SparseOctree, origins: torch.Tensor, dirs: torch.Tensor) -> 
     return keys
 
 
+class PoolRank:
+    """A resident ray pool ranked by its 62-bit coherence keys
+    (``dot_ray_keys``): ``rank[ray]`` = position in key order, ``order`` its
+    inverse (int32 each, 8 B per pool ray).  ``plan_batch(..., rank=)`` then
+    orders a batch of pool rays without a sort (``dot_plan_ranked``: a
+    one-bit-per-position counting sort over a pool-sized bitmap).  Build it
+    with ``pool_rank``.  Like ``pool_keys`` it only orders the work: rays
+    edited afterwards cost speed, never correctness.  The plan workspace
+    belongs to this object; plans through it are ordered across streams by
+    an event."""
+
+    def __init__(self, rank: torch.Tensor, order: torch.Tensor):
+        if rank.dtype != torch.int32 or order.dtype != torch.int32 or rank.shape != order.shape:
+            raise InputError("rank / order must be int32 tensors of the pool's length")
+        self.rank = rank.contiguous()
+        self.order = order.contiguous()
+        self.n_pool = int(rank.shape[0])
+        self._ws = None
+        self._ready = None  # event after the last plan that used the workspace
+
+    def workspace(self, n: int, stream) -> torch.Tensor:
+        need = int(_lib.load().dot_plan_ranked_workspace(self.n_pool, n))
+        if self._ready is not None:
+            stream.wait_event(self._ready)
+        if self._ws is None or self._ws.numel() < need:
+            with torch.cuda.stream(stream):  # zeroed where it is used
+                self._ws = torch.zeros(need, dtype=torch.uint8, device=self.rank.device)
+        return self._ws
+
+    def done(self, stream) -> None:
+        self._ready = torch.cuda.Event()
+        self._ready.record(stream)
+
+
+def pool_rank(tree: SparseOctree, origins: torch.Tensor, dirs: torch.Tensor, bits: int | None = None) -> PoolRank:
+    """Rank a resident pool once by its coherence keys for
+    ``plan_batch(..., rank=)``: ``bits`` 62 (origin Morton 3 x 10 bits, then
+    octahedral direction 2 x 16 bits, ``dot_ray_keys``) or 31 (the
+    ``pool_keys`` keys, ties in pool order)."""
+    bits = int(os.environ.get("DOT_RANK_BITS", "62")) if bits is None else bits
+    if bits not in (31, 62):
+        raise InputError(f"pool_rank: bits must be 31 or 62, got {bits}")
+    n = int(origins.shape[0])
+    if n >= 1 << 31:
+        raise InputError("pool_rank: a pool must have < 2^31 rays")
+    dev = tree.device
+    if bits == 31:
+        order = torch.argsort(pool_keys(tree, origins, dirs), stable=True)
+    else:
+        keys = torch.empty(n, dtype=torch.int64, device=dev)
+        view, _topo = tree.tree_view()
+        _lib.call("dot_ray_keys", _lib.ctypes.byref(view), _lib.ptr(origins), _lib.ptr(dirs), n, _lib.ptr(keys),
+                  _lib.stream_ptr())
+        order = torch.argsort(keys)  # keys < 2^62: the signed order is the key order
+        del keys
+    rank = torch.empty(n, dtype=torch.int32, device=dev)
+    rank.scatter_(0, order, torch.arange(n, dtype=torch.int32, device=dev))
+    return PoolRank(rank, order.to(torch.int32))
+
+
 def ray_costs(tree: SparseOctree, origins: torch.Tensor, dirs: torch.Tensor, early_stop_eps: float = EPS_T,
               t_near: float = 0.0, t_far: float = math.inf) -> torch.Tensor:
     """Per-ray schedule cost of a ray pool (``dot_ray_costs``: composited +
@@ -394,7 +454,7 @@ def ray_costs(tree: SparseOctree, origins: torch.Tensor, dirs: torch.Tensor, ear
 
 def plan_batch(tree: SparseOctree, origins: torch.Tensor, dirs: torch.Tensor, ray_index=None,
                stream=None, wait_current: bool = True, keys: torch.Tensor | None = None,
-               costs: torch.Tensor | None = None) -> RayPlan:
+               costs: torch.Tensor | None = None, rank: PoolRank | None = None) -> RayPlan:
     """Coherence order of a batch (origin / octahedral-direction Morton keys,
     dot_ray_keys32 + a radix sort).  Depends only on the rays, so it can run
     on a side stream (``stream``) ahead of the step that consumes it; the
@@ -405,7 +465,10 @@ def plan_batch(tree: SparseOctree, origins: torch.Tensor, dirs: torch.Tensor, ra
     ``costs`` (int16 per ray of the arrays, e.g. ``ray_costs``): launch the
     backward's warps longest first by these per-ray costs
     (``dot_sched_order_costs``) instead of the learned key-bucket table; the
-    backward writes its fresh counts back into ``costs``."""
+    backward writes its fresh counts back into ``costs``.  ``rank``
+    (``pool_rank``): order a batch of pool rays by the pool's 62-bit key rank
+    without a sort (``dot_plan_ranked``); the plan then carries no keys, so
+    its warp order comes only from ``costs``."""
     idx = None if ray_index is None else torch.as_tensor(ray_index, device=tree.device).reshape(-1).to(torch.int64)
     n = int(idx.shape[0]) if idx is not None else int(origins.shape[0])
     n_pool = int(origins.shape[0])
@@ -414,6 +477,13 @@ def plan_batch(tree: SparseOctree, origins: torch.Tensor, dirs: torch.Tensor, ra
                               or not costs.is_contiguous()):
         raise InputError(f"costs must be a contiguous int16 tensor with one entry per ray ({n_pool}) "
                          f"on {tree.device}")
+    if rank is not None:
+        if idx is None:
+            raise InputError("plan_batch(rank=) orders batches of a pool: pass ray_index")
+        if keys is not None:
+            raise InputError("plan_batch: pass keys= or rank=, not both")
+        if not isinstance(rank, PoolRank) or rank.n_pool != n_pool or not _on_device(rank.rank, tree.device):
+            raise InputError(f"rank must be a PoolRank of this pool ({n_pool} rays) on {tree.device}")
     view, _topo = tree.tree_view()
     cur = torch.cuda.current_stream(tree.device)
     s = stream or cur
@@ -422,11 +492,18 @@ def plan_batch(tree: SparseOctree, origins: torch.Tensor, dirs: torch.Tensor, ra
             s.wait_stream(cur)  # inputs produced on the current stream
         # the inputs (and the index temporary made above) are read on the side
         # stream: keep the allocator from recycling them before it is done
-        for t in (idx, origins, dirs, keys, costs):
+        for t in (idx, origins, dirs, keys, costs, rank and rank.rank, rank and rank.order):
             if t is not None:
                 t.record_stream(s)
     with torch.cuda.stream(s):
-        if keys is not None:
+        if rank is not None:
+            order = torch.empty(n, dtype=torch.int64, device=tree.device)
+            ws = rank.workspace(n, s)
+            _lib.call("dot_plan_ranked", _lib.ptr(rank.rank), _lib.ptr(rank.order), n_pool, _lib.ptr(idx), n,
+                      _lib.ptr(ws), ws.numel(), _lib.ptr(order), _lib.stream_ptr(s))
+            rank.done(s)
+            idx, sorted_keys = order, None
+        elif keys is not None:
             if idx is not None:
                 pk = keys
                 keys = torch.empty(n, dtype=torch.int32, device=tree.device)
@@ -436,13 +513,14 @@ def plan_batch(tree: SparseOctree, origins: torch.Tensor, dirs: torch.Tensor, ra
             keys = torch.empty(n, dtype=torch.int32, device=tree.device)
             _lib.call("dot_ray_keys32", _lib.ctypes.byref(view), _lib.ptr(origins), _lib.ptr(dirs), n_pool,
                       _lib.ptr(idx), n, _lib.ptr(keys), _lib.stream_ptr(s))
-        # one radix sort carrying the ray index: the sorted values are the
-        # kernel's ray_index directly
-        sorted_keys = torch.empty_like(keys)
-        order = torch.empty(n, dtype=torch.int64, device=tree.device)
-        _lib.call("dot_plan_sort", _lib.ptr(keys), _lib.ptr(idx), n, PLAN_SORT_BEGIN_BIT,
-                  _lib.ptr(sorted_keys), _lib.ptr(order), _lib.stream_ptr(s))
-        idx = order
+        if rank is None:
+            # one radix sort carrying the ray index: the sorted values are the
+            # kernel's ray_index directly
+            sorted_keys = torch.empty_like(keys)
+            order = torch.empty(n, dtype=torch.int64, device=tree.device)
+            _lib.call("dot_plan_sort", _lib.ptr(keys), _lib.ptr(idx), n, PLAN_SORT_BEGIN_BIT,
+                      _lib.ptr(sorted_keys), _lib.ptr(order), _lib.stream_ptr(s))
+            idx = order
         # the warp launch order too, off the critical path: from the rays'
         # costs when given, else the learned table as of its last update
         warp_order = None
@@ -451,7 +529,7 @@ def plan_batch(tree: SparseOctree, origins: torch.Tensor, dirs: torch.Tensor, ra
                 warp_order = torch.empty((n + 31) // 32, dtype=torch.int32, device=tree.device)
                 _lib.call("dot_sched_order_costs", _lib.ptr(costs), int(costs.shape[0]), _lib.ptr(idx), n, cost_chunk(n),
                           _lib.ptr(warp_order), _lib.stream_ptr(s))
-            else:
+            elif sorted_keys is not None:
                 warp_order = _sched_order(tree, sorted_keys, n, s)
         ev = None
         if s is not cur:

@@ -309,6 +309,105 @@ def test_plan_sort_and_pool_keys():
         assert torch.equal(torch.sort(p.warp_order.to(torch.int64)).values, torch.arange(nw, device="cuda"))
 
 
+def _plan_ranked(rank, order, idx, ws=None):
+    import torch
+    from paper_2307_15333_b200 import _lib
+    n_pool, n = rank.shape[0], idx.shape[0]
+    need = _lib.load().dot_plan_ranked_workspace(n_pool, n)
+    if ws is None:
+        ws = torch.zeros(need, dtype=torch.uint8, device="cuda")
+    out = torch.full((n,), -7, dtype=torch.int64, device="cuda")
+    _lib.call("dot_plan_ranked", _lib.ptr(rank), _lib.ptr(order), n_pool, _lib.ptr(idx), n, _lib.ptr(ws),
+              ws.numel(), _lib.ptr(out), _lib.stream_ptr())
+    return out, ws
+
+
+def test_plan_ranked_counting_sort():
+    """dot_plan_ranked puts a batch of distinct pool rays in rank order
+    (== order[sort(rank[batch])]) for pools that are not a multiple of the
+    bitmap word / block, reuses its workspace (left zeroed), and with
+    repeated or out-of-range indices still returns a permutation of the
+    batch: the placed rays in rank order, the rest after them."""
+    import torch
+    g = torch.Generator(device="cuda")
+    g.manual_seed(11)
+    for n_pool, n in ((1, 1), (37, 20), (65536 + 33, 4097), (300_001, 65_536), (2_000_000, 1 << 20)):
+        order = torch.randperm(n_pool, generator=g, device="cuda").to(torch.int32)
+        rank = torch.empty(n_pool, dtype=torch.int32, device="cuda")
+        rank[order.long()] = torch.arange(n_pool, dtype=torch.int32, device="cuda")
+        ws = None
+        for rep in range(2):
+            idx = torch.randperm(n_pool, generator=g, device="cuda")[:n]
+            out, ws = _plan_ranked(rank, order, idx, ws)
+            want = order[torch.sort(rank[idx].long()).values].long()
+            assert torch.equal(out, want), (n_pool, n, rep)
+            torch.cuda.synchronize()
+            words = (n_pool + 31) // 32
+            assert not bool(ws[: 4 * words].any()), "bitmap not cleared"
+    # repeats and invalid indices
+    n_pool = 5000
+    order = torch.randperm(n_pool, generator=g, device="cuda").to(torch.int32)
+    rank = torch.empty(n_pool, dtype=torch.int32, device="cuda")
+    rank[order.long()] = torch.arange(n_pool, dtype=torch.int32, device="cuda")
+    base = torch.randperm(n_pool, generator=g, device="cuda")[:3000]
+    idx = torch.cat([base, base[:500], torch.tensor([-1, n_pool, 1 << 40], device="cuda")])
+    idx = idx[torch.randperm(idx.shape[0], generator=g, device="cuda")]
+    out, _ = _plan_ranked(rank, order, idx)
+    assert torch.equal(torch.sort(out).values, torch.sort(idx).values)
+    placed = out[:3000]
+    assert torch.equal(placed, order[torch.sort(rank[base].long()).values].long())
+
+
+def test_pool_rank_plans_match_sorted_plans():
+    """pool_rank's rank / order are inverse permutations in 62-bit key
+    order; a plan_batch(rank=) plan is a permutation of the batch in key
+    order and gives the same loss / gradients / signal as a sorted plan."""
+    import torch
+    from helpers import irregular_tree, ray_batch
+    from paper_2307_15333_b200 import _lib
+    from paper_2307_15333_b200.render import (BackpropWorkspace, plan_batch, pool_keys, pool_rank, ray_costs,
+                                              render_and_backprop)
+    from paper_2307_15333_b200.errors import InputError
+    tree = irregular_tree(41, 16, depth=3, splits=40, merges=4, max_depth=6, device="cuda")
+    o, d = ray_batch(42, 90_001)
+    t = np.random.default_rng(43).uniform(0, 1, (o.shape[0], 3))
+    o, d, t = (torch.from_numpy(x).cuda() for x in (o, d, t))
+    pr = pool_rank(tree, o, d)
+    n_pool = o.shape[0]
+    assert torch.equal(pr.rank[pr.order.long()], torch.arange(n_pool, dtype=torch.int32, device="cuda"))
+    keys = torch.empty(n_pool, dtype=torch.int64, device="cuda")
+    view, _ = tree.tree_view()
+    _lib.call("dot_ray_keys", _lib.ctypes.byref(view), _lib.ptr(o), _lib.ptr(d), n_pool, _lib.ptr(keys),
+              _lib.stream_ptr())
+    assert bool((keys[pr.order.long()].diff() >= 0).all())
+    g = torch.Generator(device="cuda")
+    g.manual_seed(44)
+    idx = torch.randperm(n_pool, generator=g, device="cuda")[:70_000]
+    side = torch.cuda.Stream()
+    costs = ray_costs(tree, o, d)
+    results = []
+    for kw in ({"keys": pool_keys(tree, o, d)}, {"rank": pr}, {"rank": pr, "costs": costs}):
+        p = plan_batch(tree, o, d, idx, stream=side, **kw)
+        if "rank" in kw:
+            p.wait()
+            assert p.sorted_keys is None
+            assert torch.equal(p.idx, pr.order[torch.sort(pr.rank[idx].long()).values].long())
+            assert (p.warp_order is not None) == ("costs" in kw)
+        ws = BackpropWorkspace.for_tree(tree)
+        results.append(render_and_backprop(tree, o, d, t, 0.5, ray_index=idx, workspace=ws, plan=p))
+    (l0, g0, s0) = results[0]
+    for (l1, g1, s1) in results[1:]:
+        assert float(l1) == pytest.approx(float(l0), rel=1e-9)
+        torch.testing.assert_close(g1.dsh, g0.dsh, atol=1e-7, rtol=1e-4)
+        torch.testing.assert_close(g1.dsigma, g0.dsigma, atol=1e-7, rtol=1e-4)
+        assert torch.equal(g1.touched_mask, g0.touched_mask)
+        torch.testing.assert_close(s1, s0, rtol=1e-12, atol=1e-15)
+    with pytest.raises(InputError):
+        plan_batch(tree, o, d, None, rank=pr)
+    with pytest.raises(InputError):
+        plan_batch(tree, o[:100], d[:100], idx[:10] % 100, rank=pr)
+
+
 def test_large_batch_with_schedule_vs_oracle(oracle):
     """A batch large enough for the coherence sort and the learned warp
     schedule (several steps, so the table is warm) against the oracle."""
