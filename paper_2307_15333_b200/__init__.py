@@ -28,7 +28,7 @@ _EXPORTS = {
     "select_sample": "calibrate",
     "RmsPropState": "optim", "rmsprop_step": "optim", "TrainConfig": "optim",
     "train_epoch": "optim", "train": "optim", "train_step": "optim", "StepWorkspace": "optim",
-    "heldout_psnr": "optim", "write_history": "optim",
+    "heldout_psnr": "optim", "write_history": "optim", "ResidentRays": "optim",
     "Camera": "scene_io", "look_at": "scene_io", "orbit_cameras": "scene_io",
     "save_tree": "scene_io", "load_tree": "scene_io",
     "RayBatchStager": "staging", "LossReader": "staging",

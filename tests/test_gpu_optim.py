@@ -118,6 +118,48 @@ def test_train_step_equals_unfused_step():
     assert not bool(sws.ws.dsigma.any()) and not bool(sws.ws.dsh_store.any())
 
 
+def test_train_epoch_resident_planned_equals_plain():
+    """train_epoch over a ResidentRays pool with a coherence rank and cost
+    column (plans prepared on a side stream, no sort) == train_epoch over the
+    plain dataset (per-batch key sort): same batches from the same rng, so
+    the epoch loss and the trained payload agree to fp32-atomic noise; the
+    cost column is rewritten by the backward."""
+    from paper_2307_15333_b200.octree import from_canonical_tensors
+    from paper_2307_15333_b200.optim import ResidentRays, RmsPropState, TrainConfig, train_epoch
+    from paper_2307_15333_b200.scene_io import load_tree_bytes, tree_bytes
+    from paper_2307_15333_b200.signals import SignalBuffer
+    tree, o, d, t, _ = _batch_setup(seed=21, n=1 << 15)
+    tree = load_tree_bytes(tree_bytes(tree), device="cuda")
+    topo = tree.topology()
+
+    def clone():
+        return from_canonical_tensors(tree.center, tree.half_extent, tree.basis_count, tree.max_depth,
+                                      topo.node.clone(), tree._sigma.clone(), tree._sh_store.clone(),
+                                      topo.level_offsets)
+
+    data = _Bundle(o.cpu().numpy(), d.cpu().numpy(), t.cpu().numpy())
+    cfg = TrainConfig(batch_size=20000, background=0.5)
+    out = []
+    for planned in (False, True):
+        tr = clone()
+        st, buf = RmsPropState(tr), SignalBuffer(tr)
+        src = ResidentRays(tr, data, cfg.batch_size, plan=True) if planned else data
+        if planned:
+            assert src.rank is not None and src.costs is not None
+            src.costs.zero_()  # every ray's entry is rewritten by the backward that trains it
+        loss = train_epoch(tr, src, st, buf, cfg, np.random.default_rng(5))
+        if planned:
+            from paper_2307_15333_b200.render import ray_costs
+            assert torch.equal(src.costs > 0, ray_costs(tr, src.origins, src.dirs) > 0)
+        out.append((loss, tr, st, buf))
+    (l0, a, sa, ba), (l1, b, sb, bb) = out
+    assert l1 == pytest.approx(l0, rel=1e-5)
+    torch.testing.assert_close(b.sigma, a.sigma, atol=1e-5, rtol=1e-4)
+    torch.testing.assert_close(b.sh, a.sh, atol=1e-5, rtol=1e-4)
+    torch.testing.assert_close(bb.accumulator, ba.accumulator, atol=1e-9, rtol=1e-4)
+    assert bb.epoch_rays == ba.epoch_rays == o.shape[0]
+
+
 class _HeldoutBundle(_Bundle):
     def __init__(self, origins, dirs, targets, heldout):
         super().__init__(origins, dirs, targets)
