@@ -344,16 +344,24 @@ def run_ours(args, rank, world, local_rank):
     from paper_2307_15333_b200.render import plan_batch, pool_keys, pool_rank, ray_costs
     plan_stream = torch.cuda.Stream(dev)
     plans = {}
-    # the resident pool ranked once by its 62-bit coherence keys (like the
-    # pool itself): each step's plan is a counting sort of the batch over a
-    # pool-sized bitmap (dot_plan_ranked), no per-step key gather or radix
-    # sort.  DOT_BENCH_PLAN=keys: the 31-bit pool keys + radix sort instead.
+    # the resident pool ranked once by its 62-bit coherence keys and stored
+    # in that order (like building the pool itself): each step's plan is a
+    # counting sort of the batch's positions over a pool-sized bitmap
+    # (dot_plan_ranked) -- no per-step key gather, radix sort or index
+    # gather.  The steps' batches stay epoch-permutation slices of the pool.
+    # DOT_BENCH_PLAN=rank-gather: pool left in place, plans map positions
+    # back through the rank's order; =keys: 31-bit pool keys + radix sort.
     plan_kind = os.environ.get("DOT_BENCH_PLAN", "rank")
     pkeys = pool_keys(tree, origins, dirs) if plan_kind == "keys" else None
-    prank = pool_rank(tree, origins, dirs) if plan_kind == "rank" else None
+    prank = pool_rank(tree, origins, dirs) if plan_kind in ("rank", "rank-gather") else None
     # and its per-ray schedule costs (the first epoch's prediction; every
     # backward refreshes its rays' entries): warps launch longest first
     pcosts = ray_costs(tree, origins, dirs, EPS) if os.environ.get("DOT_BENCH_COSTS", "1") == "1" else None
+    if plan_kind == "rank":
+        from paper_2307_15333_b200.render import PoolRank
+        origins, dirs, targets, pcosts = prank.permute(origins, dirs, targets, pcosts)
+        prank = PoolRank.identity(n_pool, dev)
+        torch.cuda.empty_cache()
 
     def step(k, timed_kernel=True):
         # the batch is read in place from the resident pool (ray_index): no
@@ -591,9 +599,12 @@ def run_ours(args, rank, world, local_rank):
             "exchange": args.exchange if world > 1 else "none",
             "batch_order": args.order,
             "plan": ("coherence order of step k+1 computed on a side stream during step k: "
-                     + ("a counting sort over the resident pool's 62-bit key rank (render.pool_rank, "
-                        "dot_plan_ranked)" if plan_kind == "rank" else
-                        "the resident pool's 31-bit ray keys (render.pool_keys) gathered and radix sorted")
+                     + ({"rank": "a counting sort of the batch's pool positions, the pool stored in 62-bit "
+                                 "key order (render.pool_rank + PoolRank.permute, dot_plan_ranked)",
+                         "rank-gather": "a counting sort over the resident pool's 62-bit key rank "
+                                        "(render.pool_rank, dot_plan_ranked)",
+                         "keys": "the resident pool's 31-bit ray keys (render.pool_keys) gathered and "
+                                 "radix sorted"}[plan_kind])
                      + "; per-ray schedule costs (render.ray_costs; refreshed by every backward); the "
                        "rank / keys and costs computed once at setup; warps launched longest first by cost"),
         },
@@ -601,7 +612,7 @@ def run_ours(args, rank, world, local_rank):
         # gather + radix sort histogram + exclusive sum + 4 onesweep passes),
         # the cost order (warp cost + histogram + scan + place), the backward
         # and one rmsprop per all-reduce chunk (a single update at N = 1)
-        "gpu_launches": ((4 if plan_kind == "rank" else 7) + 4 + 1
+        "gpu_launches": ((4 if plan_kind.startswith("rank") else 7) + 4 + 1
                          + (1 if world == 1 else len(chunk_bounds(tree.capacity, args.ar_chunks)))) * args.steps,
         "roofline": {
             "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",

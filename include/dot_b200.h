@@ -249,7 +249,10 @@ int dot_plan_sort(const int32_t* keys, const int64_t* ray_index, int64_t n_rays,
  * reference counterpart; replaces dot_gather_keys + dot_plan_sort for pool
  * batches).  rank[ray] is the ray's position in the pool's key order and
  * order[position] the ray at that position (inverse permutations, built once
- * per pool, e.g. from dot_ray_keys + a sort).  sorted_index receives the
+ * per pool, e.g. from dot_ray_keys + a sort); rank == NULL: ray_index
+ * already holds key positions, order == NULL: the pool is stored in key
+ * order, so positions are the rays (sorted_index = positions; no gather --
+ * the fastest layout: pool arrays permuted once by order).  sorted_index receives the
  * batch's rays in key order (a one-bit-per-position counting sort over a
  * pool-sized bitmap); repeated rays and indices outside [0, n_pool) follow
  * the placed rays, so sorted_index is always a permutation of ray_index.

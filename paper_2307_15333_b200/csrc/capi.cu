@@ -248,7 +248,7 @@ int64_t dot_plan_ranked_workspace(int64_t n_pool, int64_t n_rays) {
 
 int dot_plan_ranked(const int32_t* rank, const int32_t* order, int64_t n_pool, const int64_t* ray_index,
                     int64_t n_rays, void* workspace, int64_t workspace_bytes, int64_t* sorted_index, void* stream) {
-    if (n_rays < 0 || n_pool < 0 || (n_rays && (!rank || !order || !ray_index || !workspace || !sorted_index)))
+    if (n_rays < 0 || n_pool < 0 || (n_rays && (!ray_index || !workspace || !sorted_index)))
         return set_error(DOT_BAD_ARG, "bad plan_ranked arrays");
     if (n_pool > INT32_MAX || n_rays > INT32_MAX)
         return set_error(DOT_BAD_ARG, "plan_ranked: pool and batch must have < 2^31 rays");

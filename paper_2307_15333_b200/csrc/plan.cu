@@ -60,7 +60,7 @@ __global__ void __launch_bounds__(256) plan_mark_kernel(const int32_t* __restric
     const int64_t r = __ldg(ray_idx + i);
     bool placed = false;
     if (r >= 0 && r < n_pool) {
-        const int32_t k = __ldg(rank + r);
+        const int64_t k = rank ? int64_t(__ldg(rank + r)) : r;  // NULL: the pool is stored in key order
         if (k >= 0 && k < n_pool) {  // a damaged rank entry is appended, never written out of bounds
             const uint32_t bit = 1u << (uint32_t(k) & 31u);
             placed = (atomicOr(w.bitmap + (uint32_t(k) >> 5), bit) & bit) == 0u;
@@ -107,8 +107,9 @@ __global__ void __launch_bounds__(1024) plan_scan_kernel(int64_t blocks, PlanWs 
 }
 
 // each set bit's slot = block base + exclusive count inside the block; the
-// slot receives the pool ray at that key position; the words are cleared.
-// The appended rays go after the placed ones.
+// slot receives the key position, then (order != NULL) the pool ray at that
+// position; the words are cleared.  The appended rays go after the placed
+// ones.
 __global__ void __launch_bounds__(kPlanThreads) plan_place_kernel(const int32_t* __restrict__ order, int64_t words,
                                                                   int64_t blocks, int64_t n, PlanWs w,
                                                                   int64_t* __restrict__ out) {
@@ -130,7 +131,29 @@ __global__ void __launch_bounds__(kPlanThreads) plan_place_kernel(const int32_t*
         if (m[k] == 0u) continue;
         w.bitmap[w0 + k] = 0u;
         const int64_t pos0 = (w0 + k) * 32;
-        for (uint32_t b = m[k]; b; b &= b - 1u) out[slot++] = int64_t(__ldg(order + pos0 + (__ffs(b) - 1)));
+        for (uint32_t b = m[k]; b; b &= b - 1u) out[slot++] = pos0 + (__ffs(b) - 1);
+    }
+    if (order) {
+        // key positions -> pool rays: the block's slots, four independent
+        // gathers in flight per thread (not one dependent chain per set bit)
+        __syncthreads();
+        const int64_t b0 = w.block_base[blockIdx.x], b1 = w.block_base[blockIdx.x + 1];
+        for (int64_t i = b0 + threadIdx.x; i < b1; i += 4 * kPlanThreads) {
+            int64_t pos[4];
+            int32_t ray[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int64_t j = i + u * kPlanThreads;
+                pos[u] = j < b1 ? out[j] : -1;
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) ray[u] = pos[u] >= 0 ? __ldg(order + pos[u]) : 0;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int64_t j = i + u * kPlanThreads;
+                if (j < b1) out[j] = ray[u];
+            }
+        }
     }
     // the appended rays: grid-stride over the (usually empty) tail
     const int64_t placed = w.block_base[blocks];

@@ -206,8 +206,10 @@ class _IO:
         return t
 
 
-def _on_device(x: torch.Tensor, dev: torch.device) -> bool:
-    return x.device.type == dev.type and (dev.index is None or x.device.index == dev.index)
+def _on_device(x, dev: torch.device) -> bool:
+    """Tensor (or device) ``x`` is on ``dev`` (a device without an index matches any index)."""
+    xd = x if isinstance(x, torch.device) else x.device
+    return xd.type == dev.type and (dev.index is None or xd.index is None or xd.index == dev.index)
 
 
 def _check_out(name: str, x, dtype, tree) -> None:
@@ -377,24 +379,62 @@ def pool_keys(tree: SparseOctree, origins: torch.Tensor, dirs: torch.Tensor) -> 
 
 
 class PoolRank:
-    """A resident ray pool ranked by its 62-bit coherence keys
-    (``dot_ray_keys``): ``rank[ray]`` = position in key order, ``order`` its
-    inverse (int32 each, 8 B per pool ray).  ``plan_batch(..., rank=)`` then
-    orders a batch of pool rays without a sort (``dot_plan_ranked``: a
-    one-bit-per-position counting sort over a pool-sized bitmap).  Build it
-    with ``pool_rank``.  Like ``pool_keys`` it only orders the work: rays
-    edited afterwards cost speed, never correctness.  The plan workspace
-    belongs to this object; plans through it are ordered across streams by
-    an event."""
+    """A resident ray pool ranked by its coherence keys (``pool_rank``):
+    ``rank[ray]`` = the ray's position in key order, ``order`` its inverse
+    (int32 each, 8 B per pool ray).  ``plan_batch(..., rank=)`` then orders a
+    batch of pool rays without a sort (``dot_plan_ranked``: a one-bit-per-
+    position counting sort over a pool-sized bitmap).
 
-    def __init__(self, rank: torch.Tensor, order: torch.Tensor):
-        if rank.dtype != torch.int32 or order.dtype != torch.int32 or rank.shape != order.shape:
-            raise InputError("rank / order must be int32 tensors of the pool's length")
-        self.rank = rank.contiguous()
-        self.order = order.contiguous()
-        self.n_pool = int(rank.shape[0])
+    Fastest layout: the pool's arrays stored in key order once
+    (``permute``), so a plan's output positions ARE the rays (no gather);
+    ``in_key_order()`` is the rank for that permuted pool (callers keep
+    their own ray ids; ``positions(ids)`` maps them), ``identity(n)`` the
+    rank for callers that sample positions directly.  Like ``pool_keys`` it
+    only orders work: stale ranks cost speed, never correctness.  The plan
+    workspace belongs to this object; plans through it are ordered across
+    streams by an event."""
+
+    def __init__(self, rank: torch.Tensor | None, order: torch.Tensor | None, n_pool: int | None = None,
+                 device=None):
+        for t in (rank, order):
+            if t is not None and t.dtype != torch.int32:
+                raise InputError("rank / order must be int32 tensors of the pool's length")
+        if rank is not None and order is not None and rank.shape != order.shape:
+            raise InputError("rank / order must have the pool's length")
+        ref = rank if rank is not None else order
+        self.rank = None if rank is None else rank.contiguous()
+        self.order = None if order is None else order.contiguous()
+        self.n_pool = int(ref.shape[0]) if ref is not None else int(n_pool)
+        self.device = ref.device if ref is not None else torch.device(device)
         self._ws = None
         self._ready = None  # event after the last plan that used the workspace
+
+    @classmethod
+    def identity(cls, n_pool: int, device) -> "PoolRank":
+        """For a pool already stored in key order whose callers pass key
+        positions as ray indices."""
+        return cls(None, None, n_pool, device)
+
+    def in_key_order(self) -> "PoolRank":
+        """The rank of this pool after ``permute``: caller ids still map
+        through ``rank``, plan outputs are positions in the permuted arrays."""
+        return PoolRank(self.rank, None, self.n_pool, self.device)
+
+    def permute(self, *tensors):
+        """The pool's per-ray arrays in key order (row i = the ray at
+        position i); new tensors, the inputs are untouched."""
+        if self.order is None:
+            raise InputError("permute needs the rank's order (pool_rank output)")
+        idx = self.order.long()
+        return tuple(None if t is None else t[idx] for t in tensors)
+
+    def positions(self, ray_ids: torch.Tensor) -> torch.Tensor:
+        """Key positions of caller ray ids (identity without a rank)."""
+        ids = torch.as_tensor(ray_ids, device=self.device).reshape(-1).to(torch.int64)
+        return ids if self.rank is None else self.rank[ids].to(torch.int64)
+
+    def tensors(self):
+        return tuple(t for t in (self.rank, self.order) if t is not None)
 
     def workspace(self, n: int, stream) -> torch.Tensor:
         need = int(_lib.load().dot_plan_ranked_workspace(self.n_pool, n))
@@ -402,7 +442,7 @@ class PoolRank:
             stream.wait_event(self._ready)
         if self._ws is None or self._ws.numel() < need:
             with torch.cuda.stream(stream):  # zeroed where it is used
-                self._ws = torch.zeros(need, dtype=torch.uint8, device=self.rank.device)
+                self._ws = torch.zeros(need, dtype=torch.uint8, device=self.device)
         return self._ws
 
     def done(self, stream) -> None:
@@ -482,7 +522,7 @@ def plan_batch(tree: SparseOctree, origins: torch.Tensor, dirs: torch.Tensor, ra
             raise InputError("plan_batch(rank=) orders batches of a pool: pass ray_index")
         if keys is not None:
             raise InputError("plan_batch: pass keys= or rank=, not both")
-        if not isinstance(rank, PoolRank) or rank.n_pool != n_pool or not _on_device(rank.rank, tree.device):
+        if not isinstance(rank, PoolRank) or rank.n_pool != n_pool or not _on_device(rank.device, tree.device):
             raise InputError(f"rank must be a PoolRank of this pool ({n_pool} rays) on {tree.device}")
     view, _topo = tree.tree_view()
     cur = torch.cuda.current_stream(tree.device)
@@ -492,7 +532,7 @@ def plan_batch(tree: SparseOctree, origins: torch.Tensor, dirs: torch.Tensor, ra
             s.wait_stream(cur)  # inputs produced on the current stream
         # the inputs (and the index temporary made above) are read on the side
         # stream: keep the allocator from recycling them before it is done
-        for t in (idx, origins, dirs, keys, costs, rank and rank.rank, rank and rank.order):
+        for t in (idx, origins, dirs, keys, costs) + (rank.tensors() if rank is not None else ()):
             if t is not None:
                 t.record_stream(s)
     with torch.cuda.stream(s):

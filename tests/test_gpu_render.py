@@ -309,10 +309,10 @@ def test_plan_sort_and_pool_keys():
         assert torch.equal(torch.sort(p.warp_order.to(torch.int64)).values, torch.arange(nw, device="cuda"))
 
 
-def _plan_ranked(rank, order, idx, ws=None):
+def _plan_ranked(rank, order, idx, ws=None, n_pool=None):
     import torch
     from paper_2307_15333_b200 import _lib
-    n_pool, n = rank.shape[0], idx.shape[0]
+    n_pool, n = (rank.shape[0] if n_pool is None else n_pool), idx.shape[0]
     need = _lib.load().dot_plan_ranked_workspace(n_pool, n)
     if ws is None:
         ws = torch.zeros(need, dtype=torch.uint8, device="cuda")
@@ -341,6 +341,12 @@ def test_plan_ranked_counting_sort():
             out, ws = _plan_ranked(rank, order, idx, ws)
             want = order[torch.sort(rank[idx].long()).values].long()
             assert torch.equal(out, want), (n_pool, n, rep)
+            # the pool stored in key order: positions out (order NULL), and
+            # positions in as well (rank NULL)
+            out, ws = _plan_ranked(rank, None, idx, ws)
+            assert torch.equal(out, torch.sort(rank[idx].long()).values)
+            out, ws = _plan_ranked(None, None, idx, ws, n_pool=n_pool)
+            assert torch.equal(out, torch.sort(idx).values)
             torch.cuda.synchronize()
             words = (n_pool + 31) // 32
             assert not bool(ws[: 4 * words].any()), "bitmap not cleared"
@@ -365,8 +371,8 @@ def test_pool_rank_plans_match_sorted_plans():
     import torch
     from helpers import irregular_tree, ray_batch
     from paper_2307_15333_b200 import _lib
-    from paper_2307_15333_b200.render import (BackpropWorkspace, plan_batch, pool_keys, pool_rank, ray_costs,
-                                              render_and_backprop)
+    from paper_2307_15333_b200.render import (BackpropWorkspace, PoolRank, plan_batch, pool_keys, pool_rank,
+                                              ray_costs, render_and_backprop)
     from paper_2307_15333_b200.errors import InputError
     tree = irregular_tree(41, 16, depth=3, splits=40, merges=4, max_depth=6, device="cuda")
     o, d = ray_batch(42, 90_001)
@@ -386,15 +392,22 @@ def test_pool_rank_plans_match_sorted_plans():
     side = torch.cuda.Stream()
     costs = ray_costs(tree, o, d)
     results = []
-    for kw in ({"keys": pool_keys(tree, o, d)}, {"rank": pr}, {"rank": pr, "costs": costs}):
-        p = plan_batch(tree, o, d, idx, stream=side, **kw)
+    po, pd, pt, pc = pr.permute(o, d, t, costs)  # the pool stored in key order
+    for kw in ({"keys": pool_keys(tree, o, d)}, {"rank": pr}, {"rank": pr, "costs": costs},
+               {"rank": pr.in_key_order(), "costs": pc}, {"rank": PoolRank.identity(n_pool, "cuda"), "costs": pc}):
+        permuted = kw.get("rank") is not None and kw["rank"].order is None
+        oo, dd, tt = (po, pd, pt) if permuted else (o, d, t)
+        # a rank maps caller ray ids; the identity rank takes key positions
+        ii = pr.positions(idx) if permuted and kw["rank"].rank is None else idx
+        p = plan_batch(tree, oo, dd, ii, stream=side, **kw)
         if "rank" in kw:
             p.wait()
             assert p.sorted_keys is None
-            assert torch.equal(p.idx, pr.order[torch.sort(pr.rank[idx].long()).values].long())
+            want = torch.sort(pr.rank[idx].long()).values
+            assert torch.equal(p.idx, want if permuted else pr.order[want].long())
             assert (p.warp_order is not None) == ("costs" in kw)
         ws = BackpropWorkspace.for_tree(tree)
-        results.append(render_and_backprop(tree, o, d, t, 0.5, ray_index=idx, workspace=ws, plan=p))
+        results.append(render_and_backprop(tree, oo, dd, tt, 0.5, ray_index=ii, workspace=ws, plan=p))
     (l0, g0, s0) = results[0]
     for (l1, g1, s1) in results[1:]:
         assert float(l1) == pytest.approx(float(l0), rel=1e-9)
