@@ -369,13 +369,22 @@ def run_ours(args, rank, world, local_rank):
         # previous step (plan_batch), and the next one is queued now
         idx = batch_index(k)
         plan = plans.pop(k, None)
-        if k + 1 < total_steps + 2:
-            plans[k + 1] = plan_batch(tree, origins, dirs, batch_index(k + 1), stream=plan_stream, keys=pkeys,
-                                      rank=prank, costs=pcosts)
+
+        def next_plan():
+            if k + 1 < total_steps + 2:
+                plans[k + 1] = plan_batch(tree, origins, dirs, batch_index(k + 1), stream=plan_stream,
+                                          keys=pkeys, rank=prank, costs=pcosts)
+        # the next plan is queued behind this step's backward, so it runs
+        # beside the (bandwidth-bound) update instead of the backward;
+        # DOT_PLAN_EARLY=1: queued before the step (runs beside the backward)
+        early = os.environ.get("DOT_PLAN_EARLY", "0") == "1"
+        if early:
+            next_plan()
         return train_step(tree, origins, dirs, targets, state, buf, sws, BG, EPS,
                           ray_index=idx, grad_scale=gs,
                           exchange=exchange if world > 1 else None,
-                          kernel_events=kev[k] if timed_kernel else None, plan=plan)
+                          kernel_events=kev[k] if timed_kernel else None, plan=plan,
+                          after_backward=None if early else next_plan)
 
     clocks = ClockSampler(local_rank).start()  # before the warm-up: its start-up is CPU-heavy
     # at most LEAD steps in flight: the host waits for step k - LEAD before
@@ -460,22 +469,29 @@ def run_ours(args, rank, world, local_rank):
     # "serial_ms_per_step": the same loop with blocking copies + reads.
     from paper_2307_15333_b200.staging import LossReader, RayBatchStager
     host = []
-    for j in range(E2E_BATCHES):  # distinct pinned host batches (rays + targets + costs), cycled
+    e2e_ranked = plan_kind == "rank"
+    for j in range(E2E_BATCHES):  # distinct pinned host batches (rays + targets + costs [+ ids]), cycled
         idx = perm[j % perm.shape[0]]
         host.append(tuple(x[idx].cpu().pin_memory() if x is not None else None
-                          for x in (origins, dirs, targets, pcosts)))
+                          for x in (origins, dirs, targets, pcosts))
+                    + ((idx.cpu().pin_memory(),) if e2e_ranked else ()))
     torch.cuda.synchronize()
+    e2e_bytes_per_ray = 72 + (2 if pcosts is not None else 0) + (8 if e2e_ranked else 0)
 
     ex = exchange if world > 1 else None
 
     def serial_loop(steps):
         for k in range(steps):
-            o_h, d_h, t_h, _ = host[k % len(host)]
+            o_h, d_h, t_h = host[k % len(host)][:3]
             loss = train_step(tree, o_h, d_h, t_h, state, buf, sws, BG, EPS, grad_scale=gs,
                               exchange=ex)
             float(loss.item())
 
-    stager = RayBatchStager(dev, max_rays=per_rank, plan_tree=tree)
+    # the host dataset is the key-ordered pool: a batch's ids (its rows) are
+    # its key positions, so the staged batch is ordered without a sort
+    # (dot_plan_ranked, slot mode); DOT_BENCH_PLAN=keys: ray keys + radix sort
+    stager = RayBatchStager(dev, max_rays=per_rank, plan_tree=tree,
+                            plan_rank=PoolRank.identity(n_pool, dev) if e2e_ranked else None)
 
     def staged_loop(steps):
         reader = LossReader()
@@ -510,7 +526,14 @@ def run_ours(args, rank, world, local_rank):
         return t
 
     e2e_serial_ms = timed(serial_loop)
+    trace_e2e = os.environ.get("DOT_TRACE_E2E")  # diagnostic (tools/step_gaps.py --e2e): never set for a bench line
+    if trace_e2e:
+        prof = torch.profiler.profile(activities=[torch.profiler.ProfilerActivity.CUDA])
+        prof.__enter__()
     e2e_ms = timed(staged_loop)
+    if trace_e2e:
+        prof.__exit__(None, None, None)
+        prof.export_chrome_trace(trace_e2e)
     e2e_value = n_global * args.steps / (e2e_ms / 1e3)
 
     # the optimizer update alone on one batch's gradients (consume=False so
@@ -623,10 +646,13 @@ def run_ours(args, rank, world, local_rank):
             "bytes_model": f"{RAY_BYTES} B/ray + {SEG_BYTES} B/composited segment",
             "atomics_per_launch": reds, "atomics_per_s": reds / (kern_ms_avg / 1e3),
         },
-        "e2e": {"value": e2e_value, "unit": "rays/s", "h2d_bytes_per_step": per_rank * (72 + 2),
+        "e2e": {"value": e2e_value, "unit": "rays/s", "h2d_bytes_per_step": per_rank * e2e_bytes_per_ray,
                 "d2h_bytes_per_step": 8, "ms_per_step": e2e_ms / args.steps,
-                "api": "RayBatchStager (H2D + coherence sort of step k+1 overlap step k) + optim.train_step "
-                       "(render_and_backprop + rmsprop_step) + LossReader (loss read one step late)",
+                "api": ("RayBatchStager (H2D of step k+1's rays, targets, costs"
+                        + (" and dataset ids; its coherence order by the dataset's rank, dot_plan_ranked slot mode"
+                           if e2e_ranked else "; its ray keys + radix sort")
+                        + ", overlapping step k) + optim.train_step (render_and_backprop + rmsprop_step) + "
+                          "LossReader (loss read one step late)"),
                 "host_batches": E2E_BATCHES,
                 "serial_ms_per_step": e2e_serial_ms / args.steps},
         "clocks": clk,

@@ -245,23 +245,35 @@ int dot_gather_keys(const int32_t* pool_keys, int64_t n_pool, const int64_t* ray
 int dot_plan_sort(const int32_t* keys, const int64_t* ray_index, int64_t n_rays, int32_t begin_bit,
                   int32_t* sorted_keys, int64_t* sorted_index, void* stream);
 
-/* Coherence order of a batch of a RANKED resident pool, without a sort (no
- * reference counterpart; replaces dot_gather_keys + dot_plan_sort for pool
- * batches).  rank[ray] is the ray's position in the pool's key order and
- * order[position] the ray at that position (inverse permutations, built once
- * per pool, e.g. from dot_ray_keys + a sort); rank == NULL: ray_index
- * already holds key positions, order == NULL: the pool is stored in key
- * order, so positions are the rays (sorted_index = positions; no gather --
- * the fastest layout: pool arrays permuted once by order).  sorted_index receives the
- * batch's rays in key order (a one-bit-per-position counting sort over a
- * pool-sized bitmap); repeated rays and indices outside [0, n_pool) follow
- * the placed rays, so sorted_index is always a permutation of ray_index.
- * workspace: dot_plan_ranked_workspace(n_pool, n_rays) bytes, 256-byte
- * aligned, ZEROED before its first use; every call leaves it reusable.
- * Calls sharing a workspace must be stream-ordered.  n_pool, n_rays < 2^31. */
-int64_t dot_plan_ranked_workspace(int64_t n_pool, int64_t n_rays);
+/* Coherence order of a batch from a RANKED ray pool, without a sort (no
+ * reference counterpart; replaces dot_gather_keys / dot_ray_keys32 +
+ * dot_plan_sort + dot_sched_order_costs).  rank[ray] is the pool ray's
+ * position in key order, order[position] the ray there (inverse
+ * permutations, built once per pool, e.g. from dot_ray_keys + a sort); rank
+ * == NULL: ray_index already holds key positions.  ray_index[i] names the
+ * batch's i-th ray in the pool.  sorted_index receives the batch in key
+ * order, as
+ *   DOT_PLAN_POSITIONS  key positions (the pool's arrays stored in key
+ *                       order: the positions ARE the rays; fastest)
+ *   DOT_PLAN_POOL_RAYS  pool rays order[position] (order required)
+ *   DOT_PLAN_SLOTS      batch slots i (a staged batch whose arrays hold the
+ *                       rays by slot; ray_index = their dataset ids)
+ * Repeated rays and indices outside [0, n_pool) follow the placed ones, so
+ * sorted_index is always a permutation of the batch.  warp_order
+ * (optional, [ceil(n_rays / 32)]): the backward's warp launch order from
+ * ray_cost (u16, indexed by sorted_index's values: [n_pool] for positions /
+ * pool rays, [n_rays] for slots): chunks of `chunk` consecutive warps by
+ * descending max cost, a short last chunk last -- what
+ * dot_sched_order_costs gives for sorted_index.  One cooperative launch
+ * (one block per SM).  workspace: dot_plan_ranked_workspace(n_pool,
+ * n_rays, mode) bytes, 256-byte aligned, ZEROED before its first use;
+ * every call leaves it reusable.  Calls sharing a workspace must be
+ * stream-ordered.  n_pool, n_rays < 2^31. */
+enum { DOT_PLAN_POSITIONS = 0, DOT_PLAN_POOL_RAYS = 1, DOT_PLAN_SLOTS = 2 };
+int64_t dot_plan_ranked_workspace(int64_t n_pool, int64_t n_rays, int32_t mode);
 int dot_plan_ranked(const int32_t* rank, const int32_t* order, int64_t n_pool, const int64_t* ray_index,
-                    int64_t n_rays, void* workspace, int64_t workspace_bytes, int64_t* sorted_index, void* stream);
+                    int64_t n_rays, int32_t mode, const uint16_t* ray_cost, int32_t chunk, int32_t* warp_order,
+                    void* workspace, int64_t workspace_bytes, int64_t* sorted_index, void* stream);
 
 /* --- workload statistics (measurement helper, no reference counterpart):
  *     totals[0] += traversed segments, totals[1] += composited (pre-cut)

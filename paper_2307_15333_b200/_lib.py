@@ -90,8 +90,9 @@ _SIGNATURES = {
     "dot_ray_keys32": (c_i32, [c_void_p, c_void_p, c_void_p, c_i64, c_void_p, c_i64, c_void_p, c_void_p]),
     "dot_gather_keys": (c_i32, [c_void_p, c_i64, c_void_p, c_i64, c_void_p, c_void_p]),
     "dot_plan_sort": (c_i32, [c_void_p, c_void_p, c_i64, c_i32, c_void_p, c_void_p, c_void_p]),
-    "dot_plan_ranked_workspace": (c_i64, [c_i64, c_i64]),
-    "dot_plan_ranked": (c_i32, [c_void_p, c_void_p, c_i64, c_void_p, c_i64, c_void_p, c_i64, c_void_p, c_void_p]),
+    "dot_plan_ranked_workspace": (c_i64, [c_i64, c_i64, c_i32]),
+    "dot_plan_ranked": (c_i32, [c_void_p, c_void_p, c_i64, c_void_p, c_i64, c_i32, c_void_p, c_i32, c_void_p,
+                                c_void_p, c_i64, c_void_p, c_void_p]),
     "dot_ray_stats":(c_i32, [c_void_p, c_void_p, c_void_p, c_i64, c_f64, c_void_p, c_void_p]),
     "dot_refine_plan_create": (c_i32, [c_void_p, c_void_p, c_void_p, c_i32, c_f64, c_f64, c_i32, c_i32,
                                        c_f64, c_void_p, c_i32, c_void_p, c_void_p, c_void_p]),

@@ -241,24 +241,30 @@ int dot_plan_sort(const int32_t* keys, const int64_t* ray_index, int64_t n_rays,
                          static_cast<cudaStream_t>(stream));
 }
 
-int64_t dot_plan_ranked_workspace(int64_t n_pool, int64_t n_rays) {
-    if (n_pool < 0 || n_rays < 0) return -1;
-    return int64_t(plan_ranked_workspace(n_pool, n_rays));
+int64_t dot_plan_ranked_workspace(int64_t n_pool, int64_t n_rays, int32_t mode) {
+    if (n_pool < 0 || n_rays < 0 || mode < DOT_PLAN_POSITIONS || mode > DOT_PLAN_SLOTS) return -1;
+    return int64_t(plan_ranked_workspace(n_pool, n_rays, mode));
 }
 
 int dot_plan_ranked(const int32_t* rank, const int32_t* order, int64_t n_pool, const int64_t* ray_index,
-                    int64_t n_rays, void* workspace, int64_t workspace_bytes, int64_t* sorted_index, void* stream) {
+                    int64_t n_rays, int32_t mode, const uint16_t* ray_cost, int32_t chunk, int32_t* warp_order,
+                    void* workspace, int64_t workspace_bytes, int64_t* sorted_index, void* stream) {
     if (n_rays < 0 || n_pool < 0 || (n_rays && (!ray_index || !workspace || !sorted_index)))
         return set_error(DOT_BAD_ARG, "bad plan_ranked arrays");
+    if (mode < DOT_PLAN_POSITIONS || mode > DOT_PLAN_SLOTS)
+        return set_error(DOT_BAD_ARG, "plan_ranked: unknown mode %d", mode);
+    if (mode == DOT_PLAN_POOL_RAYS && !order) return set_error(DOT_BAD_ARG, "plan_ranked: POOL_RAYS needs order");
     if (n_pool > INT32_MAX || n_rays > INT32_MAX)
         return set_error(DOT_BAD_ARG, "plan_ranked: pool and batch must have < 2^31 rays");
-    if (workspace_bytes < int64_t(plan_ranked_workspace(n_pool, n_rays)))
+    if (workspace_bytes < int64_t(plan_ranked_workspace(n_pool, n_rays, mode)))
         return set_error(DOT_BAD_ARG, "plan_ranked: workspace of %lld bytes, %lld needed",
-                         (long long)workspace_bytes, (long long)plan_ranked_workspace(n_pool, n_rays));
+                         (long long)workspace_bytes, (long long)plan_ranked_workspace(n_pool, n_rays, mode));
     if (reinterpret_cast<uintptr_t>(workspace) & 255)
         return set_error(DOT_BAD_ARG, "plan_ranked: workspace must be 256-byte aligned");
-    return run_plan_ranked(rank, order, n_pool, ray_index, n_rays, workspace, sorted_index,
-                           static_cast<cudaStream_t>(stream));
+    if (warp_order && (!ray_cost || chunk < 1 || chunk > 4096))
+        return set_error(DOT_BAD_ARG, "plan_ranked: a warp order needs ray_cost and chunk in 1..4096");
+    return run_plan_ranked(rank, order, n_pool, ray_index, n_rays, mode, ray_cost, chunk, warp_order, workspace,
+                           sorted_index, static_cast<cudaStream_t>(stream));
 }
 
 int dot_ray_keys32(const dot_tree_view* tree, const double* origins, const double* dirs, int64_t n_pool,

@@ -54,9 +54,10 @@ int run_plan_sort(const int32_t* keys, const int64_t* ray_index, int64_t n, int 
                   int32_t* sorted_keys, int64_t* sorted_index, cudaStream_t s);
 int launch_gather_keys(const int32_t* pool_keys, const int64_t* ray_idx, int64_t n_pool, int64_t n, int32_t* keys,
                        cudaStream_t s);
-size_t plan_ranked_workspace(int64_t n_pool, int64_t n);
+size_t plan_ranked_workspace(int64_t n_pool, int64_t n, int mode);
 int run_plan_ranked(const int32_t* rank, const int32_t* order, int64_t n_pool, const int64_t* ray_idx, int64_t n,
-                    void* ws, int64_t* out, cudaStream_t s);
+                    int mode, const uint16_t* ray_cost, int chunk, int32_t* warp_order, void* ws, int64_t* out,
+                    cudaStream_t s);
 int launch_ray_keys32(const TreeDev& T, const double* o, const double* d, const int64_t* ray_idx,
                       int64_t n_pool, int64_t n, int32_t* keys, cudaStream_t s);
 int launch_render_cameras(const TreeDev& T, const double* cam_to_world, const double* focal, int n_views,

@@ -14,6 +14,14 @@ namespace dot {
 
 constexpr int kMaxPeers = DOT_MAX_PEERS;
 
+// shared-memory carveout preference of the update (-1: driver default).  A
+// non-zero carveout keeps shared memory configured on the SMs while the
+// update runs, so the plan's cooperative blocks (plan.cu) can be resident
+// beside it.
+#ifndef DOT_RMS_CARVEOUT
+#define DOT_RMS_CARVEOUT -1
+#endif
+
 __device__ __forceinline__ float rms_update(float theta, double& v, double g, double beta,
                                             double omb, double eps, double lr, bool clamp) {
     v = __dadd_rn(__dmul_rn(beta, v), __dmul_rn(__dmul_rn(omb, g), g));
@@ -294,6 +302,9 @@ extern "C" int dot_rmsprop_step(float* sigma, float* sh, int32_t sh_stride, int3
     const unsigned grid = unsigned((total + 255) / 256);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     if (vec) {
+#if DOT_RMS_CARVEOUT >= 0
+        cudaFuncSetAttribute(rmsprop_vec_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, DOT_RMS_CARVEOUT);
+#endif
         rmsprop_vec_kernel<<<grid, 256, 0, s>>>(sigma, sh, sh_stride, n_sh, v_sigma, v_sh, grad_sigma, grad_sh,
                                                 gsh_stride, touched, capacity, quads, beta, eps, lr_sigma, lr_sh,
                                                 (flags & 1) != 0);

@@ -436,8 +436,8 @@ class PoolRank:
     def tensors(self):
         return tuple(t for t in (self.rank, self.order) if t is not None)
 
-    def workspace(self, n: int, stream) -> torch.Tensor:
-        need = int(_lib.load().dot_plan_ranked_workspace(self.n_pool, n))
+    def workspace(self, n: int, stream, mode: int) -> torch.Tensor:
+        need = int(_lib.load().dot_plan_ranked_workspace(self.n_pool, n, mode))
         if self._ready is not None:
             stream.wait_event(self._ready)
         if self._ws is None or self._ws.numel() < need:
@@ -494,7 +494,8 @@ def ray_costs(tree: SparseOctree, origins: torch.Tensor, dirs: torch.Tensor, ear
 
 def plan_batch(tree: SparseOctree, origins: torch.Tensor, dirs: torch.Tensor, ray_index=None,
                stream=None, wait_current: bool = True, keys: torch.Tensor | None = None,
-               costs: torch.Tensor | None = None, rank: PoolRank | None = None) -> RayPlan:
+               costs: torch.Tensor | None = None, rank: PoolRank | None = None,
+               ids: torch.Tensor | None = None) -> RayPlan:
     """Coherence order of a batch (origin / octahedral-direction Morton keys,
     dot_ray_keys32 + a radix sort).  Depends only on the rays, so it can run
     on a side stream (``stream``) ahead of the step that consumes it; the
@@ -507,8 +508,12 @@ def plan_batch(tree: SparseOctree, origins: torch.Tensor, dirs: torch.Tensor, ra
     (``dot_sched_order_costs``) instead of the learned key-bucket table; the
     backward writes its fresh counts back into ``costs``.  ``rank``
     (``pool_rank``): order a batch of pool rays by the pool's 62-bit key rank
-    without a sort (``dot_plan_ranked``); the plan then carries no keys, so
-    its warp order comes only from ``costs``."""
+    without a sort (``dot_plan_ranked``, one cooperative launch that also
+    builds the warp order from ``costs``); the plan then carries no keys, so
+    its warp order comes only from ``costs``.  ``ids`` (with ``rank``): the
+    rays of ``origins`` / ``dirs`` ARE the batch (a staged batch) and ``ids``
+    their ids in the ranked dataset; the plan orders the batch's slots
+    (``costs``: one entry per slot)."""
     idx = None if ray_index is None else torch.as_tensor(ray_index, device=tree.device).reshape(-1).to(torch.int64)
     n = int(idx.shape[0]) if idx is not None else int(origins.shape[0])
     n_pool = int(origins.shape[0])
@@ -517,13 +522,25 @@ def plan_batch(tree: SparseOctree, origins: torch.Tensor, dirs: torch.Tensor, ra
                               or not costs.is_contiguous()):
         raise InputError(f"costs must be a contiguous int16 tensor with one entry per ray ({n_pool}) "
                          f"on {tree.device}")
+    mode = None
+    if ids is not None:
+        if rank is None or idx is not None:
+            raise InputError("plan_batch(ids=) needs rank= and no ray_index (the arrays are the batch)")
+        idx = torch.as_tensor(ids, device=tree.device).reshape(-1).to(torch.int64)
+        n = int(idx.shape[0])
+        if n != n_pool:
+            raise InputError(f"ids has {n} entries for a batch of {n_pool} rays")
+        mode = 2  # DOT_PLAN_SLOTS
     if rank is not None:
         if idx is None:
-            raise InputError("plan_batch(rank=) orders batches of a pool: pass ray_index")
+            raise InputError("plan_batch(rank=) orders batches of a pool: pass ray_index (or ids=)")
         if keys is not None:
             raise InputError("plan_batch: pass keys= or rank=, not both")
-        if not isinstance(rank, PoolRank) or rank.n_pool != n_pool or not _on_device(rank.device, tree.device):
+        if not isinstance(rank, PoolRank) or not _on_device(rank.device, tree.device) or \
+                (mode is None and rank.n_pool != n_pool):
             raise InputError(f"rank must be a PoolRank of this pool ({n_pool} rays) on {tree.device}")
+        if mode is None:
+            mode = 0 if rank.order is None else 1  # DOT_PLAN_POSITIONS / DOT_PLAN_POOL_RAYS
     view, _topo = tree.tree_view()
     cur = torch.cuda.current_stream(tree.device)
     s = stream or cur
@@ -536,11 +553,16 @@ def plan_batch(tree: SparseOctree, origins: torch.Tensor, dirs: torch.Tensor, ra
             if t is not None:
                 t.record_stream(s)
     with torch.cuda.stream(s):
+        ranked_order = None
         if rank is not None:
             order = torch.empty(n, dtype=torch.int64, device=tree.device)
-            ws = rank.workspace(n, s)
-            _lib.call("dot_plan_ranked", _lib.ptr(rank.rank), _lib.ptr(rank.order), n_pool, _lib.ptr(idx), n,
-                      _lib.ptr(ws), ws.numel(), _lib.ptr(order), _lib.stream_ptr(s))
+            ws = rank.workspace(n, s, mode)
+            if costs is not None and WARP_SCHED and 0 < n <= SCHED_MAX_RAYS:
+                # the warp launch order in the same launch
+                ranked_order = torch.empty((n + 31) // 32, dtype=torch.int32, device=tree.device)
+            _lib.call("dot_plan_ranked", _lib.ptr(rank.rank), _lib.ptr(rank.order), rank.n_pool, _lib.ptr(idx), n,
+                      mode, _lib.ptr(costs if ranked_order is not None else None), cost_chunk(n),
+                      _lib.ptr(ranked_order), _lib.ptr(ws), ws.numel(), _lib.ptr(order), _lib.stream_ptr(s))
             rank.done(s)
             idx, sorted_keys = order, None
         elif keys is not None:
@@ -563,8 +585,8 @@ def plan_batch(tree: SparseOctree, origins: torch.Tensor, dirs: torch.Tensor, ra
             idx = order
         # the warp launch order too, off the critical path: from the rays'
         # costs when given, else the learned table as of its last update
-        warp_order = None
-        if WARP_SCHED and 0 < n <= SCHED_MAX_RAYS:
+        warp_order = ranked_order
+        if warp_order is None and WARP_SCHED and 0 < n <= SCHED_MAX_RAYS:
             if costs is not None:
                 warp_order = torch.empty((n + 31) // 32, dtype=torch.int32, device=tree.device)
                 _lib.call("dot_sched_order_costs", _lib.ptr(costs), int(costs.shape[0]), _lib.ptr(idx), n, cost_chunk(n),

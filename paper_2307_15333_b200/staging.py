@@ -35,11 +35,12 @@ from .errors import InputError
 
 
 class _Slot:
-    __slots__ = ("bufs", "n", "ready", "free", "busy", "plan", "cost")
+    __slots__ = ("bufs", "n", "ready", "free", "busy", "plan", "cost", "ids")
 
     def __init__(self):
         self.bufs = None
         self.cost = None
+        self.ids = None
         self.plan = None
         self.n = 0
         self.ready = torch.cuda.Event()
@@ -50,14 +51,19 @@ class _Slot:
 class RayBatchStager:
     """Double-buffered (``depth`` slots) host->HBM staging of ray batches."""
 
-    def __init__(self, device, max_rays: int = 0, depth: int = 2, plan_tree=None):
+    def __init__(self, device, max_rays: int = 0, depth: int = 2, plan_tree=None, plan_rank=None):
         """``plan_tree``: also compute each staged batch's coherence order
         (render.plan_batch) on the copy stream right after its copy, so the
-        step that takes it skips the key sort (``take_with_plan``)."""
+        step that takes it skips the key sort (``take_with_plan``).
+        ``plan_rank`` (render.PoolRank of the host dataset, e.g.
+        ``pool_rank`` of its rays computed once): batches staged with their
+        dataset ``ids`` are ordered by the rank without a sort
+        (``dot_plan_ranked`` in slot mode)."""
         if depth < 2:
             raise InputError("depth must be >= 2 for copy/compute overlap")
         self.device = torch.device(device)
         self.plan_tree = plan_tree
+        self.plan_rank = plan_rank
         self.copy_stream = torch.cuda.Stream(self.device)
         self.slots = [_Slot() for _ in range(depth)]
         self.pending: deque[int] = deque()
@@ -75,6 +81,7 @@ class RayBatchStager:
             torch.cuda.current_stream(self.device).synchronize()
             slot.bufs = tuple(torch.empty(n, 3, dtype=torch.float64, device=self.device) for _ in range(3))
             slot.cost = torch.empty(n, dtype=torch.int16, device=self.device)
+            slot.ids = torch.empty(n, dtype=torch.int64, device=self.device)
 
     @staticmethod
     def _host(x, name: str) -> torch.Tensor:
@@ -86,11 +93,13 @@ class RayBatchStager:
             t = t.double()
         return t.contiguous()
 
-    def stage(self, origins, dirs, targets, costs=None) -> None:
+    def stage(self, origins, dirs, targets, costs=None, ids=None) -> None:
         """Queue the H2D copy of one batch on the copy stream (returns at once).
         ``costs`` (host int16 per ray, optional, e.g. a slice of
         ``render.ray_costs`` kept with the dataset): staged too and used for the
-        batch's warp launch order (``plan_batch(costs=)``)."""
+        batch's warp launch order (``plan_batch(costs=)``).  ``ids`` (host
+        int64 per ray, optional): the rays' dataset ids, staged too; with
+        ``plan_rank`` the batch is ordered by the dataset's rank."""
         o, d, t = (self._host(x, nm) for x, nm in ((origins, "origins"), (dirs, "dirs"), (targets, "targets")))
         n = o.shape[0]
         if d.shape[0] != n or t.shape[0] != n:
@@ -100,6 +109,11 @@ class RayBatchStager:
             c = costs if isinstance(costs, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(costs))
             if c.device.type != "cpu" or c.dtype != torch.int16 or c.numel() != n:
                 raise InputError("costs must be a host int16 tensor with one entry per ray")
+        ih = None
+        if ids is not None:
+            ih = ids if isinstance(ids, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(ids))
+            if ih.device.type != "cpu" or ih.dtype != torch.int64 or ih.numel() != n:
+                raise InputError("ids must be a host int64 tensor with one entry per ray")
         i = self.next_slot
         slot = self.slots[i]
         if slot.busy:
@@ -112,16 +126,21 @@ class RayBatchStager:
                 dst[:n].copy_(src, non_blocking=True)
             if c is not None:
                 slot.cost[:n].copy_(c.reshape(-1), non_blocking=True)
+            if ih is not None:
+                slot.ids[:n].copy_(ih.reshape(-1), non_blocking=True)
             slot.plan = None
             if self.plan_tree is not None:
                 from .render import plan_batch
+                ranked = self.plan_rank is not None and ih is not None
                 slot.plan = plan_batch(self.plan_tree, slot.bufs[0][:n], slot.bufs[1][:n],
                                        stream=self.copy_stream, wait_current=False,
-                                       costs=slot.cost[:n] if c is not None else None)
+                                       costs=slot.cost[:n] if c is not None else None,
+                                       rank=self.plan_rank if ranked else None,
+                                       ids=slot.ids[:n] if ranked else None)
             slot.ready.record(self.copy_stream)
         slot.n = n
         slot.busy = True
-        self.bytes_staged += 3 * n * 24 + (2 * n if c is not None else 0)
+        self.bytes_staged += 3 * n * 24 + (2 * n if c is not None else 0) + (8 * n if ih is not None else 0)
         self.pending.append(i)
         self.next_slot = (i + 1) % len(self.slots)
 

@@ -313,13 +313,101 @@ def _plan_ranked(rank, order, idx, ws=None, n_pool=None):
     import torch
     from paper_2307_15333_b200 import _lib
     n_pool, n = (rank.shape[0] if n_pool is None else n_pool), idx.shape[0]
-    need = _lib.load().dot_plan_ranked_workspace(n_pool, n)
-    if ws is None:
+    mode = 1 if order is not None else 0
+    need = _lib.load().dot_plan_ranked_workspace(n_pool, n, mode)
+    if ws is None or ws.numel() < need:
         ws = torch.zeros(need, dtype=torch.uint8, device="cuda")
     out = torch.full((n,), -7, dtype=torch.int64, device="cuda")
-    _lib.call("dot_plan_ranked", _lib.ptr(rank), _lib.ptr(order), n_pool, _lib.ptr(idx), n, _lib.ptr(ws),
-              ws.numel(), _lib.ptr(out), _lib.stream_ptr())
+    _lib.call("dot_plan_ranked", _lib.ptr(rank), _lib.ptr(order), n_pool, _lib.ptr(idx), n, mode, None, 1, None,
+              _lib.ptr(ws), ws.numel(), _lib.ptr(out), _lib.stream_ptr())
     return out, ws
+
+
+def _a256(b):
+    return (b + 255) // 256 * 256
+
+
+def _plan_scratch_clear(ws, n_pool, n):
+    """The bitmap, counter and warp-cost regions of a plan workspace are zero."""
+    words = (n_pool + 31) // 32
+    at_extra = _a256(4 * words) + _a256(4 * ((words + 1023) // 1024 + 1))
+    at_wc = at_extra + 256 + _a256(8 * n)
+    nw = (n + 31) // 32
+    return (not bool(ws[: 4 * words].any()) and not bool(ws[at_extra: at_extra + 8].any())
+            and not bool(ws[at_wc: at_wc + 4 * nw].any()))
+
+
+def _check_warp_order(order, costs_of_slots, n, chunk):
+    """A permutation of the warps; full chunks by non-increasing max cost
+    (capped at 1023), a short last chunk last."""
+    nw = (n + 31) // 32
+    od = order.cpu().numpy()
+    assert np.array_equal(np.sort(od), np.arange(nw))
+    pad = np.zeros(nw * 32, dtype=np.int64)
+    pad[:n] = costs_of_slots
+    wc = np.minimum(pad.reshape(nw, 32).max(1), 1023)
+    nfull = nw // chunk
+    cc = wc[: nfull * chunk].reshape(nfull, chunk).max(1)
+    firsts = od[: nfull * chunk: chunk]
+    assert np.all(firsts % chunk == 0)
+    for k in range(chunk):  # chunks stay contiguous
+        assert np.array_equal(od[k: nfull * chunk: chunk], firsts + k)
+    assert np.all(np.diff(cc[firsts // chunk]) <= 0)
+    assert np.array_equal(od[nfull * chunk:], np.arange(nfull * chunk, nw))
+
+
+def test_plan_ranked_warp_order():
+    """dot_plan_ranked's fused warp order (warp costs gathered while placing)
+    is the cost-ordered launch of dot_sched_order_costs for the same plan,
+    for chunk 1 and 16, with a short last warp / chunk; its warp-cost
+    scratch is left zeroed."""
+    import torch
+    from paper_2307_15333_b200 import _lib
+    g = torch.Generator(device="cuda")
+    g.manual_seed(12)
+    n_pool = 400_003
+    order = torch.randperm(n_pool, generator=g, device="cuda").to(torch.int32)
+    rank = torch.empty(n_pool, dtype=torch.int32, device="cuda")
+    rank[order.long()] = torch.arange(n_pool, dtype=torch.int32, device="cuda")
+    costs = torch.randint(0, 1400, (n_pool,), generator=g, device="cuda").to(torch.int16)
+    for n, chunk in ((70_001, 1), (70_001, 16), (65_536, 16), (333, 1)):
+        for ordr in (order, None):
+            idx = torch.randperm(n_pool, generator=g, device="cuda")[:n]
+            mode = 1 if ordr is not None else 0
+            need = _lib.load().dot_plan_ranked_workspace(n_pool, n, mode)
+            ws = torch.zeros(need, dtype=torch.uint8, device="cuda")
+            out = torch.empty(n, dtype=torch.int64, device="cuda")
+            wo = torch.full(((n + 31) // 32,), -1, dtype=torch.int32, device="cuda")
+            for rep in range(2):  # the second call on the returned workspace
+                _lib.call("dot_plan_ranked", _lib.ptr(rank), _lib.ptr(ordr), n_pool, _lib.ptr(idx), n, mode,
+                          _lib.ptr(costs), chunk, _lib.ptr(wo), _lib.ptr(ws), ws.numel(), _lib.ptr(out),
+                          _lib.stream_ptr())
+                torch.cuda.synchronize()
+                _check_warp_order(wo, costs[out].long().cpu().numpy(), n, chunk)
+                assert _plan_scratch_clear(ws, n_pool, n), "scratch not left zeroed"
+    # slots of a staged batch: ids name its rays in the ranked dataset, the
+    # warp costs come per slot
+    for n in (1, 4097, 70_001):
+        ids = torch.randperm(n_pool, generator=g, device="cuda")[:n]
+        slot_cost = torch.randint(0, 1400, (n,), generator=g, device="cuda").to(torch.int16)
+        need = _lib.load().dot_plan_ranked_workspace(n_pool, n, 2)
+        ws = torch.zeros(need, dtype=torch.uint8, device="cuda")
+        out = torch.empty(n, dtype=torch.int64, device="cuda")
+        wo = torch.empty((n + 31) // 32, dtype=torch.int32, device="cuda")
+        _lib.call("dot_plan_ranked", _lib.ptr(rank), None, n_pool, _lib.ptr(ids), n, 2, _lib.ptr(slot_cost), 1,
+                  _lib.ptr(wo), _lib.ptr(ws), ws.numel(), _lib.ptr(out), _lib.stream_ptr())
+        torch.cuda.synchronize()
+        assert torch.equal(out, torch.sort(rank[ids].long()).indices)
+        _check_warp_order(wo, slot_cost[out].long().cpu().numpy(), n, 1)
+        assert _plan_scratch_clear(ws, n_pool, n)
+    # bad arguments are refused
+    from paper_2307_15333_b200.errors import InputError
+    with pytest.raises(InputError):
+        _lib.call("dot_plan_ranked", _lib.ptr(rank), None, n_pool, _lib.ptr(ids), n, 1, None, 1, None,
+                  _lib.ptr(ws), ws.numel(), _lib.ptr(out), _lib.stream_ptr())  # POOL_RAYS without order
+    with pytest.raises(InputError):
+        _lib.call("dot_plan_ranked", _lib.ptr(rank), None, n_pool, _lib.ptr(ids), n, 2, None, 1, None,
+                  _lib.ptr(ws), 64, _lib.ptr(out), _lib.stream_ptr())  # workspace too small
 
 
 def test_plan_ranked_counting_sort():
@@ -348,8 +436,7 @@ def test_plan_ranked_counting_sort():
             out, ws = _plan_ranked(None, None, idx, ws, n_pool=n_pool)
             assert torch.equal(out, torch.sort(idx).values)
             torch.cuda.synchronize()
-            words = (n_pool + 31) // 32
-            assert not bool(ws[: 4 * words].any()), "bitmap not cleared"
+            assert _plan_scratch_clear(ws, n_pool, n), "bitmap not cleared"
     # repeats and invalid indices
     n_pool = 5000
     order = torch.randperm(n_pool, generator=g, device="cuda").to(torch.int32)

@@ -12,7 +12,8 @@ sys.path.insert(0, ROOT)
 def main():
     import torch
     out = os.path.join(ROOT, "gpurun_out", "trace.json")
-    env = dict(os.environ, DOT_TRACE=out)
+    # --e2e: the host-fed (staged) loop instead of the resident-pool steps
+    env = dict(os.environ, **({"DOT_TRACE_E2E": out} if "--e2e" in sys.argv else {"DOT_TRACE": out}))
     subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--steps", "10", "--warmup", "3",
                     "--skip-render", "--skip-refine", "--skip-cpu"], env=env, check=True,
                    stdout=subprocess.DEVNULL)
@@ -37,7 +38,8 @@ def main():
     if len(bw) > 6:
         a, b = bw[5]["ts"], bw[6]["ts"]
         print("one step (us from its backward's start): stream  start  end  kernel")
-        for e in k:
+        cp = [e for e in ev if e.get("cat") in ("gpu_memcpy", "gpu_memset")]
+        for e in sorted(k + cp, key=lambda e: e["ts"]):
             if a - 300 <= e["ts"] < b:
                 print(f"  {e.get('args', {}).get('stream', '?'):>4} {e['ts'] - a:8.0f} {e['ts'] + e['dur'] - a:8.0f}  "
                       f"{e['name'].split('(')[0][:60]}")
