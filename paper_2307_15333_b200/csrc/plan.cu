@@ -33,13 +33,13 @@
 // memory-level parallelism: fire-and-forget REDs / stores where a return
 // value is not needed, 8 gathers in flight per thread, per-warp bitmap
 // ranges (no block barriers), one gather per placed ray in slot mode (the
-// slot and its cost packed in the position's tag).
+// slot and its cost packed in the position's tag, the only per-ray store).
 //
 // Rays the bitmap cannot place -- a repeated ray (another lane won its
 // position's tag) or an index outside [0, n_pool) -- follow the placed
 // ones, so the output is always a permutation of the batch and the backward
 // still sees (and reports) invalid indices.  Repeats are detected from the
-// placed count (a second pass runs only then).  The workspace is left
+// placed count (a second pass over the batch runs only then).  The workspace is left
 // reusable (bitmap, warp costs, histogram and counters zero).
 #include <cooperative_groups.h>
 
@@ -67,7 +67,8 @@ struct PlanWs {
     uint32_t* warp_cost;          // [ceil(n / 32)] max cost of each output warp
     uint16_t* chunk_cost;         // [ceil(n / 32)]
     int32_t* hist;                // [kPlanCostBins] chunks per cost bin, then their start chunks
-    int32_t* tag;                 // [n_pool] per marked position: batch index i (| cost << 21 when packed)
+    int32_t* tag;                 // [n_pool] slot mode: each marked position's slot (| cost << 21 when packed)
+    uint32_t* claim;              // [words] repeated rays outside slot mode: first claimant per position
 };
 
 __host__ __device__ static int64_t plan_words(int64_t n_pool) { return (n_pool + 31) / 32; }
@@ -95,6 +96,8 @@ static size_t carve(void* ws, int64_t n_pool, int64_t n, PlanWs* out) {
     p += align256(size_t(kPlanCostBins) * 4);
     w.tag = reinterpret_cast<int32_t*>(p);
     p += align256(size_t(n_pool) * 4);
+    w.claim = reinterpret_cast<uint32_t*>(p);
+    p += align256(size_t(plan_words(n_pool)) * 4);
     if (out) *out = w;
     return size_t(p - base);
 }
@@ -211,7 +214,8 @@ __global__ void __launch_bounds__(kPlanThreads, kPlanMinBlocks) plan_coop_kernel
                 continue;
             }
             red_or(w.bitmap + (uint32_t(k[u]) >> 5), 1u << (uint32_t(k[u]) & 31u));
-            w.tag[k[u]] = int32_t(a.packed ? (uint32_t(i) | (cst[u] << kTagSlotBits)) : uint32_t(i));
+            if (a.mode == DOT_PLAN_SLOTS)  // the position's slot (and cost): the only per-ray write
+                w.tag[k[u]] = int32_t(a.packed ? (uint32_t(i) | (cst[u] << kTagSlotBits)) : uint32_t(i));
         }
     }
     grid.sync();
@@ -247,16 +251,30 @@ __global__ void __launch_bounds__(kPlanThreads, kPlanMinBlocks) plan_coop_kernel
     }
     const int64_t invalid = int64_t(w.ctr[1]);
     if (placed + invalid < a.n) {
-        // repeated rays (grid-uniform branch): the one whose index the tag
-        // holds is placed, the others follow the placed rays
+        // repeated rays (grid-uniform branch, rare): one ray per position is
+        // placed -- in slot mode the one whose slot the tag holds, otherwise
+        // the first to claim the position in a second bitmap (cleared after)
+        // -- and the others follow the placed rays
         for (int64_t i = gt; i < a.n; i += GT) {
-            const int64_t k = plan_key(a, __ldg(a.ray_idx + i));
+            const int64_t r = __ldg(a.ray_idx + i);
+            const int64_t k = plan_key(a, r);
             if (k < 0) continue;
-            const uint32_t t = uint32_t(w.tag[k]);
-            const int64_t owner = a.packed ? int64_t(t & ((1u << kTagSlotBits) - 1u)) : int64_t(t);
-            if (owner != i) plan_append(w, a.mode == DOT_PLAN_SLOTS ? i : __ldg(a.ray_idx + i));
+            bool mine;
+            if (a.mode == DOT_PLAN_SLOTS) {
+                const uint32_t t = uint32_t(w.tag[k]);
+                mine = (a.packed ? int64_t(t & ((1u << kTagSlotBits) - 1u)) : int64_t(t)) == i;
+            } else {
+                const uint32_t bit = 1u << (uint32_t(k) & 31u);
+                mine = (atomicOr(w.claim + (k >> 5), bit) & bit) == 0u;
+            }
+            if (!mine) plan_append(w, a.mode == DOT_PLAN_SLOTS ? i : r);
         }
         grid.sync();
+        if (a.mode != DOT_PLAN_SLOTS)
+            for (int64_t i = gt; i < a.n; i += GT) {
+                const int64_t k = plan_key(a, __ldg(a.ray_idx + i));
+                if (k >= 0) w.claim[k >> 5] = 0u;
+            }
     }
     PLAN_STAMP(3)
 
