@@ -493,18 +493,31 @@ def run_ours(args, rank, world, local_rank):
     stager = RayBatchStager(dev, max_rays=per_rank, plan_tree=tree,
                             plan_rank=PoolRank.identity(n_pool, dev) if e2e_ranked else None)
 
+    hostprof = os.environ.get("DOT_E2E_HOSTPROF") == "1"  # diagnostic: host seconds per loop phase
+
     def staged_loop(steps):
         reader = LossReader()
         stager.stage(*host[0])
+        hp = [0.0] * 5
         for k in range(steps):
+            c0 = time.perf_counter()
             o_d, d_d, t_d, plan = stager.take_with_plan()
+            c1 = time.perf_counter()
             if k + 1 < steps:
                 stager.stage(*host[(k + 1) % len(host)])
+            c2 = time.perf_counter()
             loss = train_step(tree, o_d, d_d, t_d, state, buf, sws, BG, EPS, grad_scale=gs,
                               exchange=ex, plan=plan)
+            c3 = time.perf_counter()
             stager.release()
             reader.push(loss)
+            c4 = time.perf_counter()
+            for j, dt in enumerate((c1 - c0, c2 - c1, c3 - c2, c4 - c3, c4 - c0)):
+                hp[j] += dt
         reader.flush()
+        if hostprof and steps > 5:
+            print("e2e host ms/step: take %.3f stage %.3f train_step %.3f release+push(wait) %.3f total %.3f"
+                  % tuple(1e3 * x / steps for x in hp), file=sys.stderr)
         return reader.values
 
     def timed(loop):

@@ -183,11 +183,17 @@ class LossReader:
         self.events = [torch.cuda.Event(), torch.cuda.Event()]
         self.k = 0
         self.values: list[float] = []
+        self.stream = None  # the 8-byte copies run on their own stream, off the compute queue
 
     def push(self, loss: torch.Tensor):
         j = self.k % 2
-        self.host[j].copy_(loss.detach().reshape(()), non_blocking=True)
-        self.events[j].record()
+        if self.stream is None:
+            self.stream = torch.cuda.Stream(loss.device)
+        self.stream.wait_stream(torch.cuda.current_stream(loss.device))
+        with torch.cuda.stream(self.stream):
+            self.host[j].copy_(loss.detach().reshape(()), non_blocking=True)
+            self.events[j].record(self.stream)
+        loss.record_stream(self.stream)
         prev = None
         if self.k > 0:
             p = (self.k - 1) % 2
