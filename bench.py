@@ -644,11 +644,12 @@ def run_ours(args, rank, world, local_rank):
                      + "; per-ray schedule costs (render.ray_costs; refreshed by every backward); the "
                        "rank / keys and costs computed once at setup; warps launched longest first by cost"),
         },
-        # per step: the plan (rank: mark + count + scan + place; keys:
-        # gather + radix sort histogram + exclusive sum + 4 onesweep passes),
-        # the cost order (warp cost + histogram + scan + place), the backward
-        # and one rmsprop per all-reduce chunk (a single update at N = 1)
-        "gpu_launches": ((4 if plan_kind.startswith("rank") else 7) + 4 + 1
+        # per step: the plan (rank: one cooperative plan_coop_kernel incl.
+        # the warp order; keys: gather + radix sort histogram + exclusive sum
+        # + 4 onesweep passes, then the cost order's warp cost + histogram +
+        # scan + place), the backward and one rmsprop per all-reduce chunk (a
+        # single update at N = 1)
+        "gpu_launches": ((1 if plan_kind.startswith("rank") else 7 + 4) + 1
                          + (1 if world == 1 else len(chunk_bounds(tree.capacity, args.ar_chunks)))) * args.steps,
         "roofline": {
             "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",

@@ -13,7 +13,7 @@ DOT_PROFILE_RANGE=1 timeout 300 $CMD > $OUT/plain.log 2>&1 && \
 DOT_PROFILE_RANGE=1 timeout 600 ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none \
     --csv --log-file $OUT/launches.csv $CMD > $OUT/ncu_list.log 2>&1
 DOT_PROFILE_RANGE=1 timeout 900 ncu --profile-from-start off --set full --clock-control none --import-source on \
-    -k regex:"render_bwd_buffered|rmsprop" -c 2 -o $OUT/full -f $CMD > $OUT/ncu_full.log 2>&1
+    -k regex:"render_bwd_buffered|rmsprop|plan_coop" -c 3 -o $OUT/full -f $CMD > $OUT/ncu_full.log 2>&1
 RCMD="python bench.py --steps 3 --warmup 3 --skip-cpu --skip-refine"
 timeout 600 $RCMD > $OUT/plain_render.log 2>&1 && \
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:render_camera_kernel -s 3 -c 1 \
