@@ -507,7 +507,7 @@ def run_ours(args, rank, world, local_rank):
                 stager.stage(*host[(k + 1) % len(host)])
             c2 = time.perf_counter()
             loss = train_step(tree, o_d, d_d, t_d, state, buf, sws, BG, EPS, grad_scale=gs,
-                              exchange=ex, plan=plan)
+                              exchange=ex, plan=plan, after_backward=stager.plan_next)
             c3 = time.perf_counter()
             stager.release()
             reader.push(loss)

@@ -262,9 +262,12 @@ int dot_plan_sort(const int32_t* keys, const int64_t* ray_index, int64_t n_rays,
  * sorted_index is always a permutation of the batch.  warp_order
  * (optional, [ceil(n_rays / 32)]): the backward's warp launch order from
  * ray_cost (u16, indexed by sorted_index's values: [n_pool] for positions /
- * pool rays, [n_rays] for slots): chunks of `chunk` consecutive warps by
- * descending max cost, a short last chunk last -- what
- * dot_sched_order_costs gives for sorted_index.  One cooperative launch
+ * pool rays, [n_rays] for slots): sorted_index is then also regrouped --
+ * inside each window of 128 slots the rays are re-sorted by cost
+ * (descending, ties in key order) so each warp holds rays of similar
+ * length -- and the warps are ordered in chunks of `chunk` consecutive
+ * warps by descending max cost, a short last chunk last (what
+ * dot_sched_order_costs gives for the regrouped sorted_index).  One cooperative launch
  * (one block per SM).  workspace: dot_plan_ranked_workspace(n_pool,
  * n_rays, mode) bytes, 256-byte aligned, ZEROED before its first use;
  * every call leaves it reusable.  Calls sharing a workspace must be

@@ -509,8 +509,9 @@ def plan_batch(tree: SparseOctree, origins: torch.Tensor, dirs: torch.Tensor, ra
     backward writes its fresh counts back into ``costs``.  ``rank``
     (``pool_rank``): order a batch of pool rays by the pool's 62-bit key rank
     without a sort (``dot_plan_ranked``, one cooperative launch that also
-    builds the warp order from ``costs``); the plan then carries no keys, so
-    its warp order comes only from ``costs``.  ``ids`` (with ``rank``): the
+    builds the warp order from ``costs`` and regroups the rays by cost inside
+    128-ray windows, so each warp holds rays of similar length); the plan
+    then carries no keys, so its warp order comes only from ``costs``.  ``ids`` (with ``rank``): the
     rays of ``origins`` / ``dirs`` ARE the batch (a staged batch) and ``ids``
     their ids in the ranked dataset; the plan orders the batch's slots
     (``costs``: one entry per slot)."""

@@ -35,12 +35,14 @@ from .errors import InputError
 
 
 class _Slot:
-    __slots__ = ("bufs", "n", "ready", "free", "busy", "plan", "cost", "ids")
+    __slots__ = ("bufs", "n", "ready", "free", "busy", "plan", "cost", "ids", "meta", "plan_args")
 
     def __init__(self):
         self.bufs = None
         self.cost = None
         self.ids = None
+        self.meta = torch.cuda.Event()  # costs and ids copied (all a ranked plan reads)
+        self.plan_args = None           # a plan not launched yet (plan_next / take_with_plan)
         self.plan = None
         self.n = 0
         self.ready = torch.cuda.Event()
@@ -64,6 +66,7 @@ class RayBatchStager:
         self.device = torch.device(device)
         self.plan_tree = plan_tree
         self.plan_rank = plan_rank
+        self.plan_stream = None
         self.copy_stream = torch.cuda.Stream(self.device)
         self.slots = [_Slot() for _ in range(depth)]
         self.pending: deque[int] = deque()
@@ -119,30 +122,54 @@ class RayBatchStager:
         if slot.busy:
             raise InputError("all staging slots are in flight: take()/release() before staging more")
         self._ensure(slot, n)
+        ranked = self.plan_tree is not None and self.plan_rank is not None and ih is not None
         with torch.cuda.stream(self.copy_stream):
             if slot.free is not None:
                 self.copy_stream.wait_event(slot.free)  # the last step reading this slot is done
-            for dst, src in zip(slot.bufs, (o, d, t)):
-                dst[:n].copy_(src, non_blocking=True)
+            # costs and ids first: a ranked plan needs only them
             if c is not None:
                 slot.cost[:n].copy_(c.reshape(-1), non_blocking=True)
             if ih is not None:
                 slot.ids[:n].copy_(ih.reshape(-1), non_blocking=True)
+            slot.meta.record(self.copy_stream)
+            for dst, src in zip(slot.bufs, (o, d, t)):
+                dst[:n].copy_(src, non_blocking=True)
             slot.plan = None
-            if self.plan_tree is not None:
-                from .render import plan_batch
-                ranked = self.plan_rank is not None and ih is not None
-                slot.plan = plan_batch(self.plan_tree, slot.bufs[0][:n], slot.bufs[1][:n],
-                                       stream=self.copy_stream, wait_current=False,
-                                       costs=slot.cost[:n] if c is not None else None,
-                                       rank=self.plan_rank if ranked else None,
-                                       ids=slot.ids[:n] if ranked else None)
+            slot.plan_args = (n, c is not None, ranked) if self.plan_tree is not None else None
+            if self.plan_tree is not None and not ranked:  # key sort: needs the rays, right after the copy
+                self._launch_plan(slot, self.copy_stream)
             slot.ready.record(self.copy_stream)
         slot.n = n
         slot.busy = True
         self.bytes_staged += 3 * n * 24 + (2 * n if c is not None else 0) + (8 * n if ih is not None else 0)
         self.pending.append(i)
         self.next_slot = (i + 1) % len(self.slots)
+
+    def _launch_plan(self, slot: _Slot, stream, wait_current: bool = False) -> None:
+        from .render import plan_batch
+        n, has_cost, ranked = slot.plan_args
+        slot.plan_args = None
+        slot.plan = plan_batch(self.plan_tree, slot.bufs[0][:n], slot.bufs[1][:n], stream=stream,
+                               wait_current=wait_current, costs=slot.cost[:n] if has_cost else None,
+                               rank=self.plan_rank if ranked else None, ids=slot.ids[:n] if ranked else None)
+
+    def plan_next(self) -> None:
+        """Launch the ranked plan of the most recently staged batch now, on the
+        stager's plan stream, ordered after the work queued so far on the
+        current stream and after the batch's costs / ids copies.  Call it once
+        the current step's backward is queued (``train_step(after_backward=
+        stager.plan_next)``): the plan then runs beside the optimizer update
+        instead of the backward.  Without it ``take_with_plan`` launches the
+        plan itself."""
+        if not self.pending:
+            return
+        slot = self.slots[self.pending[-1]]
+        if slot.plan_args is None:
+            return
+        if self.plan_stream is None:
+            self.plan_stream = torch.cuda.Stream(self.device)
+        self.plan_stream.wait_event(slot.meta)
+        self._launch_plan(slot, self.plan_stream, wait_current=True)
 
     def take(self):
         """Device (origins, dirs, targets) of the oldest staged batch; the
@@ -158,6 +185,12 @@ class RayBatchStager:
     def take_with_plan(self):
         """``take()`` plus the batch's coherence plan (None without plan_tree)."""
         i = self.pending[0] if self.pending else None
+        if i is not None and self.slots[i].plan_args is not None:  # not launched by plan_next
+            slot = self.slots[i]
+            with torch.cuda.stream(self.copy_stream):
+                self.copy_stream.wait_event(slot.meta)
+                self._launch_plan(slot, self.copy_stream)
+                slot.ready.record(self.copy_stream)
         out = self.take()
         return out + (self.slots[i].plan,)
 

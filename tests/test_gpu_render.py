@@ -337,6 +337,29 @@ def _plan_scratch_clear(ws, n_pool, n):
             and not bool(ws[at_wc: at_wc + 4 * nw].any()))
 
 
+def _cost_bucket(c):
+    """plan.cu cost_bucket: three log-scale buckets per octave of cost + 1."""
+    import torch
+    x = c + 1
+    m = torch.floor(torch.log2(x.double())).long()
+    m = torch.where((1 << (m + 1)) <= x, m + 1, m)  # exact floor(log2) for integers
+    m = torch.where((1 << m) > x, m - 1, m)
+    return 3 * m + ((3 * x) >> m) - 3
+
+
+def _regrouped(key_ordered, cost_of, window=128):
+    """The plan's output with a cost column: inside each window of 128 slots
+    the key-ordered rays stably partitioned by cost bucket (costs capped at
+    1023), costliest first."""
+    import torch
+    bucket = _cost_bucket(torch.clamp(cost_of(key_ordered).long(), max=1023))
+    out = key_ordered.clone()
+    for b in range(0, key_ordered.numel(), window):
+        order = torch.sort(-bucket[b:b + window], stable=True).indices
+        out[b:b + window] = key_ordered[b:b + window][order]
+    return out
+
+
 def _check_warp_order(order, costs_of_slots, n, chunk):
     """A permutation of the warps; full chunks by non-increasing max cost
     (capped at 1023), a short last chunk last."""
@@ -378,11 +401,16 @@ def test_plan_ranked_warp_order():
             ws = torch.zeros(need, dtype=torch.uint8, device="cuda")
             out = torch.empty(n, dtype=torch.int64, device="cuda")
             wo = torch.full(((n + 31) // 32,), -1, dtype=torch.int32, device="cuda")
+            keyed = torch.sort(rank[idx].long()).values
+            if ordr is not None:
+                keyed = ordr[keyed].long()
+            want = _regrouped(keyed, lambda v: costs[v])
             for rep in range(2):  # the second call on the returned workspace
                 _lib.call("dot_plan_ranked", _lib.ptr(rank), _lib.ptr(ordr), n_pool, _lib.ptr(idx), n, mode,
                           _lib.ptr(costs), chunk, _lib.ptr(wo), _lib.ptr(ws), ws.numel(), _lib.ptr(out),
                           _lib.stream_ptr())
                 torch.cuda.synchronize()
+                assert torch.equal(out, want), "not the key order regrouped by cost in 128-ray windows"
                 _check_warp_order(wo, costs[out].long().cpu().numpy(), n, chunk)
                 assert _plan_scratch_clear(ws, n_pool, n), "scratch not left zeroed"
     # slots of a staged batch: ids name its rays in the ranked dataset, the
@@ -397,7 +425,7 @@ def test_plan_ranked_warp_order():
         _lib.call("dot_plan_ranked", _lib.ptr(rank), None, n_pool, _lib.ptr(ids), n, 2, _lib.ptr(slot_cost), 1,
                   _lib.ptr(wo), _lib.ptr(ws), ws.numel(), _lib.ptr(out), _lib.stream_ptr())
         torch.cuda.synchronize()
-        assert torch.equal(out, torch.sort(rank[ids].long()).indices)
+        assert torch.equal(out, _regrouped(torch.sort(rank[ids].long()).indices, lambda v: slot_cost[v]))
         _check_warp_order(wo, slot_cost[out].long().cpu().numpy(), n, 1)
         assert _plan_scratch_clear(ws, n_pool, n)
     # bad arguments are refused
@@ -491,7 +519,10 @@ def test_pool_rank_plans_match_sorted_plans():
             p.wait()
             assert p.sorted_keys is None
             want = torch.sort(pr.rank[idx].long()).values
-            assert torch.equal(p.idx, want if permuted else pr.order[want].long())
+            keyed = want if permuted else pr.order[want].long()
+            if "costs" in kw:  # regrouped by cost inside 128-ray windows
+                keyed = _regrouped(keyed, lambda v: kw["costs"][v])
+            assert torch.equal(p.idx, keyed)
             assert (p.warp_order is not None) == ("costs" in kw)
         ws = BackpropWorkspace.for_tree(tree)
         results.append(render_and_backprop(tree, oo, dd, tt, 0.5, ray_index=ii, workspace=ws, plan=p))
