@@ -357,6 +357,10 @@ def run_ours(args, rank, world, local_rank):
     # and its per-ray schedule costs (the first epoch's prediction; every
     # backward refreshes its rays' entries): warps launch longest first
     pcosts = ray_costs(tree, origins, dirs, EPS) if os.environ.get("DOT_BENCH_COSTS", "1") == "1" else None
+    # the plans' outputs in a ring (no allocation on the plan's path; at most
+    # LEAD = 2 steps are in flight, so a buffer is free again 4 plans later)
+    plan_ring = [(torch.empty(per_rank, dtype=torch.int64, device=dev),
+                  torch.empty((per_rank + 31) // 32, dtype=torch.int32, device=dev)) for _ in range(4)]
     if plan_kind == "rank":
         from paper_2307_15333_b200.render import PoolRank
         origins, dirs, targets, pcosts = prank.permute(origins, dirs, targets, pcosts)
@@ -373,7 +377,8 @@ def run_ours(args, rank, world, local_rank):
         def next_plan():
             if k + 1 < total_steps + 2:
                 plans[k + 1] = plan_batch(tree, origins, dirs, batch_index(k + 1), stream=plan_stream,
-                                          keys=pkeys, rank=prank, costs=pcosts)
+                                          keys=pkeys, rank=prank, costs=pcosts,
+                                          out=plan_ring[(k + 1) % len(plan_ring)] if prank is not None else None)
         # the next plan is queued behind this step's backward, so it runs
         # beside the (bandwidth-bound) update instead of the backward;
         # DOT_PLAN_EARLY=1: queued before the step (runs beside the backward)
@@ -498,7 +503,32 @@ def run_ours(args, rank, world, local_rank):
     def staged_loop(steps):
         reader = LossReader()
         stager.stage(*host[0])
-        hp = [0.0] * 5
+        hp = [0.0] * 6
+        worst = [0.0] * 6
+        call_worst = {}
+        if hostprof:  # the worst host time of each C-ABI call made inside plan_next
+            from paper_2307_15333_b200 import _lib as lib_mod
+            real_call = lib_mod.call
+
+            def timed_call(name, *a):
+                c = time.perf_counter()
+                r = real_call(name, *a)
+                call_worst[name] = max(call_worst.get(name, 0.0), time.perf_counter() - c)
+                return r
+            lib_mod.call = timed_call
+
+        import cProfile
+        cprof = cProfile.Profile() if os.environ.get("DOT_E2E_CPROFILE") == "1" else None
+
+        def plan_next_timed():
+            c = time.perf_counter()
+            if cprof:
+                cprof.enable()
+            stager.plan_next()
+            if cprof:
+                cprof.disable()
+            hp[5] += time.perf_counter() - c
+            worst[5] = max(worst[5], time.perf_counter() - c)
         for k in range(steps):
             c0 = time.perf_counter()
             o_d, d_d, t_d, plan = stager.take_with_plan()
@@ -507,17 +537,27 @@ def run_ours(args, rank, world, local_rank):
                 stager.stage(*host[(k + 1) % len(host)])
             c2 = time.perf_counter()
             loss = train_step(tree, o_d, d_d, t_d, state, buf, sws, BG, EPS, grad_scale=gs,
-                              exchange=ex, plan=plan, after_backward=stager.plan_next)
+                              exchange=ex, plan=plan,
+                              after_backward=plan_next_timed if hostprof else stager.plan_next)
             c3 = time.perf_counter()
             stager.release()
             reader.push(loss)
             c4 = time.perf_counter()
             for j, dt in enumerate((c1 - c0, c2 - c1, c3 - c2, c4 - c3, c4 - c0)):
                 hp[j] += dt
+                worst[j] = max(worst[j], dt)
         reader.flush()
         if hostprof and steps > 5:
-            print("e2e host ms/step: take %.3f stage %.3f train_step %.3f release+push(wait) %.3f total %.3f"
-                  % tuple(1e3 * x / steps for x in hp), file=sys.stderr)
+            print("e2e host ms/step: take %.3f stage %.3f train_step %.3f release+push(wait) %.3f total %.3f "
+                  "(plan_next inside train_step %.3f)" % tuple(1e3 * x / steps for x in hp), file=sys.stderr)
+            print("e2e host worst ms: take %.3f stage %.3f train_step %.3f release+push(wait) %.3f total %.3f "
+                  "plan_next %.3f" % tuple(1e3 * x for x in worst), file=sys.stderr)
+            print("e2e host worst ms per C-ABI call: " + ", ".join(
+                f"{k} {1e3 * v:.3f}" for k, v in sorted(call_worst.items(), key=lambda x: -x[1])), file=sys.stderr)
+            lib_mod.call = real_call
+            if cprof:
+                import pstats
+                pstats.Stats(cprof, stream=sys.stderr).sort_stats("tottime").print_stats(12)
         return reader.values
 
     def timed(loop):

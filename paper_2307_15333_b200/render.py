@@ -495,7 +495,7 @@ def ray_costs(tree: SparseOctree, origins: torch.Tensor, dirs: torch.Tensor, ear
 def plan_batch(tree: SparseOctree, origins: torch.Tensor, dirs: torch.Tensor, ray_index=None,
                stream=None, wait_current: bool = True, keys: torch.Tensor | None = None,
                costs: torch.Tensor | None = None, rank: PoolRank | None = None,
-               ids: torch.Tensor | None = None) -> RayPlan:
+               ids: torch.Tensor | None = None, out: tuple | None = None) -> RayPlan:
     """Coherence order of a batch (origin / octahedral-direction Morton keys,
     dot_ray_keys32 + a radix sort).  Depends only on the rays, so it can run
     on a side stream (``stream``) ahead of the step that consumes it; the
@@ -514,7 +514,9 @@ def plan_batch(tree: SparseOctree, origins: torch.Tensor, dirs: torch.Tensor, ra
     then carries no keys, so its warp order comes only from ``costs``.  ``ids`` (with ``rank``): the
     rays of ``origins`` / ``dirs`` ARE the batch (a staged batch) and ``ids``
     their ids in the ranked dataset; the plan orders the batch's slots
-    (``costs``: one entry per slot)."""
+    (``costs``: one entry per slot).  ``out`` (ranked plans): preallocated
+    (int64 [n] index, int32 [ceil(n / 32)] warp order) the plan writes into
+    -- no allocation on the plan's path (e.g. per staging slot)."""
     idx = None if ray_index is None else torch.as_tensor(ray_index, device=tree.device).reshape(-1).to(torch.int64)
     n = int(idx.shape[0]) if idx is not None else int(origins.shape[0])
     n_pool = int(origins.shape[0])
@@ -556,11 +558,20 @@ def plan_batch(tree: SparseOctree, origins: torch.Tensor, dirs: torch.Tensor, ra
     with torch.cuda.stream(s):
         ranked_order = None
         if rank is not None:
-            order = torch.empty(n, dtype=torch.int64, device=tree.device)
+            if out is not None:
+                order, ranked_order = out[0][:n], out[1][:(n + 31) // 32]
+                if order.dtype != torch.int64 or ranked_order.dtype != torch.int32 or order.numel() < n \
+                        or ranked_order.numel() < (n + 31) // 32:
+                    raise InputError("plan_batch(out=): int64 [n] index and int32 [ceil(n / 32)] warp order")
+            else:
+                order = torch.empty(n, dtype=torch.int64, device=tree.device)
             ws = rank.workspace(n, s, mode)
             if costs is not None and WARP_SCHED and 0 < n <= SCHED_MAX_RAYS:
                 # the warp launch order in the same launch
-                ranked_order = torch.empty((n + 31) // 32, dtype=torch.int32, device=tree.device)
+                if out is None:
+                    ranked_order = torch.empty((n + 31) // 32, dtype=torch.int32, device=tree.device)
+            else:
+                ranked_order = None
             _lib.call("dot_plan_ranked", _lib.ptr(rank.rank), _lib.ptr(rank.order), rank.n_pool, _lib.ptr(idx), n,
                       mode, _lib.ptr(costs if ranked_order is not None else None), cost_chunk(n),
                       _lib.ptr(ranked_order), _lib.ptr(ws), ws.numel(), _lib.ptr(order), _lib.stream_ptr(s))

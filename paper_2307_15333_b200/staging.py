@@ -35,7 +35,7 @@ from .errors import InputError
 
 
 class _Slot:
-    __slots__ = ("bufs", "n", "ready", "free", "busy", "plan", "cost", "ids", "meta", "plan_args")
+    __slots__ = ("bufs", "n", "ready", "free", "busy", "plan", "cost", "ids", "meta", "plan_args", "plan_out")
 
     def __init__(self):
         self.bufs = None
@@ -43,6 +43,7 @@ class _Slot:
         self.ids = None
         self.meta = torch.cuda.Event()  # costs and ids copied (all a ranked plan reads)
         self.plan_args = None           # a plan not launched yet (plan_next / take_with_plan)
+        self.plan_out = None            # the slot's plan index / warp order (reused with the slot)
         self.plan = None
         self.n = 0
         self.ready = torch.cuda.Event()
@@ -85,6 +86,8 @@ class RayBatchStager:
             slot.bufs = tuple(torch.empty(n, 3, dtype=torch.float64, device=self.device) for _ in range(3))
             slot.cost = torch.empty(n, dtype=torch.int16, device=self.device)
             slot.ids = torch.empty(n, dtype=torch.int64, device=self.device)
+            slot.plan_out = (torch.empty(n, dtype=torch.int64, device=self.device),
+                             torch.empty((n + 31) // 32, dtype=torch.int32, device=self.device))
 
     @staticmethod
     def _host(x, name: str) -> torch.Tensor:
@@ -151,7 +154,8 @@ class RayBatchStager:
         slot.plan_args = None
         slot.plan = plan_batch(self.plan_tree, slot.bufs[0][:n], slot.bufs[1][:n], stream=stream,
                                wait_current=wait_current, costs=slot.cost[:n] if has_cost else None,
-                               rank=self.plan_rank if ranked else None, ids=slot.ids[:n] if ranked else None)
+                               rank=self.plan_rank if ranked else None, ids=slot.ids[:n] if ranked else None,
+                               out=slot.plan_out if ranked else None)
 
     def plan_next(self) -> None:
         """Launch the ranked plan of the most recently staged batch now, on the

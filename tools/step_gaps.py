@@ -43,6 +43,17 @@ def main():
             if a - 300 <= e["ts"] < b:
                 print(f"  {e.get('args', {}).get('stream', '?'):>4} {e['ts'] - a:8.0f} {e['ts'] + e['dur'] - a:8.0f}  "
                       f"{e['name'].split('(')[0][:60]}")
+    # the plan's placement against the update, every step of the trace
+    pl = [e for e in k if "plan_coop" in e["name"]]
+    rm = [e for e in k if "rmsprop" in e["name"]]
+    if pl and rm:
+        rows = []
+        for e in pl:
+            r = min(rm, key=lambda x: abs(x["ts"] - e["ts"]))
+            rows.append((e["ts"] - r["ts"], e["ts"] + e["dur"] - (r["ts"] + r["dur"]), e["dur"]))
+        rows.sort()
+        print("plan start - update start / plan end - update end / plan dur (us), per step:")
+        print("  " + "  ".join(f"{a:.0f}/{b:.0f}/{c:.0f}" for a, b, c in rows))
     by = {}
     for e in k:
         n = e["name"].split("(")[0][:60]
