@@ -279,7 +279,9 @@ __global__ void __launch_bounds__(kPlanThreads, kPlanMinBlocks) plan_coop_kernel
                 const uint32_t bit = 1u << (uint32_t(k) & 31u);
                 mine = (atomicOr(w.claim + (k >> 5), bit) & bit) == 0u;
             }
-            if (!mine) plan_append(w, a.mode == DOT_PLAN_SLOTS ? i : r);
+            // a repeat keeps the output's meaning: its slot, its key
+            // position, or the pool ray itself
+            if (!mine) plan_append(w, a.mode == DOT_PLAN_SLOTS ? i : (a.mode == DOT_PLAN_POSITIONS ? k : r));
         }
         grid.sync();
         if (a.mode != DOT_PLAN_SLOTS)

@@ -428,6 +428,39 @@ def test_plan_ranked_warp_order():
         assert torch.equal(out, _regrouped(torch.sort(rank[ids].long()).indices, lambda v: slot_cost[v]))
         _check_warp_order(wo, slot_cost[out].long().cpu().numpy(), n, 1)
         assert _plan_scratch_clear(ws, n_pool, n)
+    # repeats and invalid indices with a cost column: still a permutation of
+    # the batch (the appended rays are regrouped like the placed ones) and a
+    # valid launch order; the workspace stays reusable
+    for mode in (0, 1, 2):
+        base = torch.randperm(n_pool, generator=g, device="cuda")[:5000]
+        idx = torch.cat([base, base[:700], torch.tensor([-5, n_pool, n_pool + 7], device="cuda")])
+        idx = idx[torch.randperm(idx.shape[0], generator=g, device="cuda")]
+        n = idx.shape[0]
+        cst = slot_cost if mode == 2 else costs
+        if mode == 2:
+            cst = torch.randint(0, 1400, (n,), generator=g, device="cuda").to(torch.int16)
+        need = _lib.load().dot_plan_ranked_workspace(n_pool, n, mode)
+        ws = torch.zeros(need, dtype=torch.uint8, device="cuda")
+        out = torch.empty(n, dtype=torch.int64, device="cuda")
+        wo = torch.empty((n + 31) // 32, dtype=torch.int32, device="cuda")
+        for rep in range(2):
+            _lib.call("dot_plan_ranked", _lib.ptr(rank), _lib.ptr(order if mode == 1 else None), n_pool, _lib.ptr(idx),
+                      n, mode, _lib.ptr(cst), 1, _lib.ptr(wo), _lib.ptr(ws), ws.numel(), _lib.ptr(out),
+                      _lib.stream_ptr())
+            torch.cuda.synchronize()
+            if mode == 2:  # slots: a permutation of 0..n-1
+                assert torch.equal(torch.sort(out).values, torch.arange(n, device="cuda"))
+                slot_costs = cst[out].long()
+            else:
+                # positions: valid ids come back as rank[id]; pool rays: as
+                # order[rank[id]] == id; invalid indices as they were
+                ok = (idx >= 0) & (idx < n_pool)
+                want = torch.where(ok, rank[idx.clamp(0, n_pool - 1)].long(), idx) if mode == 0 else idx
+                assert torch.equal(torch.sort(out).values, torch.sort(want).values)
+                valid = (out >= 0) & (out < n_pool)
+                slot_costs = torch.where(valid, cst[out.clamp(0, n_pool - 1)].long(), torch.zeros_like(out))
+            _check_warp_order(wo, slot_costs.cpu().numpy(), n, 1)
+            assert _plan_scratch_clear(ws, n_pool, n)
     # bad arguments are refused
     from paper_2307_15333_b200.errors import InputError
     with pytest.raises(InputError):
