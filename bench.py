@@ -624,18 +624,29 @@ def run_ours(args, rank, world, local_rank):
     from paper_2307_15333_b200.render import signal_pass
     sig_out = torch.zeros(tree.capacity, dtype=torch.float64, device=dev)
     sidx = perm[total_steps + 1]
+    sig_mode = os.environ.get("DOT_BENCH_SIGNAL_PLAN", "rank")  # rank (+ cost regroup) | keys
+
+    def sig_call():
+        # the batch's plan is part of the timed call: the ranked pool's order
+        # regrouped by the cost column (lane efficiency), or the ray keys
+        p = plan_batch(tree, origins, dirs, sidx, rank=prank, costs=pcosts) \
+            if sig_mode == "rank" and prank is not None else None
+        signal_pass(tree, origins, dirs, EPS, ray_index=sidx, signal=sig_out, plan=p)
     for _ in range(3):
-        signal_pass(tree, origins, dirs, EPS, ray_index=sidx, signal=sig_out)
+        sig_call()
     torch.cuda.synchronize()
     s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     s0.record()
     for _ in range(5):
-        signal_pass(tree, origins, dirs, EPS, ray_index=sidx, signal=sig_out)
+        sig_call()
     s1.record()
     torch.cuda.synchronize()
     sig_ms = s0.elapsed_time(s1) / 5
     signal_fwd = {"rays_per_s": per_rank / (sig_ms / 1e3), "ms_per_batch": sig_ms, "rays": per_rank,
-                  "api": "render.signal_pass (coherence plan + dot_signal_fwd: sum Q per leaf, no gradients)"}
+                  "api": "render.signal_pass (+ its batch plan: "
+                         + ("plan_batch(rank=, costs=), key order regrouped by cost" if sig_mode == "rank"
+                            and prank is not None else "ray keys + radix sort")
+                         + ") -> dot_signal_fwd: sum Q per leaf, no gradients"}
 
     # render (configs[2]) and refine (configs[4]) side measurements
     side = wl.key == "c2"  # render/refine/CPU legs belong to the default (configs[1]) line

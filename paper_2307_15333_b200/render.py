@@ -758,7 +758,7 @@ def render_and_backprop(tree: SparseOctree, origins, dirs, targets, background,
 
 def signal_pass(tree: SparseOctree, origins, dirs, early_stop_eps: float = EPS_T, t_near: float = 0.0,
                 t_far: float = math.inf, ray_index=None, buffer=None, signal=None, weight_sum=None,
-                weight_max=None, touched=None, coherent: bool = True):
+                weight_max=None, touched=None, coherent: bool = True, plan: "RayPlan | None" = None):
     """Training signal without gradients (``dot_signal_fwd``): per leaf the
     sum over the batch's composited segments of Q = 1 - exp(-sigma delta) --
     exactly the ``signal`` output of ``render_and_backprop`` (render.py:
@@ -773,7 +773,9 @@ def signal_pass(tree: SparseOctree, origins, dirs, early_stop_eps: float = EPS_T
     ``weight_sum`` / ``weight_max`` (f64 [capacity]) collect the sum / max
     of the compositing weight T_i Q_i, ``touched`` (u8 [capacity]) marks
     every traversed leaf (post-cut included).  numpy inputs give a numpy
-    signal; torch inputs stay on the device (no synchronisation)."""
+    signal; torch inputs stay on the device (no synchronisation).  ``plan``
+    (``plan_batch``, optional): the batch's order computed ahead, e.g. from a
+    ranked pool with its cost column (key order regrouped by cost)."""
     io = _IO(tree, origins)
     o = io.rays(origins, "origins")
     d = io.rays(dirs, "dirs")
@@ -798,7 +800,12 @@ def signal_pass(tree: SparseOctree, origins, dirs, early_stop_eps: float = EPS_T
                         ("weight_max", weight_max, torch.float64), ("touched", touched, torch.uint8)):
         _check_out(name, x, dt, tree)
     if n:
-        if coherent and n >= COHERENT_MIN_RAYS:
+        if plan is not None:
+            if plan.n != n:
+                raise InputError(f"ray plan is for {plan.n} rays, batch has {n}")
+            plan.wait()
+            idx = plan.idx
+        elif coherent and n >= COHERENT_MIN_RAYS:
             idx = plan_batch(tree, o, d, idx).idx
         view, _topo = tree.tree_view(locate_level=locate_level_train())
         invalid = torch.zeros(1, dtype=torch.int64, device=dev)
