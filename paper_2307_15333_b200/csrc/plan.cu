@@ -58,7 +58,10 @@ constexpr int kPlanCostBins = 1024;                // warp costs are capped here
 constexpr int kPlanIlp = 8;                        // rays / gathers in flight per thread
 constexpr int kTagSlotBits = 21;                   // packed tag: slot | cost << 21 (n <= 2^21)
 constexpr int kPlanStage = 512;                    // staged positions per warp range (shared memory, 4 KB per block)
-constexpr int kPlanWindow = 128;                   // rays regrouped by cost per window (a multiple of 32, <= kPlanStage)
+#ifndef DOT_PLAN_WINDOW
+#define DOT_PLAN_WINDOW 128
+#endif
+constexpr int kPlanWindow = DOT_PLAN_WINDOW;       // rays regrouped by cost per window (32..256, a multiple of 32)
 
 struct PlanWs {
     uint32_t* bitmap;             // [words + slack]
