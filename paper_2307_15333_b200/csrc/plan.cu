@@ -202,7 +202,8 @@ __global__ void __launch_bounds__(kPlanThreads, kPlanMinBlocks) plan_coop_kernel
     const int64_t n_cost = a.mode == DOT_PLAN_SLOTS ? a.n : a.n_pool;  // the cost column's length
     PLAN_STAMP(0)
 
-    // A. mark: a bit RED and a tag store per ray, kPlanIlp rays in flight
+    // A. mark: a bit RED per ray (and, in slot mode, the position's tag),
+    // kPlanIlp rays in flight per thread
     for (int64_t i0 = gt; i0 < a.n; i0 += kPlanIlp * GT) {
         int64_t r[kPlanIlp];
         int32_t k[kPlanIlp];  // key position; -1 unplaceable, -2 past the batch
