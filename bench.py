@@ -369,8 +369,9 @@ def run_ours(args, rank, world, local_rank):
 
     def step(k, timed_kernel=True):
         # the batch is read in place from the resident pool (ray_index): no
-        # gather; its coherence order was sorted on a side stream during the
-        # previous step (plan_batch), and the next one is queued now
+        # gather; its plan (key order regrouped by cost + warp launch order)
+        # ran beside the previous step's update, and the next one is queued
+        # behind this step's backward
         idx = batch_index(k)
         plan = plans.pop(k, None)
 
@@ -685,7 +686,8 @@ def run_ours(args, rank, world, local_rank):
             "parallelism": f"rays sharded dp{world}, tree replicated",
             "exchange": args.exchange if world > 1 else "none",
             "batch_order": args.order,
-            "plan": ("coherence order of step k+1 computed on a side stream during step k: "
+            "plan": ("step k+1's plan (coherence order, cost regrouping in 128-ray windows, warp launch "
+                     "order) queued behind step k's backward on a side stream, running beside its update: "
                      + ({"rank": "a counting sort of the batch's pool positions, the pool stored in 62-bit "
                                  "key order (render.pool_rank + PoolRank.permute, dot_plan_ranked)",
                          "rank-gather": "a counting sort over the resident pool's 62-bit key rank "
