@@ -267,10 +267,11 @@ int dot_plan_sort(const int32_t* keys, const int64_t* ray_index, int64_t n_rays,
  * (descending, ties in key order) so each warp holds rays of similar
  * length -- and the warps are ordered in chunks of `chunk` consecutive
  * warps by descending max cost, a short last chunk last (what
- * dot_sched_order_costs gives for the regrouped sorted_index).  One cooperative launch
- * (one block per SM).  workspace: dot_plan_ranked_workspace(n_pool,
- * n_rays, mode) bytes, 256-byte aligned, ZEROED before its first use;
- * every call leaves it reusable.  Calls sharing a workspace must be
+ * dot_sched_order_costs gives for the regrouped sorted_index).  One
+ * cooperative launch (one block per SM).  workspace:
+ * dot_plan_ranked_workspace(n_pool, n_rays, mode) bytes, 256-byte aligned,
+ * ZEROED before its first use; every call leaves it reusable, also for
+ * smaller batches of the same pool.  Calls sharing a workspace must be
  * stream-ordered.  n_pool, n_rays < 2^31. */
 enum { DOT_PLAN_POSITIONS = 0, DOT_PLAN_POOL_RAYS = 1, DOT_PLAN_SLOTS = 2 };
 int64_t dot_plan_ranked_workspace(int64_t n_pool, int64_t n_rays, int32_t mode);

@@ -80,6 +80,10 @@ __host__ __device__ static int64_t plan_words(int64_t n_pool) { return (n_pool +
 static size_t align256(size_t b) { return (b + 255) & ~size_t(255); }
 static int g_plan_grid = 0;  // blocks of the cooperative launch (one per SM), set on first use
 
+// Workspace layout: the regions that must stay zero between calls (bitmap,
+// claim bitmap, counters, histogram) and the pool-sized tag come first, at
+// offsets that depend only on n_pool, so one workspace sized for the
+// largest batch serves every smaller one; the per-batch scratch follows.
 static size_t carve(void* ws, int64_t n_pool, int64_t n, PlanWs* out) {
     char* base = static_cast<char*>(ws);
     char* p = base;
@@ -87,10 +91,17 @@ static size_t carve(void* ws, int64_t n_pool, int64_t n, PlanWs* out) {
     const int64_t nw = (n + 31) / 32;
     w.bitmap = reinterpret_cast<uint32_t*>(p);
     p += align256(size_t(plan_words(n_pool) + 32 * kPlanLaneWords) * 4);  // + a zero slack range (whole uint4 loads)
+    w.claim = reinterpret_cast<uint32_t*>(p);
+    p += align256(size_t(plan_words(n_pool)) * 4);
     w.warp_total = reinterpret_cast<int32_t*>(p);
     p += align256(size_t(4096) * 4);  // up to 2048 SMs x 2 warps
     w.ctr = reinterpret_cast<unsigned long long*>(p);
     p += 256;
+    w.hist = reinterpret_cast<int32_t*>(p);
+    p += align256(size_t(kPlanCostBins) * 4);
+    w.tag = reinterpret_cast<int32_t*>(p);
+    p += align256(size_t(n_pool) * 4);
+    // per batch: written before read in every call
     w.extra_ray = reinterpret_cast<int64_t*>(p);
     p += align256(size_t(n) * 8);
     w.warp_cost = reinterpret_cast<uint32_t*>(p);
@@ -99,12 +110,6 @@ static size_t carve(void* ws, int64_t n_pool, int64_t n, PlanWs* out) {
     p += align256(size_t(nw) * 2);
     w.slot_cost = reinterpret_cast<uint16_t*>(p);
     p += align256(size_t(n) * 2);
-    w.hist = reinterpret_cast<int32_t*>(p);
-    p += align256(size_t(kPlanCostBins) * 4);
-    w.tag = reinterpret_cast<int32_t*>(p);
-    p += align256(size_t(n_pool) * 4);
-    w.claim = reinterpret_cast<uint32_t*>(p);
-    p += align256(size_t(plan_words(n_pool)) * 4);
     if (out) *out = w;
     return size_t(p - base);
 }

@@ -160,6 +160,40 @@ def test_train_epoch_resident_planned_equals_plain():
     assert bb.epoch_rays == ba.epoch_rays == o.shape[0]
 
 
+def test_train_planned_matches_unplanned_across_refines():
+    """train() with batches large enough for the ranked plan (ResidentRays:
+    rays resident in key order, cost column, plans beside the update) over
+    epochs with calibrations in between == the same epochs through the plain
+    per-batch path: leaf counts equal every epoch, losses within fp32-atomic
+    noise, the final topology identical."""
+    from paper_2307_15333_b200.calibrate import calibrate
+    from paper_2307_15333_b200.optim import ResidentRays, RmsPropState, TrainConfig, train, train_epoch
+    from paper_2307_15333_b200.scene_io import load_tree_bytes, tree_bytes
+    from paper_2307_15333_b200.signals import SignalBuffer
+    tree, o, d, t, _ = _batch_setup(seed=51, n=1 << 15)
+    blob = tree_bytes(tree)
+    data = _Bundle(o.cpu().numpy(), d.cpu().numpy(), t.cpu().numpy())
+    cfg = TrainConfig(epochs=4, interval=2, tau=0.05, gamma=0.05, batch_size=20000, seed=9, background=0.5)
+    a = load_tree_bytes(blob, device="cuda")
+    _, hist = train(a, data, cfg)
+    # the same schedule, unplanned batches
+    b = load_tree_bytes(blob, device="cuda")
+    state = RmsPropState(b, cfg.beta, cfg.eps, cfg.lr_sigma, cfg.lr_sh)
+    buf = SignalBuffer(b, cfg.signal)
+    rng = np.random.default_rng(cfg.seed)
+    losses, leaves = [], []
+    for epoch in range(1, cfg.epochs + 1):
+        pool = ResidentRays(b, data, cfg.batch_size, cfg.early_stop_eps, plan=False)
+        losses.append(train_epoch(b, pool, state, buf, cfg, rng))
+        if epoch % cfg.interval == 0:
+            rep = calibrate(b, buf, cfg.calibration(), events=False)
+            state.remap(rep, reset=cfg.reset_state_on_calibration)
+        leaves.append(b.leaf_count)
+    assert [h["leaf_count"] for h in hist] == leaves
+    np.testing.assert_allclose([h["loss"] for h in hist], losses, rtol=1e-5)
+    np.testing.assert_array_equal(a.topology().node.cpu().numpy(), b.topology().node.cpu().numpy())
+
+
 class _HeldoutBundle(_Bundle):
     def __init__(self, origins, dirs, targets, heldout):
         super().__init__(origins, dirs, targets)

@@ -328,13 +328,15 @@ def _a256(b):
 
 
 def _plan_scratch_clear(ws, n_pool, n):
-    """The bitmap, counter and warp-cost regions of a plan workspace are zero."""
+    """The regions of a plan workspace that must be zero between calls
+    (bitmap + slack, claim bitmap, counters, cost histogram) are zero
+    (plan.cu carve(): they precede the per-batch scratch)."""
     words = (n_pool + 31) // 32
-    at_extra = _a256(4 * words) + _a256(4 * ((words + 1023) // 1024 + 1))
-    at_wc = at_extra + 256 + _a256(8 * n)
-    nw = (n + 31) // 32
-    return (not bool(ws[: 4 * words].any()) and not bool(ws[at_extra: at_extra + 8].any())
-            and not bool(ws[at_wc: at_wc + 4 * nw].any()))
+    at_claim = _a256(4 * (words + 512))
+    at_ctr = at_claim + _a256(4 * words) + _a256(4 * 4096)
+    at_hist = at_ctr + 256
+    return (not bool(ws[:at_claim].any()) and not bool(ws[at_claim:at_claim + 4 * words].any())
+            and not bool(ws[at_ctr:at_ctr + 16].any()) and not bool(ws[at_hist:at_hist + 4096].any()))
 
 
 def _cost_bucket(c):
@@ -427,6 +429,20 @@ def test_plan_ranked_warp_order():
         torch.cuda.synchronize()
         assert torch.equal(out, _regrouped(torch.sort(rank[ids].long()).indices, lambda v: slot_cost[v]))
         _check_warp_order(wo, slot_cost[out].long().cpu().numpy(), n, 1)
+        assert _plan_scratch_clear(ws, n_pool, n)
+    # one workspace sized for the largest batch serves smaller ones (the
+    # last batch of an epoch): the zero regions do not move with n
+    need = _lib.load().dot_plan_ranked_workspace(n_pool, 70_001, 0)
+    ws = torch.zeros(need, dtype=torch.uint8, device="cuda")
+    for n in (70_001, 50_000, 70_001, 333, 12_345):
+        idx = torch.randperm(n_pool, generator=g, device="cuda")[:n]
+        out = torch.empty(n, dtype=torch.int64, device="cuda")
+        wo = torch.empty((n + 31) // 32, dtype=torch.int32, device="cuda")
+        _lib.call("dot_plan_ranked", _lib.ptr(rank), None, n_pool, _lib.ptr(idx), n, 0, _lib.ptr(costs), 1,
+                  _lib.ptr(wo), _lib.ptr(ws), ws.numel(), _lib.ptr(out), _lib.stream_ptr())
+        torch.cuda.synchronize()
+        assert torch.equal(out, _regrouped(torch.sort(rank[idx].long()).values, lambda v: costs[v]))
+        _check_warp_order(wo, costs[out].long().cpu().numpy(), n, 1)
         assert _plan_scratch_clear(ws, n_pool, n)
     # repeats and invalid indices with a cost column: still a permutation of
     # the batch (the appended rays are regrouped like the placed ones) and a
