@@ -115,3 +115,64 @@ def test_stager_plans_match_in_stream_plans():
     assert float(l1) == pytest.approx(float(l2), rel=1e-12)  # f64 atomic order
     torch.testing.assert_close(g1.dsh, g2.dsh, atol=1e-7, rtol=1e-5)
     assert torch.equal(g1.touched_mask, g2.touched_mask)
+
+
+def test_stager_ranked_plans_with_ids():
+    """RayBatchStager(plan_rank=) with batches staged with their dataset ids
+    and costs: batches of varying size (a smaller last one), the plan
+    launched behind the backward (plan_next as train_step's after_backward)
+    or lazily by take_with_plan; each plan is a permutation of the batch's
+    slots regrouped in key order, and training equals the unplanned staged
+    loop to fp32-atomic noise."""
+    from paper_2307_15333_b200.optim import RmsPropState, StepWorkspace, train_step
+    from paper_2307_15333_b200.render import pool_rank, ray_costs
+    from paper_2307_15333_b200.scene_io import load_tree_bytes, tree_bytes
+    from paper_2307_15333_b200.signals import SignalBuffer
+    from paper_2307_15333_b200.staging import LossReader, RayBatchStager
+    base = irregular_tree(61, 16, depth=3, splits=40, merges=4, max_depth=6, device="cuda")
+    blob = tree_bytes(base)
+    n_pool = 60000
+    o, d = ray_batch(62, n_pool)
+    t = np.random.default_rng(63).uniform(0, 1, (n_pool, 3))
+    od, dd = torch.from_numpy(o).cuda(), torch.from_numpy(d).cuda()
+    ref_tree = load_tree_bytes(blob, device="cuda")
+    pr = pool_rank(ref_tree, od, dd)
+    costs = ray_costs(ref_tree, od, dd).cpu()
+    perm = np.random.default_rng(64).permutation(n_pool)
+    sizes = [20000, 20000, 16000, 4000]
+    batches, at = [], 0
+    for m in sizes:
+        ids = perm[at:at + m]
+        at += m
+        batches.append(tuple(torch.from_numpy(np.ascontiguousarray(x)).pin_memory() for x in (o[ids], d[ids], t[ids]))
+                       + (costs[torch.from_numpy(ids)].contiguous().pin_memory(),
+                          torch.from_numpy(ids.astype(np.int64)).pin_memory()))
+
+    def run(ranked: bool):
+        tree = load_tree_bytes(blob, device="cuda")
+        st, buf = RmsPropState(tree), SignalBuffer(tree)
+        sws = StepWorkspace(tree, buf)
+        stager = RayBatchStager("cuda", max_rays=max(sizes), plan_tree=tree if ranked else None,
+                                plan_rank=pr if ranked else None)
+        reader = LossReader()
+        stager.stage(*batches[0])
+        for k in range(len(batches)):
+            ob, db, tb, plan = stager.take_with_plan()
+            if ranked:
+                m = sizes[k]
+                assert torch.equal(torch.sort(plan.idx).values, torch.arange(m, device="cuda"))
+            if k + 1 < len(batches):
+                stager.stage(*batches[k + 1])
+            hook = stager.plan_next if (ranked and k % 2 == 0) else None  # odd steps: the lazy launch
+            loss = train_step(tree, ob, db, tb, st, buf, sws, 0.5, plan=plan, after_backward=hook)
+            stager.release()
+            reader.push(loss)
+        reader.flush()
+        torch.cuda.synchronize()
+        return reader.values, tree
+
+    la, ta = run(False)
+    lb, tb = run(True)
+    np.testing.assert_allclose(lb, la, rtol=1e-5, atol=1e-9)
+    torch.testing.assert_close(tb.sigma, ta.sigma, atol=1e-5, rtol=1e-4)
+    torch.testing.assert_close(tb.sh, ta.sh, atol=1e-5, rtol=1e-4)
