@@ -416,7 +416,24 @@ def test_plan_ranked_warp_order():
                 _check_warp_order(wo, costs[out].long().cpu().numpy(), n, chunk)
                 assert _plan_scratch_clear(ws, n_pool, n), "scratch not left zeroed"
     # slots of a staged batch: ids name its rays in the ranked dataset, the
-    # warp costs come per slot
+    # warp costs come per slot (above 2^21 rays the slot no longer packs
+    # with its cost into the tag: the cost is gathered by slot instead)
+    big = 1 << 21
+    n_pool_b = big + 5000
+    order_b = torch.randperm(n_pool_b, generator=g, device="cuda").to(torch.int32)
+    rank_b = torch.empty(n_pool_b, dtype=torch.int32, device="cuda")
+    rank_b[order_b.long()] = torch.arange(n_pool_b, dtype=torch.int32, device="cuda")
+    for n in (big, big + 1000):
+        ids = torch.randperm(n_pool_b, generator=g, device="cuda")[:n]
+        slot_cost = torch.randint(0, 1400, (n,), generator=g, device="cuda").to(torch.int16)
+        ws = torch.zeros(_lib.load().dot_plan_ranked_workspace(n_pool_b, n, 2), dtype=torch.uint8, device="cuda")
+        out = torch.empty(n, dtype=torch.int64, device="cuda")
+        wo = torch.empty((n + 31) // 32, dtype=torch.int32, device="cuda")
+        _lib.call("dot_plan_ranked", _lib.ptr(rank_b), None, n_pool_b, _lib.ptr(ids), n, 2, _lib.ptr(slot_cost), 16,
+                  _lib.ptr(wo), _lib.ptr(ws), ws.numel(), _lib.ptr(out), _lib.stream_ptr())
+        torch.cuda.synchronize()
+        assert torch.equal(out, _regrouped(torch.sort(rank_b[ids].long()).indices, lambda v: slot_cost[v]))
+        _check_warp_order(wo, slot_cost[out].long().cpu().numpy(), n, 16)
     for n in (1, 4097, 70_001):
         ids = torch.randperm(n_pool, generator=g, device="cuda")[:n]
         slot_cost = torch.randint(0, 1400, (n,), generator=g, device="cuda").to(torch.int16)
