@@ -16,7 +16,10 @@
 namespace dot {
 
 constexpr int kBlock = 128;
-constexpr int kFwdMinBlocks = 8;   // forward: 64 registers -> 8 blocks (32 warps) per SM
+#ifndef DOT_FWD_MINB
+#define DOT_FWD_MINB 8
+#endif
+constexpr int kFwdMinBlocks = DOT_FWD_MINB;   // forward: 64 registers -> 8 blocks (32 warps) per SM
 #ifndef DOT_BWD_RECORDS
 #define DOT_BWD_RECORDS 128
 #endif
