@@ -194,6 +194,30 @@ def test_train_planned_matches_unplanned_across_refines():
     np.testing.assert_array_equal(a.topology().node.cpu().numpy(), b.topology().node.cpu().numpy())
 
 
+def test_train_epoch_device_shuffle_covers_every_ray_once():
+    """TrainConfig(device_shuffle=True) draws the epoch permutation on the GPU:
+    with the learning rates at zero (the payload fixed) an epoch still sees
+    every ray exactly once -- the epoch's signal and mean loss equal the
+    numpy-permutation epoch's (batch order does not matter then)."""
+    from paper_2307_15333_b200.optim import ResidentRays, RmsPropState, TrainConfig, train_epoch
+    from paper_2307_15333_b200.scene_io import load_tree_bytes, tree_bytes
+    from paper_2307_15333_b200.signals import SignalBuffer
+    tree, o, d, t, _ = _batch_setup(seed=71, n=1 << 15)
+    blob = tree_bytes(tree)
+    data = _Bundle(o.cpu().numpy(), d.cpu().numpy(), t.cpu().numpy())
+    out = []
+    for dev_shuffle in (False, True):
+        tr = load_tree_bytes(blob, device="cuda")
+        cfg = TrainConfig(batch_size=20000, background=0.5, lr_sigma=0.0, lr_sh=0.0, device_shuffle=dev_shuffle)
+        st, buf = RmsPropState(tr, lr_sigma=0.0, lr_sh=0.0), SignalBuffer(tr)
+        pool = ResidentRays(tr, data, cfg.batch_size)
+        loss = train_epoch(tr, pool, st, buf, cfg, np.random.default_rng(3))
+        assert buf.epoch_rays == pool.n
+        out.append((loss, buf.accumulator.clone()))
+    assert out[1][0] == pytest.approx(out[0][0], rel=1e-9)
+    torch.testing.assert_close(out[1][1], out[0][1], rtol=1e-10, atol=1e-12)
+
+
 class _HeldoutBundle(_Bundle):
     def __init__(self, origins, dirs, targets, heldout):
         super().__init__(origins, dirs, targets)
