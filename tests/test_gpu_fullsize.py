@@ -2,9 +2,10 @@
 the pinned oracle (tests/test_oracle_golden.py):
 
 * configs[1]: one 2^20-ray random training batch of the 100-view pool
-  (ray_index + coherence plan + learned warp schedule): loss, dsigma, dSH
-  (scale-aware 1e-4 / 1e-3), touched set equal, signal to f64-atomic
-  rounding; the deterministic path's signal bit-equal to the reference's.
+  (ray_index + coherence plan + learned warp schedule, and the bench's
+  ranked-pool plan with cost regrouping): loss, dsigma, dSH (scale-aware
+  1e-4 / 1e-3), touched set equal, signal to f64-atomic rounding; the
+  deterministic path's signal bit-equal to the reference's.
 * configs[2]: one 800x800 view through render_rays on Camera.rays()
   (segments bit-exact, rgb / T_final / weight sum / depth within 1e-4 /
   1e-3) and through render_views (in-kernel rays).
@@ -65,6 +66,21 @@ def _batch_vs_oracle(oracle, tree, o, d, t, idx):
     assert_grads_close(g.dsigma.cpu().numpy()[touched], r_g.dsigma[touched], what="dsigma")
     assert_grads_close(g.dsh.cpu().numpy()[touched], r_g.dsh[touched], what="dsh")
     np.testing.assert_allclose(sig.cpu().numpy(), r_sig, rtol=1e-12, atol=1e-15)
+    # the bench's training path: the pool ranked by its 62-bit keys, the
+    # batch planned by the cooperative kernel (key order regrouped by cost in
+    # 128-ray windows, warps launched longest first)
+    from paper_2307_15333_b200.render import plan_batch, pool_rank, ray_costs
+    pr = pool_rank(tree, o, d)
+    plan = plan_batch(tree, o, d, idx, rank=pr, costs=ray_costs(tree, o, d))
+    assert plan.warp_order is not None and torch.equal(torch.sort(plan.idx).values, torch.sort(idx).values)
+    ws2 = BackpropWorkspace.for_tree(tree)
+    loss2, g2, sig2 = render_and_backprop(tree, o, d, t, 1.0, ray_index=idx, workspace=ws2, plan=plan)
+    del pr, plan
+    assert float(loss2) == pytest.approx(r_loss, rel=RTOL, abs=ATOL)
+    np.testing.assert_array_equal(torch.nonzero(g2.touched_mask).reshape(-1).cpu().numpy(), r_g.touched)
+    assert_grads_close(g2.dsigma.cpu().numpy()[touched], r_g.dsigma[touched], what="dsigma (ranked plan)")
+    assert_grads_close(g2.dsh.cpu().numpy()[touched], r_g.dsh[touched], what="dsh (ranked plan)")
+    np.testing.assert_allclose(sig2.cpu().numpy(), r_sig, rtol=1e-12, atol=1e-15)
     # the deterministic reduction: the reference's serial order, bit for bit
     ws.zero_()
     _, gd, sd = render_and_backprop(tree, o, d, t, 1.0, ray_index=idx, workspace=ws, deterministic=True)
