@@ -349,6 +349,16 @@ int dot_rmsprop_step(float* sigma, float* sh, int32_t sh_stride, int32_t n_sh,
                      int64_t capacity, double beta, double eps, double lr_sigma,
                      double lr_sh, int32_t flags, void* stream);
 
+/* The same update for a sparse step (a small batch touches few rows): the
+ * touched rows are listed first and only they are visited (the dense update's
+ * grid covers the whole capacity).  Same arguments and results; layouts the
+ * vectorised update does not take fall back to dot_rmsprop_step. */
+int dot_rmsprop_step_sparse(float* sigma, float* sh, int32_t sh_stride, int32_t n_sh,
+                            double* v_sigma, double* v_sh, float* grad_sigma,
+                            float* grad_sh, int32_t gsh_stride, const uint8_t* touched,
+                            int64_t capacity, double beta, double eps, double lr_sigma,
+                            double lr_sh, int32_t flags, void* stream);
+
 /* --- the same update with f32 second moments (opt-in, no reference
  *     counterpart: octrf keeps f64 state, optim.py:70-72).  Arithmetic is
  *     f64 with v widened on read and rounded once on store; results are

@@ -18,7 +18,7 @@ LIB_PATH = os.path.join(_HERE, "libdot_b200.so")
 _LIB_OVERRIDE = os.environ.get("DOT_LIB_PATH")
 
 DOT_OK, DOT_BAD_ARG, DOT_OOM, DOT_CUDA_ERR, DOT_NO_DEVICE = range(5)
-ABI_VERSION = 11
+ABI_VERSION = 12
 
 c_void_p = ctypes.c_void_p
 c_i64 = ctypes.c_int64
@@ -107,6 +107,9 @@ _SIGNATURES = {
     "dot_rmsprop_step": (c_i32, [c_void_p, c_void_p, c_i32, c_i32, c_void_p, c_void_p, c_void_p,
                                  c_void_p, c_i32, c_void_p, c_i64, c_f64, c_f64, c_f64, c_f64,
                                  c_i32, c_void_p]),
+    "dot_rmsprop_step_sparse": (c_i32, [c_void_p, c_void_p, c_i32, c_i32, c_void_p, c_void_p, c_void_p,
+                                        c_void_p, c_i32, c_void_p, c_i64, c_f64, c_f64, c_f64, c_f64,
+                                        c_i32, c_void_p]),
     "dot_rmsprop_step_f32state": (c_i32, [c_void_p, c_void_p, c_i32, c_i32, c_void_p, c_void_p, c_void_p,
                                           c_void_p, c_i32, c_void_p, c_i64, c_f64, c_f64, c_f64, c_f64,
                                           c_i32, c_void_p]),

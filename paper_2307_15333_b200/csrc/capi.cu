@@ -68,7 +68,7 @@ using namespace dot;
 
 extern "C" {
 
-int dot_abi_version(void) { return 11; }
+int dot_abi_version(void) { return 12; }
 
 const char* dot_last_error(void) { return g_err; }
 

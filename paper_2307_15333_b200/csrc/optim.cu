@@ -77,18 +77,14 @@ __global__ void __launch_bounds__(256) rmsprop_kernel(float* __restrict__ sigma,
 // warps per SM: measured against the same update with dependent loads at
 // 40 registers (step 2.50 -> 2.46 ms); 2 or 4 quads per thread (74 / 106
 // registers) and 6 / 8 blocks (40 / 32 registers, spills) were slower.
-__global__ void __launch_bounds__(256, 5) rmsprop_vec_kernel(float* __restrict__ sigma, float* __restrict__ sh,
-                                                             int sh_stride, int n_sh, double* __restrict__ v_sigma,
-                                                             double* __restrict__ v_sh, float* __restrict__ gsig,
-                                                             float* __restrict__ gsh, int gsh_stride,
-                                                             const uint8_t* __restrict__ touched, int64_t cap,
-                                                             int quads, double beta, double eps, double lr_sigma,
-                                                             double lr_sh, bool consume) {
-    const int64_t f = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (f >= cap * quads) return;
-    const int64_t r = f / quads;
-    const int j = int(f - r * quads);
-    if (!__ldg(touched + r)) return;
+// One (row, 4-column quad) of the vectorised update: the quad's gradient,
+// state and payload loads all issued before any is consumed (the payload
+// load is not held back by the zero-gradient test).
+__device__ __forceinline__ void rms_quad(int64_t r, int j, float* __restrict__ sigma, float* __restrict__ sh,
+                                         int sh_stride, int n_sh, double* __restrict__ v_sigma,
+                                         double* __restrict__ v_sh, float* __restrict__ gsig,
+                                         float* __restrict__ gsh, int gsh_stride, double beta, double eps,
+                                         double lr_sigma, double lr_sh, bool consume) {
     const double omb = __dsub_rn(1.0, beta);
     float* const gp = gsh + r * int64_t(gsh_stride) + 4 * j;
     float* const pp = sh + r * int64_t(sh_stride) + 4 * j;
@@ -123,6 +119,61 @@ __global__ void __launch_bounds__(256, 5) rmsprop_vec_kernel(float* __restrict__
     v[0] = va;
     v[1] = vb;
     if (consume) *reinterpret_cast<float4*>(gp) = make_float4(0.f, 0.f, 0.f, 0.f);
+}
+
+// Vectorised update (n_sh % 4 == 0): one thread per (row, 4-column quad),
+// the touched byte first.  __launch_bounds__(256, 5) -> 48 registers, 40
+// warps per SM: measured against the same update with dependent loads at
+// 40 registers (step 2.50 -> 2.46 ms); 2 or 4 quads per thread (74 / 106
+// registers) and 6 / 8 blocks (40 / 32 registers, spills) were slower.
+__global__ void __launch_bounds__(256, 5) rmsprop_vec_kernel(float* __restrict__ sigma, float* __restrict__ sh,
+                                                             int sh_stride, int n_sh, double* __restrict__ v_sigma,
+                                                             double* __restrict__ v_sh, float* __restrict__ gsig,
+                                                             float* __restrict__ gsh, int gsh_stride,
+                                                             const uint8_t* __restrict__ touched, int64_t cap,
+                                                             int quads, double beta, double eps, double lr_sigma,
+                                                             double lr_sh, bool consume) {
+    const int64_t f = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (f >= cap * quads) return;
+    const int64_t r = f / quads;
+    const int j = int(f - r * quads);
+    if (!__ldg(touched + r)) return;
+    rms_quad(r, j, sigma, sh, sh_stride, n_sh, v_sigma, v_sh, gsig, gsh, gsh_stride, beta, eps, lr_sigma, lr_sh,
+             consume);
+}
+
+// Sparse steps (a small batch touches few rows): the dense update's cost is
+// its capacity-sized grid (140k blocks at configs[1] whatever the batch), so
+// the touched rows are listed first (warp-aggregated, any order: rows are
+// independent) and a grid-stride kernel updates only them.
+__global__ void __launch_bounds__(256) touched_rows_kernel(const uint8_t* __restrict__ touched, int64_t cap,
+                                                           int32_t* __restrict__ rows, int32_t* __restrict__ count) {
+    const int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    const bool t = r < cap && __ldg(touched + r) != 0;
+    const unsigned m = __ballot_sync(0xffffffffu, t);
+    if (m == 0u) return;
+    const int lane = threadIdx.x & 31;
+    int base = 0;
+    if (lane == __ffs(m) - 1) base = atomicAdd(count, __popc(m));
+    base = __shfl_sync(0xffffffffu, base, __ffs(m) - 1);
+    if (t) rows[base + __popc(m & ((1u << lane) - 1u))] = int32_t(r);
+}
+
+__global__ void __launch_bounds__(256, 5) rmsprop_rows_kernel(float* __restrict__ sigma, float* __restrict__ sh,
+                                                              int sh_stride, int n_sh, double* __restrict__ v_sigma,
+                                                              double* __restrict__ v_sh, float* __restrict__ gsig,
+                                                              float* __restrict__ gsh, int gsh_stride,
+                                                              const int32_t* __restrict__ rows,
+                                                              const int32_t* __restrict__ count, int quads,
+                                                              double beta, double eps, double lr_sigma, double lr_sh,
+                                                              bool consume) {
+    const int64_t total = int64_t(*count) * quads;
+    for (int64_t f = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; f < total;
+         f += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t i = f / quads;
+        rms_quad(__ldg(rows + i), int(f - i * quads), sigma, sh, sh_stride, n_sh, v_sigma, v_sh, gsig, gsh,
+                 gsh_stride, beta, eps, lr_sigma, lr_sh, consume);
+    }
 }
 
 // Opt-in variant with f32 second moments (not the reference's dtype): the
@@ -314,6 +365,44 @@ extern "C" int dot_rmsprop_step(float* sigma, float* sh, int32_t sh_stride, int3
                                         gsh_stride, touched, capacity, quads, beta, eps, lr_sigma, lr_sh,
                                         (flags & 1) != 0);
     return check_launch("rmsprop_kernel");
+}
+
+extern "C" int dot_rmsprop_step_sparse(float* sigma, float* sh, int32_t sh_stride, int32_t n_sh, double* v_sigma,
+                                       double* v_sh, float* grad_sigma, float* grad_sh, int32_t gsh_stride,
+                                       const uint8_t* touched, int64_t capacity, double beta, double eps,
+                                       double lr_sigma, double lr_sh, int32_t flags, void* stream) {
+    if (!sigma || !sh || !v_sigma || !v_sh || !grad_sigma || !grad_sh || !touched)
+        return set_error(DOT_BAD_ARG, "rmsprop: NULL argument");
+    if (!(beta > 0.0 && beta < 1.0)) return set_error(DOT_BAD_ARG, "beta must be in (0, 1), got %g", beta);
+    if (n_sh < 1 || sh_stride < n_sh || gsh_stride < n_sh) return set_error(DOT_BAD_ARG, "rmsprop: bad strides");
+    if (capacity > INT32_MAX) return set_error(DOT_BAD_ARG, "rmsprop_sparse: capacity must be < 2^31");
+    const bool vec = (n_sh % 4 == 0) && (sh_stride % 4 == 0) && (gsh_stride % 4 == 0) &&
+                     ((reinterpret_cast<uintptr_t>(sh) | reinterpret_cast<uintptr_t>(grad_sh)) & 15) == 0 &&
+                     (reinterpret_cast<uintptr_t>(v_sh) & 31) == 0;
+    if (!vec)  // the generic layout keeps the dense update
+        return dot_rmsprop_step(sigma, sh, sh_stride, n_sh, v_sigma, v_sh, grad_sigma, grad_sh, gsh_stride, touched,
+                                capacity, beta, eps, lr_sigma, lr_sh, flags, stream);
+    if (capacity == 0) return DOT_OK;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    retain_pool_memory();
+    int32_t* rows = nullptr;
+    if (int st = check_cuda(cudaMallocAsync(reinterpret_cast<void**>(&rows), size_t(capacity + 1) * 4, s),
+                            "cudaMallocAsync"))
+        return st;
+    int32_t* count = rows + capacity;
+    int st = check_cuda(cudaMemsetAsync(count, 0, 4, s), "cudaMemsetAsync");
+    if (st == DOT_OK) {
+        touched_rows_kernel<<<unsigned((capacity + 255) / 256), 256, 0, s>>>(touched, capacity, rows, count);
+        int dev = 0, sms = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        rmsprop_rows_kernel<<<unsigned(5 * (sms > 0 ? sms : 148)), 256, 0, s>>>(
+            sigma, sh, sh_stride, n_sh, v_sigma, v_sh, grad_sigma, grad_sh, gsh_stride, rows, count, (n_sh + 3) / 4,
+            beta, eps, lr_sigma, lr_sh, (flags & 1) != 0);
+        st = check_launch("rmsprop_rows_kernel");
+    }
+    cudaFreeAsync(rows, s);
+    return st;
 }
 
 extern "C" int dot_rmsprop_step_f32state(float* sigma, float* sh, int32_t sh_stride, int32_t n_sh, float* v_sigma,

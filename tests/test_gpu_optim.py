@@ -218,6 +218,42 @@ def test_train_epoch_device_shuffle_covers_every_ray_once():
     torch.testing.assert_close(out[1][1], out[0][1], rtol=1e-10, atol=1e-12)
 
 
+def test_rmsprop_sparse_equals_dense():
+    """dot_rmsprop_step_sparse (touched rows listed first) == the dense
+    update bit for bit on the same gradients: payload, state and the
+    consumed (zeroed) gradients."""
+    from paper_2307_15333_b200.octree import from_canonical_tensors
+    from paper_2307_15333_b200.optim import RmsPropState, rmsprop_step
+    from paper_2307_15333_b200.render import BackpropWorkspace, render_and_backprop
+    from paper_2307_15333_b200.scene_io import load_tree_bytes, tree_bytes
+    tree, o, d, t, idx = _batch_setup(seed=81, n=1 << 12)
+    tree = load_tree_bytes(tree_bytes(tree), device="cuda")
+    topo = tree.topology()
+    ws = BackpropWorkspace.for_tree(tree)
+    _, g0, _ = render_and_backprop(tree, o, d, t, 0.5, workspace=ws, ray_index=idx[: 1 << 11])
+    torch.cuda.synchronize()
+    assert 0 < int(ws.touched.sum()) < tree.capacity  # a sparse step
+    outs = []
+    for sparse in (False, True):
+        tr = from_canonical_tensors(tree.center, tree.half_extent, tree.basis_count, tree.max_depth,
+                                    topo.node.clone(), tree._sigma.clone(), tree._sh_store.clone(), topo.level_offsets)
+        st = RmsPropState(tr)
+        st.v_sh.copy_(torch.linspace(0.0, 1e-6, st.v_sh.numel(), dtype=torch.float64, device="cuda")
+                      .reshape(st.v_sh.shape))
+        w2 = BackpropWorkspace.for_tree(tr)
+        w2.dsigma.copy_(ws.dsigma)
+        w2.dsh_store.copy_(ws.dsh_store)
+        w2.touched.copy_(ws.touched)
+        from paper_2307_15333_b200.render import GradBuffer
+        g = GradBuffer(w2.dsigma, w2.dsh_store[:, :3 * tr.basis_count], w2.touched, tr.generation, w2.dsh_store)
+        rmsprop_step(tr, g, st, consume=True, sparse=sparse)
+        torch.cuda.synchronize()
+        outs.append((tr.sigma.clone(), tr.sh.clone(), st.v_sigma.clone(), st.v_sh.clone(), w2.dsigma.clone(),
+                     w2.dsh_store.clone()))
+    for a, b in zip(*outs):
+        assert torch.equal(a, b)
+
+
 class _HeldoutBundle(_Bundle):
     def __init__(self, origins, dirs, targets, heldout):
         super().__init__(origins, dirs, targets)

@@ -29,7 +29,7 @@ def test_library_exports_every_header_symbol():
     for s in syms:
         assert hasattr(lib, s), s
     assert set(syms) == set(_lib.symbols())
-    assert lib.dot_abi_version() == _lib.ABI_VERSION == 11
+    assert lib.dot_abi_version() == _lib.ABI_VERSION == 12
 
 
 def test_binding_arity_matches_header():

@@ -30,7 +30,8 @@ def main():
     data = Data(o[sel].cpu().numpy(), d[sel].cpu().numpy(), t[sel].cpu().numpy())
     del o, d, t
     torch.cuda.empty_cache()
-    cfg = TrainConfig(batch_size=1 << 20, background=1.0, device_shuffle=os.environ.get("DEVICE_SHUFFLE") == "1")
+    bs = int(os.environ.get("BATCH", str(1 << 20)))
+    cfg = TrainConfig(batch_size=bs, background=1.0, device_shuffle=os.environ.get("DEVICE_SHUFFLE") == "1")
     print("device_shuffle", cfg.device_shuffle)
     c0 = time.perf_counter()
     pool = ResidentRays(tree, data, cfg.batch_size, cfg.early_stop_eps)
@@ -47,7 +48,8 @@ def main():
         b.record()
         torch.cuda.synchronize()
         ms = a.elapsed_time(b)
-        print(f"epoch of 8 batches: {ms:.2f} ms = {ms / 8:.3f} ms per 2^20-ray batch "
+        nb = ((1 << 23) + bs - 1) // bs
+        print(f"epoch of {nb} batches: {ms:.2f} ms = {ms / nb:.3f} ms per {bs}-ray batch "
               f"({(1 << 23) / (ms / 1e3):.3e} rays/s), loss {loss:.5f}")
 
 
