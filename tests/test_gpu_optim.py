@@ -118,17 +118,18 @@ def test_train_step_equals_unfused_step():
     assert not bool(sws.ws.dsigma.any()) and not bool(sws.ws.dsh_store.any())
 
 
-def test_train_epoch_resident_planned_equals_plain():
+@pytest.mark.parametrize("basis", [1, 4, 9, 16])
+def test_train_epoch_resident_planned_equals_plain(basis):
     """train_epoch over a ResidentRays pool with a coherence rank and cost
     column (plans prepared on a side stream, no sort) == train_epoch over the
     plain dataset (per-batch key sort): same batches from the same rng, so
     the epoch loss and the trained payload agree to fp32-atomic noise; the
-    cost column is rewritten by the backward."""
+    cost column is rewritten by the backward.  Every SH degree."""
     from paper_2307_15333_b200.octree import from_canonical_tensors
     from paper_2307_15333_b200.optim import ResidentRays, RmsPropState, TrainConfig, train_epoch
     from paper_2307_15333_b200.scene_io import load_tree_bytes, tree_bytes
     from paper_2307_15333_b200.signals import SignalBuffer
-    tree, o, d, t, _ = _batch_setup(seed=21, n=1 << 15)
+    tree, o, d, t, _ = _batch_setup(seed=21, B=basis, n=1 << 15)
     tree = load_tree_bytes(tree_bytes(tree), device="cuda")
     topo = tree.topology()
 
