@@ -511,12 +511,13 @@ def plan_batch(tree: SparseOctree, origins: torch.Tensor, dirs: torch.Tensor, ra
     without a sort (``dot_plan_ranked``, one cooperative launch that also
     builds the warp order from ``costs`` and regroups the rays by cost inside
     128-ray windows, so each warp holds rays of similar length); the plan
-    then carries no keys, so its warp order comes only from ``costs``.  ``ids`` (with ``rank``): the
-    rays of ``origins`` / ``dirs`` ARE the batch (a staged batch) and ``ids``
-    their ids in the ranked dataset; the plan orders the batch's slots
-    (``costs``: one entry per slot).  ``out`` (ranked plans): preallocated
-    (int64 [n] index, int32 [ceil(n / 32)] warp order) the plan writes into
-    -- no allocation on the plan's path (e.g. per staging slot)."""
+    then carries no keys, so its warp order comes only from ``costs``.
+    ``ids`` (with ``rank``): the rays of ``origins`` / ``dirs`` ARE the batch
+    (a staged batch) and ``ids`` their ids in the ranked dataset; the plan
+    orders the batch's slots (``costs``: one entry per slot).  ``out``
+    (ranked plans): preallocated (int64 [n] index, int32 [ceil(n / 32)] warp
+    order) the plan writes into -- no allocation on the plan's path (e.g. per
+    staging slot)."""
     idx = None if ray_index is None else torch.as_tensor(ray_index, device=tree.device).reshape(-1).to(torch.int64)
     n = int(idx.shape[0]) if idx is not None else int(origins.shape[0])
     n_pool = int(origins.shape[0])
