@@ -54,8 +54,18 @@ __global__ void run_lengths_kernel(const int32_t* __restrict__ head, const int32
     len_key[j] = ~uint32_t(end - head[j]);
 }
 
+#ifndef DOT_REDUCE_MINB
+#define DOT_REDUCE_MINB 1
+#endif
+// records per group of loads in flight: 4 (80 registers, 6 blocks per SM)
+// beats 8 (128 registers, 4 blocks): 1.81 -> 1.26 ms per 2^20-ray batch;
+// 2 / 3 / 6: 1.81 / 1.40 / 1.36 ms
+#ifndef DOT_REDUCE_U
+#define DOT_REDUCE_U 4
+#endif
+
 template <int B>
-__global__ void __launch_bounds__(128) reduce_runs_kernel(
+__global__ void __launch_bounds__(128, DOT_REDUCE_MINB) reduce_runs_kernel(
     const unsigned long long* __restrict__ keys, const int32_t* __restrict__ idx,
     const int32_t* __restrict__ run_start, const uint32_t* __restrict__ run_len_key,
     const int32_t* __restrict__ n_runs, int ray_bits, const float4* __restrict__ rec,
@@ -81,7 +91,7 @@ __global__ void __launch_bounds__(128) reduce_runs_kernel(
     // records in groups of U: all loads of a group are issued before its
     // (sequential, in-order) additions, so a run costs ~1 memory latency per
     // U records instead of per record
-    constexpr int U = 8;
+    constexpr int U = DOT_REDUCE_U;
     for (; j < end; j += U) {
         int32_t ix[U];
         unsigned long long kk[U];
