@@ -806,6 +806,10 @@ def signal_pass(tree: SparseOctree, origins, dirs, early_stop_eps: float = EPS_T
                 raise InputError(f"ray plan is for {plan.n} rays, batch has {n}")
             plan.wait()
             idx = plan.idx
+            if plan.warp_order is not None and n % 32 == 0:
+                # the signal kernel walks its rays in array order (128-ray
+                # blocks): materialise the plan's longest-first warp order
+                idx = idx.view(n // 32, 32)[plan.warp_order.long()].reshape(-1)
         elif coherent and n >= COHERENT_MIN_RAYS:
             idx = plan_batch(tree, o, d, idx).idx
         view, _topo = tree.tree_view(locate_level=locate_level_train())

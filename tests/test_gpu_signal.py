@@ -173,3 +173,27 @@ def test_ray_costs_and_cost_ordered_launch():
         assert np.all(np.diff(cc[firsts]) <= 0)
         if nw % chunk:
             assert np.array_equal(od[nfull * chunk:], np.arange(nfull * chunk, nw))
+
+
+def test_signal_pass_with_ranked_plan():
+    """signal_pass(plan=) with a ranked, cost-regrouped plan (its warp order
+    materialised into the ray order when the batch is whole warps) gives the
+    signal of the unplanned pass (f64 atomics: 1e-12) and the same touched
+    set, for whole-warp and ragged batches."""
+    from helpers import irregular_tree, ray_batch
+    from paper_2307_15333_b200.render import plan_batch, pool_rank, ray_costs, signal_pass
+    tree = irregular_tree(91, 16, depth=3, splits=40, merges=4, max_depth=6, device="cuda")
+    o, d = ray_batch(92, 50_000)
+    o, d = torch.from_numpy(o).cuda(), torch.from_numpy(d).cuda()
+    pr = pool_rank(tree, o, d)
+    costs = ray_costs(tree, o, d)
+    for m in (30_016, 30_011):
+        idx = torch.randperm(50_000, generator=torch.Generator().manual_seed(4))[:m].cuda()
+        plan = plan_batch(tree, o, d, idx, rank=pr, costs=costs)
+        assert plan.warp_order is not None
+        t1 = torch.zeros(tree.capacity, dtype=torch.uint8, device="cuda")
+        t2 = torch.zeros_like(t1)
+        s1 = signal_pass(tree, o, d, ray_index=idx, plan=plan, touched=t1)
+        s2 = signal_pass(tree, o, d, ray_index=idx, coherent=False, touched=t2)
+        torch.testing.assert_close(s1, s2, rtol=1e-12, atol=1e-15)
+        assert torch.equal(t1, t2)
