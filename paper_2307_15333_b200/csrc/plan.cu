@@ -461,6 +461,7 @@ __global__ void __launch_bounds__(kPlanThreads, kPlanMinBlocks) plan_coop_kernel
         }
     }
     grid.sync();
+    PLAN_STAMP(5)
 
     // E. chunk costs and their histogram (descending cost = ascending bin)
     const int64_t nfull = nw / a.chunk;
@@ -471,7 +472,7 @@ __global__ void __launch_bounds__(kPlanThreads, kPlanMinBlocks) plan_coop_kernel
         atomicAdd(w.hist + (kPlanCostBins - 1 - int(mx)), 1);
     }
     grid.sync();
-    PLAN_STAMP(5)
+    PLAN_STAMP(6)
 
     // F. bins -> start chunk (warp 0 of block 0: 32 bins per lane)
     if (blockIdx.x == 0 && threadIdx.x < 32) {
@@ -491,7 +492,7 @@ __global__ void __launch_bounds__(kPlanThreads, kPlanMinBlocks) plan_coop_kernel
         }
     }
     grid.sync();
-    PLAN_STAMP(6)
+    PLAN_STAMP(7)
 
     // G. scatter the chunks; the short last chunk goes last; scratch cleared
     for (int64_t c = gt; c < nfull; c += GT) {
@@ -501,7 +502,7 @@ __global__ void __launch_bounds__(kPlanThreads, kPlanMinBlocks) plan_coop_kernel
     for (int64_t v = nfull * a.chunk + gt; v < nw; v += GT) a.warp_order[v] = int32_t(v);
     grid.sync();
     for (int64_t b = gt; b < kPlanCostBins; b += GT) w.hist[b] = 0;
-    PLAN_STAMP(7)
+    PLAN_STAMP(8)
 }
 
 size_t plan_ranked_workspace(int64_t n_pool, int64_t n, int) { return carve(nullptr, n_pool, n, nullptr); }

@@ -2,8 +2,8 @@
 DOT_LIB_PATH=tools/variants/lib_diag.so): %globaltimer after each grid sync,
 alone and beside a bandwidth-bound copy on another stream (the optimizer's
 stand-in).  Phases: A mark, B count, C warp bases (+ repeats), D place
-(+ gathers, appended rays), E chunk costs + histogram, F bin scan, G scatter
-+ clear."""
+(+ gathers, appended rays), W cost regrouping, E chunk costs + histogram,
+F bin scan, G scatter + clear."""
 import ctypes
 import os
 import sys
@@ -32,7 +32,7 @@ def main():
     big_b = torch.empty_like(big_a)
     side = torch.cuda.Stream()
     t = (ctypes.c_ulonglong * 16)()
-    names = "ABCDEFG"
+    names = "ABCDWEFG"
     for label, mode, rk, od, cst in (("positions", 0, None, None, costs), ("pool rays", 1, rank, order, costs),
                                      ("slots", 2, None, None, costs[:n].contiguous())):
         for busy in (False, True):
@@ -45,9 +45,9 @@ def main():
                           1, _lib.ptr(wo), _lib.ptr(ws), ws.numel(), _lib.ptr(out), _lib.stream_ptr())
                 torch.cuda.synchronize()
             lib.dot_diag_plan_timeline(t)
-            ph = [(t[i + 1] - t[i]) / 1e3 for i in range(7)]
-            print(f"{label:10s} {'beside copy' if busy else 'alone':12s} total {(t[7] - t[0]) / 1e3:7.1f} us  "
-                  + " ".join(f"{names[i]} {ph[i]:6.1f}" for i in range(7)))
+            ph = [(t[i + 1] - t[i]) / 1e3 for i in range(8)]
+            print(f"{label:10s} {'beside copy' if busy else 'alone':12s} total {(t[8] - t[0]) / 1e3:7.1f} us  "
+                  + " ".join(f"{names[i]} {ph[i]:6.1f}" for i in range(8)))
 
 
 if __name__ == "__main__":
