@@ -624,3 +624,38 @@ def test_large_batch_with_schedule_vs_oracle(oracle):
     assert_grads_close(g.dsh, r_g.dsh, what="dsh")
     np.testing.assert_array_equal(g.touched, r_g.touched)
     np.testing.assert_allclose(sig, r_sig, atol=ATOL, rtol=RTOL)
+
+
+def test_pool_rank_misuse_is_refused():
+    """PoolRank / plan_batch(rank=, ids=) argument errors raise InputError
+    before any launch."""
+    import torch
+    from helpers import irregular_tree, ray_batch
+    from paper_2307_15333_b200.errors import InputError
+    from paper_2307_15333_b200.render import PoolRank, plan_batch, pool_keys, pool_rank
+    tree = irregular_tree(3, 4, depth=2, splits=5, max_depth=4, device="cuda")
+    o, d = ray_batch(4, 1000)
+    o, d = torch.from_numpy(o).cuda(), torch.from_numpy(d).cuda()
+    pr = pool_rank(tree, o, d)
+    idx = torch.arange(100, device="cuda")
+    with pytest.raises(InputError):
+        PoolRank(pr.rank.long(), pr.order)  # not int32
+    with pytest.raises(InputError):
+        PoolRank(pr.rank, pr.order[:10])  # lengths differ
+    with pytest.raises(InputError):
+        PoolRank.identity(1000, "cuda").permute(o)  # no order to permute by
+    with pytest.raises(InputError):
+        pool_rank(tree, o, d, bits=40)
+    with pytest.raises(InputError):
+        plan_batch(tree, o, d, idx, rank=pr, keys=pool_keys(tree, o, d))
+    with pytest.raises(InputError):
+        plan_batch(tree, o, d, idx, ids=idx)  # ids without a rank
+    with pytest.raises(InputError):
+        plan_batch(tree, o[:100], d[:100], None, rank=pr, ids=idx[:50])  # ids not one per row
+    with pytest.raises(InputError):
+        plan_batch(tree, o, d, idx, rank=pr, costs=torch.zeros(10, dtype=torch.int16, device="cuda"))
+    with pytest.raises(InputError):
+        plan_batch(tree, o, d, idx, rank=pr, out=(torch.empty(10, dtype=torch.int64, device="cuda"),
+                                                  torch.empty(1, dtype=torch.int32, device="cuda")))
+    # positions map through the rank
+    assert torch.equal(pr.positions(idx), pr.rank[idx].long())
