@@ -3,7 +3,8 @@ per-block timeline): one 2^20-ray batch in its coherence order, launched
 (a) in the learned-schedule order, (b) by each warp's exact cost
 (max over its rays of the composited + post-cut/2 count the kernel reports),
 (c) by each warp's measured duration from run (a) -- the upper bound of any
-cost-ordered launch.  Prints the kernel span of each."""
+cost-ordered launch.  Prints the kernel span of each.  RANKED=1: the
+batch planned as in the bench (ranked pool, cost-regrouped windows)."""
 import ctypes
 import os
 import sys
@@ -14,7 +15,8 @@ import torch  # noqa: E402
 
 import bench  # noqa: E402
 from paper_2307_15333_b200 import _lib, scenes  # noqa: E402
-from paper_2307_15333_b200.render import BackpropWorkspace, plan_batch, render_and_backprop  # noqa: E402
+from paper_2307_15333_b200.render import (BackpropWorkspace, PoolRank, plan_batch, pool_rank, ray_costs,
+                                          render_and_backprop)  # noqa: E402
 
 
 def timeline(nb):
@@ -35,8 +37,15 @@ def main():
         idx = torch.randperm(o.shape[0], generator=g, device=dev)[: 1 << 20]
         render_and_backprop(tree, o, d, t, 1.0, ray_index=idx, workspace=BackpropWorkspace.for_tree(tree))
     g.manual_seed(999)
-    idx = torch.randperm(o.shape[0], generator=g, device=dev)[: 1 << 20]
-    p = plan_batch(tree, o, d, idx)
+    if os.environ.get("RANKED"):  # the bench's plan: ranked pool in key order, regrouped windows
+        pr = pool_rank(tree, o, d)
+        costs = ray_costs(tree, o, d)
+        o, d, t, costs = pr.permute(o, d, t, costs)
+        idx = torch.randperm(o.shape[0], generator=g, device=dev)[: 1 << 20]
+        p = plan_batch(tree, o, d, idx, rank=PoolRank.identity(o.shape[0], dev), costs=costs)
+    else:
+        idx = torch.randperm(o.shape[0], generator=g, device=dev)[: 1 << 20]
+        p = plan_batch(tree, o, d, idx)
     n = p.n
     nb = n // 32
     view, _ = tree.tree_view(locate_level=7)
