@@ -384,6 +384,10 @@ def run_ours(args, rank, world, local_rank):
         # beside the (bandwidth-bound) update instead of the backward;
         # DOT_PLAN_EARLY=1: queued before the step (runs beside the backward)
         early = os.environ.get("DOT_PLAN_EARLY", "0") == "1"
+        if pre_planned:  # diagnostic: every plan made before the loop (the plan's cost on the step)
+            return train_step(tree, origins, dirs, targets, state, buf, sws, BG, EPS, ray_index=idx,
+                              grad_scale=gs, exchange=exchange if world > 1 else None,
+                              kernel_events=kev[k] if timed_kernel else None, plan=plan)
         if early:
             next_plan()
         return train_step(tree, origins, dirs, targets, state, buf, sws, BG, EPS,
@@ -392,6 +396,13 @@ def run_ours(args, rank, world, local_rank):
                           kernel_events=kev[k] if timed_kernel else None, plan=plan,
                           after_backward=None if early else next_plan)
 
+    # DOT_PLAN_PRE=1 (diagnostic, never a bench line): all plans made up
+    # front with their own outputs, none inside the steps
+    pre_planned = os.environ.get("DOT_PLAN_PRE", "0") == "1"
+    if pre_planned:
+        for k in range(total_steps):
+            plans[k] = plan_batch(tree, origins, dirs, batch_index(k), keys=pkeys, rank=prank, costs=pcosts)
+        torch.cuda.synchronize()
     clocks = ClockSampler(local_rank).start()  # before the warm-up: its start-up is CPU-heavy
     # at most LEAD steps in flight: the host waits for step k - LEAD before
     # queuing step k, so the caching allocator recycles the plans' buffers
