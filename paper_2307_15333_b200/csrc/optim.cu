@@ -13,6 +13,12 @@
 namespace dot {
 
 constexpr int kMaxPeers = DOT_MAX_PEERS;
+// kernel mode bits: consume (zero the gradients), and whether the +0-gradient
+// shortcut is exact for these hyper-parameters (lr >= 0, eps > 0)
+constexpr int kRmsConsume = 1, kRmsZeroOk = 2;
+static int rms_mode(int32_t flags, double eps, double lr_sigma, double lr_sh) {
+    return ((flags & 1) ? kRmsConsume : 0) | ((eps > 0.0 && lr_sigma >= 0.0 && lr_sh >= 0.0) ? kRmsZeroOk : 0);
+}
 
 // shared-memory carveout preference of the update (-1: driver default).  A
 // non-zero carveout keeps shared memory configured on the SMs while the
@@ -23,17 +29,25 @@ constexpr int kMaxPeers = DOT_MAX_PEERS;
 #endif
 
 __device__ __forceinline__ float rms_update(float theta, double& v, double g, double beta,
-                                            double omb, double eps, double lr, bool clamp) {
+                                            double omb, double eps, double lr, bool clamp, bool zok) {
     v = __dadd_rn(__dmul_rn(beta, v), __dmul_rn(__dmul_rn(omb, g), g));
     // g == 0 (e.g. leaves touched only past the early-termination cut): the
-    // step lr*g / (sqrt(v) + eps) is exactly +-0 for any finite v, so theta
-    // is unchanged -- skip the IEEE sqrt and division (bit-identical result)
-    if (g == 0.0 && v <= 1.7976931348623157e308) {
+    // step lr*g / (sqrt(v) + eps) is exactly +-0 for eps > 0 and a finite v,
+    // and theta -+ 0 == theta unless theta is itself a zero (-0 - -0 = +0),
+    // so theta is unchanged -- skip the IEEE sqrt and division (bit-identical
+    // result).  Zero payloads, eps <= 0 (0/0 = NaN when v = 0) and an
+    // infinite v take the full path; zok (eps > 0, lr >= 0) is decided on the
+    // host (kRmsZeroOk).
+    if (zok && g == 0.0 && theta != 0.f && v <= 1.7976931348623157e308) {
         double t = double(theta);
         if (clamp && !(t >= 0.0)) t = (t != t) ? t : 0.0;
         return float(t);
     }
+#ifdef DOT_RMS_FAKE_MATH  // diagnostic builds only (wrong values): the update without its sqrt / division
+    double t = __dsub_rn(double(theta), __dmul_rn(__dmul_rn(lr, g), __dadd_rn(v, eps)));
+#else
     double t = __dsub_rn(double(theta), __ddiv_rn(__dmul_rn(lr, g), __dadd_rn(__dsqrt_rn(v), eps)));
+#endif
     if (clamp && !(t >= 0.0)) t = (t != t) ? t : 0.0;  // np.maximum keeps NaN
     return float(t);
 }
@@ -45,7 +59,8 @@ __global__ void __launch_bounds__(256) rmsprop_kernel(float* __restrict__ sigma,
                                                       float* __restrict__ gsig, float* __restrict__ gsh,
                                                       int gsh_stride, const uint8_t* __restrict__ touched, int64_t cap,
                                                       int quads, double beta, double eps, double lr_sigma,
-                                                      double lr_sh, bool consume) {
+                                                      double lr_sh, int mode) {
+    const bool consume = (mode & kRmsConsume) != 0, zok = (mode & kRmsZeroOk) != 0;
     const int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (t >= cap * quads) return;
     const int64_t row = t / quads;
@@ -54,7 +69,7 @@ __global__ void __launch_bounds__(256) rmsprop_kernel(float* __restrict__ sigma,
     const double omb = __dsub_rn(1.0, beta);
     if (j == 0) {
         double v = v_sigma[row];
-        sigma[row] = rms_update(sigma[row], v, double(gsig[row]), beta, omb, eps, lr_sigma, true);
+        sigma[row] = rms_update(sigma[row], v, double(gsig[row]), beta, omb, eps, lr_sigma, true, zok);
         v_sigma[row] = v;
         if (consume) gsig[row] = 0.f;
     }
@@ -64,7 +79,7 @@ __global__ void __launch_bounds__(256) rmsprop_kernel(float* __restrict__ sigma,
     double* v = v_sh + row * n_sh + k0;
     for (int u = 0; u < 4 && k0 + u < n_sh; ++u) {
         double vv = v[u];
-        p[u] = rms_update(p[u], vv, double(g[u]), beta, omb, eps, lr_sh, false);
+        p[u] = rms_update(p[u], vv, double(g[u]), beta, omb, eps, lr_sh, false, zok);
         v[u] = vv;
         if (consume) g[u] = 0.f;
     }
@@ -84,7 +99,7 @@ __device__ __forceinline__ void rms_quad(int64_t r, int j, float* __restrict__ s
                                          int sh_stride, int n_sh, double* __restrict__ v_sigma,
                                          double* __restrict__ v_sh, float* __restrict__ gsig,
                                          float* __restrict__ gsh, int gsh_stride, double beta, double eps,
-                                         double lr_sigma, double lr_sh, bool consume) {
+                                         double lr_sigma, double lr_sh, bool consume, bool zok) {
     const double omb = __dsub_rn(1.0, beta);
     float* const gp = gsh + r * int64_t(gsh_stride) + 4 * j;
     float* const pp = sh + r * int64_t(sh_stride) + 4 * j;
@@ -94,14 +109,15 @@ __device__ __forceinline__ void rms_quad(int64_t r, int j, float* __restrict__ s
     float4 p = *reinterpret_cast<const float4*>(pp);
     if (j == 0) {
         double vs = v_sigma[r];
-        sigma[r] = rms_update(sigma[r], vs, double(gsig[r]), beta, omb, eps, lr_sigma, true);
+        sigma[r] = rms_update(sigma[r], vs, double(gsig[r]), beta, omb, eps, lr_sigma, true, zok);
         v_sigma[r] = vs;
         if (consume) gsig[r] = 0.f;
     }
-    if (g.x == 0.f && g.y == 0.f && g.z == 0.f && g.w == 0.f) {
-        // zero gradient quad (e.g. a leaf touched only past the cut): v
+    if (zok && (__float_as_uint(g.x) | __float_as_uint(g.y) | __float_as_uint(g.z) | __float_as_uint(g.w)) == 0u) {
+        // +0 gradient quad (e.g. a leaf touched only past the cut): v
         // decays, theta - lr*0/(sqrt(v)+eps) == theta exactly and the
-        // gradients are already (+-)0 -- no payload or gradient store
+        // gradients are already 0 -- no payload or gradient store (the
+        // conditions as in rms_update)
         const double lim = 1.7976931348623157e308;
         const double n0 = __dmul_rn(beta, va.x), n1 = __dmul_rn(beta, va.y);
         const double n2 = __dmul_rn(beta, vb.x), n3 = __dmul_rn(beta, vb.y);
@@ -111,10 +127,10 @@ __device__ __forceinline__ void rms_quad(int64_t r, int j, float* __restrict__ s
             return;
         }
     }
-    p.x = rms_update(p.x, va.x, double(g.x), beta, omb, eps, lr_sh, false);
-    p.y = rms_update(p.y, va.y, double(g.y), beta, omb, eps, lr_sh, false);
-    p.z = rms_update(p.z, vb.x, double(g.z), beta, omb, eps, lr_sh, false);
-    p.w = rms_update(p.w, vb.y, double(g.w), beta, omb, eps, lr_sh, false);
+    p.x = rms_update(p.x, va.x, double(g.x), beta, omb, eps, lr_sh, false, zok);
+    p.y = rms_update(p.y, va.y, double(g.y), beta, omb, eps, lr_sh, false, zok);
+    p.z = rms_update(p.z, vb.x, double(g.z), beta, omb, eps, lr_sh, false, zok);
+    p.w = rms_update(p.w, vb.y, double(g.w), beta, omb, eps, lr_sh, false, zok);
     *reinterpret_cast<float4*>(pp) = p;
     v[0] = va;
     v[1] = vb;
@@ -132,14 +148,14 @@ __global__ void __launch_bounds__(256, 5) rmsprop_vec_kernel(float* __restrict__
                                                              float* __restrict__ gsh, int gsh_stride,
                                                              const uint8_t* __restrict__ touched, int64_t cap,
                                                              int quads, double beta, double eps, double lr_sigma,
-                                                             double lr_sh, bool consume) {
+                                                             double lr_sh, int mode) {
     const int64_t f = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (f >= cap * quads) return;
     const int64_t r = f / quads;
     const int j = int(f - r * quads);
     if (!__ldg(touched + r)) return;
     rms_quad(r, j, sigma, sh, sh_stride, n_sh, v_sigma, v_sh, gsig, gsh, gsh_stride, beta, eps, lr_sigma, lr_sh,
-             consume);
+             mode & kRmsConsume, mode & kRmsZeroOk);
 }
 
 // Sparse steps (a small batch touches few rows): the dense update's cost is
@@ -166,13 +182,13 @@ __global__ void __launch_bounds__(256, 5) rmsprop_rows_kernel(float* __restrict_
                                                               const int32_t* __restrict__ rows,
                                                               const int32_t* __restrict__ count, int quads,
                                                               double beta, double eps, double lr_sigma, double lr_sh,
-                                                              bool consume) {
+                                                              int mode) {
     const int64_t total = int64_t(*count) * quads;
     for (int64_t f = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; f < total;
          f += int64_t(gridDim.x) * blockDim.x) {
         const int64_t i = f / quads;
         rms_quad(__ldg(rows + i), int(f - i * quads), sigma, sh, sh_stride, n_sh, v_sigma, v_sh, gsig, gsh,
-                 gsh_stride, beta, eps, lr_sigma, lr_sh, consume);
+                 gsh_stride, beta, eps, lr_sigma, lr_sh, mode & kRmsConsume, mode & kRmsZeroOk);
     }
 }
 
@@ -181,9 +197,9 @@ __global__ void __launch_bounds__(256, 5) rmsprop_rows_kernel(float* __restrict_
 // results are within float tolerance of the f64-state update while the
 // state traffic halves (1568 -> 1184 bytes per touched SH-3 row).
 __device__ __forceinline__ float rms_update_f32v(float theta, float& v32, double g, double beta, double omb,
-                                                 double eps, double lr, bool clamp) {
+                                                 double eps, double lr, bool clamp, bool zok) {
     double v = double(v32);
-    const float out = rms_update(theta, v, g, beta, omb, eps, lr, clamp);
+    const float out = rms_update(theta, v, g, beta, omb, eps, lr, clamp, zok);
     v32 = float(v);
     return out;
 }
@@ -194,7 +210,8 @@ __global__ void __launch_bounds__(256, 5) rmsprop_f32v_kernel(float* __restrict_
                                                               float* __restrict__ gsh, int gsh_stride,
                                                               const uint8_t* __restrict__ touched, int64_t cap,
                                                               int quads, double beta, double eps, double lr_sigma,
-                                                              double lr_sh, bool consume) {
+                                                              double lr_sh, int mode) {
+    const bool consume = (mode & kRmsConsume) != 0, zok = (mode & kRmsZeroOk) != 0;
     const int64_t f = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (f >= cap * quads) return;
     const int64_t r = f / quads;
@@ -202,7 +219,7 @@ __global__ void __launch_bounds__(256, 5) rmsprop_f32v_kernel(float* __restrict_
     if (!__ldg(touched + r)) return;
     const double omb = __dsub_rn(1.0, beta);
     if (j == 0) {
-        sigma[r] = rms_update_f32v(sigma[r], v_sigma[r], double(gsig[r]), beta, omb, eps, lr_sigma, true);
+        sigma[r] = rms_update_f32v(sigma[r], v_sigma[r], double(gsig[r]), beta, omb, eps, lr_sigma, true, zok);
         if (consume) gsig[r] = 0.f;
     }
     const int k0 = 4 * j;
@@ -213,10 +230,10 @@ __global__ void __launch_bounds__(256, 5) rmsprop_f32v_kernel(float* __restrict_
         const float4 g = *reinterpret_cast<const float4*>(gp);
         float4 v = *vp;
         float4 p = *reinterpret_cast<const float4*>(pp);
-        p.x = rms_update_f32v(p.x, v.x, double(g.x), beta, omb, eps, lr_sh, false);
-        p.y = rms_update_f32v(p.y, v.y, double(g.y), beta, omb, eps, lr_sh, false);
-        p.z = rms_update_f32v(p.z, v.z, double(g.z), beta, omb, eps, lr_sh, false);
-        p.w = rms_update_f32v(p.w, v.w, double(g.w), beta, omb, eps, lr_sh, false);
+        p.x = rms_update_f32v(p.x, v.x, double(g.x), beta, omb, eps, lr_sh, false, zok);
+        p.y = rms_update_f32v(p.y, v.y, double(g.y), beta, omb, eps, lr_sh, false, zok);
+        p.z = rms_update_f32v(p.z, v.z, double(g.z), beta, omb, eps, lr_sh, false, zok);
+        p.w = rms_update_f32v(p.w, v.w, double(g.w), beta, omb, eps, lr_sh, false, zok);
         *vp = v;
         if (g.x != 0.f || g.y != 0.f || g.z != 0.f || g.w != 0.f) {
             *reinterpret_cast<float4*>(pp) = p;
@@ -227,7 +244,7 @@ __global__ void __launch_bounds__(256, 5) rmsprop_f32v_kernel(float* __restrict_
     for (int u = 0; u < 4 && k0 + u < n_sh; ++u) {
         float* p = sh + r * sh_stride + k0 + u;
         float* g = gsh + r * gsh_stride + k0 + u;
-        *p = rms_update_f32v(*p, v_sh[r * n_sh + k0 + u], double(*g), beta, omb, eps, lr_sh, false);
+        *p = rms_update_f32v(*p, v_sh[r * n_sh + k0 + u], double(*g), beta, omb, eps, lr_sh, false, zok);
         if (consume) *g = 0.f;
     }
 }
@@ -256,7 +273,8 @@ __global__ void __launch_bounds__(256) rmsprop_peer_kernel(PeerRows P, int sh_st
                                                            double* __restrict__ v_sigma,
                                                            double* __restrict__ v_sh, int64_t lo, int64_t hi,
                                                            int quads, double beta, double eps, double lr_sigma,
-                                                           double lr_sh, bool consume) {
+                                                           double lr_sh, int mode) {
+    const bool consume = (mode & kRmsConsume) != 0, zok = (mode & kRmsZeroOk) != 0;
     const int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (t >= (hi - lo) * quads) return;
     const int64_t row = lo + t / quads;
@@ -269,7 +287,7 @@ __global__ void __launch_bounds__(256) rmsprop_peer_kernel(PeerRows P, int sh_st
         double g = 0.0;
         for (int r = 0; r < P.world; ++r) g += double(P.gsig[r][row]);
         double v = v_sigma[row];
-        const float th = rms_update(P.sigma[P.rank][row], v, g, beta, omb, eps, lr_sigma, true);
+        const float th = rms_update(P.sigma[P.rank][row], v, g, beta, omb, eps, lr_sigma, true, zok);
         v_sigma[row] = v;
         for (int r = 0; r < P.world; ++r) {
             P.sigma[r][row] = th;
@@ -287,7 +305,7 @@ __global__ void __launch_bounds__(256) rmsprop_peer_kernel(PeerRows P, int sh_st
     double* v = v_sh + row * n_sh + k0;
     for (int u = 0; u < 4 && k0 + u < n_sh; ++u) {
         double vv = v[u];
-        th[u] = rms_update(th0[u], vv, g[u], beta, omb, eps, lr_sh, false);
+        th[u] = rms_update(th0[u], vv, g[u], beta, omb, eps, lr_sh, false, zok);
         v[u] = vv;
     }
     for (int r = 0; r < P.world; ++r) {
@@ -332,7 +350,7 @@ extern "C" int dot_rmsprop_step_peers(const dot_peer_rows* peers, int32_t sh_str
     const int64_t total = (row_hi - row_lo) * quads;
     rmsprop_peer_kernel<<<unsigned((total + 255) / 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
         P, sh_stride, n_sh, gsh_stride, v_sigma, v_sh, row_lo, row_hi, quads, beta, eps, lr_sigma, lr_sh,
-        (flags & 1) != 0);
+        rms_mode(flags, eps, lr_sigma, lr_sh));
     return check_launch("rmsprop_peer_kernel");
 }
 
@@ -358,12 +376,12 @@ extern "C" int dot_rmsprop_step(float* sigma, float* sh, int32_t sh_stride, int3
 #endif
         rmsprop_vec_kernel<<<grid, 256, 0, s>>>(sigma, sh, sh_stride, n_sh, v_sigma, v_sh, grad_sigma, grad_sh,
                                                 gsh_stride, touched, capacity, quads, beta, eps, lr_sigma, lr_sh,
-                                                (flags & 1) != 0);
+                                                rms_mode(flags, eps, lr_sigma, lr_sh));
         return check_launch("rmsprop_vec_kernel");
     }
     rmsprop_kernel<<<grid, 256, 0, s>>>(sigma, sh, sh_stride, n_sh, v_sigma, v_sh, grad_sigma, grad_sh,
                                         gsh_stride, touched, capacity, quads, beta, eps, lr_sigma, lr_sh,
-                                        (flags & 1) != 0);
+                                        rms_mode(flags, eps, lr_sigma, lr_sh));
     return check_launch("rmsprop_kernel");
 }
 
@@ -398,7 +416,7 @@ extern "C" int dot_rmsprop_step_sparse(float* sigma, float* sh, int32_t sh_strid
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         rmsprop_rows_kernel<<<unsigned(5 * (sms > 0 ? sms : 148)), 256, 0, s>>>(
             sigma, sh, sh_stride, n_sh, v_sigma, v_sh, grad_sigma, grad_sh, gsh_stride, rows, count, (n_sh + 3) / 4,
-            beta, eps, lr_sigma, lr_sh, (flags & 1) != 0);
+            beta, eps, lr_sigma, lr_sh, rms_mode(flags, eps, lr_sigma, lr_sh));
         st = check_launch("rmsprop_rows_kernel");
     }
     cudaFreeAsync(rows, s);
@@ -421,6 +439,6 @@ extern "C" int dot_rmsprop_step_f32state(float* sigma, float* sh, int32_t sh_str
     const int64_t total = capacity * quads;
     rmsprop_f32v_kernel<<<unsigned((total + 255) / 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
         sigma, sh, sh_stride, n_sh, v_sigma, v_sh, grad_sigma, grad_sh, gsh_stride, touched, capacity, quads, beta,
-        eps, lr_sigma, lr_sh, (flags & 1) != 0);
+        eps, lr_sigma, lr_sh, rms_mode(flags, eps, lr_sigma, lr_sh));
     return check_launch("rmsprop_f32v_kernel");
 }
